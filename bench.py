@@ -1,0 +1,317 @@
+"""Benchmark: spark fitness evaluations/s and ms/generation of the B200
+MGFWA engine on BASELINE.json's configs[1] (C2: MLP-weights black box
+784-32-10, S = 1024 synthetic samples, B = 1, mu = 5 fireworks x lambda = 300
+sparks, M = 3 guides).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2|c1|c4]
+
+A "step" is one MGFWA generation (the body of run()'s loop,
+engine.cpp:359-417) on synthetic data.  value = whole-job evaluations per
+second, device-timed with CUDA events on the engine's stream over exactly K
+generations (max over ranks).  e2e = the same metric through the one-shot
+C-ABI run() drop-in (mgfwa_run_once) with host buffers in and out.
+Multi-GPU (torchrun): one independent run per rank (replicas, weak scaling;
+see DESIGN.md §5).  ``--impl reference`` times the compiled reference
+(oracle/_ref, /root/reference/proj/src/engine.cpp run()) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+WORKLOADS = {
+    # BASELINE.json configs[1] (headline)
+    "c2": dict(desc="C2 MLP-weights 784-32-10, S=1024, B=1, mu=5, lambda=300, M=3", kind="mlp", D=25450,
+               B=1, mu=5, lam=300, M=3, lo=-1.0, hi=1.0, in_dim=784, hidden=32, out_dim=10, samples=1024),
+    # configs[0]
+    "c1": dict(desc="C1 sphere D=30, B=1, mu=5, lambda=30, M=3", kind="sphere", D=30, B=1, mu=5, lam=30, M=3,
+               lo=-10.0, hi=10.0),
+    # configs[3]
+    "c4": dict(desc="C4 Rastrigin D=1e5, B=1, mu=5, lambda=30, M=3", kind="rastrigin", D=100000, B=1, mu=5,
+               lam=30, M=3, lo=-5.12, hi=5.12),
+}
+FLOP_PER_EVAL_C2 = 2 * 1024 * (784 * 32 + 32 * 10)  # 52,035,584
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+def make_objective(P, w):
+    if w["kind"] == "mlp":
+        return P.MlpWeights(w["in_dim"], w["hidden"], w["out_dim"], w["samples"], 1)
+    return {"sphere": P.Sphere(), "rastrigin": P.Rastrigin(), "ackley": P.Ackley()}[w["kind"]]
+
+
+def make_config(P, w, max_evals):
+    return P.MgfwaConfig(batches=w["B"], fireworks=w["mu"], sparks_per_firework=w["lam"],
+                         guides_per_firework=w["M"], boosts=[1.0, 2.0, 4.0][: w["M"]],
+                         max_evaluations=max_evals)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+                self.lines = [l for l in out.splitlines() if l.strip()]
+            except Exception:
+                pass
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+                for n, v in zip(names, f[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference_generation(w, seed: int, workers: int):
+    """One full reference generation (run() with budget init + 1 wave) on the
+    host cores via the compiled reference; returns (evals, seconds)."""
+    import oracle as O
+
+    ref = O.Reference()
+    cfg = O.Config(batches=w["B"], fireworks=w["mu"], sparks_per_firework=w["lam"], guides_per_firework=w["M"],
+                   boosts=[1.0, 2.0, 4.0][: w["M"]],
+                   max_evaluations=w["B"] * w["mu"] + w["B"] * w["mu"] * (w["lam"] + w["M"]))
+    kind = {"mlp": O.OBJ_MLP_WEIGHTS, "sphere": O.OBJ_SPHERE, "rastrigin": O.OBJ_RASTRIGIN}[w["kind"]]
+    desc = O.ObjectiveDesc(kind=kind, in_dim=w.get("in_dim", 784), hidden=w.get("hidden", 32),
+                           out_dim=w.get("out_dim", 10), samples=w.get("samples", 1024))
+    lo, hi = np.full(w["D"], w["lo"]), np.full(w["D"], w["hi"])
+    t = time.perf_counter()
+    r = ref.run(cfg, lo, hi, desc, seed, workers=workers)
+    return r.evaluations_used, time.perf_counter() - t
+
+
+def run_reference_arm(args, w):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    evals, secs, steps = 0, 0.0, 0
+    t0 = time.perf_counter()
+    for _ in range(args.warmup):  # bounded warm-up
+        cpu_reference_generation(w, 1000, cores)
+        if time.perf_counter() - t0 > 30:
+            break
+    t1 = time.perf_counter()
+    for k in range(args.steps):
+        e, s = cpu_reference_generation(w, k, cores)
+        evals += e
+        secs += s
+        steps += 1
+        if time.perf_counter() - t1 > 150:  # keep the arm within a few minutes
+            break
+    v = evals / secs
+    line = {"metric": "spark fitness evals/sec", "value": v, "unit": "evals/s", "n_gpus": args.gpus,
+            "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w["desc"], "budget_per_step": "init + 1 generation"}, "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": "evals/s", "cores": cores, "kind": "reference",
+                             "sample": f"{steps} x mgfwa::run() of one generation (init + 1 wave), "
+                                       f"EvalBackend::data_parallel({cores})"},
+            "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    w = WORKLOADS[args.workload]
+
+    if args.impl == "reference":
+        run_reference_arm(args, w)
+        return
+
+    import torch
+
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    import paper_2501_03944_b200 as P
+
+    dev = torch.cuda.current_device()
+    stream = torch.cuda.Stream()
+    obj = make_objective(P, w)
+    space = P.SearchSpace.box(w["D"], w["lo"], w["hi"])
+    eng = P.Engine(make_config(P, w, 1 << 62), space, obj, seed=rank, device=dev)
+    eng.set_stream(stream.cuda_stream)
+    eng.initialize()
+    kpg = eng.kernels_per_generation()
+    eng.enqueue(args.warmup)
+    eng.sync()
+    before = eng.counters()["evaluations_used"]
+
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        with torch.cuda.stream(stream):
+            start.record(stream)
+            eng.enqueue(args.steps)
+            end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    eng.sync()
+    ms = start.elapsed_time(end)
+    evals = eng.counters()["evaluations_used"] - before
+    if world > 1:
+        t = torch.tensor([ms, float(evals)], dtype=torch.float64, device="cuda")
+        mx = t.clone()
+        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+        sm = t.clone()
+        torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
+        ms_max, evals_total = float(mx[0]), float(sm[1])
+    else:
+        ms_max, evals_total = ms, float(evals)
+
+    # dominant kernel: spark fitness (tcgen05 GEMM) timed alone, CUDA events
+    fit_ms, units = eng.time_fitness(20)
+    pk, pk_kind = peaks()
+    if w["kind"] == "mlp":
+        achieved = FLOP_PER_EVAL_C2 * units / (fit_ms * 1e-3) / 1e12
+        roof = {"kernel": "k_mlp_fitness<32> (tcgen05.mma kind::f16, TMA, TMEM)", "bound": "tensor",
+                "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / pk["bf16_tflops"], "traffic": None,
+                "algorithmic_per_launch": f"{units} sparks x {FLOP_PER_EVAL_C2} FLOP",
+                "ms_per_launch": fit_ms, "peak_source": f"{pk_kind} bf16 burst (MEASURED_PEAKS.json)"}
+    else:
+        byts = units * w["D"] * 4 + w["B"] * w["mu"] * w["D"] * 4
+        achieved = byts / (fit_ms * 1e-3) / 1e9
+        roof = {"kernel": "k_explode_map (fused explode+map+fitness)", "bound": "hbm", "achieved": achieved,
+                "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                "ms_per_launch": fit_ms, "peak_source": f"{pk_kind} hbm copy"}
+
+    line = {"metric": "spark fitness evals/sec", "value": evals_total / (ms_max * 1e-3), "unit": "evals/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16" if w["kind"] == "mlp" else "f32", "data": "synthetic",
+            "config": {"workload": w["desc"], "D": w["D"], "per_rank": "independent run (replica)",
+                       "l2": "inputs larger than L2: spark matrix fp32+bf16 229 MB/generation > 126 MB"
+                       if args.workload == "c2" else "n/a"},
+            "gpu_launches": kpg * args.steps, "roofline": roof}
+    line["clocks"] = clk.summary()
+
+    if rank == 0 and not args.no_e2e:
+        # e2e: one-shot run() drop-in over host buffers (mgfwa_run_once):
+        # budget = init + K generations; includes context setup, H2D of the
+        # search bounds, the K generations and D2H of best/trace.
+        import ctypes as C
+
+        from paper_2501_03944_b200 import _capi as A
+
+        cfg = make_config(P, w, w["B"] * w["mu"] + args.steps * w["B"] * w["mu"] * (w["lam"] + w["M"]))
+        c, keep = cfg._c()
+        sp, ob = space._c(), obj._c()
+        B, D = w["B"], w["D"]
+        bf, bp = np.empty(B), np.empty((B, D))
+        cap = args.steps + 2
+        te, tb, tw = np.zeros((B, cap), np.uint64), np.zeros((B, cap)), np.zeros((B, cap))
+        cnt = A.mgfwa_counters_t()
+        pdp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+
+        def once():
+            rc = A.lib().mgfwa_run_once(C.byref(c), C.byref(sp), C.byref(ob), 7, dev, pdp(bf), pdp(bp),
+                                        te.ctypes.data_as(C.POINTER(C.c_uint64)), pdp(tb), pdp(tw), cap,
+                                        C.byref(cnt))
+            assert rc == 0, A.lib().mgfwa_last_error(None)
+
+        once()  # warm (module load, first-touch)
+        t = time.perf_counter()
+        once()
+        dt = time.perf_counter() - t
+        line["e2e"] = {"value": cnt.evaluations_used / dt, "unit": "evals/s",
+                       "h2d_bytes_per_step": (2 * D * 8 + 8 * 12) / args.steps,
+                       "d2h_bytes_per_step": (B * D * 8 + B * 8 + cap * B * 24) / args.steps,
+                       "what": f"mgfwa_run_once(): create + init + {args.steps} generations + D2H, host-timed"}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cores = os.cpu_count() or 1
+            e, s = cpu_reference_generation(w, 0, cores)
+            line["cpu_baseline"] = {"value": e / s, "unit": "evals/s", "cores": cores, "kind": "reference",
+                                    "sample": f"1 x mgfwa::run() of one generation (init + 1 wave) of the same "
+                                              f"workload, compiled reference, data_parallel({cores}), {s:.1f} s"}
+        except Exception as ex:  # the reference build travels in oracle/_ref
+            line["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

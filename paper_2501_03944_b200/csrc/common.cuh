@@ -1,0 +1,121 @@
+// common.cuh — shared device helpers for the B200 MGFWA engine (sm_100a).
+//
+// Counter-based RNG (bit-exact restatement of rng.hpp:33-65), fp64 draw
+// arithmetic without FMA contraction (so that spark/guide/mapping values are
+// the correctly-rounded fp32 image of the reference's fp64 values on equal
+// inputs), warp reductions, error helpers.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mgfwa_b200 {
+
+// RngStream, rng.hpp:11-18, plus kData (builder-defined synthetic data).
+enum : uint64_t {
+  kInit = 1,
+  kExplode = 2,
+  kMapping = 3,
+  kGuide = 4,
+  kReinit = 5,
+  kWeights = 6,
+  kData = 7
+};
+
+// Objective kinds (include/mgfwa_b200.h MGFWA_OBJ_*).
+enum : int {
+  OBJ_SPHERE = 1,
+  OBJ_RASTRIGIN = 2,
+  OBJ_ACKLEY = 3,
+  OBJ_MLP_WEIGHTS = 4,
+  OBJ_LENET = 5
+};
+
+// rng.hpp:33-38
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+// rng.hpp:43-52 absorbed up to and including field k; the per-coordinate
+// hash is then splitmix64(prefix ^ d) — one mixer round per draw.
+__host__ __device__ __forceinline__ uint64_t key_prefix(uint64_t seed,
+                                                        uint64_t stream,
+                                                        uint64_t it, uint64_t b,
+                                                        uint64_t n,
+                                                        uint64_t k) {
+  uint64_t h = splitmix64(seed);
+  h = splitmix64(h ^ stream);
+  h = splitmix64(h ^ it);
+  h = splitmix64(h ^ b);
+  h = splitmix64(h ^ n);
+  return splitmix64(h ^ k);
+}
+
+// rng.hpp:55-57: (h >> 11) * 2^-53, exact (53-bit integer -> double).
+__device__ __forceinline__ double unit_u53(uint64_t h) {
+  return __dmul_rn(__ull2double_rn(h >> 11), 0x1.0p-53);
+}
+
+// rng.hpp:60-65: lo + u * (hi - lo) (no contraction, same op order).
+__device__ __forceinline__ double uniform_draw(uint64_t h, double lo,
+                                               double hi) {
+  return __dadd_rn(lo, __dmul_rn(unit_u53(h), __dsub_rn(hi, lo)));
+}
+
+// Round an in-box fp64 value to fp32 and keep it inside the fp32 image of
+// the box [lo_f, hi_f] (the largest float interval inside [lower, upper]).
+// Differs from a plain rounding only when rounding would leave the box.
+__device__ __forceinline__ float to_f32_in_box(double x, float lo_f,
+                                               float hi_f) {
+  float f = __double2float_rn(x);
+  f = f < lo_f ? lo_f : f;
+  f = f > hi_f ? hi_f : f;
+  return f;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Per-coordinate analytic terms; partial sums are fp32.
+//   sphere     : x^2                                   (nets.cpp:80-84)
+//   rastrigin  : x^2 + 20 sin^2(pi x)   == x^2 - 10 cos(2 pi x) + 10
+//   ackley     : (x^2, cos 2 pi x)  two sums
+__device__ __forceinline__ void analytic_terms(int kind, float x, float& s0,
+                                               float& s1) {
+  if (kind == OBJ_SPHERE) {
+    s0 = fmaf(x, x, s0);
+  } else if (kind == OBJ_RASTRIGIN) {
+    const float s = sinpif(x);
+    s0 += fmaf(x, x, 20.0f * s * s);
+  } else {  // ackley
+    s0 = fmaf(x, x, s0);
+    s1 += cospif(2.0f * x);
+  }
+}
+
+// Final value from the (deterministically ordered) partial sums.
+__device__ __forceinline__ float analytic_finalize(int kind, float s0,
+                                                   float s1, uint64_t D) {
+  if (kind == OBJ_ACKLEY) {
+    const float inv = 1.0f / (float)D;
+    return -20.0f * expf(-0.2f * sqrtf(s0 * inv)) - expf(s1 * inv) + 20.0f +
+           2.718281828459045f;
+  }
+  return s0;
+}
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+}  // namespace mgfwa_b200

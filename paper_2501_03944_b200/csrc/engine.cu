@@ -1,0 +1,1051 @@
+// engine.cu — host side of the B200 MGFWA engine and its C-ABI
+// (include/mgfwa_b200.h).
+//
+// The Engine owns every device buffer of one run (layout: engine_view.cuh),
+// captures one generation (engine.cpp:359-417) as a CUDA graph, and replays
+// it; loop control (iteration counter, evaluation accounting, termination)
+// lives in a device control block so the host only syncs once per chunk of
+// generations.  The reference's run() (engine.cpp:313-423) maps to
+// mgfwa_run(); its operators (engine.hpp:71-125) map to mgfwa_op_*.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mgfwa_b200.h"
+#include "common.cuh"
+#include "engine_view.cuh"
+#include "kernels.h"
+
+namespace mgfwa_b200 {
+
+// ----------------------------------------------------------------- errors
+struct Status {
+  int code;
+  std::string msg;
+};
+
+static thread_local std::string g_last_error;
+
+#define CUDA_TRY(expr)                                                        \
+  do {                                                                        \
+    cudaError_t e__ = (expr);                                                 \
+    if (e__ != cudaSuccess)                                                   \
+      return Status{MGFWA_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e__)}; \
+  } while (0)
+
+#define STATUS_TRY(expr)                      \
+  do {                                        \
+    Status s__ = (expr);                      \
+    if (s__.code != MGFWA_OK) return s__;     \
+  } while (0)
+
+static Status ok() { return Status{MGFWA_OK, ""}; }
+static Status invalid(const std::string& m) { return Status{MGFWA_EINVAL, m}; }
+
+// --------------------------------------------------------- config checks
+struct HostConfig {
+  uint64_t B = 8, mu = 5, lam = 30, M = 3;
+  double sigma = 0.2;
+  std::vector<double> boosts{1.0, 2.0, 4.0};
+  double amp_amplify = 1.2, amp_reduce = 0.9, a0 = 0.0;
+  uint64_t max_evals = 0;
+  double wall_ms = 0.0;
+  uint64_t top() const { return (uint64_t)std::ceil(sigma * (double)lam); }
+  uint64_t wave() const { return B * mu * (lam + M); }
+};
+
+static HostConfig to_host(const mgfwa_config_t* c) {
+  HostConfig h;
+  h.B = c->batches;
+  h.mu = c->fireworks;
+  h.lam = c->sparks_per_firework;
+  h.M = c->guides_per_firework;
+  h.sigma = c->guide_fraction;
+  h.boosts.assign(c->boosts, c->boosts + (c->boosts ? c->n_boosts : 0));
+  h.amp_amplify = c->amp_amplify;
+  h.amp_reduce = c->amp_reduce;
+  h.a0 = c->initial_amplitude;
+  h.max_evals = c->max_evaluations;
+  h.wall_ms = c->wall_clock_budget_ms;
+  return h;
+}
+
+// MgfwaConfig::validate, config.cpp:42-79 (same messages, same order).
+static Status validate_config(const HostConfig& c) {
+  if (c.B == 0 || c.mu == 0 || c.lam == 0)
+    return invalid("MgfwaConfig: batches, fireworks and sparks must be positive");
+  if (!(c.amp_amplify > 1.0)) return invalid("MgfwaConfig: amp_amplify must be > 1");
+  if (!(c.amp_reduce > 0.0 && c.amp_reduce < 1.0))
+    return invalid("MgfwaConfig: amp_reduce must be in (0, 1)");
+  if (c.max_evals == 0 && !(c.wall_ms > 0.0))
+    return invalid("MgfwaConfig: at least one budget must be positive");
+  if (c.M > 0) {
+    if (!(c.sigma > 0.0 && c.sigma <= 0.5))
+      return invalid("MgfwaConfig: guide_fraction must be in (0, 0.5]");
+    if (c.sigma * (double)c.lam < 1.0)
+      return invalid("MgfwaConfig: guide_fraction * sparks must be >= 1");
+    if (c.lam < 2 * c.top())
+      return invalid(
+          "MgfwaConfig: sparks must cover disjoint elite and poor sets "
+          "(lambda >= 2 * ceil(sigma * lambda))");
+    if (c.boosts.size() != c.M)
+      return invalid("MgfwaConfig: boosts must list one coefficient per guide");
+    if (c.boosts.front() != 1.0) return invalid("MgfwaConfig: first boost coefficient must be 1");
+    for (double b : c.boosts)
+      if (!(b > 0.0) || !std::isfinite(b))
+        return invalid("MgfwaConfig: boost coefficients must be positive finite");
+    if (c.M > 16) return invalid("mgfwa_b200: guides_per_firework > 16 is not supported");
+  }
+  return ok();
+}
+
+// SearchSpace::validate, config.cpp:25-35.
+static Status validate_space(const mgfwa_space_t* s) {
+  if (s == nullptr || s->dim == 0 || s->lower == nullptr || s->upper == nullptr)
+    return invalid("SearchSpace: lower/upper must be non-empty and equal length");
+  for (uint64_t d = 0; d < s->dim; ++d)
+    if (!std::isfinite(s->lower[d]) || !std::isfinite(s->upper[d]) || !(s->lower[d] < s->upper[d]))
+      return invalid("SearchSpace: requires lower[d] < upper[d] for all d");
+  return ok();
+}
+
+static uint64_t objective_dim(const mgfwa_objective_t* o) {
+  if (o->kind == MGFWA_OBJ_MLP_WEIGHTS)
+    return (uint64_t)o->hidden * o->in_dim + o->hidden + (uint64_t)o->out_dim * o->hidden +
+           o->out_dim;
+  return 0;
+}
+
+static Status validate_objective(const mgfwa_objective_t* o, uint64_t D) {
+  if (o == nullptr) return invalid("batched_apply: empty objective");
+  switch (o->kind) {
+    case MGFWA_OBJ_SPHERE:
+    case MGFWA_OBJ_RASTRIGIN:
+    case MGFWA_OBJ_ACKLEY:
+      return ok();
+    case MGFWA_OBJ_MLP_WEIGHTS:
+      if (o->samples == 0 || o->in_dim == 0 || o->hidden == 0 || o->out_dim == 0)
+        return invalid("MLP objective: all dimensions must be positive");
+      if (objective_dim(o) != D)
+        return invalid("forward: input dimension mismatch");
+      return ok();
+    case MGFWA_OBJ_LENET:
+      return invalid("mgfwa_b200: the LeNet objective is not available on the GPU engine yet");
+    default:
+      return invalid("unknown objective kind");
+  }
+}
+
+// Builder-defined synthetic dataset (kData stream; oracle/mgfwa_oracle.c
+// orc_make_dataset restates the same definition): 8-bit pixels
+// X = (H(seed,kData,0,0,s,0,i) >> 56) / 256 (exact in bf16), labels from a
+// random linear teacher, fp64 host arithmetic in the same order.
+static void make_dataset(uint32_t S, uint32_t I, uint32_t O, uint64_t seed,
+                         std::vector<__nv_bfloat16>& Xh, std::vector<int32_t>& y) {
+  std::vector<double> T((size_t)O * I), X((size_t)S * I);
+  for (uint32_t o = 0; o < O; ++o)
+    for (uint32_t i = 0; i < I; ++i) {
+      const uint64_t h = splitmix64(key_prefix(seed, kData, 1, 0, o, 0) ^ i);
+      const double u = (double)(h >> 11) * 0x1.0p-53;
+      T[(size_t)o * I + i] = -1.0 + u * (1.0 - -1.0);
+    }
+  Xh.resize((size_t)S * I);
+  y.resize(S);
+  for (uint32_t s = 0; s < S; ++s) {
+    const uint64_t pre = key_prefix(seed, kData, 0, 0, s, 0);
+    for (uint32_t i = 0; i < I; ++i) {
+      const double x = (double)(splitmix64(pre ^ i) >> 56) / 256.0;
+      X[(size_t)s * I + i] = x;
+      Xh[(size_t)s * I + i] = __float2bfloat16_rn((float)x);
+    }
+    int32_t best = 0;
+    double best_v = 0.0;
+    for (uint32_t o = 0; o < O; ++o) {
+      double acc = 0.0;
+      for (uint32_t i = 0; i < I; ++i) acc += T[(size_t)o * I + i] * (X[(size_t)s * I + i] - 0.5);
+      if (o == 0 || acc > best_v) best_v = acc, best = (int32_t)o;
+    }
+    y[s] = best;
+  }
+}
+
+static float f32_ceil_of(double x) {  // smallest float >= x
+  float f = (float)x;
+  if ((double)f < x) f = std::nextafter(f, std::numeric_limits<float>::infinity());
+  return f;
+}
+static float f32_floor_of(double x) {  // largest float <= x
+  float f = (float)x;
+  if ((double)f > x) f = std::nextafter(f, -std::numeric_limits<float>::infinity());
+  return f;
+}
+
+static uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+// ------------------------------------------------------------- workspace
+// One device arena holding every buffer of a run; builds the EngineView.
+struct Workspace {
+  EngineView v{};
+  void* arena = nullptr;
+  size_t arena_bytes = 0;
+  __nv_bfloat16* X = nullptr;  // NN dataset
+  int32_t* y = nullptr;
+  MlpPlan* plan_sparks = nullptr;
+  MlpPlan* plan_guides = nullptr;
+  MlpPlan* plan_fresh = nullptr;
+  int nsm = 148;
+  int device = 0;
+
+  ~Workspace() {
+    mlp_plan_destroy(plan_sparks);
+    mlp_plan_destroy(plan_guides);
+    mlp_plan_destroy(plan_fresh);
+    if (arena) cudaFree(arena);
+  }
+
+  Status build(const HostConfig& c, const mgfwa_space_t* space, const mgfwa_objective_t* obj,
+               uint64_t seed, int dev, uint64_t trace_cap) {
+    device = dev;
+    CUDA_TRY(cudaSetDevice(dev));
+    CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const uint64_t D = space->dim;
+    v.B = c.B;
+    v.mu = c.mu;
+    v.lam = c.lam;
+    v.M = c.M;
+    v.D = D;
+    v.Dp = round_up(D, 64);
+    v.top = c.M > 0 ? c.top() : 0;
+    v.F = c.B * c.mu;
+    v.nch = (uint32_t)((D + kChunk - 1) / kChunk);
+    v.obj_kind = obj->kind;
+    v.nn = obj->kind == MGFWA_OBJ_MLP_WEIGHTS;
+    v.samples = v.nn ? obj->samples : 0;
+    v.nparts = v.nn ? mlp_num_parts(obj->samples) : v.nch;
+    v.seed = seed;
+    v.amp_amplify = c.amp_amplify;
+    v.amp_reduce = c.amp_reduce;
+    double max_range = 0.0;
+    for (uint64_t d = 0; d < D; ++d) max_range = std::max(max_range, space->upper[d] - space->lower[d]);
+    v.max_range = max_range;
+    v.amp_floor = 1e-12 * max_range;
+    v.a0 = c.a0 > 0.0 ? c.a0 : 0.5 * max_range;
+    v.max_evals = c.max_evals;
+    v.wall_budget_ms = c.wall_ms;
+    v.wave = c.wave();
+    v.trace_cap = trace_cap;
+
+    // ---- arena layout
+    struct Slot {
+      void** dst;
+      size_t bytes;
+    };
+    std::vector<Slot> slots;
+    auto add = [&](auto** p, size_t bytes) { slots.push_back({reinterpret_cast<void**>(p), bytes}); };
+    const uint64_t F = v.F, Dp = v.Dp, P = F * v.lam, G = F * v.M, np2 = (uint64_t)v.nparts * 2;
+    double *lower, *upper, *boosts;
+    float *lower_f, *upper_f;
+    add(&lower, D * 8);
+    add(&upper, D * 8);
+    add(&lower_f, D * 4);
+    add(&upper_f, D * 4);
+    add(&boosts, std::max<uint64_t>(v.M, 1) * 8);
+    add(&v.pos, F * Dp * 4);
+    add(&v.fit, F * 8);
+    add(&v.amp, F * 8);
+    add(&v.li, F * 8);
+    add(&v.improved, F * 4);
+    add(&v.winner, F * 4);
+    add(&v.loser, F * 4);
+    add(&v.pop_lo, c.B * Dp * 4);
+    add(&v.pop_hi, c.B * Dp * 4);
+    add(&v.sparks, P * Dp * 4);
+    if (v.nn) add(&v.sparks_h, P * Dp * 2);
+    add(&v.sfit, P * 4);
+    add(&v.spart, P * np2 * 4);
+    add(&v.rank_idx, std::max<uint64_t>(F * 2 * v.top, 1) * 4);
+    add(&v.guides, std::max<uint64_t>(G, 1) * Dp * 4);
+    if (v.nn) add(&v.guides_h, std::max<uint64_t>(G, 1) * Dp * 2);
+    add(&v.gfit, std::max<uint64_t>(G, 1) * 4);
+    add(&v.gpart, std::max<uint64_t>(G, 1) * np2 * 4);
+    if (v.nn) add(&v.fresh_h, F * Dp * 2);
+    add(&v.fpart, F * np2 * 4);
+    add(&v.best_fit, c.B * 8);
+    add(&v.best_pos, c.B * Dp * 4);
+    add(&v.best_idx, c.B * 4);
+    add(&v.rec_flag, c.B * 4);
+    add(&v.tr_evals, trace_cap * c.B * 8);
+    add(&v.tr_best, trace_cap * c.B * 8);
+    add(&v.tr_ns, trace_cap * c.B * 8);
+    add(&v.ctl, sizeof(Ctl));
+    if (v.nn) {
+      add(&X, (size_t)obj->samples * obj->in_dim * 2);
+      add(&y, (size_t)obj->samples * 4);
+    }
+    size_t total = 0;
+    for (auto& s : slots) total += round_up(s.bytes, 256);
+    cudaError_t e = cudaMalloc(&arena, total);
+    if (e != cudaSuccess) {
+      arena = nullptr;
+      return Status{MGFWA_ENOMEM, std::string("cudaMalloc(") + std::to_string(total) +
+                                      " bytes): " + cudaGetErrorString(e)};
+    }
+    arena_bytes = total;
+    CUDA_TRY(cudaMemset(arena, 0, total));
+    size_t off = 0;
+    for (auto& s : slots) {
+      *s.dst = static_cast<char*>(arena) + off;
+      off += round_up(s.bytes, 256);
+    }
+    v.lower = lower;
+    v.upper = upper;
+    v.lower_f = lower_f;
+    v.upper_f = upper_f;
+    v.boosts = boosts;
+
+    std::vector<float> lf(D), uf(D);
+    for (uint64_t d = 0; d < D; ++d) {
+      lf[d] = f32_ceil_of(space->lower[d]);
+      uf[d] = f32_floor_of(space->upper[d]);
+    }
+    CUDA_TRY(cudaMemcpy(lower, space->lower, D * 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(upper, space->upper, D * 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(lower_f, lf.data(), D * 4, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(upper_f, uf.data(), D * 4, cudaMemcpyHostToDevice));
+    if (v.M > 0) CUDA_TRY(cudaMemcpy(boosts, c.boosts.data(), v.M * 8, cudaMemcpyHostToDevice));
+
+    if (v.nn) {
+      std::vector<__nv_bfloat16> Xh;
+      std::vector<int32_t> yh;
+      make_dataset(obj->samples, obj->in_dim, obj->out_dim, obj->data_seed, Xh, yh);
+      CUDA_TRY(cudaMemcpy(X, Xh.data(), Xh.size() * 2, cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(y, yh.data(), yh.size() * 4, cudaMemcpyHostToDevice));
+      char err[256] = {0};
+      plan_sparks = mlp_plan_create(X, y, obj->samples, obj->in_dim, obj->hidden, obj->out_dim,
+                                    v.sparks_h, P, Dp, nsm, err, sizeof err);
+      if (!plan_sparks) return invalid(err);
+      if (G > 0) {
+        plan_guides = mlp_plan_create(X, y, obj->samples, obj->in_dim, obj->hidden, obj->out_dim,
+                                      v.guides_h, G, Dp, nsm, err, sizeof err);
+        if (!plan_guides) return invalid(err);
+      }
+      plan_fresh = mlp_plan_create(X, y, obj->samples, obj->in_dim, obj->hidden, obj->out_dim,
+                                   v.fresh_h, F, Dp, nsm, err, sizeof err);
+      if (!plan_fresh) return invalid(err);
+    }
+    return ok();
+  }
+};
+
+// NN fitness hooks used inside the captured generation.
+static void hook_sparks(void* p, cudaStream_t s) {
+  auto* w = static_cast<Workspace*>(p);
+  mlp_fitness_launch(w->plan_sparks, w->v.spart, &w->v.ctl->active, s);
+}
+static void hook_guides(void* p, cudaStream_t s) {
+  auto* w = static_cast<Workspace*>(p);
+  mlp_fitness_launch(w->plan_guides, w->v.gpart, &w->v.ctl->active, s);
+}
+static void hook_fresh(void* p, cudaStream_t s) {
+  auto* w = static_cast<Workspace*>(p);
+  mlp_fitness_launch(w->plan_fresh, w->v.fpart, &w->v.ctl->n_losers, s);
+}
+static void hook_fresh_all(void* p, cudaStream_t s) {
+  auto* w = static_cast<Workspace*>(p);
+  mlp_fitness_launch(w->plan_fresh, w->v.fpart, nullptr, s);
+}
+
+// ----------------------------------------------------------------- engine
+class Engine {
+ public:
+  HostConfig cfg;
+  std::unique_ptr<Workspace> ws;
+  GenerationHooks hooks{};
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaGraphExec_t gen_exec = nullptr;
+  uint64_t kernels_per_gen = 0;
+  Ctl* host_ctl = nullptr;  // pinned
+  bool initialized = false;
+  std::string last_error;
+  // host copy of the trace, [B][wave]
+  std::vector<std::vector<uint64_t>> tr_evals;
+  std::vector<std::vector<double>> tr_best, tr_wall;
+  uint64_t host_trace_n = 0;
+  std::vector<uint64_t> ring_e;
+  std::vector<double> ring_b;
+  std::vector<uint64_t> ring_t;
+
+  ~Engine() {
+    if (gen_exec) cudaGraphExecDestroy(gen_exec);
+    if (own_stream) cudaStreamDestroy(own_stream);
+    if (host_ctl) cudaFreeHost(host_ctl);
+  }
+
+  Status create(const mgfwa_config_t* c, const mgfwa_space_t* space, const mgfwa_objective_t* obj,
+                uint64_t seed, int device) {
+    if (c == nullptr) return invalid("MgfwaConfig: null config");
+    cfg = to_host(c);
+    STATUS_TRY(validate_config(cfg));
+    STATUS_TRY(validate_space(space));
+    STATUS_TRY(validate_objective(obj, space->dim));
+    // engine.cpp:319-323
+    if (cfg.max_evals > 0 && cfg.max_evals < cfg.B * cfg.mu)
+      return invalid("budget too small: needs at least B * mu evaluations");
+    ws = std::make_unique<Workspace>();
+    STATUS_TRY(ws->build(cfg, space, obj, seed, device, 1024));
+    CUDA_TRY(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
+    stream = own_stream;
+    CUDA_TRY(cudaMallocHost(&host_ctl, sizeof(Ctl)));
+    memset(host_ctl, 0, sizeof(Ctl));
+    hooks = GenerationHooks{ws.get(), hook_sparks, hook_guides, hook_fresh, hook_fresh_all};
+    ring_e.resize(ws->v.trace_cap * cfg.B);
+    ring_b.resize(ws->v.trace_cap * cfg.B);
+    ring_t.resize(ws->v.trace_cap * cfg.B);
+    return ok();
+  }
+
+  Status capture() {
+    if (gen_exec) return ok();
+    cudaGraph_t g = nullptr;
+    CUDA_TRY(cudaStreamBeginCapture(own_stream, cudaStreamCaptureModeThreadLocal));
+    launch_generation_kernels(ws->v, ws->nsm, own_stream, &hooks);
+    cudaError_t e = cudaStreamEndCapture(own_stream, &g);
+    if (e != cudaSuccess) return Status{MGFWA_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e)};
+    size_t n = 0;
+    cudaGraphGetNodes(g, nullptr, &n);
+    kernels_per_gen = n;
+    e = cudaGraphInstantiate(&gen_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return Status{MGFWA_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e)};
+    return ok();
+  }
+
+  Status initialize() {
+    CUDA_TRY(cudaSetDevice(ws->device));
+    CUDA_TRY(cudaMemsetAsync(ws->v.ctl, 0, sizeof(Ctl), stream));
+    launch_initialize_kernels(ws->v, ws->nsm, stream, &hooks);
+    CUDA_TRY(cudaGetLastError());
+    tr_evals.assign(cfg.B, {});
+    tr_best.assign(cfg.B, {});
+    tr_wall.assign(cfg.B, {});
+    host_trace_n = 0;
+    STATUS_TRY(sync());
+    initialized = true;
+    return capture();
+  }
+
+  // D2H of the control block and of the new trace points.
+  Status sync() {
+    CUDA_TRY(cudaMemcpyAsync(host_ctl, ws->v.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    const uint64_t n = host_ctl->trace_n;
+    if (n > host_trace_n) {
+      const uint64_t cap = ws->v.trace_cap, B = cfg.B;
+      CUDA_TRY(cudaMemcpyAsync(ring_e.data(), ws->v.tr_evals, cap * B * 8, cudaMemcpyDeviceToHost, stream));
+      CUDA_TRY(cudaMemcpyAsync(ring_b.data(), ws->v.tr_best, cap * B * 8, cudaMemcpyDeviceToHost, stream));
+      CUDA_TRY(cudaMemcpyAsync(ring_t.data(), ws->v.tr_ns, cap * B * 8, cudaMemcpyDeviceToHost, stream));
+      CUDA_TRY(cudaStreamSynchronize(stream));
+      const uint64_t first = n > cap && host_trace_n < n - cap ? n - cap : host_trace_n;
+      for (uint64_t w = first; w < n; ++w) {
+        const uint64_t slot = w % cap;
+        for (uint64_t b = 0; b < B; ++b) {
+          tr_evals[b].push_back(ring_e[slot * B + b]);
+          tr_best[b].push_back(ring_b[slot * B + b]);
+          tr_wall[b].push_back((double)ring_t[slot * B + b] * 1e-6);
+        }
+      }
+      host_trace_n = n;
+    }
+    return ok();
+  }
+
+  Status enqueue(uint64_t n) {
+    if (!initialized) return Status{MGFWA_ESTATE, "mgfwa: initialize() must precede the loop"};
+    for (uint64_t i = 0; i < n; ++i) CUDA_TRY(cudaGraphLaunch(gen_exec, stream));
+    return ok();
+  }
+
+  uint64_t chunk_limit() const {
+    const uint64_t cap = std::min<uint64_t>(64, ws->v.trace_cap - 2);
+    if (cfg.max_evals > 0) {
+      const uint64_t used = host_ctl->used;
+      const uint64_t left = cfg.max_evals > used ? cfg.max_evals - used : 0;
+      const uint64_t ub = (left + cfg.wave() - 1) / cfg.wave();
+      return std::max<uint64_t>(1, std::min(cap, ub));
+    }
+    return 4;
+  }
+
+  Status step(uint64_t max_gens, uint64_t* ran) {
+    if (!initialized) return Status{MGFWA_ESTATE, "mgfwa: initialize() must precede the loop"};
+    CUDA_TRY(cudaSetDevice(ws->device));
+    uint64_t done = 0;
+    while (done < max_gens && host_ctl->active) {
+      const uint64_t before = host_ctl->gens_run;
+      const uint64_t n = std::min(max_gens - done, chunk_limit());
+      STATUS_TRY(enqueue(n));
+      STATUS_TRY(sync());
+      done += host_ctl->gens_run - before;
+      if (host_ctl->gens_run == before) break;
+    }
+    if (ran) *ran = done;
+    return ok();
+  }
+
+  Status run(mgfwa_counters_t* out) {
+    STATUS_TRY(initialize());
+    uint64_t ran = 0;
+    STATUS_TRY(step(std::numeric_limits<uint64_t>::max(), &ran));
+    if (out) counters(out);
+    return ok();
+  }
+
+  void counters(mgfwa_counters_t* out) const {
+    out->evaluations_used = host_ctl->used;
+    out->iterations = host_ctl->gens_run;
+    out->losers_reinitialized = host_ctl->losers_total;
+    out->nan_evaluations = host_ctl->nan_count;
+    out->trace_waves = host_trace_n;
+  }
+
+  Status best(double* fit, double* pos) {
+    const uint64_t B = cfg.B, D = ws->v.D, Dp = ws->v.Dp;
+    std::vector<double> bf(B);
+    std::vector<float> bp(B * Dp);
+    CUDA_TRY(cudaMemcpyAsync(bf.data(), ws->v.best_fit, B * 8, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaMemcpyAsync(bp.data(), ws->v.best_pos, B * Dp * 4, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    for (uint64_t b = 0; b < B; ++b) {
+      if (fit) fit[b] = bf[b];
+      if (pos)
+        for (uint64_t d = 0; d < D; ++d) pos[b * D + d] = bp[b * Dp + d];
+    }
+    return ok();
+  }
+
+  Status state(double* pos, double* fit, double* amp, double* li) {
+    const uint64_t F = ws->v.F, D = ws->v.D, Dp = ws->v.Dp;
+    std::vector<float> p(F * Dp);
+    std::vector<double> f(F), a(F), l(F);
+    CUDA_TRY(cudaMemcpyAsync(p.data(), ws->v.pos, F * Dp * 4, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaMemcpyAsync(f.data(), ws->v.fit, F * 8, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaMemcpyAsync(a.data(), ws->v.amp, F * 8, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaMemcpyAsync(l.data(), ws->v.li, F * 8, cudaMemcpyDeviceToHost, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    for (uint64_t i = 0; i < F; ++i) {
+      if (pos)
+        for (uint64_t d = 0; d < D; ++d) pos[i * D + d] = p[i * Dp + d];
+      if (fit) fit[i] = f[i];
+      if (amp) amp[i] = a[i];
+      if (li) li[i] = l[i];
+    }
+    return ok();
+  }
+};
+
+// ------------------------------------------------------- operator helpers
+// Host fp64 [rows][D] <-> device fp32 [rows][Dp].
+static Status upload_rows(float* dst, const double* src, uint64_t rows, uint64_t D, uint64_t Dp,
+                          cudaStream_t s) {
+  std::vector<float> h(rows * Dp, 0.0f);
+  for (uint64_t r = 0; r < rows; ++r)
+    for (uint64_t d = 0; d < D; ++d) h[r * Dp + d] = (float)src[r * D + d];
+  CUDA_TRY(cudaMemcpyAsync(dst, h.data(), h.size() * 4, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return ok();
+}
+static Status download_rows(double* dst, const float* src, uint64_t rows, uint64_t D, uint64_t Dp,
+                            cudaStream_t s) {
+  std::vector<float> h(rows * Dp);
+  CUDA_TRY(cudaMemcpyAsync(h.data(), src, h.size() * 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  for (uint64_t r = 0; r < rows; ++r)
+    for (uint64_t d = 0; d < D; ++d) dst[r * D + d] = (double)h[r * Dp + d];
+  return ok();
+}
+template <typename T>
+static Status upload(T* dst, const T* src, uint64_t n, cudaStream_t s) {
+  CUDA_TRY(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return ok();
+}
+template <typename T>
+static Status download(T* dst, const T* src, uint64_t n, cudaStream_t s) {
+  CUDA_TRY(cudaMemcpyAsync(dst, src, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return ok();
+}
+
+// A workspace for operator seams: an analytic objective unless given.
+static Status op_workspace(std::unique_ptr<Workspace>& ws, const HostConfig& c,
+                           const mgfwa_space_t* space, const mgfwa_objective_t* obj) {
+  mgfwa_objective_t sphere{MGFWA_OBJ_SPHERE, 0, 0, 0, 0, 0};
+  ws = std::make_unique<Workspace>();
+  STATUS_TRY(ws->build(c, space, obj ? obj : &sphere, 0, 0, 4));
+  return ok();
+}
+
+static Status set_ctl(Workspace& w, uint64_t iteration, uint64_t used, int active) {
+  Ctl c{};
+  c.iteration = iteration;
+  c.used = used;
+  c.active = active;
+  CUDA_TRY(cudaMemcpy(w.v.ctl, &c, sizeof(Ctl), cudaMemcpyHostToDevice));
+  return ok();
+}
+
+static mgfwa_space_t wide_space(uint64_t D, std::vector<double>& lo, std::vector<double>& hi) {
+  lo.assign(D, -3.0e38);
+  hi.assign(D, 3.0e38);
+  return mgfwa_space_t{lo.data(), hi.data(), D};
+}
+
+static HostConfig relaxed(const mgfwa_config_t* c) {
+  HostConfig h = to_host(c);
+  if (h.max_evals == 0 && !(h.wall_ms > 0.0)) h.max_evals = 1ull << 62;
+  return h;
+}
+
+}  // namespace mgfwa_b200
+
+// ===================================================================== C-ABI
+using namespace mgfwa_b200;
+
+struct mgfwa_ctx {
+  Engine engine;
+};
+
+static int fail(mgfwa_ctx* ctx, const Status& s) {
+  if (s.code == MGFWA_OK) return MGFWA_OK;
+  if (ctx) ctx->engine.last_error = s.msg;
+  g_last_error = s.msg;
+  return s.code;
+}
+
+extern "C" {
+
+const char* mgfwa_version(void) { return "mgfwa_b200 0.1 (sm_100a)"; }
+
+const char* mgfwa_last_error(mgfwa_ctx_t ctx) {
+  return ctx ? ctx->engine.last_error.c_str() : g_last_error.c_str();
+}
+
+int mgfwa_create(const mgfwa_config_t* config, const mgfwa_space_t* space,
+                 const mgfwa_objective_t* objective, uint64_t seed, int device, mgfwa_ctx_t* out) {
+  if (!out) return fail(nullptr, invalid("mgfwa_create: null output"));
+  *out = nullptr;
+  auto* ctx = new (std::nothrow) mgfwa_ctx();
+  if (!ctx) return fail(nullptr, Status{MGFWA_ENOMEM, "host allocation"});
+  Status s = ctx->engine.create(config, space, objective, seed, device);
+  if (s.code != MGFWA_OK) {
+    fail(nullptr, s);
+    delete ctx;
+    return s.code;
+  }
+  *out = ctx;
+  return MGFWA_OK;
+}
+
+int mgfwa_destroy(mgfwa_ctx_t ctx) {
+  delete ctx;
+  return MGFWA_OK;
+}
+
+int mgfwa_set_stream(mgfwa_ctx_t ctx, void* s) {
+  ctx->engine.stream = s ? static_cast<cudaStream_t>(s) : ctx->engine.own_stream;
+  return MGFWA_OK;
+}
+
+int mgfwa_kernels_per_generation(mgfwa_ctx_t ctx, uint64_t* n) {
+  Status s = ctx->engine.capture();
+  if (s.code) return fail(ctx, s);
+  *n = ctx->engine.kernels_per_gen;
+  return MGFWA_OK;
+}
+
+int mgfwa_initialize(mgfwa_ctx_t ctx) { return fail(ctx, ctx->engine.initialize()); }
+
+int mgfwa_step(mgfwa_ctx_t ctx, uint64_t max_generations, uint64_t* generations_run) {
+  return fail(ctx, ctx->engine.step(max_generations, generations_run));
+}
+
+int mgfwa_enqueue_generations(mgfwa_ctx_t ctx, uint64_t n) { return fail(ctx, ctx->engine.enqueue(n)); }
+
+int mgfwa_sync(mgfwa_ctx_t ctx) { return fail(ctx, ctx->engine.sync()); }
+
+int mgfwa_run(mgfwa_ctx_t ctx, mgfwa_counters_t* counters) {
+  return fail(ctx, ctx->engine.run(counters));
+}
+
+int mgfwa_get_counters(mgfwa_ctx_t ctx, mgfwa_counters_t* out) {
+  ctx->engine.counters(out);
+  return MGFWA_OK;
+}
+
+int mgfwa_get_best(mgfwa_ctx_t ctx, double* best_fitness, double* best_position) {
+  return fail(ctx, ctx->engine.best(best_fitness, best_position));
+}
+
+int mgfwa_get_trace(mgfwa_ctx_t ctx, uint64_t* evaluations, double* best, double* wall_ms,
+                    uint64_t cap, uint64_t* waves) {
+  Engine& e = ctx->engine;
+  const uint64_t n = e.host_trace_n;
+  if (waves) *waves = n;
+  for (uint64_t b = 0; b < e.cfg.B; ++b)
+    for (uint64_t w = 0; w < n && w < cap; ++w) {
+      if (evaluations) evaluations[b * cap + w] = e.tr_evals[b][w];
+      if (best) best[b * cap + w] = e.tr_best[b][w];
+      if (wall_ms) wall_ms[b * cap + w] = e.tr_wall[b][w];
+    }
+  return MGFWA_OK;
+}
+
+int mgfwa_get_state(mgfwa_ctx_t ctx, double* positions, double* fitness, double* amplitudes,
+                    double* last_improvement) {
+  return fail(ctx, ctx->engine.state(positions, fitness, amplitudes, last_improvement));
+}
+
+int mgfwa_run_once(const mgfwa_config_t* config, const mgfwa_space_t* space,
+                   const mgfwa_objective_t* objective, uint64_t seed, int device,
+                   double* best_fitness, double* best_position, uint64_t* trace_evaluations,
+                   double* trace_best, double* trace_wall_ms, uint64_t trace_cap,
+                   mgfwa_counters_t* counters) {
+  mgfwa_ctx_t ctx = nullptr;
+  int rc = mgfwa_create(config, space, objective, seed, device, &ctx);
+  if (rc) return rc;
+  rc = mgfwa_run(ctx, counters);
+  if (!rc) rc = mgfwa_get_best(ctx, best_fitness, best_position);
+  if (!rc && (trace_evaluations || trace_best || trace_wall_ms))
+    rc = mgfwa_get_trace(ctx, trace_evaluations, trace_best, trace_wall_ms, trace_cap, nullptr);
+  if (rc) g_last_error = ctx->engine.last_error;
+  mgfwa_destroy(ctx);
+  return rc;
+}
+
+// ------------------------------------------------------------------ ops
+int mgfwa_op_initialize(const mgfwa_config_t* config, const mgfwa_space_t* space,
+                        const mgfwa_objective_t* objective, uint64_t seed, double* positions,
+                        double* fitness, double* amplitudes) {
+  mgfwa_ctx_t ctx = nullptr;
+  mgfwa_config_t c = *config;
+  if (c.max_evaluations == 0 && !(c.wall_clock_budget_ms > 0)) c.max_evaluations = 1ull << 62;
+  int rc = mgfwa_create(&c, space, objective, seed, 0, &ctx);
+  if (rc) return rc;
+  rc = mgfwa_initialize(ctx);
+  if (!rc) rc = mgfwa_get_state(ctx, positions, fitness, amplitudes, nullptr);
+  if (rc) g_last_error = ctx->engine.last_error;
+  mgfwa_destroy(ctx);
+  return rc;
+}
+
+int mgfwa_op_explode_map(const mgfwa_config_t* config, const mgfwa_space_t* space,
+                         const double* positions, const double* amplitudes, uint64_t iteration,
+                         uint64_t seed, double* sparks) {
+  auto body = [&]() -> Status {
+    HostConfig c = relaxed(config);
+    STATUS_TRY(validate_space(space));
+    std::unique_ptr<Workspace> w;
+    STATUS_TRY(op_workspace(w, c, space, nullptr));
+    EngineView v = w->v;
+    v.seed = seed;
+    cudaStream_t s = 0;
+    STATUS_TRY(upload_rows(v.pos, positions, v.F, v.D, v.Dp, s));
+    STATUS_TRY(upload(v.amp, amplitudes, v.F, s));
+    STATUS_TRY(set_ctl(*w, iteration, 0, 1));
+    launch_pop_range(v, w->nsm, s);
+    launch_explode_map(v, w->nsm, s);
+    CUDA_TRY(cudaGetLastError());
+    return download_rows(sparks, v.sparks, v.F * v.lam, v.D, v.Dp, s);
+  };
+  return fail(nullptr, body());
+}
+
+int mgfwa_op_random_mapping(const mgfwa_space_t* space, const double* cand, uint64_t B,
+                            uint64_t rows, uint64_t per, const double* positions, uint64_t mu,
+                            uint64_t iteration, uint64_t seed, uint64_t stream, double* out) {
+  auto body = [&]() -> Status {
+    STATUS_TRY(validate_space(space));
+    HostConfig c;
+    c.B = B;
+    c.mu = mu;
+    c.lam = 2 * rows;  // sparks buffer holds the candidates and the output
+    c.M = 0;
+    c.max_evals = 1;
+    std::unique_ptr<Workspace> w;
+    STATUS_TRY(op_workspace(w, c, space, nullptr));
+    EngineView v = w->v;
+    v.seed = seed;
+    // the candidate cube is B x rows; stage it in the (F*lam >= B*rows) sparks buffer
+    cudaStream_t s = 0;
+    STATUS_TRY(upload_rows(v.pos, positions, v.F, v.D, v.Dp, s));
+    STATUS_TRY(upload_rows(v.sparks, cand, B * rows, v.D, v.Dp, s));
+    STATUS_TRY(set_ctl(*w, iteration, 0, 1));
+    launch_pop_range(v, w->nsm, s);
+    float* outd = v.sparks + B * rows * v.Dp;  // second half of the buffer (F*lam >= 2*B*rows)
+    if (v.F * v.lam < 2 * B * rows) return invalid("random_mapping: internal sizing");
+    launch_map_rows(v, v.sparks, outd, rows, per, stream, iteration, s);
+    CUDA_TRY(cudaGetLastError());
+    return download_rows(out, outd, B * rows, v.D, v.Dp, s);
+  };
+  return fail(nullptr, body());
+}
+
+int mgfwa_op_guides(const mgfwa_config_t* config, const mgfwa_space_t* space,
+                    const double* positions, const double* sparks, const double* spark_fitness,
+                    uint64_t iteration, uint64_t seed, double* guides) {
+  auto body = [&]() -> Status {
+    HostConfig c = relaxed(config);
+    STATUS_TRY(validate_config(c));
+    STATUS_TRY(validate_space(space));
+    if (c.M == 0) return invalid("guides: M must be positive");
+    std::unique_ptr<Workspace> w;
+    STATUS_TRY(op_workspace(w, c, space, nullptr));
+    EngineView v = w->v;
+    v.seed = seed;
+    v.injected_fitness = 1;
+    cudaStream_t s = 0;
+    STATUS_TRY(upload_rows(v.pos, positions, v.F, v.D, v.Dp, s));
+    STATUS_TRY(upload_rows(v.sparks, sparks, v.F * v.lam, v.D, v.Dp, s));
+    std::vector<float> sf(v.F * v.lam);
+    for (uint64_t i = 0; i < sf.size(); ++i) sf[i] = (float)spark_fitness[i];
+    STATUS_TRY(upload(v.sfit, sf.data(), sf.size(), s));
+    STATUS_TRY(set_ctl(*w, iteration, 0, 1));
+    launch_pop_range(v, w->nsm, s);
+    launch_rank(v, s);
+    launch_guides(v, w->nsm, s);
+    CUDA_TRY(cudaGetLastError());
+    return download_rows(guides, v.guides, v.F * v.M, v.D, v.Dp, s);
+  };
+  return fail(nullptr, body());
+}
+
+int mgfwa_op_guiding_vector(const mgfwa_config_t* config, uint64_t dim, const double* sparks,
+                            const double* spark_fitness, double* delta) {
+  // guiding_vector through the production kernels: pos = 0, one guide with
+  // beta = 1 and an unbounded box, so guide = 0 + 1 * delta exactly.
+  auto body = [&]() -> Status {
+    HostConfig c = relaxed(config);
+    if (c.lam < 2 * c.top()) return invalid("guiding_vector: elite and poor sets overlap");
+    c.M = 1;
+    c.boosts = {1.0};
+    std::vector<double> lo, hi;
+    mgfwa_space_t sp = wide_space(dim, lo, hi);
+    std::unique_ptr<Workspace> w;
+    STATUS_TRY(op_workspace(w, c, &sp, nullptr));
+    EngineView v = w->v;
+    v.injected_fitness = 1;
+    cudaStream_t s = 0;
+    STATUS_TRY(upload_rows(v.sparks, sparks, v.F * v.lam, v.D, v.Dp, s));
+    std::vector<float> sf(v.F * v.lam);
+    for (uint64_t i = 0; i < sf.size(); ++i) sf[i] = (float)spark_fitness[i];
+    STATUS_TRY(upload(v.sfit, sf.data(), sf.size(), s));
+    STATUS_TRY(set_ctl(*w, 1, 0, 1));
+    launch_rank(v, s);
+    launch_guides(v, w->nsm, s);
+    CUDA_TRY(cudaGetLastError());
+    return download_rows(delta, v.guides, v.F, v.D, v.Dp, s);
+  };
+  return fail(nullptr, body());
+}
+
+int mgfwa_op_select_best(const mgfwa_config_t* config, const mgfwa_space_t* space,
+                         const double* positions, const double* fitness, const double* amplitudes,
+                         const double* sparks, const double* spark_fitness, const double* guides,
+                         const double* guide_fitness, double* new_positions, double* new_fitness,
+                         double* new_last_improvement, double* improved, double* new_amplitudes) {
+  auto body = [&]() -> Status {
+    HostConfig c = relaxed(config);
+    STATUS_TRY(validate_space(space));
+    if (guides == nullptr) c.M = 0, c.boosts.clear();
+    std::unique_ptr<Workspace> w;
+    STATUS_TRY(op_workspace(w, c, space, nullptr));
+    EngineView v = w->v;
+    v.injected_fitness = 1;
+    cudaStream_t s = 0;
+    STATUS_TRY(upload_rows(v.pos, positions, v.F, v.D, v.Dp, s));
+    STATUS_TRY(upload(v.fit, fitness, v.F, s));
+    STATUS_TRY(upload(v.amp, amplitudes, v.F, s));
+    STATUS_TRY(upload_rows(v.sparks, sparks, v.F * v.lam, v.D, v.Dp, s));
+    std::vector<float> sf(v.F * v.lam);
+    for (uint64_t i = 0; i < sf.size(); ++i) sf[i] = (float)spark_fitness[i];
+    STATUS_TRY(upload(v.sfit, sf.data(), sf.size(), s));
+    if (v.M > 0) {
+      STATUS_TRY(upload_rows(v.guides, guides, v.F * v.M, v.D, v.Dp, s));
+      std::vector<float> gf(v.F * v.M);
+      for (uint64_t i = 0; i < gf.size(); ++i) gf[i] = (float)guide_fitness[i];
+      STATUS_TRY(upload(v.gfit, gf.data(), gf.size(), s));
+    }
+    STATUS_TRY(set_ctl(*w, 1, 0, 1));
+    launch_select(v, w->nsm, s);
+    CUDA_TRY(cudaGetLastError());
+    STATUS_TRY(download_rows(new_positions, v.pos, v.F, v.D, v.Dp, s));
+    STATUS_TRY(download(new_fitness, v.fit, v.F, s));
+    STATUS_TRY(download(new_last_improvement, v.li, v.F, s));
+    std::vector<int> imp(v.F);
+    STATUS_TRY(download(imp.data(), v.improved, v.F, s));
+    for (uint64_t i = 0; i < v.F; ++i) improved[i] = imp[i] ? 1.0 : 0.0;
+    if (new_amplitudes) STATUS_TRY(download(new_amplitudes, v.amp, v.F, s));
+    return ok();
+  };
+  return fail(nullptr, body());
+}
+
+int mgfwa_op_loser_out(const mgfwa_config_t* config, const mgfwa_space_t* space,
+                       const mgfwa_objective_t* objective, double* positions, double* fitness,
+                       double* amplitudes, double* last_improvement, uint64_t* used,
+                       uint64_t iteration, uint64_t seed, double iterations_remaining,
+                       uint64_t* reinit) {
+  auto body = [&]() -> Status {
+    HostConfig c = relaxed(config);
+    STATUS_TRY(validate_space(space));
+    STATUS_TRY(validate_objective(objective, space->dim));
+    std::unique_ptr<Workspace> w;
+    STATUS_TRY(op_workspace(w, c, space, objective));
+    EngineView v = w->v;
+    v.seed = seed;
+    v.has_iters_override = 1;
+    v.iters_override = iterations_remaining;
+    v.max_evals = 0;
+    v.wall_budget_ms = 0;
+    cudaStream_t s = 0;
+    STATUS_TRY(upload_rows(v.pos, positions, v.F, v.D, v.Dp, s));
+    STATUS_TRY(upload(v.fit, fitness, v.F, s));
+    STATUS_TRY(upload(v.amp, amplitudes, v.F, s));
+    STATUS_TRY(upload(v.li, last_improvement, v.F, s));
+    STATUS_TRY(set_ctl(*w, iteration, *used, 1));
+    launch_loser(v, w->nsm, s);
+    if (v.nn) {
+      w->v = v;
+      hook_fresh(w.get(), s);
+    }
+    launch_loser_commit(v, w->nsm, s);
+    CUDA_TRY(cudaGetLastError());
+    STATUS_TRY(download_rows(positions, v.pos, v.F, v.D, v.Dp, s));
+    STATUS_TRY(download(fitness, v.fit, v.F, s));
+    STATUS_TRY(download(amplitudes, v.amp, v.F, s));
+    STATUS_TRY(download(last_improvement, v.li, v.F, s));
+    Ctl ctl;
+    STATUS_TRY(download(&ctl, v.ctl, 1, s));
+    *reinit = (uint64_t)ctl.n_losers;
+    *used = ctl.used;
+    return ok();
+  };
+  return fail(nullptr, body());
+}
+
+int mgfwa_op_batched_apply(const mgfwa_objective_t* objective, const double* rows, uint64_t n,
+                           uint64_t dim, double* fitness, uint64_t* nan_count) {
+  auto body = [&]() -> Status {
+    STATUS_TRY(validate_objective(objective, dim));
+    HostConfig c;
+    c.B = 1;
+    c.mu = n;
+    c.lam = 1;
+    c.M = 0;
+    c.max_evals = 1ull << 62;
+    std::vector<double> lo, hi;
+    mgfwa_space_t sp = wide_space(dim, lo, hi);
+    std::unique_ptr<Workspace> w;
+    STATUS_TRY(op_workspace(w, c, &sp, objective));
+    EngineView v = w->v;
+    cudaStream_t s = 0;
+    STATUS_TRY(upload_rows(v.pos, rows, n, dim, v.Dp, s));
+    if (v.nn) {
+      launch_to_bf16(v.pos, v.fresh_h, n * v.Dp, s);
+      hook_fresh_all(w.get(), s);
+    } else {
+      launch_analytic_partials(v.pos, n, dim, v.Dp, v.nch, v.obj_kind, v.fpart, w->nsm, s);
+    }
+    unsigned long long* dnan = reinterpret_cast<unsigned long long*>(&v.ctl->nan_count);
+    launch_finalize_rows(v, v.fpart, n, v.sfit, dnan, s);
+    CUDA_TRY(cudaGetLastError());
+    std::vector<float> f(n);
+    STATUS_TRY(download(f.data(), v.sfit, n, s));
+    for (uint64_t i = 0; i < n; ++i) fitness[i] = (double)f[i];
+    Ctl ctl;
+    STATUS_TRY(download(&ctl, v.ctl, 1, s));
+    if (nan_count) *nan_count = ctl.nan_count;
+    return ok();
+  };
+  return fail(nullptr, body());
+}
+
+int mgfwa_op_argmin_per_population(const double* fitness, uint64_t rows, uint64_t cols,
+                                   uint64_t* index, double* value) {
+  auto body = [&]() -> Status {
+    double* df = nullptr;
+    uint64_t* di = nullptr;
+    double* dv = nullptr;
+    CUDA_TRY(cudaMalloc(&df, rows * cols * 8));
+    CUDA_TRY(cudaMalloc(&di, rows * 8));
+    CUDA_TRY(cudaMalloc(&dv, rows * 8));
+    CUDA_TRY(cudaMemcpy(df, fitness, rows * cols * 8, cudaMemcpyHostToDevice));
+    launch_argmin_rows(df, rows, cols, di, dv, 0);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpy(index, di, rows * 8, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(value, dv, rows * 8, cudaMemcpyDeviceToHost));
+    cudaFree(df);
+    cudaFree(di);
+    cudaFree(dv);
+    return ok();
+  };
+  return fail(nullptr, body());
+}
+
+int mgfwa_time_fitness(mgfwa_ctx_t ctx, uint64_t iters, double* ms, uint64_t* units) {
+  Engine& e = ctx->engine;
+  auto body = [&]() -> Status {
+    if (!e.initialized) return Status{MGFWA_ESTATE, "mgfwa: initialize() must precede timing"};
+    Workspace& w = *e.ws;
+    cudaEvent_t a, b;
+    CUDA_TRY(cudaEventCreate(&a));
+    CUDA_TRY(cudaEventCreate(&b));
+    auto launch = [&]() {
+      if (w.v.nn)
+        mlp_fitness_launch(w.plan_sparks, w.v.spart, nullptr, e.stream);
+      else
+        launch_explode_map(w.v, w.nsm, e.stream);
+    };
+    launch();
+    CUDA_TRY(cudaEventRecord(a, e.stream));
+    for (uint64_t i = 0; i < iters; ++i) launch();
+    CUDA_TRY(cudaEventRecord(b, e.stream));
+    CUDA_TRY(cudaEventSynchronize(b));
+    float t = 0.0f;
+    CUDA_TRY(cudaEventElapsedTime(&t, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *ms = (double)t / (double)(iters ? iters : 1);
+    *units = w.v.F * w.v.lam;
+    return ok();
+  };
+  return fail(ctx, body());
+}
+
+int mgfwa_key_hash(const uint64_t* keys, uint64_t n, uint64_t* out) {
+  auto body = [&]() -> Status {
+    uint64_t *dk = nullptr, *dout = nullptr;
+    CUDA_TRY(cudaMalloc(&dk, n * 7 * 8));
+    CUDA_TRY(cudaMalloc(&dout, n * 8));
+    CUDA_TRY(cudaMemcpy(dk, keys, n * 7 * 8, cudaMemcpyHostToDevice));
+    launch_key_hash(dk, n, dout, 0);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpy(out, dout, n * 8, cudaMemcpyDeviceToHost));
+    cudaFree(dk);
+    cudaFree(dout);
+    return ok();
+  };
+  return fail(nullptr, body());
+}
+
+}  // extern "C"

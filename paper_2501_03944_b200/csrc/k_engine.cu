@@ -1,0 +1,790 @@
+// k_engine.cu — the MGFWA generation kernels (everything except the tensor-
+// core NN fitness, which lives in k_mlp_tc.cu).
+//
+// One generation = the body of run()'s loop, engine.cpp:359-417:
+//   k_pop_range      population_range            engine.cpp:22-41
+//   k_explode_map    explode + random_mapping    engine.cpp:78-131 (+ fused
+//                    analytic fitness partials, + bf16 shadow for NN)
+//   [NN fitness]     batched_apply(sparks)       backend.cpp:28-67
+//   k_rank           finalize spark fitness (NaN->+inf, backend.cpp:15-24)
+//                    + stable (fitness, index) ranking, engine.cpp:151-157
+//   k_guides         guiding_vector + multi_guiding_sparks + random_mapping
+//                    (kGuide), engine.cpp:133-196 (+ fused partials)
+//   [NN fitness]     batched_apply(guides)
+//   k_select         finalize guide fitness + select_best argmin +
+//                    update_amplitudes, engine.cpp:198-256
+//   k_select_copy    winner row copy (engine.cpp:232-233)
+//   k_loser          loser_out decision, engine.cpp:258-286, 394-410
+//   k_fresh_rows     loser reinit rows (kReinit), engine.cpp:287-294
+//   [NN fitness]     batched_apply(losers)
+//   k_finalize_record loser fitness commit + record_wave, engine.cpp:340-351
+//   k_record_copy    best-position copy on strict improvement
+// All kernels read ctl->active / ctl->iteration from HBM so that one CUDA
+// graph replays every generation unchanged.
+#include "common.cuh"
+#include "engine_view.cuh"
+#include "kernels.h"
+
+namespace mgfwa_b200 {
+
+namespace {
+
+constexpr int kWarps = 8;  // warps per block for the work-item kernels
+
+__device__ __forceinline__ bool gen_inactive(const EngineView& v) {
+  return *(volatile int*)&v.ctl->active == 0;
+}
+
+// Partial sums of one row -> fitness (fp32), NaN -> +inf (backend.cpp:15-24).
+__device__ __forceinline__ float finalize_row(const EngineView& v,
+                                              const float* part, uint64_t row,
+                                              bool* was_nan) {
+  const float* p = part + row * (uint64_t)v.nparts * 2;
+  float f;
+  if (v.nn) {
+    float s = 0.0f;
+    for (uint32_t m = 0; m < v.nparts; ++m) s += p[2 * m];
+    f = s / (float)v.samples;
+  } else {
+    float s0 = 0.0f, s1 = 0.0f;
+    for (uint32_t c = 0; c < v.nparts; ++c) {
+      s0 += p[2 * c];
+      s1 += p[2 * c + 1];
+    }
+    f = analytic_finalize(v.obj_kind, s0, s1, v.D);
+  }
+  *was_nan = isnan(f);
+  return *was_nan ? __int_as_float(0x7f800000) : f;
+}
+
+// Random-mapping repair of one coordinate (engine.cpp:119-125):
+// out-of-box (inclusive test, config.hpp:22-24) -> U[pop_lo, pop_hi).
+__device__ __forceinline__ float map_coord(const EngineView& v, double x,
+                                           uint64_t d, uint64_t map_prefix,
+                                           const float* plo, const float* phi) {
+  if (!(x >= v.lower[d] && x <= v.upper[d])) {
+    x = uniform_draw(splitmix64(map_prefix ^ d), (double)plo[d], (double)phi[d]);
+  }
+  return to_f32_in_box(x, v.lower_f[d], v.upper_f[d]);
+}
+
+__device__ __forceinline__ void store_row4(float* dst, __nv_bfloat16* dst_h,
+                                           uint64_t off, const float (&x)[4]) {
+  *reinterpret_cast<float4*>(dst + off) = make_float4(x[0], x[1], x[2], x[3]);
+  if (dst_h != nullptr) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(x[0], x[1]);
+    __nv_bfloat162 b = __floats2bfloat162_rn(x[2], x[3]);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(dst_h + off) = u;
+  }
+}
+
+__device__ __forceinline__ void store_bf16x4(__nv_bfloat16* dst_h, uint64_t off,
+                                             const float (&x)[4]) {
+  __nv_bfloat162 a = __floats2bfloat162_rn(x[0], x[1]);
+  __nv_bfloat162 b = __floats2bfloat162_rn(x[2], x[3]);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&a);
+  u.y = *reinterpret_cast<uint32_t*>(&b);
+  *reinterpret_cast<uint2*>(dst_h + off) = u;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ range
+// population_range, engine.cpp:22-41 (std::min/std::max keep-first order).
+__global__ void k_pop_range(EngineView v) {
+  if (gen_inactive(v)) return;
+  const uint64_t total = v.B * v.D;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t b = i / v.D, d = i % v.D;
+    const float* p = v.pos + (b * v.mu) * v.Dp + d;
+    float mn = p[0], mx = p[0];
+    for (uint64_t n = 1; n < v.mu; ++n) {
+      const float x = p[n * v.Dp];
+      mn = (x < mn) ? x : mn;
+      mx = (mx < x) ? x : mx;
+    }
+    v.pop_lo[b * v.Dp + d] = mn;
+    v.pop_hi[b * v.Dp + d] = mx;
+  }
+}
+
+// ---------------------------------------------------------------- explode
+// explode (engine.cpp:78-101) fused with random_mapping(kMapping)
+// (engine.cpp:103-131), the fp32 store, the bf16 shadow (NN) and the
+// analytic fitness partial sums.  Work item = (spark row, 512-coord chunk).
+__global__ void __launch_bounds__(256) k_explode_map(EngineView v) {
+  if (gen_inactive(v)) return;
+  const int lane = threadIdx.x & 31;
+  const uint64_t it = v.ctl->iteration;
+  const uint64_t rows = v.F * v.lam;
+  const uint64_t items = rows * v.nch;
+  for (uint64_t item = blockIdx.x * (uint64_t)kWarps + (threadIdx.x >> 5);
+       item < items; item += (uint64_t)gridDim.x * kWarps) {
+    const uint64_t r = item / v.nch, c = item % v.nch;
+    const uint64_t f = r / v.lam, k = r % v.lam;
+    const uint64_t b = f / v.mu, n = f % v.mu;
+    const uint64_t pe = key_prefix(v.seed, kExplode, it, b, n, k);
+    const uint64_t pm = key_prefix(v.seed, kMapping, it, b, n, k);
+    const double a = v.amp[f];
+    const float* prow = v.pos + f * v.Dp;
+    const float* plo = v.pop_lo + b * v.Dp;
+    const float* phi = v.pop_hi + b * v.Dp;
+    float s0 = 0.0f, s1 = 0.0f;
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t d0 = c * kChunk + q * 128 + lane * 4;
+      if (d0 >= v.D) break;
+      const float4 p4 = *reinterpret_cast<const float4*>(prow + d0);
+      const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
+      float x[4];
+      float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint64_t d = d0 + e;
+        if (d < v.D) {
+          // uniform_sample(key, -1, 1) = -1 + u * 2 ; spark = pos + t * amp
+          const double t = __dadd_rn(-1.0, __dmul_rn(unit_u53(splitmix64(pe ^ d)), 2.0));
+          const double s = __dadd_rn((double)pv[e], __dmul_rn(t, a));
+          x[e] = map_coord(v, s, d, pm, plo, phi);
+          if (!v.nn) analytic_terms(v.obj_kind, x[e], a0, a1);
+        } else {
+          x[e] = 0.0f;
+        }
+      }
+      s0 += a0;
+      s1 += a1;
+      store_row4(v.sparks, v.nn ? v.sparks_h : nullptr, r * v.Dp + d0, x);
+    }
+    if (!v.nn) {
+      s0 = warp_sum(s0);
+      s1 = warp_sum(s1);
+      if (lane == 0) {
+        v.spart[(r * v.nparts + c) * 2] = s0;
+        v.spart[(r * v.nparts + c) * 2 + 1] = s1;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------- rank
+// Finalize spark fitness, then the stable ranking of guiding_vector
+// (engine.cpp:151-157): order by (fitness asc, index asc); record the top
+// `top` indices (best first) and the bottom `top` (rank order).
+// One block per firework.
+__global__ void __launch_bounds__(256) k_rank(EngineView v) {
+  if (gen_inactive(v)) return;
+  extern __shared__ float sf[];
+  const uint64_t f = blockIdx.x;
+  unsigned nan_local = 0;
+  for (uint64_t k = threadIdx.x; k < v.lam; k += blockDim.x) {
+    if (v.injected_fitness) {
+      sf[k] = v.sfit[f * v.lam + k];
+      continue;
+    }
+    bool nan;
+    const float x = finalize_row(v, v.spart, f * v.lam + k, &nan);
+    nan_local += nan;
+    sf[k] = x;
+    v.sfit[f * v.lam + k] = x;
+  }
+  nan_local = __reduce_add_sync(0xffffffffu, nan_local);
+  if ((threadIdx.x & 31) == 0 && nan_local)
+    atomicAdd((unsigned long long*)&v.ctl->nan_count, (unsigned long long)nan_local);
+  if (v.M == 0) return;
+  __syncthreads();
+  const uint64_t lam = v.lam, top = v.top;
+  for (uint64_t k = threadIdx.x; k < lam; k += blockDim.x) {
+    const float fk = sf[k];
+    uint32_t rk = 0;
+    for (uint64_t j = 0; j < lam; ++j) {
+      const float fj = sf[j];
+      rk += (fj < fk) || (fj == fk && j < k);
+    }
+    if (rk < top) v.rank_idx[f * 2 * top + rk] = (int)k;
+    if (rk >= lam - top) v.rank_idx[f * 2 * top + top + (rk - (lam - top))] = (int)k;
+  }
+}
+
+// ----------------------------------------------------------------- guides
+// guiding_vector (engine.cpp:159-168, fp64, pairwise in rank order, then
+// / top) + multi_guiding_sparks (pos + beta_m * delta, engine.cpp:189) +
+// random_mapping(kGuide) + fp32 / bf16 stores + analytic partials.
+// Work item = (firework, chunk); produces the chunk of all M guide rows.
+__global__ void __launch_bounds__(256) k_guides(EngineView v) {
+  if (gen_inactive(v)) return;
+  constexpr int kMaxM = 16;
+  const int lane = threadIdx.x & 31;
+  const uint64_t it = v.ctl->iteration;
+  const uint64_t items = v.F * v.nch;
+  for (uint64_t item = blockIdx.x * (uint64_t)kWarps + (threadIdx.x >> 5);
+       item < items; item += (uint64_t)gridDim.x * kWarps) {
+    const uint64_t f = item / v.nch, c = item % v.nch;
+    const uint64_t b = f / v.mu, n = f % v.mu;
+    const int* ridx = v.rank_idx + f * 2 * v.top;
+    const float* prow = v.pos + f * v.Dp;
+    const float* plo = v.pop_lo + b * v.Dp;
+    const float* phi = v.pop_hi + b * v.Dp;
+    float s0[kMaxM], s1[kMaxM];
+#pragma unroll
+    for (int m = 0; m < kMaxM; ++m) s0[m] = s1[m] = 0.0f;
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t d0 = c * kChunk + q * 128 + lane * 4;
+      if (d0 >= v.D) break;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (uint64_t t = 0; t < v.top; ++t) {
+        const float4 bt = *reinterpret_cast<const float4*>(
+            v.sparks + (f * v.lam + ridx[t]) * v.Dp + d0);
+        const float4 wt = *reinterpret_cast<const float4*>(
+            v.sparks + (f * v.lam + ridx[v.top + t]) * v.Dp + d0);
+        acc[0] = __dadd_rn(acc[0], __dsub_rn((double)bt.x, (double)wt.x));
+        acc[1] = __dadd_rn(acc[1], __dsub_rn((double)bt.y, (double)wt.y));
+        acc[2] = __dadd_rn(acc[2], __dsub_rn((double)bt.z, (double)wt.z));
+        acc[3] = __dadd_rn(acc[3], __dsub_rn((double)bt.w, (double)wt.w));
+      }
+      const double dtop = (double)v.top;
+      const float4 p4 = *reinterpret_cast<const float4*>(prow + d0);
+      const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
+      double delta[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) delta[e] = __ddiv_rn(acc[e], dtop);
+#pragma unroll 1
+      for (uint64_t m = 0; m < v.M; ++m) {
+        const double beta = v.boosts[m];
+        const uint64_t pg = key_prefix(v.seed, kGuide, it, b, n, m);
+        float x[4];
+        float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint64_t d = d0 + e;
+          if (d < v.D) {
+            const double gx = __dadd_rn((double)pv[e], __dmul_rn(beta, delta[e]));
+            x[e] = map_coord(v, gx, d, pg, plo, phi);
+            if (!v.nn) analytic_terms(v.obj_kind, x[e], a0, a1);
+          } else {
+            x[e] = 0.0f;
+          }
+        }
+        store_row4(v.guides, v.nn ? v.guides_h : nullptr, (f * v.M + m) * v.Dp + d0, x);
+        // m is warp-uniform; registers indexed through a small switch-free
+        // loop (kMaxM unrolled compare) keep the partials in registers.
+#pragma unroll
+        for (int mm = 0; mm < kMaxM; ++mm)
+          if ((uint64_t)mm == m) {
+            s0[mm] += a0;
+            s1[mm] += a1;
+          }
+      }
+    }
+    if (!v.nn) {
+#pragma unroll
+      for (int mm = 0; mm < kMaxM; ++mm) {
+        if ((uint64_t)mm >= v.M) break;
+        const float t0 = warp_sum(s0[mm]);
+        const float t1 = warp_sum(s1[mm]);
+        if (lane == 0) {
+          const uint64_t row = f * v.M + mm;
+          v.gpart[(row * v.nparts + c) * 2] = t0;
+          v.gpart[(row * v.nparts + c) * 2 + 1] = t1;
+        }
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------- select
+// select_best (engine.cpp:198-242): strict-< scan firework -> sparks k up ->
+// guides m up == lexicographic min of (value, scan order).  Then
+// update_amplitudes (engine.cpp:244-256) and the wave accounting
+// (engine.cpp:388-390).  One block per firework.
+__global__ void __launch_bounds__(256) k_select(EngineView v) {
+  if (gen_inactive(v)) return;
+  const uint64_t f = blockIdx.x;
+  __shared__ double sv[8];
+  __shared__ int so[8];
+  unsigned nan_local = 0;
+  double best_v = v.fit[f];
+  int best_o = 0;
+  if (threadIdx.x != 0) best_v = __longlong_as_double(0x7ff0000000000000ll), best_o = 0x7fffffff;
+  for (uint64_t k = threadIdx.x; k < v.lam; k += blockDim.x) {
+    const double x = (double)v.sfit[f * v.lam + k];
+    const int o = 1 + (int)k;
+    if (x < best_v || (x == best_v && o < best_o)) best_v = x, best_o = o;
+  }
+  for (uint64_t m = threadIdx.x; m < v.M; m += blockDim.x) {
+    float g;
+    if (v.injected_fitness) {
+      g = v.gfit[f * v.M + m];
+    } else {
+      bool nan;
+      g = finalize_row(v, v.gpart, f * v.M + m, &nan);
+      nan_local += nan;
+      v.gfit[f * v.M + m] = g;
+    }
+    const double x = (double)g;
+    const int o = 1 + (int)v.lam + (int)m;
+    if (x < best_v || (x == best_v && o < best_o)) best_v = x, best_o = o;
+  }
+  // warp then block lexicographic min
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best_v, off);
+    const int oo = __shfl_xor_sync(0xffffffffu, best_o, off);
+    if (ov < best_v || (ov == best_v && oo < best_o)) best_v = ov, best_o = oo;
+  }
+  nan_local = __reduce_add_sync(0xffffffffu, nan_local);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sv[w] = best_v;
+    so[w] = best_o;
+    if (nan_local)
+      atomicAdd((unsigned long long*)&v.ctl->nan_count, (unsigned long long)nan_local);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
+      if (sv[i] < best_v || (sv[i] == best_v && so[i] < best_o)) best_v = sv[i], best_o = so[i];
+    // If every candidate is NaN-free but the firework is +inf and all are
+    // +inf, the firework (order 0) wins: strict < never fires.
+    if (!(best_v < v.fit[f])) {
+      best_v = v.fit[f];
+      best_o = 0;
+    }
+    const double old = v.fit[f];
+    const double gain = old - best_v;
+    v.fit[f] = best_v;
+    v.li[f] = (0.0 < gain) ? gain : 0.0;
+    const int imp = best_v < old;
+    v.improved[f] = imp;
+    v.winner[f] = best_o;
+    const double a = v.amp[f] * (imp ? v.amp_amplify : v.amp_reduce);
+    v.amp[f] = a < v.amp_floor ? v.amp_floor : (v.max_range < a ? v.max_range : a);
+    if (f == 0) v.ctl->used += v.wave;
+  }
+}
+
+// Copy the winning row into the firework (engine.cpp:232-233).
+__global__ void __launch_bounds__(256) k_select_copy(EngineView v) {
+  if (gen_inactive(v)) return;
+  const int lane = threadIdx.x & 31;
+  const uint64_t items = v.F * v.nch;
+  for (uint64_t item = blockIdx.x * (uint64_t)kWarps + (threadIdx.x >> 5);
+       item < items; item += (uint64_t)gridDim.x * kWarps) {
+    const uint64_t f = item / v.nch, c = item % v.nch;
+    const int w = v.winner[f];
+    if (w == 0) continue;
+    const float* src = (uint64_t)w <= v.lam
+                           ? v.sparks + (f * v.lam + (w - 1)) * v.Dp
+                           : v.guides + (f * v.M + (w - 1 - v.lam)) * v.Dp;
+    float* dst = v.pos + f * v.Dp;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t d0 = c * kChunk + q * 128 + lane * 4;
+      if (d0 < v.D)
+        *reinterpret_cast<float4*>(dst + d0) = *reinterpret_cast<const float4*>(src + d0);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ loser
+// loser_out decision (engine.cpp:258-286) with iterations_remaining from
+// engine.cpp:394-410 (device clock for the wall-clock budget).  One block.
+__global__ void k_loser(EngineView v) {
+  __shared__ int count;
+  if (threadIdx.x == 0) count = 0;
+  __syncthreads();
+  if (gen_inactive(v)) {
+    if (threadIdx.x == 0) v.ctl->n_losers = 0;
+    return;
+  }
+  double iters_rem = 0.0;
+  if (v.has_iters_override) {
+    iters_rem = v.iters_override;
+  } else if (v.max_evals > 0) {
+    const uint64_t used = v.ctl->used;
+    const uint64_t left = v.max_evals > used ? v.max_evals - used : 0;
+    iters_rem = (double)left / (double)v.wave;
+  } else {
+    const double now_ms = (double)(global_ns() - v.ctl->start_ns) * 1e-6;
+    const double avg = (now_ms - v.ctl->init_ms) / (double)v.ctl->iteration;
+    if (avg > 0.0) {
+      const double rem = v.wall_budget_ms - now_ms;
+      iters_rem = (rem > 0.0 ? rem : 0.0) / avg;
+    }
+  }
+  for (uint64_t b = threadIdx.x; b < v.B; b += blockDim.x) {
+    // argmin_per_population (backend.cpp:69-83)
+    uint64_t bi = 0;
+    double bv = v.fit[b * v.mu];
+    for (uint64_t n = 1; n < v.mu; ++n)
+      if (v.fit[b * v.mu + n] < bv) bv = v.fit[b * v.mu + n], bi = n;
+    int cnt = 0;
+    for (uint64_t n = 0; n < v.mu; ++n) {
+      const uint64_t f = b * v.mu + n;
+      int is_loser = 0;
+      if (iters_rem > 0.0 && n != bi) {
+        const double projected = v.fit[f] - v.li[f] * iters_rem;
+        is_loser = projected > bv;
+      }
+      v.loser[f] = is_loser;
+      if (is_loser) {
+        v.amp[f] = v.a0;
+        v.li[f] = 0.0;
+        ++cnt;
+      }
+    }
+    atomicAdd(&count, cnt);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    v.ctl->iters_rem = iters_rem;
+    v.ctl->n_losers = count;
+    v.ctl->used += (uint64_t)count;
+    v.ctl->losers_total += (uint64_t)count;
+  }
+}
+
+// ------------------------------------------------------------ fresh rows
+// mode 0: initialize (engine.cpp:56-64): every firework, kInit, iteration 0.
+// mode 1: loser reinit (engine.cpp:287-294): losers only, kReinit.
+__global__ void __launch_bounds__(256) k_fresh_rows(EngineView v, int mode) {
+  if (mode == 1 && (gen_inactive(v) || v.ctl->n_losers == 0)) return;
+  if (mode == 0 && blockIdx.x == 0 && threadIdx.x == 0) v.ctl->start_ns = global_ns();
+  const int lane = threadIdx.x & 31;
+  const uint64_t it = mode == 0 ? 0 : v.ctl->iteration;
+  const uint64_t stream = mode == 0 ? kInit : kReinit;
+  const uint64_t items = v.F * v.nch;
+  for (uint64_t item = blockIdx.x * (uint64_t)kWarps + (threadIdx.x >> 5);
+       item < items; item += (uint64_t)gridDim.x * kWarps) {
+    const uint64_t f = item / v.nch, c = item % v.nch;
+    if (mode == 1 && !v.loser[f]) continue;
+    const uint64_t b = f / v.mu, n = f % v.mu;
+    const uint64_t pk = key_prefix(v.seed, stream, it, b, n, 0);
+    float s0 = 0.0f, s1 = 0.0f;
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t d0 = c * kChunk + q * 128 + lane * 4;
+      if (d0 >= v.D) break;
+      float x[4];
+      float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint64_t d = d0 + e;
+        if (d < v.D) {
+          const double u = uniform_draw(splitmix64(pk ^ d), v.lower[d], v.upper[d]);
+          x[e] = to_f32_in_box(u, v.lower_f[d], v.upper_f[d]);
+          if (!v.nn) analytic_terms(v.obj_kind, x[e], a0, a1);
+        } else {
+          x[e] = 0.0f;
+        }
+      }
+      s0 += a0;
+      s1 += a1;
+      *reinterpret_cast<float4*>(v.pos + f * v.Dp + d0) = make_float4(x[0], x[1], x[2], x[3]);
+      if (v.nn) store_bf16x4(v.fresh_h, f * v.Dp + d0, x);
+    }
+    if (!v.nn) {
+      s0 = warp_sum(s0);
+      s1 = warp_sum(s1);
+      if (lane == 0) {
+        v.fpart[(f * v.nparts + c) * 2] = s0;
+        v.fpart[(f * v.nparts + c) * 2 + 1] = s1;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------- finalize/record
+// mode 0 (end of initialize, engine.cpp:66-74 + record_wave #0) or mode 1
+// (loser fitness commit engine.cpp:298-309 + record_wave engine.cpp:416).
+// record_wave (engine.cpp:340-351): per-batch argmin; best only on strict
+// improvement; one trace point per batch.  Then the loop-top termination
+// test (engine.cpp:360-367) for the next generation.  One block.
+__global__ void k_finalize_record(EngineView v, int mode) {
+  Ctl* ctl = v.ctl;
+  if (mode == 1 && gen_inactive(v)) {
+    for (uint64_t b = threadIdx.x; b < v.B; b += blockDim.x) v.rec_flag[b] = 0;
+    return;
+  }
+  unsigned nan_local = 0;
+  for (uint64_t f = threadIdx.x; f < v.F; f += blockDim.x) {
+    if (mode == 0 || v.loser[f]) {
+      bool nan;
+      const float x = finalize_row(v, v.fpart, f, &nan);
+      nan_local += nan;
+      v.fit[f] = (double)x;
+      if (mode == 0) {
+        v.amp[f] = v.a0;
+        v.li[f] = 0.0;
+      }
+    }
+  }
+  if (nan_local) atomicAdd((unsigned long long*)&ctl->nan_count, (unsigned long long)nan_local);
+  __syncthreads();
+  if (mode == 0 && threadIdx.x == 0) {
+    ctl->used = v.F;
+    ctl->losers_total = 0;
+    ctl->trace_n = 0;
+    ctl->gens_run = 0;
+  }
+  __syncthreads();
+  const uint64_t now = global_ns();
+  const uint64_t slot = ctl->trace_n % v.trace_cap;
+  for (uint64_t b = threadIdx.x; b < v.B; b += blockDim.x) {
+    uint64_t bi = 0;
+    double bv = v.fit[b * v.mu];
+    for (uint64_t n = 1; n < v.mu; ++n)
+      if (v.fit[b * v.mu + n] < bv) bv = v.fit[b * v.mu + n], bi = n;
+    double cur = mode == 0 ? __longlong_as_double(0x7ff0000000000000ll) : v.best_fit[b];
+    int flag = 0;
+    if (bv < cur) {
+      cur = bv;
+      v.best_idx[b] = (int)bi;
+      flag = 1;
+    }
+    v.best_fit[b] = cur;
+    v.rec_flag[b] = flag;
+    v.tr_evals[slot * v.B + b] = ctl->used;
+    v.tr_best[slot * v.B + b] = cur;
+    v.tr_ns[slot * v.B + b] = now - ctl->start_ns;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ctl->trace_n += 1;
+    const double now_ms = (double)(now - ctl->start_ns) * 1e-6;
+    if (mode == 0) {
+      ctl->init_ms = now_ms;
+      ctl->iteration = 0;
+    } else {
+      ctl->gens_run += 1;
+    }
+    int active = 1;
+    if (v.max_evals > 0 && ctl->used >= v.max_evals) active = 0;
+    if (v.wall_budget_ms > 0.0 && now_ms >= v.wall_budget_ms) active = 0;
+    ctl->active = active;
+    if (active) ctl->iteration += 1;
+  }
+}
+
+// Best-position copy on strict improvement (engine.cpp:343-346).
+__global__ void __launch_bounds__(256) k_record_copy(EngineView v) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t items = v.B * v.nch;
+  for (uint64_t item = blockIdx.x * (uint64_t)kWarps + (threadIdx.x >> 5);
+       item < items; item += (uint64_t)gridDim.x * kWarps) {
+    const uint64_t b = item / v.nch, c = item % v.nch;
+    if (!v.rec_flag[b]) continue;
+    const float* src = v.pos + (b * v.mu + v.best_idx[b]) * v.Dp;
+    float* dst = v.best_pos + b * v.Dp;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t d0 = c * kChunk + q * 128 + lane * 4;
+      if (d0 < v.D)
+        *reinterpret_cast<float4*>(dst + d0) = *reinterpret_cast<const float4*>(src + d0);
+    }
+  }
+}
+
+// ------------------------------------------------------- operator seams
+// Analytic partial sums of arbitrary fp32 rows (batched_apply seam).
+__global__ void __launch_bounds__(256) k_analytic_partials(const float* rows,
+                                                          uint64_t nrows,
+                                                          uint64_t D,
+                                                          uint64_t Dp,
+                                                          uint32_t nch,
+                                                          int kind,
+                                                          float* part) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t items = nrows * nch;
+  for (uint64_t item = blockIdx.x * (uint64_t)kWarps + (threadIdx.x >> 5);
+       item < items; item += (uint64_t)gridDim.x * kWarps) {
+    const uint64_t r = item / nch, c = item % nch;
+    float s0 = 0.0f, s1 = 0.0f;
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t d0 = c * kChunk + q * 128 + lane * 4;
+      if (d0 >= D) break;
+      const float4 x4 = *reinterpret_cast<const float4*>(rows + r * Dp + d0);
+      const float xs[4] = {x4.x, x4.y, x4.z, x4.w};
+      // same grouping as the generating kernels: per-4 group, then chunk
+      float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (d0 + e < D) analytic_terms(kind, xs[e], a0, a1);
+      s0 += a0;
+      s1 += a1;
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    if (lane == 0) {
+      part[(r * nch + c) * 2] = s0;
+      part[(r * nch + c) * 2 + 1] = s1;
+    }
+  }
+}
+
+// fitness[r] = finalize(part[r]) with NaN -> +inf; *nan += #NaN.
+__global__ void k_finalize_rows(EngineView v, const float* part, uint64_t nrows,
+                                float* fitness, unsigned long long* nan) {
+  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < nrows;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    bool isnan_;
+    fitness[r] = finalize_row(v, part, r, &isnan_);
+    if (isnan_) atomicAdd(nan, 1ull);
+  }
+}
+
+// fp32 rows -> bf16 rows (tensor-core operand), padding untouched.
+__global__ void k_to_bf16(const float* src, __nv_bfloat16* dst, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+// Standalone random_mapping over given rows (engine.cpp:103-131); shares
+// map_coord with the fused kernels.  cand/out [B][rows][Dp], pop from v.pos.
+__global__ void k_map_rows(EngineView v, const float* cand, float* out,
+                           uint64_t rows, uint64_t per, uint64_t stream,
+                           uint64_t it) {
+  const uint64_t total = v.B * rows * v.D;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t d = i % v.D, r = (i / v.D) % rows, b = i / (v.D * rows);
+    const uint64_t n = r / per, k = r % per;
+    const uint64_t pm = key_prefix(v.seed, stream, it, b, n, k);
+    const float x = cand[(b * rows + r) * v.Dp + d];
+    out[(b * rows + r) * v.Dp + d] =
+        map_coord(v, (double)x, d, pm, v.pop_lo + b * v.Dp, v.pop_hi + b * v.Dp);
+  }
+}
+
+// argmin_per_population (backend.cpp:69-83): strict <, lowest index wins.
+__global__ void k_argmin_rows(const double* fit, uint64_t rows, uint64_t cols,
+                              uint64_t* idx, double* val) {
+  for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < rows;
+       b += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t bi = 0;
+    double bv = fit[b * cols];
+    for (uint64_t n = 1; n < cols; ++n)
+      if (fit[b * cols + n] < bv) bv = fit[b * cols + n], bi = n;
+    idx[b] = bi;
+    val[b] = bv;
+  }
+}
+
+// key_hash (rng.hpp:43-52) for n keys [n][7].
+__global__ void k_key_hash(const uint64_t* keys, uint64_t n, uint64_t* out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t* k = keys + 7 * i;
+    out[i] = splitmix64(key_prefix(k[0], k[1], k[2], k[3], k[4], k[5]) ^ k[6]);
+  }
+}
+
+void launch_map_rows(const EngineView& v, const float* cand, float* out,
+                     uint64_t rows, uint64_t per, uint64_t stream, uint64_t it,
+                     cudaStream_t s) {
+  const uint64_t total = v.B * rows * v.D;
+  const unsigned g = (unsigned)((total + 255) / 256);
+  k_map_rows<<<g < 4096 ? (g ? g : 1) : 4096, 256, 0, s>>>(v, cand, out, rows, per, stream, it);
+}
+
+void launch_argmin_rows(const double* fit, uint64_t rows, uint64_t cols,
+                        uint64_t* idx, double* val, cudaStream_t s) {
+  k_argmin_rows<<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(fit, rows, cols, idx, val);
+}
+
+void launch_key_hash(const uint64_t* keys, uint64_t n, uint64_t* out,
+                     cudaStream_t s) {
+  k_key_hash<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(keys, n, out);
+}
+
+// ---------------------------------------------------------------- launch
+
+void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
+                               GenerationHooks* hooks) {
+  const unsigned items_sparks = (unsigned)((v.F * v.lam * v.nch + kWarps - 1) / kWarps);
+  const unsigned items_f = (unsigned)((v.F * v.nch + kWarps - 1) / kWarps);
+  auto cap = [&](unsigned g) { return g < (unsigned)nsm * 16 ? (g ? g : 1) : (unsigned)nsm * 16; };
+  const unsigned rng_blocks = cap((unsigned)((v.B * v.D + 255) / 256));
+  k_pop_range<<<rng_blocks, 256, 0, s>>>(v);
+  k_explode_map<<<cap(items_sparks), 256, 0, s>>>(v);
+  if (v.nn) hooks->eval_sparks(hooks->ctx, s);
+  k_rank<<<(unsigned)v.F, 256, v.lam * sizeof(float), s>>>(v);
+  if (v.M > 0) {
+    k_guides<<<cap(items_f), 256, 0, s>>>(v);
+    if (v.nn) hooks->eval_guides(hooks->ctx, s);
+  }
+  k_select<<<(unsigned)v.F, 256, 0, s>>>(v);
+  k_select_copy<<<cap(items_f), 256, 0, s>>>(v);
+  k_loser<<<1, 128, 0, s>>>(v);
+  k_fresh_rows<<<cap(items_f), 256, 0, s>>>(v, 1);
+  if (v.nn) hooks->eval_fresh(hooks->ctx, s);
+  k_finalize_record<<<1, 256, 0, s>>>(v, 1);
+  k_record_copy<<<cap((unsigned)((v.B * v.nch + kWarps - 1) / kWarps)), 256, 0, s>>>(v);
+}
+
+void launch_initialize_kernels(const EngineView& v, int nsm, cudaStream_t s,
+                               GenerationHooks* hooks) {
+  const unsigned items_f = (unsigned)((v.F * v.nch + kWarps - 1) / kWarps);
+  auto cap = [&](unsigned g) { return g < (unsigned)nsm * 16 ? (g ? g : 1) : (unsigned)nsm * 16; };
+  k_fresh_rows<<<cap(items_f), 256, 0, s>>>(v, 0);
+  if (v.nn) hooks->eval_fresh_all(hooks->ctx, s);
+  k_finalize_record<<<1, 256, 0, s>>>(v, 0);
+  k_record_copy<<<cap((unsigned)((v.B * v.nch + kWarps - 1) / kWarps)), 256, 0, s>>>(v);
+}
+
+void launch_analytic_partials(const float* rows, uint64_t nrows, uint64_t D,
+                              uint64_t Dp, uint32_t nch, int kind, float* part,
+                              int nsm, cudaStream_t s) {
+  const unsigned g = (unsigned)((nrows * nch + kWarps - 1) / kWarps);
+  k_analytic_partials<<<g < (unsigned)nsm * 16 ? (g ? g : 1) : nsm * 16, 256, 0, s>>>(
+      rows, nrows, D, Dp, nch, kind, part);
+}
+
+void launch_finalize_rows(const EngineView& v, const float* part, uint64_t nrows,
+                          float* fitness, unsigned long long* nan, cudaStream_t s) {
+  k_finalize_rows<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(v, part, nrows, fitness, nan);
+}
+
+void launch_to_bf16(const float* src, __nv_bfloat16* dst, uint64_t n, cudaStream_t s) {
+  k_to_bf16<<<(unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, s>>>(src, dst, n);
+}
+
+// Individual kernels for the operator seams (tests).
+void launch_pop_range(const EngineView& v, int nsm, cudaStream_t s) {
+  const unsigned g = (unsigned)((v.B * v.D + 255) / 256);
+  k_pop_range<<<g < (unsigned)nsm * 16 ? g : nsm * 16, 256, 0, s>>>(v);
+}
+void launch_explode_map(const EngineView& v, int nsm, cudaStream_t s) {
+  const unsigned g = (unsigned)((v.F * v.lam * v.nch + kWarps - 1) / kWarps);
+  k_explode_map<<<g < (unsigned)nsm * 16 ? g : nsm * 16, 256, 0, s>>>(v);
+}
+void launch_rank(const EngineView& v, cudaStream_t s) {
+  k_rank<<<(unsigned)v.F, 256, v.lam * sizeof(float), s>>>(v);
+}
+void launch_guides(const EngineView& v, int nsm, cudaStream_t s) {
+  const unsigned g = (unsigned)((v.F * v.nch + kWarps - 1) / kWarps);
+  k_guides<<<g < (unsigned)nsm * 16 ? g : nsm * 16, 256, 0, s>>>(v);
+}
+void launch_select(const EngineView& v, int nsm, cudaStream_t s) {
+  const unsigned g = (unsigned)((v.F * v.nch + kWarps - 1) / kWarps);
+  k_select<<<(unsigned)v.F, 256, 0, s>>>(v);
+  k_select_copy<<<g < (unsigned)nsm * 16 ? g : nsm * 16, 256, 0, s>>>(v);
+}
+void launch_loser(const EngineView& v, int nsm, cudaStream_t s) {
+  const unsigned g = (unsigned)((v.F * v.nch + kWarps - 1) / kWarps);
+  k_loser<<<1, 128, 0, s>>>(v);
+  k_fresh_rows<<<g < (unsigned)nsm * 16 ? g : nsm * 16, 256, 0, s>>>(v, 1);
+}
+void launch_loser_commit(const EngineView& v, int nsm, cudaStream_t s) {
+  k_finalize_record<<<1, 256, 0, s>>>(v, 1);
+  const unsigned g = (unsigned)((v.B * v.nch + kWarps - 1) / kWarps);
+  k_record_copy<<<g < (unsigned)nsm * 16 ? (g ? g : 1) : nsm * 16, 256, 0, s>>>(v);
+}
+
+}  // namespace mgfwa_b200

@@ -1,0 +1,67 @@
+// kernels.h — host-side launch entry points of the device kernels.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "engine_view.cuh"
+
+namespace mgfwa_b200 {
+
+// Tensor-core fitness calls the engine interleaves with its own kernels.
+struct GenerationHooks {
+  void* ctx;
+  void (*eval_sparks)(void* ctx, cudaStream_t s);
+  void (*eval_guides)(void* ctx, cudaStream_t s);
+  void (*eval_fresh)(void* ctx, cudaStream_t s);      // gated on n_losers
+  void (*eval_fresh_all)(void* ctx, cudaStream_t s);  // initialize()
+};
+
+void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
+                               GenerationHooks* hooks);
+void launch_initialize_kernels(const EngineView& v, int nsm, cudaStream_t s,
+                               GenerationHooks* hooks);
+
+// operator seams
+void launch_pop_range(const EngineView& v, int nsm, cudaStream_t s);
+void launch_explode_map(const EngineView& v, int nsm, cudaStream_t s);
+void launch_rank(const EngineView& v, cudaStream_t s);
+void launch_guides(const EngineView& v, int nsm, cudaStream_t s);
+void launch_select(const EngineView& v, int nsm, cudaStream_t s);
+void launch_loser(const EngineView& v, int nsm, cudaStream_t s);
+void launch_loser_commit(const EngineView& v, int nsm, cudaStream_t s);
+void launch_analytic_partials(const float* rows, uint64_t nrows, uint64_t D,
+                              uint64_t Dp, uint32_t nch, int kind, float* part,
+                              int nsm, cudaStream_t s);
+void launch_finalize_rows(const EngineView& v, const float* part,
+                          uint64_t nrows, float* fitness,
+                          unsigned long long* nan, cudaStream_t s);
+void launch_map_rows(const EngineView& v, const float* cand, float* out,
+                     uint64_t rows, uint64_t per, uint64_t stream, uint64_t it,
+                     cudaStream_t s);
+void launch_argmin_rows(const double* fit, uint64_t rows, uint64_t cols,
+                        uint64_t* idx, double* val, cudaStream_t s);
+void launch_key_hash(const uint64_t* keys, uint64_t n, uint64_t* out,
+                     cudaStream_t s);
+void launch_to_bf16(const float* src, __nv_bfloat16* dst, uint64_t n,
+                    cudaStream_t s);
+
+// ---- tensor-core MLP fitness (k_mlp_tc.cu) ----
+// Opaque plan: TMA descriptors for the shared dataset X [S][I] and for one
+// candidate buffer W (bf16 rows of stride Dp holding W1 [H][I] at offset 0,
+// then b1, W2 [O][H], b2).
+struct MlpPlan;
+// Returns nullptr and fills err on an unsupported shape.
+MlpPlan* mlp_plan_create(const __nv_bfloat16* X, const int32_t* y,
+                         uint32_t S, uint32_t I, uint32_t H, uint32_t O,
+                         const __nv_bfloat16* W, uint64_t rows, uint64_t Dp,
+                         int nsm, char* err, size_t errlen);
+void mlp_plan_destroy(MlpPlan* p);
+// part[row][m_tile][2] (slot 0 = sum of CE over the m-tile's samples).
+// gate: if non-null and *gate == 0 the kernel exits immediately.
+cudaError_t mlp_fitness_launch(const MlpPlan* p, float* part,
+                               const int* gate, cudaStream_t s);
+uint32_t mlp_num_parts(uint32_t S);
+
+}  // namespace mgfwa_b200
