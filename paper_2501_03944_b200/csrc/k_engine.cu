@@ -213,86 +213,74 @@ __global__ void __launch_bounds__(256) k_rank(EngineView v) {
 // ----------------------------------------------------------------- guides
 // guiding_vector (engine.cpp:159-168, fp64, pairwise in rank order, then
 // / top) + multi_guiding_sparks (pos + beta_m * delta, engine.cpp:189) +
-// random_mapping(kGuide) + fp32 / bf16 stores + analytic partials.
-// Work item = (firework, chunk); produces the chunk of all M guide rows.
+// random_mapping(kGuide) + fp32 / bf16 stores.  Work item = (firework,
+// 128-coordinate slice): one float4 per lane, the top-row loop unrolled by 4
+// so each lane keeps 8 independent 16-byte loads in flight (the kernel is a
+// gather-reduce over 2*top spark rows, HBM-bound).  The analytic fitness of
+// the guides is computed afterwards by k_analytic_partials (same grouping as
+// every other fitness, so cached fitness == re-evaluated fitness bit-wise).
 __global__ void __launch_bounds__(256) k_guides(EngineView v) {
   if (gen_inactive(v)) return;
-  constexpr int kMaxM = 16;
   const int lane = threadIdx.x & 31;
   const uint64_t it = v.ctl->iteration;
-  const uint64_t items = v.F * v.nch;
+  const uint64_t nsl = (v.D + 127) / 128;
+  const uint64_t items = v.F * nsl;
+  const uint64_t top = v.top;
   for (uint64_t item = blockIdx.x * (uint64_t)kWarps + (threadIdx.x >> 5);
        item < items; item += (uint64_t)gridDim.x * kWarps) {
-    const uint64_t f = item / v.nch, c = item % v.nch;
+    const uint64_t f = item / nsl, c = item % nsl;
+    const uint64_t d0 = c * 128 + lane * 4;
+    if (d0 >= v.D) continue;
     const uint64_t b = f / v.mu, n = f % v.mu;
-    const int* ridx = v.rank_idx + f * 2 * v.top;
-    const float* prow = v.pos + f * v.Dp;
-    const float* plo = v.pop_lo + b * v.Dp;
-    const float* phi = v.pop_hi + b * v.Dp;
-    float s0[kMaxM], s1[kMaxM];
+    const int* ridx = v.rank_idx + f * 2 * top;
+    const float* sb = v.sparks + f * v.lam * v.Dp + d0;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+    uint64_t t = 0;
+    for (; t + 4 <= top; t += 4) {
+      float4 bb[4], ww[4];
 #pragma unroll
-    for (int m = 0; m < kMaxM; ++m) s0[m] = s1[m] = 0.0f;
-#pragma unroll 1
-    for (int q = 0; q < 4; ++q) {
-      const uint64_t d0 = c * kChunk + q * 128 + lane * 4;
-      if (d0 >= v.D) break;
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (uint64_t t = 0; t < v.top; ++t) {
-        const float4 bt = *reinterpret_cast<const float4*>(
-            v.sparks + (f * v.lam + ridx[t]) * v.Dp + d0);
-        const float4 wt = *reinterpret_cast<const float4*>(
-            v.sparks + (f * v.lam + ridx[v.top + t]) * v.Dp + d0);
-        acc[0] = __dadd_rn(acc[0], __dsub_rn((double)bt.x, (double)wt.x));
-        acc[1] = __dadd_rn(acc[1], __dsub_rn((double)bt.y, (double)wt.y));
-        acc[2] = __dadd_rn(acc[2], __dsub_rn((double)bt.z, (double)wt.z));
-        acc[3] = __dadd_rn(acc[3], __dsub_rn((double)bt.w, (double)wt.w));
+      for (int i = 0; i < 4; ++i) {
+        bb[i] = *reinterpret_cast<const float4*>(sb + (uint64_t)ridx[t + i] * v.Dp);
+        ww[i] = *reinterpret_cast<const float4*>(sb + (uint64_t)ridx[top + t + i] * v.Dp);
       }
-      const double dtop = (double)v.top;
-      const float4 p4 = *reinterpret_cast<const float4*>(prow + d0);
-      const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
-      double delta[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) delta[e] = __ddiv_rn(acc[e], dtop);
-#pragma unroll 1
-      for (uint64_t m = 0; m < v.M; ++m) {
-        const double beta = v.boosts[m];
-        const uint64_t pg = key_prefix(v.seed, kGuide, it, b, n, m);
-        float x[4];
-        float a0 = 0.0f, a1 = 0.0f;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint64_t d = d0 + e;
-          if (d < v.D) {
-            const double gx = __dadd_rn((double)pv[e], __dmul_rn(beta, delta[e]));
-            x[e] = map_coord(v, gx, d, pg, plo, phi);
-            if (!v.nn) analytic_terms(v.obj_kind, x[e], a0, a1);
-          } else {
-            x[e] = 0.0f;
-          }
-        }
-        store_row4(v.guides, v.nn ? v.guides_h : nullptr, (f * v.M + m) * v.Dp + d0, x);
-        // m is warp-uniform; registers indexed through a small switch-free
-        // loop (kMaxM unrolled compare) keep the partials in registers.
-#pragma unroll
-        for (int mm = 0; mm < kMaxM; ++mm)
-          if ((uint64_t)mm == m) {
-            s0[mm] += a0;
-            s1[mm] += a1;
-          }
+      for (int i = 0; i < 4; ++i) {
+        acc0 = __dadd_rn(acc0, __dsub_rn((double)bb[i].x, (double)ww[i].x));
+        acc1 = __dadd_rn(acc1, __dsub_rn((double)bb[i].y, (double)ww[i].y));
+        acc2 = __dadd_rn(acc2, __dsub_rn((double)bb[i].z, (double)ww[i].z));
+        acc3 = __dadd_rn(acc3, __dsub_rn((double)bb[i].w, (double)ww[i].w));
       }
     }
-    if (!v.nn) {
+    for (; t < top; ++t) {
+      const float4 bt = *reinterpret_cast<const float4*>(sb + (uint64_t)ridx[t] * v.Dp);
+      const float4 wt = *reinterpret_cast<const float4*>(sb + (uint64_t)ridx[top + t] * v.Dp);
+      acc0 = __dadd_rn(acc0, __dsub_rn((double)bt.x, (double)wt.x));
+      acc1 = __dadd_rn(acc1, __dsub_rn((double)bt.y, (double)wt.y));
+      acc2 = __dadd_rn(acc2, __dsub_rn((double)bt.z, (double)wt.z));
+      acc3 = __dadd_rn(acc3, __dsub_rn((double)bt.w, (double)wt.w));
+    }
+    const double dtop = (double)top;
+    const double delta[4] = {__ddiv_rn(acc0, dtop), __ddiv_rn(acc1, dtop), __ddiv_rn(acc2, dtop),
+                             __ddiv_rn(acc3, dtop)};
+    const float4 p4 = *reinterpret_cast<const float4*>(v.pos + f * v.Dp + d0);
+    const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
+    const float* plo = v.pop_lo + b * v.Dp;
+    const float* phi = v.pop_hi + b * v.Dp;
+    for (uint64_t m = 0; m < v.M; ++m) {
+      const double beta = v.boosts[m];
+      const uint64_t pg = key_prefix(v.seed, kGuide, it, b, n, m);
+      float x[4];
 #pragma unroll
-      for (int mm = 0; mm < kMaxM; ++mm) {
-        if ((uint64_t)mm >= v.M) break;
-        const float t0 = warp_sum(s0[mm]);
-        const float t1 = warp_sum(s1[mm]);
-        if (lane == 0) {
-          const uint64_t row = f * v.M + mm;
-          v.gpart[(row * v.nparts + c) * 2] = t0;
-          v.gpart[(row * v.nparts + c) * 2 + 1] = t1;
+      for (int e = 0; e < 4; ++e) {
+        const uint64_t d = d0 + e;
+        if (d < v.D) {
+          const double gx = __dadd_rn((double)pv[e], __dmul_rn(beta, delta[e]));
+          x[e] = map_coord(v, gx, d, pg, plo, phi);
+        } else {
+          x[e] = 0.0f;
         }
       }
+      store_row4(v.guides, v.nn ? v.guides_h : nullptr, (f * v.M + m) * v.Dp + d0, x);
     }
   }
 }
@@ -716,8 +704,12 @@ void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
   if (v.nn) hooks->eval_sparks(hooks->ctx, s);
   k_rank<<<(unsigned)v.F, 256, v.lam * sizeof(float), s>>>(v);
   if (v.M > 0) {
-    k_guides<<<cap(items_f), 256, 0, s>>>(v);
-    if (v.nn) hooks->eval_guides(hooks->ctx, s);
+    const unsigned items_g = (unsigned)((v.F * ((v.D + 127) / 128) + kWarps - 1) / kWarps);
+    k_guides<<<cap(items_g), 256, 0, s>>>(v);
+    if (v.nn)
+      hooks->eval_guides(hooks->ctx, s);
+    else
+      launch_analytic_partials(v.guides, v.F * v.M, v.D, v.Dp, v.nch, v.obj_kind, v.gpart, nsm, s);
   }
   k_select<<<(unsigned)v.F, 256, 0, s>>>(v);
   k_select_copy<<<cap(items_f), 256, 0, s>>>(v);
@@ -768,8 +760,9 @@ void launch_rank(const EngineView& v, cudaStream_t s) {
   k_rank<<<(unsigned)v.F, 256, v.lam * sizeof(float), s>>>(v);
 }
 void launch_guides(const EngineView& v, int nsm, cudaStream_t s) {
-  const unsigned g = (unsigned)((v.F * v.nch + kWarps - 1) / kWarps);
+  const unsigned g = (unsigned)((v.F * ((v.D + 127) / 128) + kWarps - 1) / kWarps);
   k_guides<<<g < (unsigned)nsm * 16 ? g : nsm * 16, 256, 0, s>>>(v);
+  if (!v.nn) launch_analytic_partials(v.guides, v.F * v.M, v.D, v.Dp, v.nch, v.obj_kind, v.gpart, nsm, s);
 }
 void launch_select(const EngineView& v, int nsm, cudaStream_t s) {
   const unsigned g = (unsigned)((v.F * v.nch + kWarps - 1) / kWarps);
