@@ -217,6 +217,7 @@ struct Workspace {
     device = dev;
     CUDA_TRY(cudaSetDevice(dev));
     CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    CUDA_TRY(prepare_engine_kernels());
     const uint64_t D = space->dim;
     v.B = c.B;
     v.mu = c.mu;

@@ -116,58 +116,267 @@ __global__ void k_pop_range(EngineView v) {
 // ---------------------------------------------------------------- explode
 // explode (engine.cpp:78-101) fused with random_mapping(kMapping)
 // (engine.cpp:103-131), the fp32 store, the bf16 shadow (NN) and the
-// analytic fitness partial sums.  Work item = (spark row, 512-coord chunk).
-__global__ void __launch_bounds__(256) k_explode_map(EngineView v) {
+// analytic fitness partial sums.
+//
+// Work item = (firework, group of kSparkGroup sparks, 512-coordinate chunk):
+// the firework row, the box images and the pos -> fp64 conversions are
+// loaded once and reused by the 8 sparks of the group.  Per coordinate the
+// cost is one splitmix64 round (hoisted key prefix), an exact bit-built
+// t = -1 + 2u (no int->fp conversion), one DMUL + DADD in fp64 and one
+// rounding to fp32.  The in-box test runs on the rounded float against the
+// fp32 box images (exact whenever strictly inside, see in_box_fast); the
+// rare remaining coordinates — out of the box (random mapping) or on the
+// 1-ulp boundary — are compacted across the warp and finished by one lane
+// each, so mapping work is paid per mapped coordinate, not per warp.
+constexpr int kSparkGroup = 4;
+
+// t = -1 + u * 2 for u = (h >> 11) * 2^-53, exactly as the reference's
+// uniform_sample(key, -1, 1) (rng.hpp:55-65): with m = h >> 11 and
+// D1 = 1 + (m mod 2^52) 2^-52 in [1, 2), t = D1 - (2 - (m >> 52)); both
+// subtractions are exact (Sterbenz), so t is bit-identical to the fp64
+// reference value without an int -> fp conversion.
+__device__ __forceinline__ double unit_pm1(uint64_t h) {
+  const uint32_t hi = (uint32_t)(h >> 32);
+  const uint32_t lo = __funnelshift_r((uint32_t)h, hi, 11);  // bits 11..42 of h
+  const uint32_t mhi = (hi >> 11) & 0xFFFFFu;                 // bits 43..62 of h
+  const double d1 = __hiloint2double((int)(0x3FF00000u | mhi), (int)lo);
+  return __dsub_rn(d1, (hi >> 31) ? 1.0 : 2.0);
+}
+
+// Exact in-box test for x = round_f32(s): strictly between the fp32 box
+// images implies lower <= s <= upper (lo_f >= lower, and s > lo_f because
+// s rounds to a float above lo_f); callers fall back to map_coord otherwise.
+__device__ __forceinline__ bool in_box_fast(float x, float lo_f, float hi_f) {
+  return x > lo_f && x < hi_f;
+}
+
+// Dynamic shared memory of k_explode_map: the block's 512-coordinate chunk
+// of the box (fp64 and its fp32 images) and of the population range,
+// staged once per work item, plus the per-warp slow-path queue.
+struct ExplodeChunk {
+  double lo[kChunk], hi[kChunk];
+  float lof[kChunk], hif[kChunk], plo[kChunk], phi[kChunk];
+};
+struct ExplodeWarp {
+  double val[32 * kSparkGroup * 4];  // exact fp64 spark of each slow coordinate,
+                                     // then (aliased) its fp32 result
+  uint16_t slot[32 * kSparkGroup * 4];
+  uint64_t pre[2 * kSparkGroup];     // explode / mapping key prefixes
+};
+constexpr size_t kExplodeSmem = sizeof(ExplodeChunk) + kWarps * sizeof(ExplodeWarp);
+
+// Exact repair of one coordinate from the staged chunk (== map_coord).
+__device__ __forceinline__ float map_coord_staged(const ExplodeChunk& ch, double x, uint32_t i,
+                                                  uint32_t d, uint64_t map_prefix) {
+  if (!(x >= ch.lo[i] && x <= ch.hi[i]))
+    x = uniform_draw(splitmix64(map_prefix ^ (uint64_t)d), (double)ch.plo[i], (double)ch.phi[i]);
+  return to_f32_in_box(x, ch.lof[i], ch.hif[i]);
+}
+
+// One 128-coordinate slice of kSparkGroup sparks.  FULL: every spark of the
+// group exists and the slice lies inside [0, D) (no per-element guards).
+template <int KIND, bool FULL>
+__device__ __forceinline__ void explode_slice(const EngineView& v, const ExplodeChunk& ch,
+                                              ExplodeWarp& wq, int lane, uint32_t cbase,
+                                              uint32_t qoff, uint64_t f, uint64_t k0, int kn,
+                                              double a, const uint64_t (&pe)[kSparkGroup],
+                                              float (&s0)[kSparkGroup], float (&s1)[kSparkGroup]) {
+  constexpr int KG = kSparkGroup;
+  constexpr int NSLOT = KG * 4;
+  const uint32_t D = (uint32_t)v.D;
+  const uint32_t li0 = qoff + lane * 4;  // index inside the staged chunk
+  const uint32_t d0 = cbase + li0;
+  const bool on = FULL || d0 < D;
+  const int nvalid = FULL ? 4 : (on ? (D - d0 < 4 ? (int)(D - d0) : 4) : 0);
+  float4 p4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (on) p4 = *reinterpret_cast<const float4*>(v.pos + f * v.Dp + d0);
+  const float4 lf4 = *reinterpret_cast<const float4*>(&ch.lof[li0]);
+  const float4 uf4 = *reinterpret_cast<const float4*>(&ch.hif[li0]);
+  const double pd[4] = {(double)p4.x, (double)p4.y, (double)p4.z, (double)p4.w};
+  const float lf[4] = {lf4.x, lf4.y, lf4.z, lf4.w};
+  const float uf[4] = {uf4.x, uf4.y, uf4.z, uf4.w};
+  float x[KG][4];
+  double sv[KG][4];
+  unsigned slow = 0;
+#pragma unroll
+  for (int kk = 0; kk < KG; ++kk) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint64_t h = splitmix64(pe[kk] ^ (uint64_t)(d0 + e));
+      sv[kk][e] = __dadd_rn(pd[e], __dmul_rn(unit_pm1(h), a));
+      x[kk][e] = __double2float_rn(sv[kk][e]);
+      const bool need = !in_box_fast(x[kk][e], lf[e], uf[e]);
+      if (FULL ? need : (kk < kn && e < nvalid && need)) slow |= 1u << (kk * 4 + e);
+    }
+  }
+  // Out-of-box / boundary coordinates: compact across the warp, finish one
+  // per lane with the exact test + random mapping (shared-memory operands).
+  if (__any_sync(0xffffffffu, slow != 0)) {
+    const unsigned cnt = __popc(slow);
+    unsigned incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+    unsigned p = incl - cnt;
+#pragma unroll
+    for (int j = 0; j < NSLOT; ++j)
+      if (slow & (1u << j)) {
+        wq.val[p] = sv[j >> 2][j & 3];
+        wq.slot[p] = (uint16_t)((lane << 4) | j);
+        ++p;
+      }
+    __syncwarp();
+    for (unsigned i = lane; i < total; i += 32) {
+      const unsigned sl = wq.slot[i];
+      const unsigned j = sl & 15u;
+      const uint32_t li = qoff + (sl >> 4) * 4 + (j & 3u);
+      const float r = map_coord_staged(ch, wq.val[i], li, cbase + li, wq.pre[KG + (j >> 2)]);
+      *reinterpret_cast<float*>(&wq.val[i]) = r;
+    }
+    __syncwarp();
+    p = incl - cnt;
+#pragma unroll
+    for (int j = 0; j < NSLOT; ++j)
+      if (slow & (1u << j)) x[j >> 2][j & 3] = *reinterpret_cast<const float*>(&wq.val[p++]);
+    __syncwarp();
+  }
+  if (on) {
+#pragma unroll
+    for (int kk = 0; kk < KG; ++kk) {
+      if (!FULL && kk >= kn) break;
+      if (!FULL) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (e >= nvalid) x[kk][e] = 0.0f;
+      }
+      if (KIND != 0) {
+        float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (FULL || e < nvalid) analytic_terms(KIND, x[kk][e], a0, a1);
+        s0[kk] += a0;
+        s1[kk] += a1;
+      }
+      const uint64_t off = (f * v.lam + k0 + kk) * v.Dp + d0;
+      *reinterpret_cast<float4*>(v.sparks + off) = make_float4(x[kk][0], x[kk][1], x[kk][2], x[kk][3]);
+      if (KIND == 0) store_bf16x4(v.sparks_h, off, x[kk]);
+    }
+  }
+}
+
+// Work item = (firework f, 512-coordinate chunk c, 8 consecutive spark
+// groups): the block stages the chunk's box / population range once; warp w
+// takes spark group 8*item_group + w.
+// KIND == 0: NN objective (bf16 shadow, no analytic partials); otherwise the
+// analytic objective kind whose partial sums are fused in.
+template <int KIND>
+__global__ void __launch_bounds__(256, 2) k_explode_map(EngineView v) {
   if (gen_inactive(v)) return;
-  const int lane = threadIdx.x & 31;
+  constexpr int KG = kSparkGroup;
+  extern __shared__ __align__(16) uint8_t ex_smem[];
+  ExplodeChunk& ch = *reinterpret_cast<ExplodeChunk*>(ex_smem);
+  ExplodeWarp* wqs = reinterpret_cast<ExplodeWarp*>(ex_smem + sizeof(ExplodeChunk));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  ExplodeWarp& wq = wqs[warp];
   const uint64_t it = v.ctl->iteration;
-  const uint64_t rows = v.F * v.lam;
-  const uint64_t items = rows * v.nch;
-  for (uint64_t item = blockIdx.x * (uint64_t)kWarps + (threadIdx.x >> 5);
-       item < items; item += (uint64_t)gridDim.x * kWarps) {
-    const uint64_t r = item / v.nch, c = item % v.nch;
-    const uint64_t f = r / v.lam, k = r % v.lam;
+  const uint64_t ngrp = (v.lam + KG - 1) / KG;
+  const uint64_t nsup = (ngrp + kWarps - 1) / kWarps;  // groups of 8 spark groups
+  const uint64_t items = v.F * v.nch * nsup;
+  const uint32_t D = (uint32_t)v.D;
+  for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const uint64_t sup = item % nsup, rest = item / nsup;
+    const uint32_t c = (uint32_t)(rest % v.nch);
+    const uint64_t f = rest / v.nch;
     const uint64_t b = f / v.mu, n = f % v.mu;
-    const uint64_t pe = key_prefix(v.seed, kExplode, it, b, n, k);
-    const uint64_t pm = key_prefix(v.seed, kMapping, it, b, n, k);
+    const uint32_t cbase = c * kChunk;
+    __syncthreads();  // previous item's readers are done with the chunk
+    for (uint32_t i = threadIdx.x; i < kChunk; i += blockDim.x) {
+      const uint32_t d = cbase + i;
+      const bool in = d < D;
+      ch.lo[i] = in ? v.lower[d] : 0.0;
+      ch.hi[i] = in ? v.upper[d] : 0.0;
+      ch.lof[i] = in ? v.lower_f[d] : 0.0f;
+      ch.hif[i] = in ? v.upper_f[d] : 0.0f;
+      ch.plo[i] = in ? v.pop_lo[b * v.Dp + d] : 0.0f;
+      ch.phi[i] = in ? v.pop_hi[b * v.Dp + d] : 0.0f;
+    }
+    __syncthreads();
+    const uint64_t g = sup * kWarps + warp;
+    if (g >= ngrp) continue;  // warp-uniform
+    const uint64_t k0 = g * KG;
+    const int kn = (int)(v.lam - k0 < (uint64_t)KG ? v.lam - k0 : KG);
+    // key prefixes: lanes [0, KG) explode, [KG, 2KG) mapping (hoisted
+    // rng.hpp:43-51 up to field k; each draw is then one splitmix64 round)
+    if (lane < kn)
+      wq.pre[lane] = key_prefix(v.seed, kExplode, it, b, n, k0 + lane);
+    else if (lane >= KG && lane < KG + kn)
+      wq.pre[lane] = key_prefix(v.seed, kMapping, it, b, n, k0 + lane - KG);
+    __syncwarp();
+    uint64_t pe[KG];
+#pragma unroll
+    for (int kk = 0; kk < KG; ++kk) pe[kk] = wq.pre[kk];
     const double a = v.amp[f];
-    const float* prow = v.pos + f * v.Dp;
-    const float* plo = v.pop_lo + b * v.Dp;
-    const float* phi = v.pop_hi + b * v.Dp;
-    float s0 = 0.0f, s1 = 0.0f;
+    float s0[KG], s1[KG];
+#pragma unroll
+    for (int kk = 0; kk < KG; ++kk) s0[kk] = s1[kk] = 0.0f;
 #pragma unroll 1
     for (int q = 0; q < 4; ++q) {
-      const uint64_t d0 = c * kChunk + q * 128 + lane * 4;
-      if (d0 >= v.D) break;
-      const float4 p4 = *reinterpret_cast<const float4*>(prow + d0);
-      const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
-      float x[4];
-      float a0 = 0.0f, a1 = 0.0f;
+      const uint32_t qoff = q * 128;
+      if (cbase + qoff >= D) break;  // warp-uniform
+      if (kn == KG && cbase + qoff + 128 <= D)
+        explode_slice<KIND, true>(v, ch, wq, lane, cbase, qoff, f, k0, kn, a, pe, s0, s1);
+      else
+        explode_slice<KIND, false>(v, ch, wq, lane, cbase, qoff, f, k0, kn, a, pe, s0, s1);
+    }
+    if (KIND != 0) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const uint64_t d = d0 + e;
-        if (d < v.D) {
-          // uniform_sample(key, -1, 1) = -1 + u * 2 ; spark = pos + t * amp
-          const double t = __dadd_rn(-1.0, __dmul_rn(unit_u53(splitmix64(pe ^ d)), 2.0));
-          const double s = __dadd_rn((double)pv[e], __dmul_rn(t, a));
-          x[e] = map_coord(v, s, d, pm, plo, phi);
-          if (!v.nn) analytic_terms(v.obj_kind, x[e], a0, a1);
-        } else {
-          x[e] = 0.0f;
+      for (int kk = 0; kk < KG; ++kk) {
+        if (kk >= kn) break;
+        const float t0 = warp_sum(s0[kk]);
+        const float t1 = warp_sum(s1[kk]);
+        if (lane == 0) {
+          const uint64_t r = f * v.lam + k0 + kk;
+          v.spart[(r * v.nparts + c) * 2] = t0;
+          v.spart[(r * v.nparts + c) * 2 + 1] = t1;
         }
       }
-      s0 += a0;
-      s1 += a1;
-      store_row4(v.sparks, v.nn ? v.sparks_h : nullptr, r * v.Dp + d0, x);
     }
-    if (!v.nn) {
-      s0 = warp_sum(s0);
-      s1 = warp_sum(s1);
-      if (lane == 0) {
-        v.spart[(r * v.nparts + c) * 2] = s0;
-        v.spart[(r * v.nparts + c) * 2 + 1] = s1;
-      }
-    }
+  }
+}
+
+static unsigned explode_blocks(const EngineView& v, int nsm) {
+  const uint64_t ngrp = (v.lam + kSparkGroup - 1) / kSparkGroup;
+  const uint64_t items = v.F * v.nch * ((ngrp + kWarps - 1) / kWarps);
+  const uint64_t cap = (uint64_t)nsm * 8;
+  return (unsigned)(items < cap ? items : cap);
+}
+
+template <int KIND>
+static void explode_launch_k(const EngineView& v, unsigned grid, cudaStream_t s) {
+  k_explode_map<KIND><<<grid, 256, kExplodeSmem, s>>>(v);
+}
+
+cudaError_t prepare_engine_kernels() {
+  cudaError_t e = cudaSuccess;
+  const int bytes = (int)kExplodeSmem;
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<OBJ_SPHERE>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<OBJ_RASTRIGIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<OBJ_ACKLEY>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  return e;
+}
+
+static void launch_explode_map_impl(const EngineView& v, int nsm, cudaStream_t s) {
+  const unsigned grid = explode_blocks(v, nsm);
+  const int kind = v.nn ? 0 : v.obj_kind;
+  switch (kind) {
+    case 0: explode_launch_k<0>(v, grid, s); break;
+    case OBJ_SPHERE: explode_launch_k<OBJ_SPHERE>(v, grid, s); break;
+    case OBJ_RASTRIGIN: explode_launch_k<OBJ_RASTRIGIN>(v, grid, s); break;
+    default: explode_launch_k<OBJ_ACKLEY>(v, grid, s); break;
   }
 }
 
@@ -221,30 +430,34 @@ __global__ void __launch_bounds__(256) k_rank(EngineView v) {
 // every other fitness, so cached fitness == re-evaluated fitness bit-wise).
 __global__ void __launch_bounds__(256) k_guides(EngineView v) {
   if (gen_inactive(v)) return;
-  const int lane = threadIdx.x & 31;
+  extern __shared__ int s_idx[];  // [2*top]: rank lists of the block's firework
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t it = v.ctl->iteration;
   const uint64_t nsl = (v.D + 127) / 128;
-  const uint64_t items = v.F * nsl;
+  const uint64_t bpf = (nsl + kWarps - 1) / kWarps;  // blocks per firework
   const uint64_t top = v.top;
-  for (uint64_t item = blockIdx.x * (uint64_t)kWarps + (threadIdx.x >> 5);
-       item < items; item += (uint64_t)gridDim.x * kWarps) {
-    const uint64_t f = item / nsl, c = item % nsl;
+  for (uint64_t blk = blockIdx.x; blk < v.F * bpf; blk += gridDim.x) {
+    const uint64_t f = blk / bpf;
+    const uint64_t c = (blk % bpf) * kWarps + warp;
+    __syncthreads();
+    for (uint64_t i = threadIdx.x; i < 2 * top; i += blockDim.x) s_idx[i] = v.rank_idx[f * 2 * top + i];
+    __syncthreads();
     const uint64_t d0 = c * 128 + lane * 4;
-    if (d0 >= v.D) continue;
+    if (c >= nsl || d0 >= v.D) continue;
     const uint64_t b = f / v.mu, n = f % v.mu;
-    const int* ridx = v.rank_idx + f * 2 * top;
     const float* sb = v.sparks + f * v.lam * v.Dp + d0;
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
     uint64_t t = 0;
-    for (; t + 4 <= top; t += 4) {
-      float4 bb[4], ww[4];
+    // 16 independent 16-byte loads in flight per lane, summed in rank order
+    for (; t + 8 <= top; t += 8) {
+      float4 bb[8], ww[8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        bb[i] = *reinterpret_cast<const float4*>(sb + (uint64_t)ridx[t + i] * v.Dp);
-        ww[i] = *reinterpret_cast<const float4*>(sb + (uint64_t)ridx[top + t + i] * v.Dp);
+      for (int i = 0; i < 8; ++i) {
+        bb[i] = *reinterpret_cast<const float4*>(sb + (uint64_t)s_idx[t + i] * v.Dp);
+        ww[i] = *reinterpret_cast<const float4*>(sb + (uint64_t)s_idx[top + t + i] * v.Dp);
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < 8; ++i) {
         acc0 = __dadd_rn(acc0, __dsub_rn((double)bb[i].x, (double)ww[i].x));
         acc1 = __dadd_rn(acc1, __dsub_rn((double)bb[i].y, (double)ww[i].y));
         acc2 = __dadd_rn(acc2, __dsub_rn((double)bb[i].z, (double)ww[i].z));
@@ -252,8 +465,8 @@ __global__ void __launch_bounds__(256) k_guides(EngineView v) {
       }
     }
     for (; t < top; ++t) {
-      const float4 bt = *reinterpret_cast<const float4*>(sb + (uint64_t)ridx[t] * v.Dp);
-      const float4 wt = *reinterpret_cast<const float4*>(sb + (uint64_t)ridx[top + t] * v.Dp);
+      const float4 bt = *reinterpret_cast<const float4*>(sb + (uint64_t)s_idx[t] * v.Dp);
+      const float4 wt = *reinterpret_cast<const float4*>(sb + (uint64_t)s_idx[top + t] * v.Dp);
       acc0 = __dadd_rn(acc0, __dsub_rn((double)bt.x, (double)wt.x));
       acc1 = __dadd_rn(acc1, __dsub_rn((double)bt.y, (double)wt.y));
       acc2 = __dadd_rn(acc2, __dsub_rn((double)bt.z, (double)wt.z));
@@ -693,19 +906,23 @@ void launch_key_hash(const uint64_t* keys, uint64_t n, uint64_t* out,
 
 // ---------------------------------------------------------------- launch
 
+static unsigned guide_blocks(const EngineView& v, int nsm) {
+  const uint64_t nsl = (v.D + 127) / 128;
+  const uint64_t blocks = v.F * ((nsl + kWarps - 1) / kWarps);
+  return (unsigned)(blocks < (uint64_t)nsm * 8 ? blocks : (uint64_t)nsm * 8);
+}
+
 void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
                                GenerationHooks* hooks) {
-  const unsigned items_sparks = (unsigned)((v.F * v.lam * v.nch + kWarps - 1) / kWarps);
   const unsigned items_f = (unsigned)((v.F * v.nch + kWarps - 1) / kWarps);
   auto cap = [&](unsigned g) { return g < (unsigned)nsm * 16 ? (g ? g : 1) : (unsigned)nsm * 16; };
   const unsigned rng_blocks = cap((unsigned)((v.B * v.D + 255) / 256));
   k_pop_range<<<rng_blocks, 256, 0, s>>>(v);
-  k_explode_map<<<cap(items_sparks), 256, 0, s>>>(v);
+  launch_explode_map_impl(v, nsm, s);
   if (v.nn) hooks->eval_sparks(hooks->ctx, s);
   k_rank<<<(unsigned)v.F, 256, v.lam * sizeof(float), s>>>(v);
   if (v.M > 0) {
-    const unsigned items_g = (unsigned)((v.F * ((v.D + 127) / 128) + kWarps - 1) / kWarps);
-    k_guides<<<cap(items_g), 256, 0, s>>>(v);
+    k_guides<<<guide_blocks(v, nsm), 256, 2 * v.top * sizeof(int), s>>>(v);
     if (v.nn)
       hooks->eval_guides(hooks->ctx, s);
     else
@@ -753,15 +970,15 @@ void launch_pop_range(const EngineView& v, int nsm, cudaStream_t s) {
   k_pop_range<<<g < (unsigned)nsm * 16 ? g : nsm * 16, 256, 0, s>>>(v);
 }
 void launch_explode_map(const EngineView& v, int nsm, cudaStream_t s) {
-  const unsigned g = (unsigned)((v.F * v.lam * v.nch + kWarps - 1) / kWarps);
-  k_explode_map<<<g < (unsigned)nsm * 16 ? g : nsm * 16, 256, 0, s>>>(v);
+  const unsigned g = (unsigned)((v.F * ((v.lam + kSparkGroup - 1) / kSparkGroup) * v.nch + kWarps - 1) / kWarps);
+  (void)g;
+  launch_explode_map_impl(v, nsm, s);
 }
 void launch_rank(const EngineView& v, cudaStream_t s) {
   k_rank<<<(unsigned)v.F, 256, v.lam * sizeof(float), s>>>(v);
 }
 void launch_guides(const EngineView& v, int nsm, cudaStream_t s) {
-  const unsigned g = (unsigned)((v.F * ((v.D + 127) / 128) + kWarps - 1) / kWarps);
-  k_guides<<<g < (unsigned)nsm * 16 ? g : nsm * 16, 256, 0, s>>>(v);
+  k_guides<<<guide_blocks(v, nsm), 256, 2 * v.top * sizeof(int), s>>>(v);
   if (!v.nn) launch_analytic_partials(v.guides, v.F * v.M, v.D, v.Dp, v.nch, v.obj_kind, v.gpart, nsm, s);
 }
 void launch_select(const EngineView& v, int nsm, cudaStream_t s) {

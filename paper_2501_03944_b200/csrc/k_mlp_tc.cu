@@ -184,9 +184,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr bool kSplitSpark = H > 128;
   static_assert(BN % H == 0 && H % 32 == 0, "H must divide 256 and be a multiple of 32");
 
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned (SWIZZLE_128B atoms); no static shared memory is used,
+  // so the dynamic window starts at the aligned base.  Deriving every
+  // pointer from this array keeps the accesses in the shared state space
+  // (LDS/STS, not generic LD/ST).
+  extern __shared__ __align__(1024) uint8_t smem[];
   float* s_b1 = reinterpret_cast<float*>(smem + SmemLayout::b1);
   float* s_w2t = reinterpret_cast<float*>(smem + SmemLayout::w2t);
   float* s_b2 = reinterpret_cast<float*>(smem + SmemLayout::b2);
@@ -294,18 +296,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int idx = et; idx < SPT * H; idx += kEpiThreads) {
         const int j = idx / H, h = idx % H;
         const uint64_t p = (uint64_t)n_tile * SPT + j;
-        float b1v = 0.0f;
-        float w2v[kMaxO];
+        const bool ok = p < args.rows;
+        const __nv_bfloat16* base = args.W + (ok ? p : 0) * args.Dp + (uint64_t)H * args.I;
+        s_b1[idx] = ok ? __bfloat162float(base[h]) : 0.0f;
 #pragma unroll
-        for (int o = 0; o < kMaxO; ++o) w2v[o] = 0.0f;
-        if (p < args.rows) {
-          const __nv_bfloat16* base = args.W + p * args.Dp + (uint64_t)H * args.I;
-          b1v = __bfloat162float(base[h]);
-          for (uint32_t o = 0; o < O; ++o) w2v[o] = __bfloat162float(base[H + o * H + h]);
-        }
-        s_b1[idx] = b1v;
-#pragma unroll
-        for (int o = 0; o < kOPad; ++o) s_w2t[idx * kOPad + o] = w2v[o];
+        for (int o = 0; o < kOPad; ++o)
+          s_w2t[idx * kOPad + o] =
+              (ok && (uint32_t)o < O) ? __bfloat162float(base[H + o * H + h]) : 0.0f;
       }
       for (int idx = et; idx < SPT * kOPad; idx += kEpiThreads) {
         const int j = idx / kOPad, o = idx % kOPad;

@@ -18,6 +18,10 @@ struct GenerationHooks {
   void (*eval_fresh_all)(void* ctx, cudaStream_t s);  // initialize()
 };
 
+// One-time kernel attributes (dynamic shared memory opt-in); call before
+// the first launch / graph capture.
+cudaError_t prepare_engine_kernels();
+
 void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
                                GenerationHooks* hooks);
 void launch_initialize_kernels(const EngineView& v, int nsm, cudaStream_t s,
