@@ -385,38 +385,70 @@ static void launch_explode_map_impl(const EngineView& v, int nsm, cudaStream_t s
 // (engine.cpp:151-157): order by (fitness asc, index asc); record the top
 // `top` indices (best first) and the bottom `top` (rank order).
 // One block per firework.
+// Total-order key of (fitness asc, index asc): -0.0 == +0.0 as in the
+// reference's comparator (fi != fj is false for them), so -0 is canonicalised.
+__device__ __forceinline__ uint64_t rank_key(float x, uint32_t k) {
+  uint32_t u = __float_as_uint(x == 0.0f ? 0.0f : x);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return ((uint64_t)u << 32) | k;
+}
+
 __global__ void __launch_bounds__(256) k_rank(EngineView v) {
   if (gen_inactive(v)) return;
-  extern __shared__ float sf[];
+  extern __shared__ uint64_t keys[];  // next_pow2(lambda) sort keys
   const uint64_t f = blockIdx.x;
+  const uint32_t lam = (uint32_t)v.lam;
+  uint32_t n = 1;
+  while (n < lam) n <<= 1;
   unsigned nan_local = 0;
-  for (uint64_t k = threadIdx.x; k < v.lam; k += blockDim.x) {
-    if (v.injected_fitness) {
-      sf[k] = v.sfit[f * v.lam + k];
+  for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
+    if (k >= lam) {
+      keys[k] = ~0ull;
       continue;
     }
-    bool nan;
-    const float x = finalize_row(v, v.spart, f * v.lam + k, &nan);
-    nan_local += nan;
-    sf[k] = x;
-    v.sfit[f * v.lam + k] = x;
+    float x;
+    if (v.injected_fitness) {
+      x = v.sfit[f * lam + k];
+    } else {
+      bool nan;
+      x = finalize_row(v, v.spart, f * lam + k, &nan);
+      nan_local += nan;
+      v.sfit[f * lam + k] = x;
+    }
+    keys[k] = rank_key(x, k);
   }
   nan_local = __reduce_add_sync(0xffffffffu, nan_local);
   if ((threadIdx.x & 31) == 0 && nan_local)
     atomicAdd((unsigned long long*)&v.ctl->nan_count, (unsigned long long)nan_local);
   if (v.M == 0) return;
   __syncthreads();
-  const uint64_t lam = v.lam, top = v.top;
-  for (uint64_t k = threadIdx.x; k < lam; k += blockDim.x) {
-    const float fk = sf[k];
-    uint32_t rk = 0;
-    for (uint64_t j = 0; j < lam; ++j) {
-      const float fj = sf[j];
-      rk += (fj < fk) || (fj == fk && j < k);
+  // bitonic sort of the keys (ascending) — a total order, so the result is
+  // exactly std::sort with the reference comparator (engine.cpp:152-157)
+  for (uint32_t k = 2; k <= n; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t ixj = i ^ j;
+        if (ixj > i) {
+          const uint64_t a = keys[i], b = keys[ixj];
+          if ((a > b) == ((i & k) == 0)) {
+            keys[i] = b;
+            keys[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
     }
-    if (rk < top) v.rank_idx[f * 2 * top + rk] = (int)k;
-    if (rk >= lam - top) v.rank_idx[f * 2 * top + top + (rk - (lam - top))] = (int)k;
+  const uint32_t top = (uint32_t)v.top;
+  for (uint32_t t = threadIdx.x; t < top; t += blockDim.x) {
+    v.rank_idx[f * 2 * top + t] = (int)(uint32_t)keys[t];
+    v.rank_idx[f * 2 * top + top + t] = (int)(uint32_t)keys[lam - top + t];
   }
+}
+
+static size_t rank_smem(const EngineView& v) {
+  uint64_t n = 1;
+  while (n < v.lam) n <<= 1;
+  return n * sizeof(uint64_t);
 }
 
 // ----------------------------------------------------------------- guides
@@ -433,7 +465,7 @@ __global__ void __launch_bounds__(256) k_guides(EngineView v) {
   extern __shared__ int s_idx[];  // [2*top]: rank lists of the block's firework
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t it = v.ctl->iteration;
-  const uint64_t nsl = (v.D + 127) / 128;
+  const uint64_t nsl = (v.D + 63) / 64;  // 64-coordinate slices (float2 per lane)
   const uint64_t bpf = (nsl + kWarps - 1) / kWarps;  // blocks per firework
   const uint64_t top = v.top;
   for (uint64_t blk = blockIdx.x; blk < v.F * bpf; blk += gridDim.x) {
@@ -442,49 +474,44 @@ __global__ void __launch_bounds__(256) k_guides(EngineView v) {
     __syncthreads();
     for (uint64_t i = threadIdx.x; i < 2 * top; i += blockDim.x) s_idx[i] = v.rank_idx[f * 2 * top + i];
     __syncthreads();
-    const uint64_t d0 = c * 128 + lane * 4;
+    const uint64_t d0 = c * 64 + lane * 2;
     if (c >= nsl || d0 >= v.D) continue;
     const uint64_t b = f / v.mu, n = f % v.mu;
     const float* sb = v.sparks + f * v.lam * v.Dp + d0;
-    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+    double acc0 = 0.0, acc1 = 0.0;
     uint64_t t = 0;
-    // 16 independent 16-byte loads in flight per lane, summed in rank order
-    for (; t + 8 <= top; t += 8) {
-      float4 bb[8], ww[8];
+    // 32 independent 8-byte loads in flight per lane, summed in rank order
+    for (; t + 16 <= top; t += 16) {
+      float2 bb[16], ww[16];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        bb[i] = *reinterpret_cast<const float4*>(sb + (uint64_t)s_idx[t + i] * v.Dp);
-        ww[i] = *reinterpret_cast<const float4*>(sb + (uint64_t)s_idx[top + t + i] * v.Dp);
+      for (int i = 0; i < 16; ++i) {
+        bb[i] = *reinterpret_cast<const float2*>(sb + (uint64_t)s_idx[t + i] * v.Dp);
+        ww[i] = *reinterpret_cast<const float2*>(sb + (uint64_t)s_idx[top + t + i] * v.Dp);
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < 16; ++i) {
         acc0 = __dadd_rn(acc0, __dsub_rn((double)bb[i].x, (double)ww[i].x));
         acc1 = __dadd_rn(acc1, __dsub_rn((double)bb[i].y, (double)ww[i].y));
-        acc2 = __dadd_rn(acc2, __dsub_rn((double)bb[i].z, (double)ww[i].z));
-        acc3 = __dadd_rn(acc3, __dsub_rn((double)bb[i].w, (double)ww[i].w));
       }
     }
     for (; t < top; ++t) {
-      const float4 bt = *reinterpret_cast<const float4*>(sb + (uint64_t)s_idx[t] * v.Dp);
-      const float4 wt = *reinterpret_cast<const float4*>(sb + (uint64_t)s_idx[top + t] * v.Dp);
+      const float2 bt = *reinterpret_cast<const float2*>(sb + (uint64_t)s_idx[t] * v.Dp);
+      const float2 wt = *reinterpret_cast<const float2*>(sb + (uint64_t)s_idx[top + t] * v.Dp);
       acc0 = __dadd_rn(acc0, __dsub_rn((double)bt.x, (double)wt.x));
       acc1 = __dadd_rn(acc1, __dsub_rn((double)bt.y, (double)wt.y));
-      acc2 = __dadd_rn(acc2, __dsub_rn((double)bt.z, (double)wt.z));
-      acc3 = __dadd_rn(acc3, __dsub_rn((double)bt.w, (double)wt.w));
     }
     const double dtop = (double)top;
-    const double delta[4] = {__ddiv_rn(acc0, dtop), __ddiv_rn(acc1, dtop), __ddiv_rn(acc2, dtop),
-                             __ddiv_rn(acc3, dtop)};
-    const float4 p4 = *reinterpret_cast<const float4*>(v.pos + f * v.Dp + d0);
-    const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
+    const double delta[2] = {__ddiv_rn(acc0, dtop), __ddiv_rn(acc1, dtop)};
+    const float2 p2 = *reinterpret_cast<const float2*>(v.pos + f * v.Dp + d0);
+    const float pv[2] = {p2.x, p2.y};
     const float* plo = v.pop_lo + b * v.Dp;
     const float* phi = v.pop_hi + b * v.Dp;
     for (uint64_t m = 0; m < v.M; ++m) {
       const double beta = v.boosts[m];
       const uint64_t pg = key_prefix(v.seed, kGuide, it, b, n, m);
-      float x[4];
+      float x[2];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
+      for (int e = 0; e < 2; ++e) {
         const uint64_t d = d0 + e;
         if (d < v.D) {
           const double gx = __dadd_rn((double)pv[e], __dmul_rn(beta, delta[e]));
@@ -493,7 +520,9 @@ __global__ void __launch_bounds__(256) k_guides(EngineView v) {
           x[e] = 0.0f;
         }
       }
-      store_row4(v.guides, v.nn ? v.guides_h : nullptr, (f * v.M + m) * v.Dp + d0, x);
+      const uint64_t off = (f * v.M + m) * v.Dp + d0;
+      *reinterpret_cast<float2*>(v.guides + off) = make_float2(x[0], x[1]);
+      if (v.nn) *reinterpret_cast<__nv_bfloat162*>(v.guides_h + off) = __floats2bfloat162_rn(x[0], x[1]);
     }
   }
 }
@@ -907,7 +936,7 @@ void launch_key_hash(const uint64_t* keys, uint64_t n, uint64_t* out,
 // ---------------------------------------------------------------- launch
 
 static unsigned guide_blocks(const EngineView& v, int nsm) {
-  const uint64_t nsl = (v.D + 127) / 128;
+  const uint64_t nsl = (v.D + 63) / 64;
   const uint64_t blocks = v.F * ((nsl + kWarps - 1) / kWarps);
   return (unsigned)(blocks < (uint64_t)nsm * 8 ? blocks : (uint64_t)nsm * 8);
 }
@@ -920,7 +949,7 @@ void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
   k_pop_range<<<rng_blocks, 256, 0, s>>>(v);
   launch_explode_map_impl(v, nsm, s);
   if (v.nn) hooks->eval_sparks(hooks->ctx, s);
-  k_rank<<<(unsigned)v.F, 256, v.lam * sizeof(float), s>>>(v);
+  k_rank<<<(unsigned)v.F, 256, rank_smem(v), s>>>(v);
   if (v.M > 0) {
     k_guides<<<guide_blocks(v, nsm), 256, 2 * v.top * sizeof(int), s>>>(v);
     if (v.nn)
@@ -975,7 +1004,7 @@ void launch_explode_map(const EngineView& v, int nsm, cudaStream_t s) {
   launch_explode_map_impl(v, nsm, s);
 }
 void launch_rank(const EngineView& v, cudaStream_t s) {
-  k_rank<<<(unsigned)v.F, 256, v.lam * sizeof(float), s>>>(v);
+  k_rank<<<(unsigned)v.F, 256, rank_smem(v), s>>>(v);
 }
 void launch_guides(const EngineView& v, int nsm, cudaStream_t s) {
   k_guides<<<guide_blocks(v, nsm), 256, 2 * v.top * sizeof(int), s>>>(v);

@@ -1,29 +1,37 @@
-// k_mlp_tc.cu — population-batched MLP-weights fitness on the 5th-gen
-// tensor cores (tcgen05.mma kind::f16, bf16 x bf16 -> fp32 in TMEM, operands
-// staged by TMA with the 128-byte swizzle).
+// k_mlp_tc.cu — population-batched MLP-weights fitness entirely on the
+// 5th-gen tensor cores (tcgen05.mma kind::f16, bf16 x bf16 -> fp32 in TMEM).
 //
 // Objective (builder-defined, pattern nets.cpp:138-167): candidate w holds
 // W1[H][I], b1[H], W2[O][H], b2[O] (reference Layer order, nets.hpp:60-65);
 // f(w) = mean_s CE(softmax(W2 relu(W1 x_s + b1) + b2), y_s) over S samples.
 //
-// GEMM view of layer 1 for the whole population:
-//   D[s][(p,h)] = sum_i X[s][i] * W1_p[h][i]
-//   M = samples (tile 128 = TMEM lanes), N = (spark, hidden) (tile 256 =
-//   256/H sparks), K = I (784 = 12 x 64 + 16).  Both operands are K-major,
-//   which is exactly the reference weight layout (weights[out x in]).
+// Layer 1 for the whole population is one GEMM:
+//   D1[s][(p,h)] = sum_i X[s][i] * W1_p[h][i]
+//   M = samples (128-row tiles = TMEM lanes), N = (spark, hidden) (256 =
+//   256/H sparks), K = I (784 = 12 x 64 + 16).  Both operands are K-major —
+//   exactly the reference weight layout — and are staged by TMA with the
+//   128-byte swizzle; W1 is read straight out of the bf16 spark matrix
+//   through a 3-D tensor map (i, h, spark): no repacking pass.
+// Layer 2 also runs on the tensor cores: the epilogue turns each fp32 D1
+//   column block into bf16 ReLU(D1 + b1) and writes it back into the SAME
+//   TMEM columns (tcgen05.st), then one tcgen05.mma per spark with the A
+//   operand read from TMEM (M = 128 samples, N = 16 >= O outputs, K = H) and
+//   W2^T staged in shared memory produces the logits next to it.  The CUDA
+//   cores only do +b1/ReLU/pack and the log-softmax CE.
 // Persistent, warp-specialised, one CTA per SM:
-//   warp 0      TMA producer (X tile 128x64 + W tile 256x64 per stage, 4 stages)
-//   warp 1      MMA issuer (one thread; 4 x tcgen05.mma 128x256x16 per stage)
-//   warp 2      TMEM allocator (512 columns = 2 accumulator buffers)
-//   warps 4-11  epilogue: tcgen05.ld -> +b1, ReLU -> layer 2 (CUDA cores) ->
-//               log-softmax CE -> per-(spark, m-tile) partial loss.
-// Double-buffered TMEM lets the epilogue of tile t overlap the MMAs of t+1.
+//   warp 0      TMA producer (X 128x64 + W1 256x64 per stage, 4 stages)
+//   warp 1      MMA issuer (one thread): layer-1 k-steps of tile t, with the
+//               layer-2 MMAs of tile t-1 slotted in as soon as its
+//               activations are in TMEM (non-blocking barrier probe)
+//   warp 2      TMEM allocator (512 columns = 2 tile buffers)
+//   warps 4-11  epilogue
 // Output: part[p][m_tile][0] = sum of CE over the m-tile's samples (the
 // deterministic finalize divides by S).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "common.cuh"
@@ -33,9 +41,9 @@ namespace mgfwa_b200 {
 
 namespace {
 
-constexpr int BM = 128;
-constexpr int BN = 256;
-constexpr int BK = 64;
+constexpr int BM = 128;  // samples per tile (TMEM lanes)
+constexpr int BN = 256;  // (spark, hidden) columns per tile
+constexpr int BK = 64;   // K per pipeline stage (one 128-byte swizzle atom)
 constexpr int kStages = 4;
 constexpr int kABytes = BM * BK * 2;  // 16 KB
 constexpr int kBBytes = BN * BK * 2;  // 32 KB
@@ -43,22 +51,20 @@ constexpr int kStageBytes = kABytes + kBBytes;
 constexpr int kThreads = 384;
 constexpr int kEpiWarps = 8;
 constexpr int kEpiThreads = kEpiWarps * 32;
-constexpr int kOPad = 12;  // logits padded to 3 x float4
-constexpr int kMaxO = 12;
+constexpr int kN2 = 16;  // layer-2 MMA N (outputs padded to 16)
+constexpr int kMaxO = 10;
 
 struct SmemLayout {
-  static constexpr int stages = 0;
-  static constexpr int b1 = kStages * kStageBytes;           // float[BN]
-  static constexpr int w2t = b1 + BN * 4;                    // float[BN][kOPad]
-  static constexpr int b2 = w2t + BN * kOPad * 4;            // float[8][kOPad]
-  static constexpr int zsh = b2 + 8 * kOPad * 4;             // float[BM][kOPad] (H > 128)
-  static constexpr int red = zsh + BM * kOPad * 4;           // float[kEpiWarps][8]
-  static constexpr int bars = red + kEpiWarps * 8 * 4;       // u64 barriers
-  static constexpr int nbars = 2 * kStages + 4;
+  static constexpr int w2 = kStages * kStageBytes;       // bf16 W2^T, [spark][16][H] interleaved
+  static constexpr int b1 = w2 + kN2 * BN * 2;           // float[BN]
+  static constexpr int b2 = b1 + BN * 4;                 // float[8][kN2]
+  static constexpr int red = b2 + 8 * kN2 * 4;           // float[kEpiWarps][8]
+  static constexpr int bars = red + kEpiWarps * 8 * 4;   // u64 barriers
+  static constexpr int nbars = 2 * kStages + 8;
   static constexpr int tmem_slot = bars + nbars * 8;
   static constexpr int total = tmem_slot + 16;
 };
-constexpr int kSmemBytes = SmemLayout::total + 1024;  // + alignment slack
+constexpr int kSmemBytes = SmemLayout::total;
 
 struct MlpArgs {
   uint32_t S, I, H, O;
@@ -98,6 +104,19 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
+// Non-blocking probe: has the phase with the given parity completed?
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
                                             int x, int y) {
   asm volatile(
@@ -127,19 +146,41 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return d;
 }
 
+// K-major operand without swizzle: 8-row x 16-byte core matrices; LBO =
+// byte stride between core matrices along K, SBO = along M/N.
+__device__ __forceinline__ uint64_t interleaved_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1u << 46;  // version; layout type 0 = SWIZZLE_NONE
+  return d;
+}
+
 // kind::f16 instruction descriptor: D=f32, A=B=bf16, both K-major.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
          ((uint32_t)(M >> 4) << 24);
 }
 
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
-                                         uint32_t accumulate) {
+// D[tmem] (+)= A[smem] . B[smem]
+__device__ __forceinline__ void mma_ss(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                       uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+// D[tmem] (+)= A[tmem] . B[smem]
+__device__ __forceinline__ void mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
@@ -174,6 +215,52 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&r)[16]) {
+  uint32_t* u = reinterpret_cast<uint32_t*>(r);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]),
+        "=r"(u[7]), "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]),
+        "=r"(u[14]), "=r"(u[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&u)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(u[0]), "r"(u[1]), "r"(u[2]), "r"(u[3]), "r"(u[4]), "r"(u[5]), "r"(u[6]), "r"(u[7]),
+      "r"(u[8]), "r"(u[9]), "r"(u[10]), "r"(u[11]), "r"(u[12]), "r"(u[13]), "r"(u[14]),
+      "r"(u[15])
+      : "memory");
+}
+
+// ----------------------------------------------------- TMEM column plan
+// Tile buffer (256 columns).  Spark j of the tile owns D1 columns
+// [j*H, (j+1)*H).  After the epilogue has read them, its bf16 activations
+// (H values = H/2 columns) and its 16 logit columns are placed inside that
+// same range, so no column is written before its owner warp has read it:
+//   H <= 128: A2 at [jH, jH + H/2), D2 at [jH + H/2, jH + H/2 + 16)
+//   H == 256: A2 halves at [0, 64) and [128, 192) (one per column half),
+//             D2 at [64, 80)
+template <int H>
+__device__ __forceinline__ uint32_t a2_col(int n0) {  // packed column of D1 column n0
+  if (H <= 128) return (uint32_t)((n0 / H) * H + (n0 % H) / 2);
+  return (uint32_t)((n0 / 128) * 128 + (n0 % 128) / 2);
+}
+template <int H>
+__device__ __forceinline__ uint32_t a2_kcol(int j, int kk) {  // A column of K16 step kk
+  if (H <= 128) return (uint32_t)(j * H + kk * 8);
+  return (uint32_t)((kk < 8 ? 0 : 128) + (kk & 7) * 8);
+}
+template <int H>
+__device__ __forceinline__ uint32_t d2_col(int j) {
+  if (H <= 128) return (uint32_t)(j * H + H / 2);
+  return 64u;
+}
+
 // ------------------------------------------------------------------ kernel
 template <int H>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -181,18 +268,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const __grid_constant__ CUtensorMap tmap_w, MlpArgs args) {
   if (args.gate != nullptr && *args.gate == 0) return;
   constexpr int SPT = BN / H;  // sparks per N tile (1 when H == 256)
-  constexpr bool kSplitSpark = H > 128;
   static_assert(BN % H == 0 && H % 32 == 0, "H must divide 256 and be a multiple of 32");
 
   // 1024-byte aligned (SWIZZLE_128B atoms); no static shared memory is used,
-  // so the dynamic window starts at the aligned base.  Deriving every
-  // pointer from this array keeps the accesses in the shared state space
-  // (LDS/STS, not generic LD/ST).
+  // so the dynamic window starts at the aligned base.
   extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* s_w2 = smem + SmemLayout::w2;
   float* s_b1 = reinterpret_cast<float*>(smem + SmemLayout::b1);
-  float* s_w2t = reinterpret_cast<float*>(smem + SmemLayout::w2t);
   float* s_b2 = reinterpret_cast<float*>(smem + SmemLayout::b2);
-  float* s_z = reinterpret_cast<float*>(smem + SmemLayout::zsh);
   float* s_red = reinterpret_cast<float*>(smem + SmemLayout::red);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemLayout::bars);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SmemLayout::tmem_slot);
@@ -201,8 +284,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x & 31;
   const uint32_t bar_full = smem_u32(bars);
   const uint32_t bar_empty = smem_u32(bars + kStages);
-  const uint32_t bar_tfull = smem_u32(bars + 2 * kStages);
-  const uint32_t bar_tempty = smem_u32(bars + 2 * kStages + 2);
+  const uint32_t bar_tfull = smem_u32(bars + 2 * kStages);       // D1 ready
+  const uint32_t bar_tempty = smem_u32(bars + 2 * kStages + 2);  // buffer free
+  const uint32_t bar_a2full = smem_u32(bars + 2 * kStages + 4);  // activations in TMEM
+  const uint32_t bar_d2full = smem_u32(bars + 2 * kStages + 6);  // logits ready
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
@@ -212,6 +297,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar_tfull + 8 * i, 1);
       mbar_init(bar_tempty + 8 * i, kEpiWarps);
+      mbar_init(bar_a2full + 8 * i, kEpiWarps);
+      mbar_init(bar_d2full + 8 * i, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x)));
@@ -227,9 +314,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // static contiguous tile range per CTA: tile t -> (n_tile = t / m_tiles,
+  // Static contiguous tile range per CTA: tile t -> (n_tile = t / m_tiles,
   // m_tile = t % m_tiles), so one CTA walks all m-tiles of an N tile in turn
-  // (its W tile stays hot in L2; X is L2-resident for everyone).
+  // (its W1 tile stays hot in L2; X is L2-resident for everyone).
   const uint32_t total = args.m_tiles * args.n_tiles;
   const uint32_t t_begin = (uint32_t)(((uint64_t)total * blockIdx.x) / gridDim.x);
   const uint32_t t_end = (uint32_t)(((uint64_t)total * (blockIdx.x + 1)) / gridDim.x);
@@ -243,10 +330,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (uint32_t kb = 0; kb < args.k_blocks; ++kb) {
           mbar_wait(bar_empty + 8 * stage, phase ^ 1);
           const uint32_t sa = smem_u32(smem + stage * kStageBytes);
-          const uint32_t sb = sa + kABytes;
           mbar_expect_tx(bar_full + 8 * stage, kStageBytes);
           tma_load_2d(sa, &tmap_x, bar_full + 8 * stage, (int)(kb * BK), m_tile * BM);
-          tma_load_3d(sb, &tmap_w, bar_full + 8 * stage, (int)(kb * BK), 0, n_tile * SPT);
+          tma_load_3d(sa + kABytes, &tmap_w, bar_full + 8 * stage, (int)(kb * BK), 0, n_tile * SPT);
           if (++stage == kStages) stage = 0, phase ^= 1;
         }
       }
@@ -255,9 +341,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer
-      constexpr uint32_t idesc = idesc_bf16(BM, BN);
-      uint32_t stage = 0, phase = 0;
-      uint32_t i = 0;
+      constexpr uint32_t idesc1 = idesc_bf16(BM, BN);
+      constexpr uint32_t idesc2 = idesc_bf16(BM, kN2);
+      const uint32_t w2_base = smem_u32(s_w2);
+      // layer-2 MMAs of the tile whose activations sit in buffer `b`
+      auto issue_layer2 = [&](uint32_t b) {
+        tc_fence_after();
+        const uint32_t cb = tmem_base + b * BN;
+#pragma unroll
+        for (int j = 0; j < SPT; ++j) {
+          const uint32_t bj = w2_base + (uint32_t)(j * kN2 * H * 2);
+#pragma unroll
+          for (int kk = 0; kk < H / 16; ++kk)
+            mma_ts(cb + d2_col<H>(j), cb + a2_kcol<H>(j, kk),
+                   interleaved_desc(bj + kk * 512, 256, 128), idesc2, kk != 0);
+        }
+        mma_commit(bar_d2full + 8 * b);
+      };
+      uint32_t stage = 0, phase = 0, i = 0;
+      bool pend = false;
+      uint32_t pbuf = 0, puse = 0;
       for (uint32_t t = t_begin; t < t_end; ++t, ++i) {
         const uint32_t buf = i & 1, use = (i >> 1) & 1;
         mbar_wait(bar_tempty + 8 * buf, use ^ 1);
@@ -271,11 +374,26 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t rem = args.I - kb * BK;
           const uint32_t nk = rem >= BK ? BK / 16 : (rem + 15) / 16;
           for (uint32_t kk = 0; kk < nk; ++kk)
-            mma_bf16(d_tmem, da + 2 * kk, db + 2 * kk, idesc, (kb | kk) != 0);
+            mma_ss(d_tmem, da + 2 * kk, db + 2 * kk, idesc1, (kb | kk) != 0);
           mma_commit(bar_empty + 8 * stage);
           if (++stage == kStages) stage = 0, phase ^= 1;
+          if (pend && mbar_test(bar_a2full + 8 * pbuf, puse)) {
+            issue_layer2(pbuf);
+            pend = false;
+          }
         }
         mma_commit(bar_tfull + 8 * buf);
+        if (pend) {
+          mbar_wait(bar_a2full + 8 * pbuf, puse);
+          issue_layer2(pbuf);
+        }
+        pend = true;
+        pbuf = buf;
+        puse = use;
+      }
+      if (pend) {
+        mbar_wait(bar_a2full + 8 * pbuf, puse);
+        issue_layer2(pbuf);
       }
     }
     __syncwarp();
@@ -283,138 +401,118 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- epilogue
     const int e = warp - 4;            // 0..7
     const int q = warp & 3;            // TMEM lane quarter (warp % 4)
-    const int half = e >> 2;           // column half: [half*128, half*128+128)
+    const int half = e >> 2;           // D1 column half: [half*128, half*128+128)
     const int row = q * 32 + lane;     // accumulator row == sample within tile
     const int et = threadIdx.x - 128;  // 0..255
     const uint32_t O = args.O;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     uint32_t i = 0;
+    uint32_t staged_n = 0xFFFFFFFFu;
     for (uint32_t t = t_begin; t < t_end; ++t, ++i) {
       const uint32_t m_tile = t % args.m_tiles, n_tile = t / args.m_tiles;
       const uint32_t buf = i & 1, use = (i >> 1) & 1;
-      // stage this tile's per-spark b1 / W2^T / b2 (fp32) in shared memory
+      const uint32_t cb = tmem_base + buf * BN + lane_off;
+      const uint32_t s = m_tile * BM + row;
+      const bool valid = s < args.S;
+      const int label = valid ? args.y[s] : 0;
+      // Stage b1 (fp32), b2 (fp32) and W2^T (bf16, interleaved core-matrix
+      // layout: element (o, h) of spark j at j*16*H*2 + ((h/8)*2 + o/8)*128
+      // + (o%8)*16 + (h%8)*2) when the N tile changes (every m_tiles tiles).
+      // The previous tile's layer-2 MMAs finished before this warp group
+      // passed its logits barrier, and the barrier below orders s_red.
       epi_bar();
+      if (n_tile != staged_n) {
+      staged_n = n_tile;
       for (int idx = et; idx < SPT * H; idx += kEpiThreads) {
         const int j = idx / H, h = idx % H;
         const uint64_t p = (uint64_t)n_tile * SPT + j;
         const bool ok = p < args.rows;
         const __nv_bfloat16* base = args.W + (ok ? p : 0) * args.Dp + (uint64_t)H * args.I;
         s_b1[idx] = ok ? __bfloat162float(base[h]) : 0.0f;
+        __nv_bfloat16* w2j = reinterpret_cast<__nv_bfloat16*>(s_w2 + j * kN2 * H * 2);
 #pragma unroll
-        for (int o = 0; o < kOPad; ++o)
-          s_w2t[idx * kOPad + o] =
-              (ok && (uint32_t)o < O) ? __bfloat162float(base[H + o * H + h]) : 0.0f;
+        for (int o = 0; o < kN2; ++o) {
+          const __nv_bfloat16 wv =
+              (ok && (uint32_t)o < O) ? base[H + o * H + h] : __float2bfloat16_rn(0.0f);
+          w2j[(((h >> 3) * 2 + (o >> 3)) * 128 + (o & 7) * 16 + (h & 7) * 2) / 2] = wv;
+        }
       }
-      for (int idx = et; idx < SPT * kOPad; idx += kEpiThreads) {
-        const int j = idx / kOPad, o = idx % kOPad;
+      for (int idx = et; idx < SPT * kN2; idx += kEpiThreads) {
+        const int j = idx / kN2, o = idx % kN2;
         const uint64_t p = (uint64_t)n_tile * SPT + j;
         float v = 0.0f;
         if (p < args.rows && (uint32_t)o < O)
           v = __bfloat162float(args.W[p * args.Dp + (uint64_t)H * args.I + H + (uint64_t)O * H + o]);
         s_b2[idx] = v;
       }
-      const uint32_t s = m_tile * BM + row;
-      const bool valid = s < args.S;
-      const int label = valid ? args.y[s] : 0;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // W2 visible to the MMA
       epi_bar();
+      }
 
+      // ---- layer-1 epilogue: bf16(ReLU(D1 + b1)) back into TMEM
       mbar_wait(bar_tfull + 8 * buf, use);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + buf * BN + ((uint32_t)(q * 32) << 16);
-      float z[kOPad];
-#pragma unroll
-      for (int o = 0; o < kOPad; ++o) z[o] = 0.0f;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         const int col0 = half * 128 + c * 32;
         float acc[32];
-        tmem_ld32(taddr + col0, acc);
+        tmem_ld32(cb + col0, acc);
+        uint32_t pk[16];
 #pragma unroll
-        for (int u = 0; u < 32; ++u) {
-          const int n = col0 + u;
-          const float hv = fmaxf(acc[u] + s_b1[n], 0.0f);
-          const float4* w = reinterpret_cast<const float4*>(s_w2t + n * kOPad);
-          const float4 w0 = w[0], w1 = w[1], w2 = w[2];
-          z[0] = fmaf(w0.x, hv, z[0]);
-          z[1] = fmaf(w0.y, hv, z[1]);
-          z[2] = fmaf(w0.z, hv, z[2]);
-          z[3] = fmaf(w0.w, hv, z[3]);
-          z[4] = fmaf(w1.x, hv, z[4]);
-          z[5] = fmaf(w1.y, hv, z[5]);
-          z[6] = fmaf(w1.z, hv, z[6]);
-          z[7] = fmaf(w1.w, hv, z[7]);
-          z[8] = fmaf(w2.x, hv, z[8]);
-          z[9] = fmaf(w2.y, hv, z[9]);
-          z[10] = fmaf(w2.z, hv, z[10]);
-          z[11] = fmaf(w2.w, hv, z[11]);
+        for (int u = 0; u < 16; ++u) {
+          const float h0 = fmaxf(acc[2 * u] + s_b1[col0 + 2 * u], 0.0f);
+          const float h1 = fmaxf(acc[2 * u + 1] + s_b1[col0 + 2 * u + 1], 0.0f);
+          __nv_bfloat162 v2 = __floats2bfloat162_rn(h0, h1);
+          pk[u] = *reinterpret_cast<uint32_t*>(&v2);
         }
-        if (!kSplitSpark && ((col0 + 32) % H) == 0) {
-          const int j = col0 / H;  // spark within tile
-          float loss = 0.0f;
-          if (valid) {
-            float zz[kOPad];
-            float mx = -INFINITY;
-#pragma unroll
-            for (int o = 0; o < kOPad; ++o) {
-              zz[o] = z[o] + s_b2[j * kOPad + o];
-              if ((uint32_t)o < O) mx = fmaxf(mx, zz[o]);
-            }
-            float se = 0.0f, zl = 0.0f;
-#pragma unroll
-            for (int o = 0; o < kOPad; ++o) {
-              if ((uint32_t)o < O) se += expf(zz[o] - mx);
-              if (o == label) zl = zz[o];
-            }
-            loss = (mx + logf(se)) - zl;
-          }
-          loss = warp_sum(loss);
-          if (lane == 0) s_red[e * 8 + (j - half * (SPT / 2))] = loss;
-#pragma unroll
-          for (int o = 0; o < kOPad; ++o) z[o] = 0.0f;
-        }
+        tmem_st16(cb + a2_col<H>(col0), pk);
       }
-      // accumulator buffer consumed: hand it back to the MMA warp
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_a2full + 8 * buf);
+
+      // ---- logits (layer-2 MMA result) -> log-softmax CE
+      mbar_wait(bar_d2full + 8 * buf, use);
+      tc_fence_after();
+      const int jb = H > 128 ? 0 : half * (SPT / 2);
+      const int jn = H > 128 ? (half == 0 ? 1 : 0) : SPT / 2;
+      for (int jj = 0; jj < jn; ++jj) {
+        const int j = jb + jj;
+        float z[kN2];
+        tmem_ld16(cb + d2_col<H>(j), z);
+        float loss = 0.0f;
+        if (valid) {
+          float mx = -INFINITY;
+#pragma unroll
+          for (int o = 0; o < kN2; ++o) {
+            z[o] += s_b2[j * kN2 + o];
+            if ((uint32_t)o < O) mx = fmaxf(mx, z[o]);
+          }
+          float se = 0.0f, zl = 0.0f;
+#pragma unroll
+          for (int o = 0; o < kN2; ++o) {
+            if ((uint32_t)o < O) se += expf(z[o] - mx);
+            if (o == label) zl = z[o];
+          }
+          loss = (mx + logf(se)) - zl;
+        }
+        loss = warp_sum(loss);
+        if (lane == 0) s_red[e * 8 + jj] = loss;
+      }
+      // tile buffer consumed: hand it back to the MMA warp
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
-
-      if (kSplitSpark) {
-        // H > 128: half 0 holds the partial logits of hidden [0,128)
-        if (half == 0) {
-#pragma unroll
-          for (int o = 0; o < kOPad; ++o) s_z[row * kOPad + o] = z[o];
-        }
-        epi_bar();
-        if (half == 1) {
-          float loss = 0.0f;
-          if (valid) {
-            float zz[kOPad];
-            float mx = -INFINITY;
-#pragma unroll
-            for (int o = 0; o < kOPad; ++o) {
-              zz[o] = z[o] + s_z[row * kOPad + o] + s_b2[o];
-              if ((uint32_t)o < O) mx = fmaxf(mx, zz[o]);
-            }
-            float se = 0.0f, zl = 0.0f;
-#pragma unroll
-            for (int o = 0; o < kOPad; ++o) {
-              if ((uint32_t)o < O) se += expf(zz[o] - mx);
-              if (o == label) zl = zz[o];
-            }
-            loss = (mx + logf(se)) - zl;
-          }
-          loss = warp_sum(loss);
-          if (lane == 0) s_red[e * 8] = loss;
-        }
-      }
       epi_bar();
-      // deterministic per-(spark, m-tile) partial: sum of the 4 lane quarters
+      // deterministic per-(spark, m-tile) partial: the 4 lane quarters in order
       if (et < SPT) {
         const int j = et;
-        const int h = kSplitSpark ? 1 : (j * H) / 128;
-        const int jl = kSplitSpark ? 0 : j - h * (SPT / 2);
+        const int hh = H > 128 ? 0 : (j * H) / 128;
+        const int jl = H > 128 ? 0 : j - hh * (SPT / 2);
         float sum = 0.0f;
 #pragma unroll
-        for (int qq = 0; qq < 4; ++qq) sum += s_red[(h * 4 + qq) * 8 + jl];
+        for (int qq = 0; qq < 4; ++qq) sum += s_red[(hh * 4 + qq) * 8 + jl];
         const uint64_t p = (uint64_t)n_tile * SPT + j;
         if (p < args.rows) {
           args.part[(p * args.m_tiles + m_tile) * 2] = sum;
@@ -450,10 +548,20 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-}  // namespace
+template <int H>
+cudaError_t prepare_h() {
+  return cudaFuncSetAttribute(k_mlp_fitness<H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kSmemBytes);
+}
 
 template <int H>
-static cudaError_t prepare_h();
+cudaError_t launch_h(const CUtensorMap& tx, const CUtensorMap& tw, int grid, const MlpArgs& a,
+                     cudaStream_t s) {
+  k_mlp_fitness<H><<<grid, kThreads, kSmemBytes, s>>>(tx, tw, a);
+  return cudaGetLastError();
+}
+
+}  // namespace
 
 struct MlpPlan {
   CUtensorMap tmap_x;
@@ -474,7 +582,7 @@ MlpPlan* mlp_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t S, u
   };
   if (H != 32 && H != 64 && H != 128 && H != 256)
     return fail("MLP fitness: hidden width must be 32, 64, 128 or 256");
-  if (O < 2 || O > (uint32_t)kMaxO - 2) return fail("MLP fitness: out_dim must be in [2, 10]");
+  if (O < 2 || O > (uint32_t)kMaxO) return fail("MLP fitness: out_dim must be in [2, 10]");
   if (I % 16 != 0 || I < 16) return fail("MLP fitness: in_dim must be a multiple of 16");
   if ((Dp * 2) % 16 != 0) return fail("MLP fitness: row stride must be 16-byte aligned");
   EncodeTiledFn enc = get_encode_fn();
@@ -521,10 +629,10 @@ MlpPlan* mlp_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t S, u
   p->args.y = y;
   const uint32_t tiles = p->args.m_tiles * p->args.n_tiles;
   p->grid = (int)(tiles < (uint32_t)nsm ? tiles : (uint32_t)nsm);
-  cudaError_t e = H == 32    ? prepare_h<32>()
-                  : H == 64  ? prepare_h<64>()
-                  : H == 128 ? prepare_h<128>()
-                             : prepare_h<256>();
+  const cudaError_t e = H == 32    ? prepare_h<32>()
+                        : H == 64  ? prepare_h<64>()
+                        : H == 128 ? prepare_h<128>()
+                                   : prepare_h<256>();
   if (e != cudaSuccess) {
     delete p;
     return fail(cudaGetErrorString(e));
@@ -534,27 +642,15 @@ MlpPlan* mlp_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t S, u
 
 void mlp_plan_destroy(MlpPlan* p) { delete p; }
 
-template <int H>
-static cudaError_t launch_h(const MlpPlan* p, const MlpArgs& a, cudaStream_t s) {
-  k_mlp_fitness<H><<<p->grid, kThreads, kSmemBytes, s>>>(p->tmap_x, p->tmap_w, a);
-  return cudaGetLastError();
-}
-
-template <int H>
-static cudaError_t prepare_h() {
-  return cudaFuncSetAttribute(k_mlp_fitness<H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              kSmemBytes);
-}
-
 cudaError_t mlp_fitness_launch(const MlpPlan* p, float* part, const int* gate, cudaStream_t s) {
   MlpArgs a = p->args;
   a.part = part;
   a.gate = gate;
   switch (p->H) {
-    case 32: return launch_h<32>(p, a, s);
-    case 64: return launch_h<64>(p, a, s);
-    case 128: return launch_h<128>(p, a, s);
-    case 256: return launch_h<256>(p, a, s);
+    case 32: return launch_h<32>(p->tmap_x, p->tmap_w, p->grid, a, s);
+    case 64: return launch_h<64>(p->tmap_x, p->tmap_w, p->grid, a, s);
+    case 128: return launch_h<128>(p->tmap_x, p->tmap_w, p->grid, a, s);
+    case 256: return launch_h<256>(p->tmap_x, p->tmap_w, p->grid, a, s);
   }
   return cudaErrorInvalidValue;
 }
