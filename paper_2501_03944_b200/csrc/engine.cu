@@ -16,6 +16,7 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -212,9 +213,52 @@ struct Workspace {
     if (arena) cudaFree(arena);
   }
 
+  // Everything that sizes device memory or the dataset; workspaces with an
+  // equal key are reused across runs (see WorkspaceCache).
+  std::vector<uint64_t> key;
+
+  static std::vector<uint64_t> make_key(const HostConfig& c, const mgfwa_space_t* space,
+                                        const mgfwa_objective_t* obj, int dev, uint64_t trace_cap) {
+    return {c.B, c.mu, c.lam, c.M, c.M > 0 ? c.top() : 0, space->dim, (uint64_t)obj->kind,
+            obj->in_dim, obj->hidden, obj->out_dim, obj->samples,
+            obj->kind == MGFWA_OBJ_MLP_WEIGHTS ? obj->data_seed : 0, (uint64_t)dev, trace_cap};
+  }
+
+  // Run-specific scalars and the search box (cheap; H2D of 2 x D bounds).
+  Status configure(const HostConfig& c, const mgfwa_space_t* space, uint64_t seed) {
+    const uint64_t D = space->dim;
+    v.seed = seed;
+    v.amp_amplify = c.amp_amplify;
+    v.amp_reduce = c.amp_reduce;
+    double max_range = 0.0;
+    for (uint64_t d = 0; d < D; ++d) max_range = std::max(max_range, space->upper[d] - space->lower[d]);
+    v.max_range = max_range;
+    v.amp_floor = 1e-12 * max_range;
+    v.a0 = c.a0 > 0.0 ? c.a0 : 0.5 * max_range;
+    v.max_evals = c.max_evals;
+    v.wall_budget_ms = c.wall_ms;
+    v.wave = c.wave();
+    v.injected_fitness = 0;
+    v.has_iters_override = 0;
+    std::vector<float> lf(D), uf(D);
+    for (uint64_t d = 0; d < D; ++d) {
+      lf[d] = f32_ceil_of(space->lower[d]);
+      uf[d] = f32_floor_of(space->upper[d]);
+    }
+    CUDA_TRY(cudaSetDevice(device));
+    CUDA_TRY(cudaMemcpy(const_cast<double*>(v.lower), space->lower, D * 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(const_cast<double*>(v.upper), space->upper, D * 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(const_cast<float*>(v.lower_f), lf.data(), D * 4, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(const_cast<float*>(v.upper_f), uf.data(), D * 4, cudaMemcpyHostToDevice));
+    if (v.M > 0)
+      CUDA_TRY(cudaMemcpy(const_cast<double*>(v.boosts), c.boosts.data(), v.M * 8, cudaMemcpyHostToDevice));
+    return ok();
+  }
+
   Status build(const HostConfig& c, const mgfwa_space_t* space, const mgfwa_objective_t* obj,
                uint64_t seed, int dev, uint64_t trace_cap) {
     device = dev;
+    key = make_key(c, space, obj, dev, trace_cap);
     CUDA_TRY(cudaSetDevice(dev));
     CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     CUDA_TRY(prepare_engine_kernels());
@@ -232,17 +276,6 @@ struct Workspace {
     v.nn = obj->kind == MGFWA_OBJ_MLP_WEIGHTS;
     v.samples = v.nn ? obj->samples : 0;
     v.nparts = v.nn ? mlp_num_parts(obj->samples) : v.nch;
-    v.seed = seed;
-    v.amp_amplify = c.amp_amplify;
-    v.amp_reduce = c.amp_reduce;
-    double max_range = 0.0;
-    for (uint64_t d = 0; d < D; ++d) max_range = std::max(max_range, space->upper[d] - space->lower[d]);
-    v.max_range = max_range;
-    v.amp_floor = 1e-12 * max_range;
-    v.a0 = c.a0 > 0.0 ? c.a0 : 0.5 * max_range;
-    v.max_evals = c.max_evals;
-    v.wall_budget_ms = c.wall_ms;
-    v.wave = c.wave();
     v.trace_cap = trace_cap;
 
     // ---- arena layout
@@ -312,17 +345,7 @@ struct Workspace {
     v.lower_f = lower_f;
     v.upper_f = upper_f;
     v.boosts = boosts;
-
-    std::vector<float> lf(D), uf(D);
-    for (uint64_t d = 0; d < D; ++d) {
-      lf[d] = f32_ceil_of(space->lower[d]);
-      uf[d] = f32_floor_of(space->upper[d]);
-    }
-    CUDA_TRY(cudaMemcpy(lower, space->lower, D * 8, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(upper, space->upper, D * 8, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(lower_f, lf.data(), D * 4, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(upper_f, uf.data(), D * 4, cudaMemcpyHostToDevice));
-    if (v.M > 0) CUDA_TRY(cudaMemcpy(boosts, c.boosts.data(), v.M * 8, cudaMemcpyHostToDevice));
+    STATUS_TRY(configure(c, space, seed));
 
     if (v.nn) {
       std::vector<__nv_bfloat16> Xh;
@@ -344,6 +367,41 @@ struct Workspace {
       if (!plan_fresh) return invalid(err);
     }
     return ok();
+  }
+};
+
+// One-entry workspace cache: the device arena, the synthetic dataset and the
+// TMA plans of the last destroyed context are kept and handed to the next
+// context with the same shape key (the cuFFT-plan / caching-allocator
+// pattern), so a repeated run() pays only configure() + initialize().
+class WorkspaceCache {
+ public:
+  static std::unique_ptr<Workspace> take(const std::vector<uint64_t>& key) {
+    std::lock_guard<std::mutex> g(mu());
+    auto& c = slot();
+    if (c && c->key == key) return std::move(c);
+    return nullptr;
+  }
+  static void give(std::unique_ptr<Workspace> w) {
+    if (!w) return;
+    std::lock_guard<std::mutex> g(mu());
+    slot() = std::move(w);  // frees the previous entry
+  }
+  static void clear() {
+    std::lock_guard<std::mutex> g(mu());
+    slot().reset();
+  }
+
+ private:
+  static std::mutex& mu() {
+    static std::mutex m;
+    return m;
+  }
+  static std::unique_ptr<Workspace>& slot() {
+    // intentionally never destroyed: freeing device memory from a static
+    // destructor can run after the CUDA runtime has been torn down
+    static auto* s = new std::unique_ptr<Workspace>();
+    return *s;
   }
 };
 
@@ -388,8 +446,10 @@ class Engine {
 
   ~Engine() {
     if (gen_exec) cudaGraphExecDestroy(gen_exec);
+    if (stream) cudaStreamSynchronize(stream);
     if (own_stream) cudaStreamDestroy(own_stream);
     if (host_ctl) cudaFreeHost(host_ctl);
+    WorkspaceCache::give(std::move(ws));
   }
 
   Status create(const mgfwa_config_t* c, const mgfwa_space_t* space, const mgfwa_objective_t* obj,
@@ -402,8 +462,13 @@ class Engine {
     // engine.cpp:319-323
     if (cfg.max_evals > 0 && cfg.max_evals < cfg.B * cfg.mu)
       return invalid("budget too small: needs at least B * mu evaluations");
-    ws = std::make_unique<Workspace>();
-    STATUS_TRY(ws->build(cfg, space, obj, seed, device, 1024));
+    ws = WorkspaceCache::take(Workspace::make_key(cfg, space, obj, device, 1024));
+    if (ws) {
+      STATUS_TRY(ws->configure(cfg, space, seed));
+    } else {
+      ws = std::make_unique<Workspace>();
+      STATUS_TRY(ws->build(cfg, space, obj, seed, device, 1024));
+    }
     CUDA_TRY(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
     stream = own_stream;
     CUDA_TRY(cudaMallocHost(&host_ctl, sizeof(Ctl)));

@@ -36,25 +36,46 @@ __device__ __forceinline__ bool gen_inactive(const EngineView& v) {
 }
 
 // Partial sums of one row -> fitness (fp32), NaN -> +inf (backend.cpp:15-24).
+// Warp-cooperative with a fixed order (lane-strided sums, butterfly, lane 0's
+// value broadcast), used by every caller, so a candidate's cached fitness and
+// its re-evaluation are bit-identical.  All 32 lanes must call it.
+// R rows at once (their loads in flight together); rows[r] < 0 are skipped.
+template <int R>
+__device__ __forceinline__ void finalize_rows(const EngineView& v, const float* part,
+                                              const int64_t (&rows)[R], float (&out)[R],
+                                              unsigned& nan_count) {
+  const int lane = threadIdx.x & 31;
+  float s0[R], s1[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    s0[r] = s1[r] = 0.0f;
+    if (rows[r] < 0) continue;
+    const float* p = part + (uint64_t)rows[r] * (uint64_t)v.nparts * 2;
+    for (uint32_t c = lane; c < v.nparts; c += 32) {
+      s0[r] += p[2 * c];
+      s1[r] += p[2 * c + 1];
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const float a = __shfl_sync(0xffffffffu, warp_sum(s0[r]), 0);
+    const float b = __shfl_sync(0xffffffffu, warp_sum(s1[r]), 0);
+    const float f = v.nn ? a / (float)v.samples : analytic_finalize(v.obj_kind, a, b, v.D);
+    const bool nan = isnan(f) && rows[r] >= 0;
+    nan_count += nan;
+    out[r] = isnan(f) ? __int_as_float(0x7f800000) : f;
+  }
+}
+
 __device__ __forceinline__ float finalize_row(const EngineView& v,
                                               const float* part, uint64_t row,
                                               bool* was_nan) {
-  const float* p = part + row * (uint64_t)v.nparts * 2;
-  float f;
-  if (v.nn) {
-    float s = 0.0f;
-    for (uint32_t m = 0; m < v.nparts; ++m) s += p[2 * m];
-    f = s / (float)v.samples;
-  } else {
-    float s0 = 0.0f, s1 = 0.0f;
-    for (uint32_t c = 0; c < v.nparts; ++c) {
-      s0 += p[2 * c];
-      s1 += p[2 * c + 1];
-    }
-    f = analytic_finalize(v.obj_kind, s0, s1, v.D);
-  }
-  *was_nan = isnan(f);
-  return *was_nan ? __int_as_float(0x7f800000) : f;
+  const int64_t rows[1] = {(int64_t)row};
+  float out[1];
+  unsigned n = 0;
+  finalize_rows<1>(v, part, rows, out, n);
+  *was_nan = n != 0;
+  return out[0];
 }
 
 // Random-mapping repair of one coordinate (engine.cpp:119-125):
@@ -401,24 +422,30 @@ __global__ void __launch_bounds__(256) k_rank(EngineView v) {
   uint32_t n = 1;
   while (n < lam) n <<= 1;
   unsigned nan_local = 0;
-  for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
-    if (k >= lam) {
-      keys[k] = ~0ull;
-      continue;
-    }
-    float x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  for (uint32_t k = lam + threadIdx.x; k < n; k += blockDim.x) keys[k] = ~0ull;
+  constexpr int R = 4;  // rows per warp step (loads of 4 rows in flight)
+  for (uint32_t k0 = warp * R; k0 < lam; k0 += nwarp * R) {
+    int64_t rows[R];
+    float x[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) rows[r] = (k0 + r < lam) ? (int64_t)(f * lam + k0 + r) : -1;
     if (v.injected_fitness) {
-      x = v.sfit[f * lam + k];
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r] = rows[r] >= 0 ? v.sfit[rows[r]] : 0.0f;
     } else {
-      bool nan;
-      x = finalize_row(v, v.spart, f * lam + k, &nan);
-      nan_local += nan;
-      v.sfit[f * lam + k] = x;
+      finalize_rows<R>(v, v.spart, rows, x, nan_local);
     }
-    keys[k] = rank_key(x, k);
+    if (lane == 0) {
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (rows[r] >= 0) {
+          if (!v.injected_fitness) v.sfit[rows[r]] = x[r];
+          keys[k0 + r] = rank_key(x[r], k0 + r);
+        }
+    }
   }
-  nan_local = __reduce_add_sync(0xffffffffu, nan_local);
-  if ((threadIdx.x & 31) == 0 && nan_local)
+  if (lane == 0 && nan_local)
     atomicAdd((unsigned long long*)&v.ctl->nan_count, (unsigned long long)nan_local);
   if (v.M == 0) return;
   __syncthreads();
@@ -537,7 +564,22 @@ __global__ void __launch_bounds__(256) k_select(EngineView v) {
   const uint64_t f = blockIdx.x;
   __shared__ double sv[8];
   __shared__ int so[8];
+  __shared__ float gs[16];
   unsigned nan_local = 0;
+  // guide fitness: one warp per guide row (warp-cooperative finalize)
+  for (uint64_t m = threadIdx.x >> 5; m < v.M; m += blockDim.x >> 5) {
+    float g;
+    if (v.injected_fitness) {
+      g = v.gfit[f * v.M + m];
+    } else {
+      bool nan;
+      g = finalize_row(v, v.gpart, f * v.M + m, &nan);
+      nan_local += nan;
+      if ((threadIdx.x & 31) == 0) v.gfit[f * v.M + m] = g;
+    }
+    if ((threadIdx.x & 31) == 0) gs[m] = g;
+  }
+  __syncthreads();
   double best_v = v.fit[f];
   int best_o = 0;
   if (threadIdx.x != 0) best_v = __longlong_as_double(0x7ff0000000000000ll), best_o = 0x7fffffff;
@@ -547,16 +589,7 @@ __global__ void __launch_bounds__(256) k_select(EngineView v) {
     if (x < best_v || (x == best_v && o < best_o)) best_v = x, best_o = o;
   }
   for (uint64_t m = threadIdx.x; m < v.M; m += blockDim.x) {
-    float g;
-    if (v.injected_fitness) {
-      g = v.gfit[f * v.M + m];
-    } else {
-      bool nan;
-      g = finalize_row(v, v.gpart, f * v.M + m, &nan);
-      nan_local += nan;
-      v.gfit[f * v.M + m] = g;
-    }
-    const double x = (double)g;
+    const double x = (double)gs[m];
     const int o = 1 + (int)v.lam + (int)m;
     if (x < best_v || (x == best_v && o < best_o)) best_v = x, best_o = o;
   }
@@ -742,19 +775,23 @@ __global__ void k_finalize_record(EngineView v, int mode) {
     return;
   }
   unsigned nan_local = 0;
-  for (uint64_t f = threadIdx.x; f < v.F; f += blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (uint64_t f = threadIdx.x >> 5; f < v.F; f += blockDim.x >> 5) {  // one warp per row
     if (mode == 0 || v.loser[f]) {
       bool nan;
       const float x = finalize_row(v, v.fpart, f, &nan);
       nan_local += nan;
-      v.fit[f] = (double)x;
-      if (mode == 0) {
-        v.amp[f] = v.a0;
-        v.li[f] = 0.0;
+      if (lane == 0) {
+        v.fit[f] = (double)x;
+        if (mode == 0) {
+          v.amp[f] = v.a0;
+          v.li[f] = 0.0;
+        }
       }
     }
   }
-  if (nan_local) atomicAdd((unsigned long long*)&ctl->nan_count, (unsigned long long)nan_local);
+  if (lane == 0 && nan_local)
+    atomicAdd((unsigned long long*)&ctl->nan_count, (unsigned long long)nan_local);
   __syncthreads();
   if (mode == 0 && threadIdx.x == 0) {
     ctl->used = v.F;
@@ -860,11 +897,15 @@ __global__ void __launch_bounds__(256) k_analytic_partials(const float* rows,
 // fitness[r] = finalize(part[r]) with NaN -> +inf; *nan += #NaN.
 __global__ void k_finalize_rows(EngineView v, const float* part, uint64_t nrows,
                                 float* fitness, unsigned long long* nan) {
-  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < nrows;
-       r += (uint64_t)gridDim.x * blockDim.x) {
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t r = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < nrows;
+       r += warps) {  // one warp per row
     bool isnan_;
-    fitness[r] = finalize_row(v, part, r, &isnan_);
-    if (isnan_) atomicAdd(nan, 1ull);
+    const float x = finalize_row(v, part, r, &isnan_);
+    if ((threadIdx.x & 31) == 0) {
+      fitness[r] = x;
+      if (isnan_) atomicAdd(nan, 1ull);
+    }
   }
 }
 
@@ -986,7 +1027,7 @@ void launch_analytic_partials(const float* rows, uint64_t nrows, uint64_t D,
 
 void launch_finalize_rows(const EngineView& v, const float* part, uint64_t nrows,
                           float* fitness, unsigned long long* nan, cudaStream_t s) {
-  k_finalize_rows<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(v, part, nrows, fitness, nan);
+  k_finalize_rows<<<(unsigned)((nrows + 7) / 8), 256, 0, s>>>(v, part, nrows, fitness, nan);
 }
 
 void launch_to_bf16(const float* src, __nv_bfloat16* dst, uint64_t n, cudaStream_t s) {
