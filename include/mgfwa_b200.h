@@ -196,6 +196,29 @@ int mgfwa_op_argmin_per_population(const double* fitness, uint64_t rows,
                                    uint64_t cols, uint64_t* index,
                                    double* value);
 
+/* ---- firework sharding across GPUs ---------------------
+ * The B*mu fireworks are split into `world` equal contiguous shards; rank r
+ * explodes, evaluates, guides and selects fireworks [r*F/world, (r+1)*F/world)
+ * and keeps a replica of every firework's {position, fitness, amplitude,
+ * last improvement}, refreshed once per generation by an in-place NCCL
+ * all-gather (NVLink).  Population range, loser-out (all losers are re-drawn
+ * from kReinit and evaluated by every rank) and record_wave then run
+ * identically on all ranks, so a sharded run is bit-identical to the
+ * single-GPU run.  Requires F % world == 0 and an evaluation budget (no
+ * wall-clock budget: every rank must take the same termination decision). */
+int mgfwa_create_shard(const mgfwa_config_t* config, const mgfwa_space_t* space,
+                       const mgfwa_objective_t* objective, uint64_t seed,
+                       int device, int rank, int world, mgfwa_ctx_t* out);
+/* 128-byte ncclUniqueId (created on rank 0, broadcast by the caller). */
+int mgfwa_nccl_unique_id(void* out128);
+int mgfwa_attach_nccl(mgfwa_ctx_t ctx, const void* unique_id128, int nranks,
+                      int rank);
+/* Manual stepping without NCCL (tests, one-process emulation): phase 1 =
+ * pop range .. selection, phase 2 = loser-out .. record_wave; between them
+ * every shard imports every other shard's owned rows. */
+int mgfwa_generation_phase(mgfwa_ctx_t ctx, int phase);
+int mgfwa_shard_exchange(mgfwa_ctx_t dst, mgfwa_ctx_t src);
+
 /* ---- measurement -------------------------------------------------------- */
 /* Times the dominant kernel of a generation in isolation on the context
  * stream with CUDA events: the spark fitness (tcgen05 GEMM for the NN

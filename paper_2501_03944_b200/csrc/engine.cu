@@ -9,6 +9,8 @@
 // mgfwa_run(); its operators (engine.hpp:71-125) map to mgfwa_op_*.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only; the library is bound at run time (dlopen)
 
 #include <algorithm>
 #include <cmath>
@@ -218,10 +220,12 @@ struct Workspace {
   std::vector<uint64_t> key;
 
   static std::vector<uint64_t> make_key(const HostConfig& c, const mgfwa_space_t* space,
-                                        const mgfwa_objective_t* obj, int dev, uint64_t trace_cap) {
+                                        const mgfwa_objective_t* obj, int dev, uint64_t trace_cap,
+                                        uint64_t rank = 0, uint64_t world = 1) {
     return {c.B, c.mu, c.lam, c.M, c.M > 0 ? c.top() : 0, space->dim, (uint64_t)obj->kind,
             obj->in_dim, obj->hidden, obj->out_dim, obj->samples,
-            obj->kind == MGFWA_OBJ_MLP_WEIGHTS ? obj->data_seed : 0, (uint64_t)dev, trace_cap};
+            obj->kind == MGFWA_OBJ_MLP_WEIGHTS ? obj->data_seed : 0, (uint64_t)dev, trace_cap,
+            rank, world};
   }
 
   // Run-specific scalars and the search box (cheap; H2D of 2 x D bounds).
@@ -256,9 +260,10 @@ struct Workspace {
   }
 
   Status build(const HostConfig& c, const mgfwa_space_t* space, const mgfwa_objective_t* obj,
-               uint64_t seed, int dev, uint64_t trace_cap) {
+               uint64_t seed, int dev, uint64_t trace_cap, uint64_t rank = 0,
+               uint64_t world = 1) {
     device = dev;
-    key = make_key(c, space, obj, dev, trace_cap);
+    key = make_key(c, space, obj, dev, trace_cap, rank, world);
     CUDA_TRY(cudaSetDevice(dev));
     CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     CUDA_TRY(prepare_engine_kernels());
@@ -271,6 +276,10 @@ struct Workspace {
     v.Dp = round_up(D, 64);
     v.top = c.M > 0 ? c.top() : 0;
     v.F = c.B * c.mu;
+    if (world == 0 || v.F % world != 0)
+      return invalid("mgfwa_b200: batches * fireworks must be divisible by the number of ranks");
+    v.Fl = v.F / world;
+    v.f_lo = rank * v.Fl;
     v.nch = (uint32_t)((D + kChunk - 1) / kChunk);
     v.obj_kind = obj->kind;
     v.nn = obj->kind == MGFWA_OBJ_MLP_WEIGHTS;
@@ -285,7 +294,8 @@ struct Workspace {
     };
     std::vector<Slot> slots;
     auto add = [&](auto** p, size_t bytes) { slots.push_back({reinterpret_cast<void**>(p), bytes}); };
-    const uint64_t F = v.F, Dp = v.Dp, P = F * v.lam, G = F * v.M, np2 = (uint64_t)v.nparts * 2;
+    // sparks / guides / rank lists for the owned fireworks only
+    const uint64_t F = v.F, Dp = v.Dp, P = v.Fl * v.lam, G = v.Fl * v.M, np2 = (uint64_t)v.nparts * 2;
     double *lower, *upper, *boosts;
     float *lower_f, *upper_f;
     add(&lower, D * 8);
@@ -306,7 +316,7 @@ struct Workspace {
     if (v.nn) add(&v.sparks_h, P * Dp * 2);
     add(&v.sfit, P * 4);
     add(&v.spart, P * np2 * 4);
-    add(&v.rank_idx, std::max<uint64_t>(F * 2 * v.top, 1) * 4);
+    add(&v.rank_idx, std::max<uint64_t>(v.Fl * 2 * v.top, 1) * 4);
     add(&v.guides, std::max<uint64_t>(G, 1) * Dp * 4);
     if (v.nn) add(&v.guides_h, std::max<uint64_t>(G, 1) * Dp * 2);
     add(&v.gfit, std::max<uint64_t>(G, 1) * 4);
@@ -424,6 +434,47 @@ static void hook_fresh_all(void* p, cudaStream_t s) {
 }
 
 // ----------------------------------------------------------------- engine
+// NCCL, bound at run time (dlopen "libnccl.so.2": the copy already loaded in
+// the process — e.g. PyTorch's — or the system one), so the library has no
+// link-time NCCL dependency and single-GPU users never load it.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+static const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(h, "ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    a.ok = a.GetUniqueId && a.CommInitRank && a.AllGather && a.GroupStart && a.GroupEnd &&
+           a.CommDestroy && a.GetErrorString;
+    return a;
+  }();
+  return api;
+}
+
+#define NCCL_TRY(expr)                                                                \
+  do {                                                                                \
+    ncclResult_t r__ = (expr);                                                        \
+    if (r__ != ncclSuccess)                                                           \
+      return Status{MGFWA_ENCCL, std::string(#expr) + ": " + nccl().GetErrorString(r__)}; \
+  } while (0)
+
 class Engine {
  public:
   HostConfig cfg;
@@ -431,7 +482,11 @@ class Engine {
   GenerationHooks hooks{};
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
-  cudaGraphExec_t gen_exec = nullptr;
+  cudaGraphExec_t gen_exec = nullptr;    // whole loop body (one rank)
+  cudaGraphExec_t gen_exec_a = nullptr;  // sharded: up to selection
+  cudaGraphExec_t gen_exec_b = nullptr;  // sharded: loser-out .. record
+  uint64_t rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
   uint64_t kernels_per_gen = 0;
   Ctl* host_ctl = nullptr;  // pinned
   bool initialized = false;
@@ -446,14 +501,17 @@ class Engine {
 
   ~Engine() {
     if (gen_exec) cudaGraphExecDestroy(gen_exec);
+    if (gen_exec_a) cudaGraphExecDestroy(gen_exec_a);
+    if (gen_exec_b) cudaGraphExecDestroy(gen_exec_b);
     if (stream) cudaStreamSynchronize(stream);
+    if (comm) nccl().CommDestroy(comm);
     if (own_stream) cudaStreamDestroy(own_stream);
     if (host_ctl) cudaFreeHost(host_ctl);
     WorkspaceCache::give(std::move(ws));
   }
 
   Status create(const mgfwa_config_t* c, const mgfwa_space_t* space, const mgfwa_objective_t* obj,
-                uint64_t seed, int device) {
+                uint64_t seed, int device, uint64_t shard_rank = 0, uint64_t shard_world = 1) {
     if (c == nullptr) return invalid("MgfwaConfig: null config");
     cfg = to_host(c);
     STATUS_TRY(validate_config(cfg));
@@ -462,12 +520,19 @@ class Engine {
     // engine.cpp:319-323
     if (cfg.max_evals > 0 && cfg.max_evals < cfg.B * cfg.mu)
       return invalid("budget too small: needs at least B * mu evaluations");
-    ws = WorkspaceCache::take(Workspace::make_key(cfg, space, obj, device, 1024));
+    if (shard_world == 0 || shard_rank >= shard_world) return invalid("mgfwa_b200: bad shard rank");
+    if (shard_world > 1 && (cfg.max_evals == 0 || cfg.wall_ms > 0.0))
+      return invalid(
+          "mgfwa_b200: sharded runs need an evaluation budget and no wall-clock budget "
+          "(every rank must take the same termination decision)");
+    rank = shard_rank;
+    world = shard_world;
+    ws = WorkspaceCache::take(Workspace::make_key(cfg, space, obj, device, 1024, rank, world));
     if (ws) {
       STATUS_TRY(ws->configure(cfg, space, seed));
     } else {
       ws = std::make_unique<Workspace>();
-      STATUS_TRY(ws->build(cfg, space, obj, seed, device, 1024));
+      STATUS_TRY(ws->build(cfg, space, obj, seed, device, 1024, rank, world));
     }
     CUDA_TRY(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
     stream = own_stream;
@@ -480,19 +545,87 @@ class Engine {
     return ok();
   }
 
-  Status capture() {
-    if (gen_exec) return ok();
+  Status capture_one(int phase, cudaGraphExec_t* out, size_t* nodes) {
     cudaGraph_t g = nullptr;
     CUDA_TRY(cudaStreamBeginCapture(own_stream, cudaStreamCaptureModeThreadLocal));
-    launch_generation_kernels(ws->v, ws->nsm, own_stream, &hooks);
+    launch_generation_kernels(ws->v, ws->nsm, own_stream, &hooks, phase);
     cudaError_t e = cudaStreamEndCapture(own_stream, &g);
     if (e != cudaSuccess) return Status{MGFWA_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e)};
-    size_t n = 0;
-    cudaGraphGetNodes(g, nullptr, &n);
-    kernels_per_gen = n;
-    e = cudaGraphInstantiate(&gen_exec, g, 0);
+    cudaGraphGetNodes(g, nullptr, nodes);
+    e = cudaGraphInstantiate(out, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return Status{MGFWA_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(e)};
+    return ok();
+  }
+
+  // Sharded stepping (phase A, all-gather, phase B) whenever the context is
+  // one of several shards or has a communicator (a 1-rank communicator
+  // exercises the exchange path on a single GPU).
+  bool sharded() const { return world > 1 || comm != nullptr; }
+
+  Status capture() {
+    if (!sharded()) {
+      if (gen_exec) return ok();
+      size_t n = 0;
+      STATUS_TRY(capture_one(kGenAll, &gen_exec, &n));
+      kernels_per_gen = n;
+      return ok();
+    }
+    if (gen_exec_a) return ok();
+    size_t na = 0, nb = 0;
+    STATUS_TRY(capture_one(kGenA, &gen_exec_a, &na));
+    STATUS_TRY(capture_one(kGenB, &gen_exec_b, &nb));
+    kernels_per_gen = na + nb;
+    return ok();
+  }
+
+  // ---- firework sharding: the per-generation exchange.
+  // After selection every rank holds the new state of its own fireworks;
+  // one all-gather (in place) replicates {position row, fitness,
+  // amplitude, last improvement} of all F fireworks on every rank.
+  Status attach_nccl(const void* unique_id, int nranks, int r) {
+    if ((uint64_t)nranks != world || (uint64_t)r != rank)
+      return invalid("mgfwa_attach_nccl: rank / world do not match the shard");
+    if (!nccl().ok) return Status{MGFWA_ENCCL, "libnccl.so.2 not loadable"};
+    ncclUniqueId id;
+    memcpy(&id, unique_id, sizeof(id));
+    CUDA_TRY(cudaSetDevice(ws->device));
+    NCCL_TRY(nccl().CommInitRank(&comm, nranks, id, r));
+    return ok();
+  }
+
+  Status exchange_nccl() {
+    const EngineView& v = ws->v;
+    const size_t rows = v.Fl * v.Dp;
+    NCCL_TRY(nccl().GroupStart());
+    NCCL_TRY(nccl().AllGather(v.pos + v.f_lo * v.Dp, v.pos, rows, ncclFloat, comm, stream));
+    NCCL_TRY(nccl().AllGather(v.fit + v.f_lo, v.fit, v.Fl, ncclFloat64, comm, stream));
+    NCCL_TRY(nccl().AllGather(v.amp + v.f_lo, v.amp, v.Fl, ncclFloat64, comm, stream));
+    NCCL_TRY(nccl().AllGather(v.li + v.f_lo, v.li, v.Fl, ncclFloat64, comm, stream));
+    NCCL_TRY(nccl().GroupEnd());
+    return ok();
+  }
+
+  // In-process exchange (tests / one-GPU emulation of several shards): copy
+  // the owned rows of `src` into this shard's replica.
+  Status import_shard(const Engine& src) {
+    const EngineView& a = ws->v;
+    const EngineView& b = src.ws->v;
+    if (a.F != b.F || a.Dp != b.Dp || a.Fl != b.Fl) return invalid("mgfwa_shard_exchange: shape mismatch");
+    CUDA_TRY(cudaMemcpyAsync(a.pos + b.f_lo * a.Dp, b.pos + b.f_lo * b.Dp, b.Fl * b.Dp * 4,
+                             cudaMemcpyDeviceToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(a.fit + b.f_lo, b.fit + b.f_lo, b.Fl * 8, cudaMemcpyDeviceToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(a.amp + b.f_lo, b.amp + b.f_lo, b.Fl * 8, cudaMemcpyDeviceToDevice, stream));
+    CUDA_TRY(cudaMemcpyAsync(a.li + b.f_lo, b.li + b.f_lo, b.Fl * 8, cudaMemcpyDeviceToDevice, stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    return ok();
+  }
+
+  Status phase(int ph) {
+    if (!initialized) return Status{MGFWA_ESTATE, "mgfwa: initialize() must precede the loop"};
+    launch_generation_kernels(ws->v, ws->nsm, stream, &hooks, ph);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(stream));
     return ok();
   }
 
@@ -537,7 +670,18 @@ class Engine {
 
   Status enqueue(uint64_t n) {
     if (!initialized) return Status{MGFWA_ESTATE, "mgfwa: initialize() must precede the loop"};
-    for (uint64_t i = 0; i < n; ++i) CUDA_TRY(cudaGraphLaunch(gen_exec, stream));
+    if (!sharded()) {
+      for (uint64_t i = 0; i < n; ++i) CUDA_TRY(cudaGraphLaunch(gen_exec, stream));
+      return ok();
+    }
+    STATUS_TRY(capture());
+    if (comm == nullptr)
+      return Status{MGFWA_ESTATE, "mgfwa: sharded context needs mgfwa_attach_nccl (or phases + exchange)"};
+    for (uint64_t i = 0; i < n; ++i) {
+      CUDA_TRY(cudaGraphLaunch(gen_exec_a, stream));
+      STATUS_TRY(exchange_nccl());
+      CUDA_TRY(cudaGraphLaunch(gen_exec_b, stream));
+    }
     return ok();
   }
 
@@ -725,6 +869,49 @@ int mgfwa_create(const mgfwa_config_t* config, const mgfwa_space_t* space,
 int mgfwa_destroy(mgfwa_ctx_t ctx) {
   delete ctx;
   return MGFWA_OK;
+}
+
+int mgfwa_create_shard(const mgfwa_config_t* config, const mgfwa_space_t* space,
+                       const mgfwa_objective_t* objective, uint64_t seed, int device, int rank,
+                       int world, mgfwa_ctx_t* out) {
+  if (!out) return fail(nullptr, invalid("mgfwa_create_shard: null output"));
+  *out = nullptr;
+  if (rank < 0 || world < 1) return fail(nullptr, invalid("mgfwa_b200: bad shard rank"));
+  auto* ctx = new (std::nothrow) mgfwa_ctx();
+  if (!ctx) return fail(nullptr, Status{MGFWA_ENOMEM, "host allocation"});
+  Status s = ctx->engine.create(config, space, objective, seed, device, (uint64_t)rank,
+                                (uint64_t)world);
+  if (s.code != MGFWA_OK) {
+    fail(nullptr, s);
+    delete ctx;
+    return s.code;
+  }
+  *out = ctx;
+  return MGFWA_OK;
+}
+
+int mgfwa_nccl_unique_id(void* out128) {
+  if (!nccl().ok) return fail(nullptr, Status{MGFWA_ENCCL, "libnccl.so.2 not loadable"});
+  ncclUniqueId id;
+  const ncclResult_t r = nccl().GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, Status{MGFWA_ENCCL, nccl().GetErrorString(r)});
+  memcpy(out128, &id, sizeof(id));
+  return MGFWA_OK;
+}
+
+int mgfwa_attach_nccl(mgfwa_ctx_t ctx, const void* unique_id128, int nranks, int rank) {
+  return fail(ctx, ctx->engine.attach_nccl(unique_id128, nranks, rank));
+}
+
+int mgfwa_generation_phase(mgfwa_ctx_t ctx, int phase) {
+  if (phase != 1 && phase != 2) return fail(ctx, invalid("mgfwa_generation_phase: phase is 1 or 2"));
+  Status s = ctx->engine.phase(phase == 1 ? kGenA : kGenB);
+  if (s.code == MGFWA_OK && phase == 2) s = ctx->engine.sync();
+  return fail(ctx, s);
+}
+
+int mgfwa_shard_exchange(mgfwa_ctx_t dst, mgfwa_ctx_t src) {
+  return fail(dst, dst->engine.import_shard(src->engine));
 }
 
 int mgfwa_set_stream(mgfwa_ctx_t ctx, void* s) {

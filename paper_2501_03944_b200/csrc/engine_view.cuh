@@ -34,8 +34,15 @@ struct Ctl {
 };
 
 struct EngineView {
-  // shape
+  // shape.  F = B * mu fireworks in total; this context owns the contiguous
+  // range [f_lo, f_lo + Fl) (firework sharding across ranks).
+  // Spark / guide buffers hold only the owned fireworks (local row
+  // (f - f_lo) * lam + k); positions, fitness, amplitudes and improvement
+  // rates are replicated for all F (refreshed by the per-generation
+  // all-gather), so population range, loser-out and record_wave run
+  // identically on every rank.
   uint64_t B, mu, lam, M, D, Dp, top, F;
+  uint64_t Fl, f_lo;
   uint32_t nparts;     // partial-sum slots per row
   uint32_t nch;        // coordinate chunks per row (kChunk each)
   int obj_kind;

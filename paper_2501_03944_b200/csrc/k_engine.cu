@@ -281,7 +281,7 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
         s0[kk] += a0;
         s1[kk] += a1;
       }
-      const uint64_t off = (f * v.lam + k0 + kk) * v.Dp + d0;
+      const uint64_t off = ((f - v.f_lo) * v.lam + k0 + kk) * v.Dp + d0;  // local spark row
       *reinterpret_cast<float4*>(v.sparks + off) = make_float4(x[kk][0], x[kk][1], x[kk][2], x[kk][3]);
       if (KIND == 0) store_bf16x4(v.sparks_h, off, x[kk]);
     }
@@ -305,12 +305,12 @@ __global__ void __launch_bounds__(256, 2) k_explode_map(EngineView v) {
   const uint64_t it = v.ctl->iteration;
   const uint64_t ngrp = (v.lam + KG - 1) / KG;
   const uint64_t nsup = (ngrp + kWarps - 1) / kWarps;  // groups of 8 spark groups
-  const uint64_t items = v.F * v.nch * nsup;
+  const uint64_t items = v.Fl * v.nch * nsup;
   const uint32_t D = (uint32_t)v.D;
   for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
     const uint64_t sup = item % nsup, rest = item / nsup;
     const uint32_t c = (uint32_t)(rest % v.nch);
-    const uint64_t f = rest / v.nch;
+    const uint64_t fl = rest / v.nch, f = v.f_lo + fl;
     const uint64_t b = f / v.mu, n = f % v.mu;
     const uint32_t cbase = c * kChunk;
     __syncthreads();  // previous item's readers are done with the chunk
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(256, 2) k_explode_map(EngineView v) {
         const float t0 = warp_sum(s0[kk]);
         const float t1 = warp_sum(s1[kk]);
         if (lane == 0) {
-          const uint64_t r = f * v.lam + k0 + kk;
+          const uint64_t r = fl * v.lam + k0 + kk;
           v.spart[(r * v.nparts + c) * 2] = t0;
           v.spart[(r * v.nparts + c) * 2 + 1] = t1;
         }
@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(256, 2) k_explode_map(EngineView v) {
 
 static unsigned explode_blocks(const EngineView& v, int nsm) {
   const uint64_t ngrp = (v.lam + kSparkGroup - 1) / kSparkGroup;
-  const uint64_t items = v.F * v.nch * ((ngrp + kWarps - 1) / kWarps);
+  const uint64_t items = v.Fl * v.nch * ((ngrp + kWarps - 1) / kWarps);
   const uint64_t cap = (uint64_t)nsm * 8;
   return (unsigned)(items < cap ? items : cap);
 }
@@ -495,16 +495,16 @@ __global__ void __launch_bounds__(256) k_guides(EngineView v) {
   const uint64_t nsl = (v.D + 63) / 64;  // 64-coordinate slices (float2 per lane)
   const uint64_t bpf = (nsl + kWarps - 1) / kWarps;  // blocks per firework
   const uint64_t top = v.top;
-  for (uint64_t blk = blockIdx.x; blk < v.F * bpf; blk += gridDim.x) {
-    const uint64_t f = blk / bpf;
+  for (uint64_t blk = blockIdx.x; blk < v.Fl * bpf; blk += gridDim.x) {
+    const uint64_t fl = blk / bpf, f = v.f_lo + fl;  // local / global firework
     const uint64_t c = (blk % bpf) * kWarps + warp;
     __syncthreads();
-    for (uint64_t i = threadIdx.x; i < 2 * top; i += blockDim.x) s_idx[i] = v.rank_idx[f * 2 * top + i];
+    for (uint64_t i = threadIdx.x; i < 2 * top; i += blockDim.x) s_idx[i] = v.rank_idx[fl * 2 * top + i];
     __syncthreads();
     const uint64_t d0 = c * 64 + lane * 2;
     if (c >= nsl || d0 >= v.D) continue;
     const uint64_t b = f / v.mu, n = f % v.mu;
-    const float* sb = v.sparks + f * v.lam * v.Dp + d0;
+    const float* sb = v.sparks + fl * v.lam * v.Dp + d0;
     double acc0 = 0.0, acc1 = 0.0;
     uint64_t t = 0;
     // 32 independent 8-byte loads in flight per lane, summed in rank order
@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(256) k_guides(EngineView v) {
           x[e] = 0.0f;
         }
       }
-      const uint64_t off = (f * v.M + m) * v.Dp + d0;
+      const uint64_t off = (fl * v.M + m) * v.Dp + d0;  // local guide row
       *reinterpret_cast<float2*>(v.guides + off) = make_float2(x[0], x[1]);
       if (v.nn) *reinterpret_cast<__nv_bfloat162*>(v.guides_h + off) = __floats2bfloat162_rn(x[0], x[1]);
     }
@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(256) k_guides(EngineView v) {
 // (engine.cpp:388-390).  One block per firework.
 __global__ void __launch_bounds__(256) k_select(EngineView v) {
   if (gen_inactive(v)) return;
-  const uint64_t f = blockIdx.x;
+  const uint64_t fl = blockIdx.x, f = v.f_lo + fl;  // local / global firework
   __shared__ double sv[8];
   __shared__ int so[8];
   __shared__ float gs[16];
@@ -570,12 +570,12 @@ __global__ void __launch_bounds__(256) k_select(EngineView v) {
   for (uint64_t m = threadIdx.x >> 5; m < v.M; m += blockDim.x >> 5) {
     float g;
     if (v.injected_fitness) {
-      g = v.gfit[f * v.M + m];
+      g = v.gfit[fl * v.M + m];
     } else {
       bool nan;
-      g = finalize_row(v, v.gpart, f * v.M + m, &nan);
+      g = finalize_row(v, v.gpart, fl * v.M + m, &nan);
       nan_local += nan;
-      if ((threadIdx.x & 31) == 0) v.gfit[f * v.M + m] = g;
+      if ((threadIdx.x & 31) == 0) v.gfit[fl * v.M + m] = g;
     }
     if ((threadIdx.x & 31) == 0) gs[m] = g;
   }
@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(256) k_select(EngineView v) {
   int best_o = 0;
   if (threadIdx.x != 0) best_v = __longlong_as_double(0x7ff0000000000000ll), best_o = 0x7fffffff;
   for (uint64_t k = threadIdx.x; k < v.lam; k += blockDim.x) {
-    const double x = (double)v.sfit[f * v.lam + k];
+    const double x = (double)v.sfit[fl * v.lam + k];
     const int o = 1 + (int)k;
     if (x < best_v || (x == best_v && o < best_o)) best_v = x, best_o = o;
   }
@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(256) k_select(EngineView v) {
     v.winner[f] = best_o;
     const double a = v.amp[f] * (imp ? v.amp_amplify : v.amp_reduce);
     v.amp[f] = a < v.amp_floor ? v.amp_floor : (v.max_range < a ? v.max_range : a);
-    if (f == 0) v.ctl->used += v.wave;
+    if (fl == 0) v.ctl->used += v.wave;  // the global wave, on every rank
   }
 }
 
@@ -635,15 +635,15 @@ __global__ void __launch_bounds__(256) k_select(EngineView v) {
 __global__ void __launch_bounds__(256) k_select_copy(EngineView v) {
   if (gen_inactive(v)) return;
   const int lane = threadIdx.x & 31;
-  const uint64_t items = v.F * v.nch;
+  const uint64_t items = v.Fl * v.nch;
   for (uint64_t item = blockIdx.x * (uint64_t)kWarps + (threadIdx.x >> 5);
        item < items; item += (uint64_t)gridDim.x * kWarps) {
-    const uint64_t f = item / v.nch, c = item % v.nch;
+    const uint64_t fl = item / v.nch, c = item % v.nch, f = v.f_lo + fl;
     const int w = v.winner[f];
     if (w == 0) continue;
     const float* src = (uint64_t)w <= v.lam
-                           ? v.sparks + (f * v.lam + (w - 1)) * v.Dp
-                           : v.guides + (f * v.M + (w - 1 - v.lam)) * v.Dp;
+                           ? v.sparks + (fl * v.lam + (w - 1)) * v.Dp
+                           : v.guides + (fl * v.M + (w - 1 - v.lam)) * v.Dp;
     float* dst = v.pos + f * v.Dp;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -978,33 +978,42 @@ void launch_key_hash(const uint64_t* keys, uint64_t n, uint64_t* out,
 
 static unsigned guide_blocks(const EngineView& v, int nsm) {
   const uint64_t nsl = (v.D + 63) / 64;
-  const uint64_t blocks = v.F * ((nsl + kWarps - 1) / kWarps);
-  return (unsigned)(blocks < (uint64_t)nsm * 8 ? blocks : (uint64_t)nsm * 8);
+  const uint64_t blocks = v.Fl * ((nsl + kWarps - 1) / kWarps);
+  return (unsigned)(blocks < (uint64_t)nsm * 8 ? (blocks ? blocks : 1) : (uint64_t)nsm * 8);
 }
 
+static unsigned capped(uint64_t g, int nsm) {
+  const uint64_t c = (uint64_t)nsm * 16;
+  return (unsigned)(g == 0 ? 1 : (g < c ? g : c));
+}
+
+// phase kGenAll: the whole loop body; kGenA: pop range .. selection (owned
+// fireworks); kGenB: loser-out .. record_wave (all fireworks, after the
+// per-generation all-gather of the selected fireworks).
 void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
-                               GenerationHooks* hooks) {
-  const unsigned items_f = (unsigned)((v.F * v.nch + kWarps - 1) / kWarps);
-  auto cap = [&](unsigned g) { return g < (unsigned)nsm * 16 ? (g ? g : 1) : (unsigned)nsm * 16; };
-  const unsigned rng_blocks = cap((unsigned)((v.B * v.D + 255) / 256));
-  k_pop_range<<<rng_blocks, 256, 0, s>>>(v);
-  launch_explode_map_impl(v, nsm, s);
-  if (v.nn) hooks->eval_sparks(hooks->ctx, s);
-  k_rank<<<(unsigned)v.F, 256, rank_smem(v), s>>>(v);
-  if (v.M > 0) {
-    k_guides<<<guide_blocks(v, nsm), 256, 2 * v.top * sizeof(int), s>>>(v);
-    if (v.nn)
-      hooks->eval_guides(hooks->ctx, s);
-    else
-      launch_analytic_partials(v.guides, v.F * v.M, v.D, v.Dp, v.nch, v.obj_kind, v.gpart, nsm, s);
+                               GenerationHooks* hooks, int phase) {
+  if (phase != kGenB) {
+    k_pop_range<<<capped((v.B * v.D + 255) / 256, nsm), 256, 0, s>>>(v);
+    launch_explode_map_impl(v, nsm, s);
+    if (v.nn) hooks->eval_sparks(hooks->ctx, s);
+    k_rank<<<(unsigned)v.Fl, 256, rank_smem(v), s>>>(v);
+    if (v.M > 0) {
+      k_guides<<<guide_blocks(v, nsm), 256, 2 * v.top * sizeof(int), s>>>(v);
+      if (v.nn)
+        hooks->eval_guides(hooks->ctx, s);
+      else
+        launch_analytic_partials(v.guides, v.Fl * v.M, v.D, v.Dp, v.nch, v.obj_kind, v.gpart, nsm, s);
+    }
+    k_select<<<(unsigned)v.Fl, 256, 0, s>>>(v);
+    k_select_copy<<<capped((v.Fl * v.nch + kWarps - 1) / kWarps, nsm), 256, 0, s>>>(v);
   }
-  k_select<<<(unsigned)v.F, 256, 0, s>>>(v);
-  k_select_copy<<<cap(items_f), 256, 0, s>>>(v);
-  k_loser<<<1, 128, 0, s>>>(v);
-  k_fresh_rows<<<cap(items_f), 256, 0, s>>>(v, 1);
-  if (v.nn) hooks->eval_fresh(hooks->ctx, s);
-  k_finalize_record<<<1, 256, 0, s>>>(v, 1);
-  k_record_copy<<<cap((unsigned)((v.B * v.nch + kWarps - 1) / kWarps)), 256, 0, s>>>(v);
+  if (phase != kGenA) {
+    k_loser<<<1, 128, 0, s>>>(v);
+    k_fresh_rows<<<capped((v.F * v.nch + kWarps - 1) / kWarps, nsm), 256, 0, s>>>(v, 1);
+    if (v.nn) hooks->eval_fresh(hooks->ctx, s);
+    k_finalize_record<<<1, 256, 0, s>>>(v, 1);
+    k_record_copy<<<capped((v.B * v.nch + kWarps - 1) / kWarps, nsm), 256, 0, s>>>(v);
+  }
 }
 
 void launch_initialize_kernels(const EngineView& v, int nsm, cudaStream_t s,
@@ -1045,15 +1054,15 @@ void launch_explode_map(const EngineView& v, int nsm, cudaStream_t s) {
   launch_explode_map_impl(v, nsm, s);
 }
 void launch_rank(const EngineView& v, cudaStream_t s) {
-  k_rank<<<(unsigned)v.F, 256, rank_smem(v), s>>>(v);
+  k_rank<<<(unsigned)v.Fl, 256, rank_smem(v), s>>>(v);
 }
 void launch_guides(const EngineView& v, int nsm, cudaStream_t s) {
   k_guides<<<guide_blocks(v, nsm), 256, 2 * v.top * sizeof(int), s>>>(v);
-  if (!v.nn) launch_analytic_partials(v.guides, v.F * v.M, v.D, v.Dp, v.nch, v.obj_kind, v.gpart, nsm, s);
+  if (!v.nn) launch_analytic_partials(v.guides, v.Fl * v.M, v.D, v.Dp, v.nch, v.obj_kind, v.gpart, nsm, s);
 }
 void launch_select(const EngineView& v, int nsm, cudaStream_t s) {
-  const unsigned g = (unsigned)((v.F * v.nch + kWarps - 1) / kWarps);
-  k_select<<<(unsigned)v.F, 256, 0, s>>>(v);
+  const unsigned g = (unsigned)((v.Fl * v.nch + kWarps - 1) / kWarps);
+  k_select<<<(unsigned)v.Fl, 256, 0, s>>>(v);
   k_select_copy<<<g < (unsigned)nsm * 16 ? g : nsm * 16, 256, 0, s>>>(v);
 }
 void launch_loser(const EngineView& v, int nsm, cudaStream_t s) {

@@ -22,8 +22,9 @@ struct GenerationHooks {
 // the first launch / graph capture.
 cudaError_t prepare_engine_kernels();
 
+enum { kGenAll = 0, kGenA = 1, kGenB = 2 };
 void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
-                               GenerationHooks* hooks);
+                               GenerationHooks* hooks, int phase = kGenAll);
 void launch_initialize_kernels(const EngineView& v, int nsm, cudaStream_t s,
                                GenerationHooks* hooks);
 

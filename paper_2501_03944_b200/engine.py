@@ -204,14 +204,38 @@ class Engine:
     """One device-resident run: initialize(), step()/enqueue(), results."""
 
     def __init__(self, config: MgfwaConfig, space: SearchSpace, objective: Objective, seed: int,
-                 device: int = 0):
+                 device: int = 0, rank: int = 0, world: int = 1):
         self.config, self.space, self.objective, self.seed = config, space, objective, seed
+        self.rank, self.world = rank, world
         c, self._keep = config._c()
         sp = space._c()
         ob = objective._c()
         h = C.c_void_p()
-        _check(A.lib().mgfwa_create(C.byref(c), C.byref(sp), C.byref(ob), seed, device, C.byref(h)))
+        if world == 1:
+            _check(A.lib().mgfwa_create(C.byref(c), C.byref(sp), C.byref(ob), seed, device, C.byref(h)))
+        else:
+            _check(A.lib().mgfwa_create_shard(C.byref(c), C.byref(sp), C.byref(ob), seed, device, rank, world,
+                                              C.byref(h)))
         self.h = h
+
+    # ---- firework sharding (one rank per GPU, NCCL all-gather per generation)
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(A.lib().mgfwa_nccl_unique_id(buf))
+        return buf.raw
+
+    def attach_nccl(self, unique_id: bytes):
+        buf = C.create_string_buffer(unique_id, 128)
+        _check(A.lib().mgfwa_attach_nccl(self.h, buf, self.world, self.rank), self.h)
+
+    def phase(self, p: int):
+        """Manual stepping (no NCCL): phase 1 = up to selection, 2 = loser-out .. record."""
+        _check(A.lib().mgfwa_generation_phase(self.h, p), self.h)
+
+    def import_shard(self, other: "Engine"):
+        """In-process exchange: copy `other`'s owned fireworks into this replica."""
+        _check(A.lib().mgfwa_shard_exchange(self.h, other.h), self.h)
 
     def close(self):
         if getattr(self, "h", None):
