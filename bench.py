@@ -11,8 +11,10 @@ engine.cpp:359-417) on synthetic data.  value = whole-job evaluations per
 second, device-timed with CUDA events on the engine's stream over exactly K
 generations (max over ranks).  e2e = the same metric through the one-shot
 C-ABI run() drop-in (mgfwa_run_once) with host buffers in and out.
-Multi-GPU (torchrun): one independent run per rank (replicas, weak scaling;
-see DESIGN.md §5).  ``--impl reference`` times the compiled reference
+Multi-GPU (torchrun, N ranks): weak scaling — the population grows to N x mu
+fireworks, each rank owns mu of them, and one in-place NCCL all-gather of the
+selected fireworks per generation keeps the population state replicated
+(DESIGN.md §5).  ``--impl reference`` times the compiled reference
 (oracle/_ref, /root/reference/proj/src/engine.cpp run()) on the host cores.
 """
 from __future__ import annotations
@@ -204,7 +206,18 @@ def main():
     stream = torch.cuda.Stream()
     obj = make_objective(P, w)
     space = P.SearchSpace.box(w["D"], w["lo"], w["hi"])
-    eng = P.Engine(make_config(P, w, 1 << 62), space, obj, seed=rank, device=dev)
+    # N > 1: weak scaling — the population grows to mu * N fireworks, each
+    # rank owns mu of them (firework sharding), one in-place NCCL all-gather
+    # of the selected fireworks per generation.
+    wn = dict(w)
+    wn["mu"] = w["mu"] * world
+    eng = P.Engine(make_config(P, wn, 1 << 62), space, obj, seed=0, device=dev, rank=rank, world=world)
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(P.Engine.nccl_unique_id()), dtype=torch.uint8))
+        torch.distributed.broadcast(uid, 0)
+        eng.attach_nccl(bytes(uid.cpu().numpy().tobytes()))
     eng.set_stream(stream.cuda_stream)
     eng.initialize()
     kpg = eng.kernels_per_generation()
@@ -226,14 +239,12 @@ def main():
         torch.distributed.barrier()
     eng.sync()
     ms = start.elapsed_time(end)
+    # evaluations_used is the population-wide counter, identical on every rank
     evals = eng.counters()["evaluations_used"] - before
     if world > 1:
-        t = torch.tensor([ms, float(evals)], dtype=torch.float64, device="cuda")
-        mx = t.clone()
-        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
-        sm = t.clone()
-        torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
-        ms_max, evals_total = float(mx[0]), float(sm[1])
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_max, evals_total = float(t[0]), float(evals)
     else:
         ms_max, evals_total = ms, float(evals)
 
@@ -258,7 +269,8 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16" if w["kind"] == "mlp" else "f32", "data": "synthetic",
-            "config": {"workload": w["desc"], "D": w["D"], "per_rank": "independent run (replica)",
+            "config": {"workload": w["desc"], "D": w["D"], "fireworks_total": wn["mu"] * w["B"],
+                       "parallelism": f"firework-sharded x{world}" + (" + NCCL all-gather/gen" if world > 1 else ""),
                        "l2": "inputs larger than L2: spark matrix fp32+bf16 229 MB/generation > 126 MB"
                        if args.workload == "c2" else "n/a"},
             "gpu_launches": kpg * args.steps, "roofline": roof}
