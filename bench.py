@@ -57,6 +57,26 @@ def peaks():
     return PEAKS_FALLBACK, "fallback"
 
 
+def ncu_traffic(kernel_prefix: str):
+    """DRAM bytes (read + write) per launch of a kernel from the latest
+    committed `ncu --set full` capture under profiles/ (None if absent)."""
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_full_hot_kernels.json")), reverse=True):
+        with open(path) as f:
+            for k in json.load(f):
+                if kernel_prefix in k.get("kernel", ""):
+                    def mb(s):
+                        v, unit = s.split()
+                        return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
+                    try:
+                        return {"bytes": mb(k["dram__bytes_read.sum"]) + mb(k["dram__bytes_write.sum"]),
+                                "source": os.path.relpath(path, ROOT)}
+                    except (KeyError, ValueError):
+                        return None
+    return None
+
+
 def make_objective(P, w):
     if w["kind"] == "mlp":
         return P.MlpWeights(w["in_dim"], w["hidden"], w["out_dim"], w["samples"], 1)
@@ -253,10 +273,13 @@ def main():
     pk, pk_kind = peaks()
     if w["kind"] == "mlp":
         achieved = FLOP_PER_EVAL_C2 * units / (fit_ms * 1e-3) / 1e12
+        tr = ncu_traffic("k_mlp_fitness")
         roof = {"kernel": "k_mlp_fitness<32> (tcgen05.mma kind::f16, TMA, TMEM)", "bound": "tensor",
                 "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / pk["bf16_tflops"], "traffic": None,
-                "algorithmic_per_launch": f"{units} sparks x {FLOP_PER_EVAL_C2} FLOP",
+                "frac": achieved / pk["bf16_tflops"], "traffic": tr["bytes"] if tr else None,
+                "traffic_source": tr["source"] if tr else None,
+                "algorithmic_per_launch": f"{units} sparks x {FLOP_PER_EVAL_C2} FLOP; operand bytes "
+                                          f"{units * 25472 * 2 + 1024 * 784 * 2} (bf16 W + X)",
                 "ms_per_launch": fit_ms, "peak_source": f"{pk_kind} bf16 burst (MEASURED_PEAKS.json)"}
     else:
         byts = units * w["D"] * 4 + w["B"] * w["mu"] * w["D"] * 4
