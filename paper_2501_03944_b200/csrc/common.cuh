@@ -55,9 +55,28 @@ __host__ __device__ __forceinline__ uint64_t key_prefix(uint64_t seed,
   return splitmix64(h ^ k);
 }
 
-// rng.hpp:55-57: (h >> 11) * 2^-53, exact (53-bit integer -> double).
+// D1 = 1 + (m mod 2^52) 2^-52 in [1, 2) for m = h >> 11, built from the bits
+// (no int -> fp conversion): mantissa = bits 11..62 of h.
+__device__ __forceinline__ double unit_d1(uint64_t h) {
+  const uint32_t hi = (uint32_t)(h >> 32);
+  const uint32_t lo = __funnelshift_r((uint32_t)h, hi, 11);  // bits 11..42 of h
+  const uint32_t mhi = (hi >> 11) & 0xFFFFFu;                 // bits 43..62 of h
+  return __hiloint2double((int)(0x3FF00000u | mhi), (int)lo);
+}
+
+// rng.hpp:55-57: u = (h >> 11) * 2^-53.  With top = bit 63 of h and
+// Dh = D1 / 2 in [0.5, 1) (same mantissa, exponent -1), u = Dh - (1 - top)/2:
+// the subtraction is exact (Sterbenz), so u is bit-identical to the
+// reference's value.  The constant is selected with integer ops.
 __device__ __forceinline__ double unit_u53(uint64_t h) {
-  return __dmul_rn(__ull2double_rn(h >> 11), 0x1.0p-53);
+  const uint32_t hi = (uint32_t)(h >> 32);
+  const uint32_t lo = __funnelshift_r((uint32_t)h, hi, 11);
+  const uint32_t mhi = (hi >> 11) & 0xFFFFFu;
+  const double dh = __hiloint2double((int)(0x3FE00000u | mhi), (int)lo);
+  int32_t sgn;  // arithmetic shift kept as such (not a 64-bit compare + select)
+  asm("shr.s32 %0, %1, 31;" : "=r"(sgn) : "r"(hi));
+  const uint32_t c_hi = 0x3FE00000u & ~(uint32_t)sgn;  // top ? 0 : 0.5
+  return __dsub_rn(dh, __hiloint2double((int)c_hi, 0));
 }
 
 // rng.hpp:60-65: lo + u * (hi - lo) (no contraction, same op order).

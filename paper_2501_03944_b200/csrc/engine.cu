@@ -107,6 +107,8 @@ static Status validate_config(const HostConfig& c) {
       if (!(b > 0.0) || !std::isfinite(b))
         return invalid("MgfwaConfig: boost coefficients must be positive finite");
     if (c.M > 16) return invalid("mgfwa_b200: guides_per_firework > 16 is not supported");
+    if (c.lam > kMaxSparksPerFirework)
+      return invalid("mgfwa_b200: sparks_per_firework > 16384 is not supported");
   }
   return ok();
 }

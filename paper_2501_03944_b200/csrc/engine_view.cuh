@@ -17,6 +17,7 @@
 
 namespace mgfwa_b200 {
 
+constexpr uint64_t kMaxSparksPerFirework = 16384;  // k_rank keys in shared memory
 constexpr int kChunk = 512;  // coordinates per warp work item (32 lanes x 4 x 4)
 
 struct Ctl {

@@ -2,7 +2,8 @@
 // core NN fitness, which lives in k_mlp_tc.cu).
 //
 // One generation = the body of run()'s loop, engine.cpp:359-417:
-//   k_pop_range      population_range            engine.cpp:22-41
+//   (population_range, engine.cpp:22-41, is computed by the previous
+//    generation's tail kernel k_record_copy)
 //   k_explode_map    explode + random_mapping    engine.cpp:78-131 (+ fused
 //                    analytic fitness partials, + bf16 shadow for NN)
 //   [NN fitness]     batched_apply(sparks)       backend.cpp:28-67
@@ -12,13 +13,13 @@
 //                    (kGuide), engine.cpp:133-196 (+ fused partials)
 //   [NN fitness]     batched_apply(guides)
 //   k_select         finalize guide fitness + select_best argmin +
-//                    update_amplitudes, engine.cpp:198-256
-//   k_select_copy    winner row copy (engine.cpp:232-233)
+//                    update_amplitudes + winner row copy, engine.cpp:198-256
 //   k_loser          loser_out decision, engine.cpp:258-286, 394-410
 //   k_fresh_rows     loser reinit rows (kReinit), engine.cpp:287-294
 //   [NN fitness]     batched_apply(losers)
 //   k_finalize_record loser fitness commit + record_wave, engine.cpp:340-351
-//   k_record_copy    best-position copy on strict improvement
+//   k_record_copy    best-position copy on strict improvement +
+//                    population_range of the next generation
 // All kernels read ctl->active / ctl->iteration from HBM so that one CUDA
 // graph replays every generation unchanged.
 #include "common.cuh"
@@ -141,14 +142,17 @@ __global__ void k_pop_range(EngineView v) {
 //
 // Work item = (firework, group of kSparkGroup sparks, 512-coordinate chunk):
 // the firework row, the box images and the pos -> fp64 conversions are
-// loaded once and reused by the 8 sparks of the group.  Per coordinate the
+// loaded once and reused by the sparks of the group.  Per coordinate the
 // cost is one splitmix64 round (hoisted key prefix), an exact bit-built
 // t = -1 + 2u (no int->fp conversion), one DMUL + DADD in fp64 and one
 // rounding to fp32.  The in-box test runs on the rounded float against the
-// fp32 box images (exact whenever strictly inside, see in_box_fast); the
-// rare remaining coordinates — out of the box (random mapping) or on the
-// 1-ulp boundary — are compacted across the warp and finished by one lane
-// each, so mapping work is paid per mapped coordinate, not per warp.
+// fp32 box images (exact whenever strictly inside, see in_box_fast).  The
+// remaining coordinates — out of the box (random mapping) or on the 1-ulp
+// boundary — are finished in place: whenever any lane of the warp has one
+// among a spark's 4 coordinates, the warp runs the exact test and the
+// kMapping draw for those 4 coordinates as 4 independent chains and selects
+// per lane.  Out-of-box coordinates are common (C2: about half of them once
+// the amplitudes reach the range), so this dense form beats compaction.
 constexpr int kSparkGroup = 4;
 
 // t = -1 + u * 2 for u = (h >> 11) * 2^-53, exactly as the reference's
@@ -158,52 +162,41 @@ constexpr int kSparkGroup = 4;
 // reference value without an int -> fp conversion.
 __device__ __forceinline__ double unit_pm1(uint64_t h) {
   const uint32_t hi = (uint32_t)(h >> 32);
-  const uint32_t lo = __funnelshift_r((uint32_t)h, hi, 11);  // bits 11..42 of h
-  const uint32_t mhi = (hi >> 11) & 0xFFFFFu;                 // bits 43..62 of h
-  const double d1 = __hiloint2double((int)(0x3FF00000u | mhi), (int)lo);
-  return __dsub_rn(d1, (hi >> 31) ? 1.0 : 2.0);
+  const uint32_t c_hi = 0x40000000u - ((hi >> 11) & 0x100000u);  // top ? 1.0 : 2.0
+  return __dsub_rn(unit_d1(h), __hiloint2double((int)c_hi, 0));
 }
 
 // Exact in-box test for x = round_f32(s): strictly between the fp32 box
 // images implies lower <= s <= upper (lo_f >= lower, and s > lo_f because
-// s rounds to a float above lo_f); callers fall back to map_coord otherwise.
+// s rounds to a float above lo_f); callers fall back to the exact test
+// otherwise.
 __device__ __forceinline__ bool in_box_fast(float x, float lo_f, float hi_f) {
   return x > lo_f && x < hi_f;
 }
 
 // Dynamic shared memory of k_explode_map: the block's 512-coordinate chunk
 // of the box (fp64 and its fp32 images) and of the population range,
-// staged once per work item, plus the per-warp slow-path queue.
+// staged once per work item, plus the per-warp key prefixes.
 struct ExplodeChunk {
   double lo[kChunk], hi[kChunk];
-  float lof[kChunk], hif[kChunk], plo[kChunk], phi[kChunk];
+  double plo[kChunk], pw[kChunk];  // pop_lo and (pop_hi - pop_lo) in fp64
+  float lof[kChunk], hif[kChunk];
 };
 struct ExplodeWarp {
-  double val[32 * kSparkGroup * 4];  // exact fp64 spark of each slow coordinate,
-                                     // then (aliased) its fp32 result
-  uint16_t slot[32 * kSparkGroup * 4];
-  uint64_t pre[2 * kSparkGroup];     // explode / mapping key prefixes
+  uint64_t pre[2 * kSparkGroup];  // explode / mapping key prefixes
 };
 constexpr size_t kExplodeSmem = sizeof(ExplodeChunk) + kWarps * sizeof(ExplodeWarp);
-
-// Exact repair of one coordinate from the staged chunk (== map_coord).
-__device__ __forceinline__ float map_coord_staged(const ExplodeChunk& ch, double x, uint32_t i,
-                                                  uint32_t d, uint64_t map_prefix) {
-  if (!(x >= ch.lo[i] && x <= ch.hi[i]))
-    x = uniform_draw(splitmix64(map_prefix ^ (uint64_t)d), (double)ch.plo[i], (double)ch.phi[i]);
-  return to_f32_in_box(x, ch.lof[i], ch.hif[i]);
-}
 
 // One 128-coordinate slice of kSparkGroup sparks.  FULL: every spark of the
 // group exists and the slice lies inside [0, D) (no per-element guards).
 template <int KIND, bool FULL>
 __device__ __forceinline__ void explode_slice(const EngineView& v, const ExplodeChunk& ch,
-                                              ExplodeWarp& wq, int lane, uint32_t cbase,
-                                              uint32_t qoff, uint64_t f, uint64_t k0, int kn,
-                                              double a, const uint64_t (&pe)[kSparkGroup],
+                                              int lane, uint32_t cbase, uint32_t qoff,
+                                              uint64_t f, uint64_t k0, int kn, double a,
+                                              const uint64_t (&pe)[kSparkGroup],
+                                              const uint64_t (&pm)[kSparkGroup],
                                               float (&s0)[kSparkGroup], float (&s1)[kSparkGroup]) {
   constexpr int KG = kSparkGroup;
-  constexpr int NSLOT = KG * 4;
   const uint32_t D = (uint32_t)v.D;
   const uint32_t li0 = qoff + lane * 4;  // index inside the staged chunk
   const uint32_t d0 = cbase + li0;
@@ -216,74 +209,61 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
   const double pd[4] = {(double)p4.x, (double)p4.y, (double)p4.z, (double)p4.w};
   const float lf[4] = {lf4.x, lf4.y, lf4.z, lf4.w};
   const float uf[4] = {uf4.x, uf4.y, uf4.z, uf4.w};
-  float x[KG][4];
-  double sv[KG][4];
-  unsigned slow = 0;
 #pragma unroll
   for (int kk = 0; kk < KG; ++kk) {
+    if (!FULL && kk >= kn) break;
+    float x[4];
+    double sv[4];
+    unsigned slow = 0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const uint64_t h = splitmix64(pe[kk] ^ (uint64_t)(d0 + e));
-      sv[kk][e] = __dadd_rn(pd[e], __dmul_rn(unit_pm1(h), a));
-      x[kk][e] = __double2float_rn(sv[kk][e]);
-      const bool need = !in_box_fast(x[kk][e], lf[e], uf[e]);
-      if (FULL ? need : (kk < kn && e < nvalid && need)) slow |= 1u << (kk * 4 + e);
+      sv[e] = __dadd_rn(pd[e], __dmul_rn(unit_pm1(h), a));
+      x[e] = __double2float_rn(sv[e]);
+      const bool need = !in_box_fast(x[e], lf[e], uf[e]);
+      if (FULL ? need : (e < nvalid && need)) slow |= 1u << e;
     }
-  }
-  // Out-of-box / boundary coordinates: compact across the warp, finish one
-  // per lane with the exact test + random mapping (shared-memory operands).
-  if (__any_sync(0xffffffffu, slow != 0)) {
-    const unsigned cnt = __popc(slow);
-    unsigned incl = cnt;
+    // Out-of-box / boundary coordinates of this spark: exact inclusive test
+    // (config.hpp:22-24) and the kMapping draw U[pop_lo, pop_hi)
+    // (engine.cpp:119-125), 4 independent chains, selected per lane.
+    if (__any_sync(0xffffffffu, slow != 0)) {
+      const double2 lo01 = *reinterpret_cast<const double2*>(&ch.lo[li0]);
+      const double2 lo23 = *reinterpret_cast<const double2*>(&ch.lo[li0 + 2]);
+      const double2 hi01 = *reinterpret_cast<const double2*>(&ch.hi[li0]);
+      const double2 hi23 = *reinterpret_cast<const double2*>(&ch.hi[li0 + 2]);
+      const double2 pl01 = *reinterpret_cast<const double2*>(&ch.plo[li0]);
+      const double2 pl23 = *reinterpret_cast<const double2*>(&ch.plo[li0 + 2]);
+      const double2 pw01 = *reinterpret_cast<const double2*>(&ch.pw[li0]);
+      const double2 pw23 = *reinterpret_cast<const double2*>(&ch.pw[li0 + 2]);
+      const double lo[4] = {lo01.x, lo01.y, lo23.x, lo23.y};
+      const double hi[4] = {hi01.x, hi01.y, hi23.x, hi23.y};
+      const double pl[4] = {pl01.x, pl01.y, pl23.x, pl23.y};
+      const double pw[4] = {pw01.x, pw01.y, pw23.x, pw23.y};
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
-    unsigned p = incl - cnt;
-#pragma unroll
-    for (int j = 0; j < NSLOT; ++j)
-      if (slow & (1u << j)) {
-        wq.val[p] = sv[j >> 2][j & 3];
-        wq.slot[p] = (uint16_t)((lane << 4) | j);
-        ++p;
+      for (int e = 0; e < 4; ++e) {
+        const uint64_t h = splitmix64(pm[kk] ^ (uint64_t)(d0 + e));
+        const float m = __double2float_rn(__dadd_rn(pl[e], __dmul_rn(unit_u53(h), pw[e])));
+        const float r = (sv[e] >= lo[e] && sv[e] <= hi[e]) ? x[e] : m;
+        x[e] = ((slow >> e) & 1u) ? fminf(fmaxf(r, lf[e]), uf[e]) : x[e];
       }
-    __syncwarp();
-    for (unsigned i = lane; i < total; i += 32) {
-      const unsigned sl = wq.slot[i];
-      const unsigned j = sl & 15u;
-      const uint32_t li = qoff + (sl >> 4) * 4 + (j & 3u);
-      const float r = map_coord_staged(ch, wq.val[i], li, cbase + li, wq.pre[KG + (j >> 2)]);
-      *reinterpret_cast<float*>(&wq.val[i]) = r;
     }
-    __syncwarp();
-    p = incl - cnt;
-#pragma unroll
-    for (int j = 0; j < NSLOT; ++j)
-      if (slow & (1u << j)) x[j >> 2][j & 3] = *reinterpret_cast<const float*>(&wq.val[p++]);
-    __syncwarp();
-  }
-  if (on) {
-#pragma unroll
-    for (int kk = 0; kk < KG; ++kk) {
-      if (!FULL && kk >= kn) break;
+    if (on) {
       if (!FULL) {
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-          if (e >= nvalid) x[kk][e] = 0.0f;
+          if (e >= nvalid) x[e] = 0.0f;
       }
       if (KIND != 0) {
         float a0 = 0.0f, a1 = 0.0f;
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-          if (FULL || e < nvalid) analytic_terms(KIND, x[kk][e], a0, a1);
+          if (FULL || e < nvalid) analytic_terms(KIND, x[e], a0, a1);
         s0[kk] += a0;
         s1[kk] += a1;
       }
       const uint64_t off = ((f - v.f_lo) * v.lam + k0 + kk) * v.Dp + d0;  // local spark row
-      *reinterpret_cast<float4*>(v.sparks + off) = make_float4(x[kk][0], x[kk][1], x[kk][2], x[kk][3]);
-      if (KIND == 0) store_bf16x4(v.sparks_h, off, x[kk]);
+      *reinterpret_cast<float4*>(v.sparks + off) = make_float4(x[0], x[1], x[2], x[3]);
+      if (KIND == 0) store_bf16x4(v.sparks_h, off, x);
     }
   }
 }
@@ -321,8 +301,10 @@ __global__ void __launch_bounds__(256, 2) k_explode_map(EngineView v) {
       ch.hi[i] = in ? v.upper[d] : 0.0;
       ch.lof[i] = in ? v.lower_f[d] : 0.0f;
       ch.hif[i] = in ? v.upper_f[d] : 0.0f;
-      ch.plo[i] = in ? v.pop_lo[b * v.Dp + d] : 0.0f;
-      ch.phi[i] = in ? v.pop_hi[b * v.Dp + d] : 0.0f;
+      const double pl = in ? (double)v.pop_lo[b * v.Dp + d] : 0.0;
+      const double ph = in ? (double)v.pop_hi[b * v.Dp + d] : 0.0;
+      ch.plo[i] = pl;
+      ch.pw[i] = __dsub_rn(ph, pl);
     }
     __syncthreads();
     const uint64_t g = sup * kWarps + warp;
@@ -336,9 +318,12 @@ __global__ void __launch_bounds__(256, 2) k_explode_map(EngineView v) {
     else if (lane >= KG && lane < KG + kn)
       wq.pre[lane] = key_prefix(v.seed, kMapping, it, b, n, k0 + lane - KG);
     __syncwarp();
-    uint64_t pe[KG];
+    uint64_t pe[KG], pm[KG];
 #pragma unroll
-    for (int kk = 0; kk < KG; ++kk) pe[kk] = wq.pre[kk];
+    for (int kk = 0; kk < KG; ++kk) {
+      pe[kk] = wq.pre[kk];
+      pm[kk] = wq.pre[KG + kk];
+    }
     const double a = v.amp[f];
     float s0[KG], s1[KG];
 #pragma unroll
@@ -348,9 +333,9 @@ __global__ void __launch_bounds__(256, 2) k_explode_map(EngineView v) {
       const uint32_t qoff = q * 128;
       if (cbase + qoff >= D) break;  // warp-uniform
       if (kn == KG && cbase + qoff + 128 <= D)
-        explode_slice<KIND, true>(v, ch, wq, lane, cbase, qoff, f, k0, kn, a, pe, s0, s1);
+        explode_slice<KIND, true>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, s0, s1);
       else
-        explode_slice<KIND, false>(v, ch, wq, lane, cbase, qoff, f, k0, kn, a, pe, s0, s1);
+        explode_slice<KIND, false>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, s0, s1);
     }
     if (KIND != 0) {
 #pragma unroll
@@ -380,6 +365,10 @@ static void explode_launch_k(const EngineView& v, unsigned grid, cudaStream_t s)
   k_explode_map<KIND><<<grid, 256, kExplodeSmem, s>>>(v);
 }
 
+constexpr int kRankThreads = 1024;
+constexpr int kRankSmemMax = (int)(kMaxSparksPerFirework * sizeof(uint64_t));
+__global__ void __launch_bounds__(kRankThreads) k_rank(EngineView v);
+
 cudaError_t prepare_engine_kernels() {
   cudaError_t e = cudaSuccess;
   const int bytes = (int)kExplodeSmem;
@@ -387,6 +376,7 @@ cudaError_t prepare_engine_kernels() {
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<OBJ_SPHERE>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<OBJ_RASTRIGIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<OBJ_ACKLEY>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, kRankSmemMax);
   return e;
 }
 
@@ -414,68 +404,65 @@ __device__ __forceinline__ uint64_t rank_key(float x, uint32_t k) {
   return ((uint64_t)u << 32) | k;
 }
 
-__global__ void __launch_bounds__(256) k_rank(EngineView v) {
+__global__ void __launch_bounds__(kRankThreads) k_rank(EngineView v) {
   if (gen_inactive(v)) return;
-  extern __shared__ uint64_t keys[];  // next_pow2(lambda) sort keys
-  const uint64_t f = blockIdx.x;
+  extern __shared__ uint64_t keys[];  // [lambda] sort keys
+  const uint64_t fl = blockIdx.x;     // local firework
   const uint32_t lam = (uint32_t)v.lam;
-  uint32_t n = 1;
-  while (n < lam) n <<= 1;
   unsigned nan_local = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  for (uint32_t k = lam + threadIdx.x; k < n; k += blockDim.x) keys[k] = ~0ull;
   constexpr int R = 4;  // rows per warp step (loads of 4 rows in flight)
   for (uint32_t k0 = warp * R; k0 < lam; k0 += nwarp * R) {
     int64_t rows[R];
     float x[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) rows[r] = (k0 + r < lam) ? (int64_t)(f * lam + k0 + r) : -1;
+    for (int r = 0; r < R; ++r) rows[r] = (k0 + r < lam) ? (int64_t)(fl * lam + k0 + r) : -1;
     if (v.injected_fitness) {
 #pragma unroll
       for (int r = 0; r < R; ++r) x[r] = rows[r] >= 0 ? v.sfit[rows[r]] : 0.0f;
     } else {
       finalize_rows<R>(v, v.spart, rows, x, nan_local);
     }
-    if (lane == 0) {
+    float xl = x[0];
+    int64_t rl = rows[0];
 #pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (rows[r] >= 0) {
-          if (!v.injected_fitness) v.sfit[rows[r]] = x[r];
-          keys[k0 + r] = rank_key(x[r], k0 + r);
-        }
+    for (int r = 1; r < R; ++r) {
+      xl = lane == r ? x[r] : xl;
+      rl = lane == r ? rows[r] : rl;
+    }
+    if (lane < R && rl >= 0) {
+      if (!v.injected_fitness) v.sfit[rl] = xl;
+      keys[k0 + lane] = rank_key(xl, k0 + lane);
     }
   }
   if (lane == 0 && nan_local)
     atomicAdd((unsigned long long*)&v.ctl->nan_count, (unsigned long long)nan_local);
   if (v.M == 0) return;
   __syncthreads();
-  // bitonic sort of the keys (ascending) — a total order, so the result is
-  // exactly std::sort with the reference comparator (engine.cpp:152-157)
-  for (uint32_t k = 2; k <= n; k <<= 1)
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const uint32_t ixj = i ^ j;
-        if (ixj > i) {
-          const uint64_t a = keys[i], b = keys[ixj];
-          if ((a > b) == ((i & k) == 0)) {
-            keys[i] = b;
-            keys[ixj] = a;
-          }
-        }
-      }
-      __syncthreads();
-    }
+  // Rank by counting: keys are a total order with distinct values, so
+  // rank(k) = #{j : key_j < key_k} is the position std::sort with the
+  // reference comparator (engine.cpp:152-157) gives spark k.  All threads
+  // read the same key_j at once (shared-memory broadcast); no barriers.
   const uint32_t top = (uint32_t)v.top;
-  for (uint32_t t = threadIdx.x; t < top; t += blockDim.x) {
-    v.rank_idx[f * 2 * top + t] = (int)(uint32_t)keys[t];
-    v.rank_idx[f * 2 * top + top + t] = (int)(uint32_t)keys[lam - top + t];
+  int* out = v.rank_idx + fl * 2 * top;
+  for (uint32_t k = threadIdx.x; k < lam; k += blockDim.x) {
+    const uint64_t kk = keys[k];
+    uint32_t r0 = 0, r1 = 0;
+    uint32_t j = 0;
+    for (; j + 2 <= lam; j += 2) {
+      const ulonglong2 q = *reinterpret_cast<const ulonglong2*>(&keys[j]);
+      r0 += q.x < kk;
+      r1 += q.y < kk;
+    }
+    if (j < lam) r0 += keys[j] < kk;
+    const uint32_t r = r0 + r1;
+    if (r < top) out[r] = (int)k;
+    if (r >= lam - top) out[top + (r - (lam - top))] = (int)k;
   }
 }
 
 static size_t rank_smem(const EngineView& v) {
-  uint64_t n = 1;
-  while (n < v.lam) n <<= 1;
-  return n * sizeof(uint64_t);
+  return ((v.lam + 1) & ~1ull) * sizeof(uint64_t);
 }
 
 // ----------------------------------------------------------------- guides
@@ -557,14 +544,17 @@ __global__ void __launch_bounds__(256) k_guides(EngineView v) {
 // ----------------------------------------------------------------- select
 // select_best (engine.cpp:198-242): strict-< scan firework -> sparks k up ->
 // guides m up == lexicographic min of (value, scan order).  Then
-// update_amplitudes (engine.cpp:244-256) and the wave accounting
-// (engine.cpp:388-390).  One block per firework.
-__global__ void __launch_bounds__(256) k_select(EngineView v) {
+// update_amplitudes (engine.cpp:244-256), the wave accounting
+// (engine.cpp:388-390) and the winner row copy (engine.cpp:232-233).  One
+// block per firework.
+constexpr int kSelectThreads = 512;
+__global__ void __launch_bounds__(kSelectThreads) k_select(EngineView v) {
   if (gen_inactive(v)) return;
   const uint64_t fl = blockIdx.x, f = v.f_lo + fl;  // local / global firework
-  __shared__ double sv[8];
-  __shared__ int so[8];
+  __shared__ double sv[kSelectThreads / 32];
+  __shared__ int so[kSelectThreads / 32];
   __shared__ float gs[16];
+  __shared__ int s_win;
   unsigned nan_local = 0;
   // guide fitness: one warp per guide row (warp-cooperative finalize)
   for (uint64_t m = threadIdx.x >> 5; m < v.M; m += blockDim.x >> 5) {
@@ -628,30 +618,26 @@ __global__ void __launch_bounds__(256) k_select(EngineView v) {
     const double a = v.amp[f] * (imp ? v.amp_amplify : v.amp_reduce);
     v.amp[f] = a < v.amp_floor ? v.amp_floor : (v.max_range < a ? v.max_range : a);
     if (fl == 0) v.ctl->used += v.wave;  // the global wave, on every rank
+    s_win = best_o;
   }
-}
-
-// Copy the winning row into the firework (engine.cpp:232-233).
-__global__ void __launch_bounds__(256) k_select_copy(EngineView v) {
-  if (gen_inactive(v)) return;
-  const int lane = threadIdx.x & 31;
-  const uint64_t items = v.Fl * v.nch;
-  for (uint64_t item = blockIdx.x * (uint64_t)kWarps + (threadIdx.x >> 5);
-       item < items; item += (uint64_t)gridDim.x * kWarps) {
-    const uint64_t fl = item / v.nch, c = item % v.nch, f = v.f_lo + fl;
-    const int w = v.winner[f];
-    if (w == 0) continue;
-    const float* src = (uint64_t)w <= v.lam
-                           ? v.sparks + (fl * v.lam + (w - 1)) * v.Dp
-                           : v.guides + (fl * v.M + (w - 1 - v.lam)) * v.Dp;
-    float* dst = v.pos + f * v.Dp;
+  __syncthreads();
+  // winner row -> firework row (padding included: rows are Dp wide)
+  const int w = s_win;
+  if (w == 0) return;
+  const float4* src = reinterpret_cast<const float4*>(
+      (uint64_t)w <= v.lam ? v.sparks + (fl * v.lam + (w - 1)) * v.Dp
+                           : v.guides + (fl * v.M + (w - 1 - v.lam)) * v.Dp);
+  float4* dst = reinterpret_cast<float4*>(v.pos + f * v.Dp);
+  const uint64_t n4 = (v.D + 3) / 4;
+  uint64_t i = threadIdx.x;
+  for (; i + 3 * kSelectThreads < n4; i += 4 * kSelectThreads) {
+    float4 t[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint64_t d0 = c * kChunk + q * 128 + lane * 4;
-      if (d0 < v.D)
-        *reinterpret_cast<float4*>(dst + d0) = *reinterpret_cast<const float4*>(src + d0);
-    }
+    for (int u = 0; u < 4; ++u) t[u] = src[i + u * kSelectThreads];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dst[i + u * kSelectThreads] = t[u];
   }
+  for (; i < n4; i += kSelectThreads) dst[i] = src[i];
 }
 
 // ------------------------------------------------------------------ loser
@@ -838,21 +824,40 @@ __global__ void k_finalize_record(EngineView v, int mode) {
   }
 }
 
-// Best-position copy on strict improvement (engine.cpp:343-346).
+// Tail of a generation (and of initialize): the best-position copy on strict
+// improvement (engine.cpp:343-346) and population_range (engine.cpp:22-41)
+// of the NEXT generation's pre-selection state, which is final here.  Work
+// item = (batch, 512-coordinate chunk) per warp, float4 per lane.
 __global__ void __launch_bounds__(256) k_record_copy(EngineView v) {
   const int lane = threadIdx.x & 31;
   const uint64_t items = v.B * v.nch;
   for (uint64_t item = blockIdx.x * (uint64_t)kWarps + (threadIdx.x >> 5);
        item < items; item += (uint64_t)gridDim.x * kWarps) {
     const uint64_t b = item / v.nch, c = item % v.nch;
-    if (!v.rec_flag[b]) continue;
+    const bool copy = v.rec_flag[b] != 0;
     const float* src = v.pos + (b * v.mu + v.best_idx[b]) * v.Dp;
     float* dst = v.best_pos + b * v.Dp;
+    const float* pb = v.pos + b * v.mu * v.Dp;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint64_t d0 = c * kChunk + q * 128 + lane * 4;
-      if (d0 < v.D)
-        *reinterpret_cast<float4*>(dst + d0) = *reinterpret_cast<const float4*>(src + d0);
+      if (d0 >= v.D) break;
+      if (copy) *reinterpret_cast<float4*>(dst + d0) = *reinterpret_cast<const float4*>(src + d0);
+      // std::min / std::max keep-first order over n = 0..mu-1
+      float4 mn = *reinterpret_cast<const float4*>(pb + d0), mx = mn;
+      for (uint64_t n = 1; n < v.mu; ++n) {
+        const float4 x = *reinterpret_cast<const float4*>(pb + n * v.Dp + d0);
+        mn.x = x.x < mn.x ? x.x : mn.x;
+        mn.y = x.y < mn.y ? x.y : mn.y;
+        mn.z = x.z < mn.z ? x.z : mn.z;
+        mn.w = x.w < mn.w ? x.w : mn.w;
+        mx.x = mx.x < x.x ? x.x : mx.x;
+        mx.y = mx.y < x.y ? x.y : mx.y;
+        mx.z = mx.z < x.z ? x.z : mx.z;
+        mx.w = mx.w < x.w ? x.w : mx.w;
+      }
+      *reinterpret_cast<float4*>(v.pop_lo + b * v.Dp + d0) = mn;
+      *reinterpret_cast<float4*>(v.pop_hi + b * v.Dp + d0) = mx;
     }
   }
 }
@@ -993,10 +998,11 @@ static unsigned capped(uint64_t g, int nsm) {
 void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
                                GenerationHooks* hooks, int phase) {
   if (phase != kGenB) {
-    k_pop_range<<<capped((v.B * v.D + 255) / 256, nsm), 256, 0, s>>>(v);
+    // population_range of this generation was computed by the previous
+    // generation's (or initialize's) tail kernel, k_record_copy.
     launch_explode_map_impl(v, nsm, s);
     if (v.nn) hooks->eval_sparks(hooks->ctx, s);
-    k_rank<<<(unsigned)v.Fl, 256, rank_smem(v), s>>>(v);
+    k_rank<<<(unsigned)v.Fl, kRankThreads, rank_smem(v), s>>>(v);
     if (v.M > 0) {
       k_guides<<<guide_blocks(v, nsm), 256, 2 * v.top * sizeof(int), s>>>(v);
       if (v.nn)
@@ -1004,8 +1010,7 @@ void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
       else
         launch_analytic_partials(v.guides, v.Fl * v.M, v.D, v.Dp, v.nch, v.obj_kind, v.gpart, nsm, s);
     }
-    k_select<<<(unsigned)v.Fl, 256, 0, s>>>(v);
-    k_select_copy<<<capped((v.Fl * v.nch + kWarps - 1) / kWarps, nsm), 256, 0, s>>>(v);
+    k_select<<<(unsigned)v.Fl, kSelectThreads, 0, s>>>(v);
   }
   if (phase != kGenA) {
     k_loser<<<1, 128, 0, s>>>(v);
@@ -1054,16 +1059,15 @@ void launch_explode_map(const EngineView& v, int nsm, cudaStream_t s) {
   launch_explode_map_impl(v, nsm, s);
 }
 void launch_rank(const EngineView& v, cudaStream_t s) {
-  k_rank<<<(unsigned)v.Fl, 256, rank_smem(v), s>>>(v);
+  k_rank<<<(unsigned)v.Fl, kRankThreads, rank_smem(v), s>>>(v);
 }
 void launch_guides(const EngineView& v, int nsm, cudaStream_t s) {
   k_guides<<<guide_blocks(v, nsm), 256, 2 * v.top * sizeof(int), s>>>(v);
   if (!v.nn) launch_analytic_partials(v.guides, v.Fl * v.M, v.D, v.Dp, v.nch, v.obj_kind, v.gpart, nsm, s);
 }
 void launch_select(const EngineView& v, int nsm, cudaStream_t s) {
-  const unsigned g = (unsigned)((v.Fl * v.nch + kWarps - 1) / kWarps);
-  k_select<<<(unsigned)v.Fl, 256, 0, s>>>(v);
-  k_select_copy<<<g < (unsigned)nsm * 16 ? g : nsm * 16, 256, 0, s>>>(v);
+  (void)nsm;
+  k_select<<<(unsigned)v.Fl, kSelectThreads, 0, s>>>(v);
 }
 void launch_loser(const EngineView& v, int nsm, cudaStream_t s) {
   const unsigned g = (unsigned)((v.F * v.nch + kWarps - 1) / kWarps);

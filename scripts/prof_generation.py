@@ -1,9 +1,9 @@
 """Profiling driver: a few C2 generations with a fixed kernel order, for
 `ncu -k regex:<kernel> -s <skip> -c 1` captures of the hot kernels.
 
-Launch order per generation (graph replay): k_pop_range, k_explode_map,
+Launch order per generation (graph replay): k_explode_map,
 k_mlp_fitness(sparks), k_rank, k_guides, k_mlp_fitness(guides), k_select,
-k_select_copy, k_loser, k_fresh_rows, k_mlp_fitness(fresh),
+k_loser, k_fresh_rows, k_mlp_fitness(fresh),
 k_finalize_record, k_record_copy.  initialize() launches k_fresh_rows,
 k_mlp_fitness(fresh), k_finalize_record, k_record_copy first.
 """
