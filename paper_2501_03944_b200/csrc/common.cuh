@@ -9,6 +9,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 namespace mgfwa_b200 {
 
@@ -129,6 +130,46 @@ __device__ __forceinline__ float analytic_finalize(int kind, float s0,
            2.718281828459045f;
   }
   return s0;
+}
+
+// Programmatic dependent launch (every engine kernel is launched with
+// programmatic stream serialization, see pdl_launch): wait until the
+// previous kernel has completed and its writes are visible; must precede
+// any global access.  TRIGGER: first allow the next kernel in the stream to
+// be scheduled now (used by the short latency-bound kernels only — an early
+// trigger from the long kernels measured slower).
+template <bool TRIGGER = false>
+__device__ __forceinline__ void pdl_enter() {
+  if (TRIGGER) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+// Launch with programmatic stream serialization: the launch (and block
+// scheduling) of a kernel overlaps the tail of its predecessor; the kernel's
+// pdl_enter() keeps the data dependency.  Works inside stream capture
+// (programmatic graph edges).  MGFWA_PDL=0 disables it.
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("MGFWA_PDL");
+    return e == nullptr || e[0] != '0';
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
 __device__ __forceinline__ uint64_t global_ns() {

@@ -118,6 +118,7 @@ __device__ __forceinline__ void store_bf16x4(__nv_bfloat16* dst_h, uint64_t off,
 // ------------------------------------------------------------------ range
 // population_range, engine.cpp:22-41 (std::min/std::max keep-first order).
 __global__ void k_pop_range(EngineView v) {
+  pdl_enter();
   if (gen_inactive(v)) return;
   const uint64_t total = v.B * v.D;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
@@ -275,6 +276,7 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
 // analytic objective kind whose partial sums are fused in.
 template <int KIND>
 __global__ void __launch_bounds__(256, 2) k_explode_map(EngineView v) {
+  pdl_enter();
   if (gen_inactive(v)) return;
   constexpr int KG = kSparkGroup;
   extern __shared__ __align__(16) uint8_t ex_smem[];
@@ -362,7 +364,7 @@ static unsigned explode_blocks(const EngineView& v, int nsm) {
 
 template <int KIND>
 static void explode_launch_k(const EngineView& v, unsigned grid, cudaStream_t s) {
-  k_explode_map<KIND><<<grid, 256, kExplodeSmem, s>>>(v);
+  pdl_launch(k_explode_map<KIND>, grid, 256, kExplodeSmem, s, v);
 }
 
 constexpr int kRankThreads = 1024;
@@ -405,6 +407,7 @@ __device__ __forceinline__ uint64_t rank_key(float x, uint32_t k) {
 }
 
 __global__ void __launch_bounds__(kRankThreads) k_rank(EngineView v) {
+  pdl_enter<true>();
   if (gen_inactive(v)) return;
   extern __shared__ uint64_t keys[];  // [lambda] sort keys
   const uint64_t fl = blockIdx.x;     // local firework
@@ -475,6 +478,7 @@ static size_t rank_smem(const EngineView& v) {
 // the guides is computed afterwards by k_analytic_partials (same grouping as
 // every other fitness, so cached fitness == re-evaluated fitness bit-wise).
 __global__ void __launch_bounds__(256) k_guides(EngineView v) {
+  pdl_enter();
   if (gen_inactive(v)) return;
   extern __shared__ int s_idx[];  // [2*top]: rank lists of the block's firework
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -549,6 +553,7 @@ __global__ void __launch_bounds__(256) k_guides(EngineView v) {
 // block per firework.
 constexpr int kSelectThreads = 512;
 __global__ void __launch_bounds__(kSelectThreads) k_select(EngineView v) {
+  pdl_enter<true>();
   if (gen_inactive(v)) return;
   const uint64_t fl = blockIdx.x, f = v.f_lo + fl;  // local / global firework
   __shared__ double sv[kSelectThreads / 32];
@@ -622,11 +627,11 @@ __global__ void __launch_bounds__(kSelectThreads) k_select(EngineView v) {
   }
   __syncthreads();
   // winner row -> firework row (padding included: rows are Dp wide)
-  const int w = s_win;
-  if (w == 0) return;
+  const int win = s_win;
+  if (win == 0) return;
   const float4* src = reinterpret_cast<const float4*>(
-      (uint64_t)w <= v.lam ? v.sparks + (fl * v.lam + (w - 1)) * v.Dp
-                           : v.guides + (fl * v.M + (w - 1 - v.lam)) * v.Dp);
+      (uint64_t)win <= v.lam ? v.sparks + (fl * v.lam + (win - 1)) * v.Dp
+                             : v.guides + (fl * v.M + (win - 1 - v.lam)) * v.Dp);
   float4* dst = reinterpret_cast<float4*>(v.pos + f * v.Dp);
   const uint64_t n4 = (v.D + 3) / 4;
   uint64_t i = threadIdx.x;
@@ -644,6 +649,7 @@ __global__ void __launch_bounds__(kSelectThreads) k_select(EngineView v) {
 // loser_out decision (engine.cpp:258-286) with iterations_remaining from
 // engine.cpp:394-410 (device clock for the wall-clock budget).  One block.
 __global__ void k_loser(EngineView v) {
+  pdl_enter<true>();
   __shared__ int count;
   if (threadIdx.x == 0) count = 0;
   __syncthreads();
@@ -702,6 +708,7 @@ __global__ void k_loser(EngineView v) {
 // mode 0: initialize (engine.cpp:56-64): every firework, kInit, iteration 0.
 // mode 1: loser reinit (engine.cpp:287-294): losers only, kReinit.
 __global__ void __launch_bounds__(256) k_fresh_rows(EngineView v, int mode) {
+  pdl_enter<true>();
   if (mode == 1 && (gen_inactive(v) || v.ctl->n_losers == 0)) return;
   if (mode == 0 && blockIdx.x == 0 && threadIdx.x == 0) v.ctl->start_ns = global_ns();
   const int lane = threadIdx.x & 31;
@@ -755,6 +762,7 @@ __global__ void __launch_bounds__(256) k_fresh_rows(EngineView v, int mode) {
 // improvement; one trace point per batch.  Then the loop-top termination
 // test (engine.cpp:360-367) for the next generation.  One block.
 __global__ void k_finalize_record(EngineView v, int mode) {
+  pdl_enter<true>();
   Ctl* ctl = v.ctl;
   if (mode == 1 && gen_inactive(v)) {
     for (uint64_t b = threadIdx.x; b < v.B; b += blockDim.x) v.rec_flag[b] = 0;
@@ -826,40 +834,58 @@ __global__ void k_finalize_record(EngineView v, int mode) {
 
 // Tail of a generation (and of initialize): the best-position copy on strict
 // improvement (engine.cpp:343-346) and population_range (engine.cpp:22-41)
-// of the NEXT generation's pre-selection state, which is final here.  Work
-// item = (batch, 512-coordinate chunk) per warp, float4 per lane.
+// of the NEXT generation's pre-selection state, which is final here.  One
+// float4 of coordinates per thread (grid-stride), the mu rows' loads in
+// flight together.
 __global__ void __launch_bounds__(256) k_record_copy(EngineView v) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t items = v.B * v.nch;
-  for (uint64_t item = blockIdx.x * (uint64_t)kWarps + (threadIdx.x >> 5);
-       item < items; item += (uint64_t)gridDim.x * kWarps) {
-    const uint64_t b = item / v.nch, c = item % v.nch;
-    const bool copy = v.rec_flag[b] != 0;
-    const float* src = v.pos + (b * v.mu + v.best_idx[b]) * v.Dp;
-    float* dst = v.best_pos + b * v.Dp;
-    const float* pb = v.pos + b * v.mu * v.Dp;
+  pdl_enter<true>();
+  const uint64_t n4 = (v.D + 3) / 4, items = v.B * n4;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < items;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t b = i / n4, d0 = (i % n4) * 4;
+    const float* pb = v.pos + b * v.mu * v.Dp + d0;
+    if (v.rec_flag[b])
+      *reinterpret_cast<float4*>(v.best_pos + b * v.Dp + d0) =
+          *reinterpret_cast<const float4*>(pb + (uint64_t)v.best_idx[b] * v.Dp);
+    // std::min / std::max keep-first order over n = 0..mu-1
+    float4 mn = *reinterpret_cast<const float4*>(pb), mx = mn;
+    uint64_t n = 1;
+    for (; n + 4 <= v.mu; n += 4) {
+      float4 x[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint64_t d0 = c * kChunk + q * 128 + lane * 4;
-      if (d0 >= v.D) break;
-      if (copy) *reinterpret_cast<float4*>(dst + d0) = *reinterpret_cast<const float4*>(src + d0);
-      // std::min / std::max keep-first order over n = 0..mu-1
-      float4 mn = *reinterpret_cast<const float4*>(pb + d0), mx = mn;
-      for (uint64_t n = 1; n < v.mu; ++n) {
-        const float4 x = *reinterpret_cast<const float4*>(pb + n * v.Dp + d0);
-        mn.x = x.x < mn.x ? x.x : mn.x;
-        mn.y = x.y < mn.y ? x.y : mn.y;
-        mn.z = x.z < mn.z ? x.z : mn.z;
-        mn.w = x.w < mn.w ? x.w : mn.w;
-        mx.x = mx.x < x.x ? x.x : mx.x;
-        mx.y = mx.y < x.y ? x.y : mx.y;
-        mx.z = mx.z < x.z ? x.z : mx.z;
-        mx.w = mx.w < x.w ? x.w : mx.w;
+      for (int u = 0; u < 4; ++u) x[u] = *reinterpret_cast<const float4*>(pb + (n + u) * v.Dp);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        mn.x = x[u].x < mn.x ? x[u].x : mn.x;
+        mn.y = x[u].y < mn.y ? x[u].y : mn.y;
+        mn.z = x[u].z < mn.z ? x[u].z : mn.z;
+        mn.w = x[u].w < mn.w ? x[u].w : mn.w;
+        mx.x = mx.x < x[u].x ? x[u].x : mx.x;
+        mx.y = mx.y < x[u].y ? x[u].y : mx.y;
+        mx.z = mx.z < x[u].z ? x[u].z : mx.z;
+        mx.w = mx.w < x[u].w ? x[u].w : mx.w;
       }
-      *reinterpret_cast<float4*>(v.pop_lo + b * v.Dp + d0) = mn;
-      *reinterpret_cast<float4*>(v.pop_hi + b * v.Dp + d0) = mx;
     }
+    for (; n < v.mu; ++n) {
+      const float4 x = *reinterpret_cast<const float4*>(pb + n * v.Dp);
+      mn.x = x.x < mn.x ? x.x : mn.x;
+      mn.y = x.y < mn.y ? x.y : mn.y;
+      mn.z = x.z < mn.z ? x.z : mn.z;
+      mn.w = x.w < mn.w ? x.w : mn.w;
+      mx.x = mx.x < x.x ? x.x : mx.x;
+      mx.y = mx.y < x.y ? x.y : mx.y;
+      mx.z = mx.z < x.z ? x.z : mx.z;
+      mx.w = mx.w < x.w ? x.w : mx.w;
+    }
+    *reinterpret_cast<float4*>(v.pop_lo + b * v.Dp + d0) = mn;
+    *reinterpret_cast<float4*>(v.pop_hi + b * v.Dp + d0) = mx;
   }
+}
+
+static unsigned tail_blocks(const EngineView& v, int nsm) {
+  const uint64_t g = (v.B * ((v.D + 3) / 4) + 255) / 256;
+  const uint64_t cap = (uint64_t)nsm * 8;
+  return (unsigned)(g == 0 ? 1 : (g < cap ? g : cap));
 }
 
 // ------------------------------------------------------- operator seams
@@ -871,6 +897,7 @@ __global__ void __launch_bounds__(256) k_analytic_partials(const float* rows,
                                                           uint32_t nch,
                                                           int kind,
                                                           float* part) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const uint64_t items = nrows * nch;
   for (uint64_t item = blockIdx.x * (uint64_t)kWarps + (threadIdx.x >> 5);
@@ -902,6 +929,7 @@ __global__ void __launch_bounds__(256) k_analytic_partials(const float* rows,
 // fitness[r] = finalize(part[r]) with NaN -> +inf; *nan += #NaN.
 __global__ void k_finalize_rows(EngineView v, const float* part, uint64_t nrows,
                                 float* fitness, unsigned long long* nan) {
+  pdl_enter();
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
   for (uint64_t r = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < nrows;
        r += warps) {  // one warp per row
@@ -916,6 +944,7 @@ __global__ void k_finalize_rows(EngineView v, const float* part, uint64_t nrows,
 
 // fp32 rows -> bf16 rows (tensor-core operand), padding untouched.
 __global__ void k_to_bf16(const float* src, __nv_bfloat16* dst, uint64_t n) {
+  pdl_enter();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
     dst[i] = __float2bfloat16_rn(src[i]);
@@ -926,6 +955,7 @@ __global__ void k_to_bf16(const float* src, __nv_bfloat16* dst, uint64_t n) {
 __global__ void k_map_rows(EngineView v, const float* cand, float* out,
                            uint64_t rows, uint64_t per, uint64_t stream,
                            uint64_t it) {
+  pdl_enter();
   const uint64_t total = v.B * rows * v.D;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
        i += (uint64_t)gridDim.x * blockDim.x) {
@@ -941,6 +971,7 @@ __global__ void k_map_rows(EngineView v, const float* cand, float* out,
 // argmin_per_population (backend.cpp:69-83): strict <, lowest index wins.
 __global__ void k_argmin_rows(const double* fit, uint64_t rows, uint64_t cols,
                               uint64_t* idx, double* val) {
+  pdl_enter();
   for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < rows;
        b += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t bi = 0;
@@ -954,6 +985,7 @@ __global__ void k_argmin_rows(const double* fit, uint64_t rows, uint64_t cols,
 
 // key_hash (rng.hpp:43-52) for n keys [n][7].
 __global__ void k_key_hash(const uint64_t* keys, uint64_t n, uint64_t* out) {
+  pdl_enter();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t* k = keys + 7 * i;
@@ -966,17 +998,17 @@ void launch_map_rows(const EngineView& v, const float* cand, float* out,
                      cudaStream_t s) {
   const uint64_t total = v.B * rows * v.D;
   const unsigned g = (unsigned)((total + 255) / 256);
-  k_map_rows<<<g < 4096 ? (g ? g : 1) : 4096, 256, 0, s>>>(v, cand, out, rows, per, stream, it);
+  pdl_launch(k_map_rows, g < 4096 ? (g ? g : 1) : 4096, 256, 0, s, v, cand, out, rows, per, stream, it);
 }
 
 void launch_argmin_rows(const double* fit, uint64_t rows, uint64_t cols,
                         uint64_t* idx, double* val, cudaStream_t s) {
-  k_argmin_rows<<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(fit, rows, cols, idx, val);
+  pdl_launch(k_argmin_rows, (unsigned)((rows + 127) / 128), 128, 0, s, fit, rows, cols, idx, val);
 }
 
 void launch_key_hash(const uint64_t* keys, uint64_t n, uint64_t* out,
                      cudaStream_t s) {
-  k_key_hash<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(keys, n, out);
+  pdl_launch(k_key_hash, (unsigned)((n + 255) / 256), 256, 0, s, keys, n, out);
 }
 
 // ---------------------------------------------------------------- launch
@@ -1002,22 +1034,22 @@ void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
     // generation's (or initialize's) tail kernel, k_record_copy.
     launch_explode_map_impl(v, nsm, s);
     if (v.nn) hooks->eval_sparks(hooks->ctx, s);
-    k_rank<<<(unsigned)v.Fl, kRankThreads, rank_smem(v), s>>>(v);
+    pdl_launch(k_rank, (unsigned)v.Fl, kRankThreads, rank_smem(v), s, v);
     if (v.M > 0) {
-      k_guides<<<guide_blocks(v, nsm), 256, 2 * v.top * sizeof(int), s>>>(v);
+      pdl_launch(k_guides, guide_blocks(v, nsm), 256, 2 * v.top * sizeof(int), s, v);
       if (v.nn)
         hooks->eval_guides(hooks->ctx, s);
       else
         launch_analytic_partials(v.guides, v.Fl * v.M, v.D, v.Dp, v.nch, v.obj_kind, v.gpart, nsm, s);
     }
-    k_select<<<(unsigned)v.Fl, kSelectThreads, 0, s>>>(v);
+    pdl_launch(k_select, (unsigned)v.Fl, kSelectThreads, 0, s, v);
   }
   if (phase != kGenA) {
-    k_loser<<<1, 128, 0, s>>>(v);
-    k_fresh_rows<<<capped((v.F * v.nch + kWarps - 1) / kWarps, nsm), 256, 0, s>>>(v, 1);
+    pdl_launch(k_loser, 1, 128, 0, s, v);
+    pdl_launch(k_fresh_rows, capped((v.F * v.nch + kWarps - 1) / kWarps, nsm), 256, 0, s, v, 1);
     if (v.nn) hooks->eval_fresh(hooks->ctx, s);
-    k_finalize_record<<<1, 256, 0, s>>>(v, 1);
-    k_record_copy<<<capped((v.B * v.nch + kWarps - 1) / kWarps, nsm), 256, 0, s>>>(v);
+    pdl_launch(k_finalize_record, 1, 256, 0, s, v, 1);
+    pdl_launch(k_record_copy, tail_blocks(v, nsm), 256, 0, s, v);
   }
 }
 
@@ -1025,33 +1057,33 @@ void launch_initialize_kernels(const EngineView& v, int nsm, cudaStream_t s,
                                GenerationHooks* hooks) {
   const unsigned items_f = (unsigned)((v.F * v.nch + kWarps - 1) / kWarps);
   auto cap = [&](unsigned g) { return g < (unsigned)nsm * 16 ? (g ? g : 1) : (unsigned)nsm * 16; };
-  k_fresh_rows<<<cap(items_f), 256, 0, s>>>(v, 0);
+  pdl_launch(k_fresh_rows, cap(items_f), 256, 0, s, v, 0);
   if (v.nn) hooks->eval_fresh_all(hooks->ctx, s);
-  k_finalize_record<<<1, 256, 0, s>>>(v, 0);
-  k_record_copy<<<cap((unsigned)((v.B * v.nch + kWarps - 1) / kWarps)), 256, 0, s>>>(v);
+  pdl_launch(k_finalize_record, 1, 256, 0, s, v, 0);
+  pdl_launch(k_record_copy, tail_blocks(v, nsm), 256, 0, s, v);
 }
 
 void launch_analytic_partials(const float* rows, uint64_t nrows, uint64_t D,
                               uint64_t Dp, uint32_t nch, int kind, float* part,
                               int nsm, cudaStream_t s) {
   const unsigned g = (unsigned)((nrows * nch + kWarps - 1) / kWarps);
-  k_analytic_partials<<<g < (unsigned)nsm * 16 ? (g ? g : 1) : nsm * 16, 256, 0, s>>>(
+  pdl_launch(k_analytic_partials, g < (unsigned)nsm * 16 ? (g ? g : 1) : nsm * 16, 256, 0, s, 
       rows, nrows, D, Dp, nch, kind, part);
 }
 
 void launch_finalize_rows(const EngineView& v, const float* part, uint64_t nrows,
                           float* fitness, unsigned long long* nan, cudaStream_t s) {
-  k_finalize_rows<<<(unsigned)((nrows + 7) / 8), 256, 0, s>>>(v, part, nrows, fitness, nan);
+  pdl_launch(k_finalize_rows, (unsigned)((nrows + 7) / 8), 256, 0, s, v, part, nrows, fitness, nan);
 }
 
 void launch_to_bf16(const float* src, __nv_bfloat16* dst, uint64_t n, cudaStream_t s) {
-  k_to_bf16<<<(unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, s>>>(src, dst, n);
+  pdl_launch(k_to_bf16, (unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, s, src, dst, n);
 }
 
 // Individual kernels for the operator seams (tests).
 void launch_pop_range(const EngineView& v, int nsm, cudaStream_t s) {
   const unsigned g = (unsigned)((v.B * v.D + 255) / 256);
-  k_pop_range<<<g < (unsigned)nsm * 16 ? g : nsm * 16, 256, 0, s>>>(v);
+  pdl_launch(k_pop_range, g < (unsigned)nsm * 16 ? g : nsm * 16, 256, 0, s, v);
 }
 void launch_explode_map(const EngineView& v, int nsm, cudaStream_t s) {
   const unsigned g = (unsigned)((v.F * ((v.lam + kSparkGroup - 1) / kSparkGroup) * v.nch + kWarps - 1) / kWarps);
@@ -1059,25 +1091,24 @@ void launch_explode_map(const EngineView& v, int nsm, cudaStream_t s) {
   launch_explode_map_impl(v, nsm, s);
 }
 void launch_rank(const EngineView& v, cudaStream_t s) {
-  k_rank<<<(unsigned)v.Fl, kRankThreads, rank_smem(v), s>>>(v);
+  pdl_launch(k_rank, (unsigned)v.Fl, kRankThreads, rank_smem(v), s, v);
 }
 void launch_guides(const EngineView& v, int nsm, cudaStream_t s) {
-  k_guides<<<guide_blocks(v, nsm), 256, 2 * v.top * sizeof(int), s>>>(v);
+  pdl_launch(k_guides, guide_blocks(v, nsm), 256, 2 * v.top * sizeof(int), s, v);
   if (!v.nn) launch_analytic_partials(v.guides, v.Fl * v.M, v.D, v.Dp, v.nch, v.obj_kind, v.gpart, nsm, s);
 }
 void launch_select(const EngineView& v, int nsm, cudaStream_t s) {
   (void)nsm;
-  k_select<<<(unsigned)v.Fl, kSelectThreads, 0, s>>>(v);
+  pdl_launch(k_select, (unsigned)v.Fl, kSelectThreads, 0, s, v);
 }
 void launch_loser(const EngineView& v, int nsm, cudaStream_t s) {
   const unsigned g = (unsigned)((v.F * v.nch + kWarps - 1) / kWarps);
-  k_loser<<<1, 128, 0, s>>>(v);
-  k_fresh_rows<<<g < (unsigned)nsm * 16 ? g : nsm * 16, 256, 0, s>>>(v, 1);
+  pdl_launch(k_loser, 1, 128, 0, s, v);
+  pdl_launch(k_fresh_rows, g < (unsigned)nsm * 16 ? g : nsm * 16, 256, 0, s, v, 1);
 }
 void launch_loser_commit(const EngineView& v, int nsm, cudaStream_t s) {
-  k_finalize_record<<<1, 256, 0, s>>>(v, 1);
-  const unsigned g = (unsigned)((v.B * v.nch + kWarps - 1) / kWarps);
-  k_record_copy<<<g < (unsigned)nsm * 16 ? (g ? g : 1) : nsm * 16, 256, 0, s>>>(v);
+  pdl_launch(k_finalize_record, 1, 256, 0, s, v, 1);
+  pdl_launch(k_record_copy, tail_blocks(v, nsm), 256, 0, s, v);
 }
 
 }  // namespace mgfwa_b200

@@ -266,6 +266,7 @@ template <int H>
 __global__ void __launch_bounds__(kThreads, 1)
     k_mlp_fitness(const __grid_constant__ CUtensorMap tmap_x,
                   const __grid_constant__ CUtensorMap tmap_w, MlpArgs args) {
+  pdl_enter();
   if (args.gate != nullptr && *args.gate == 0) return;
   constexpr int SPT = BN / H;  // sparks per N tile (1 when H == 256)
   static_assert(BN % H == 0 && H % 32 == 0, "H must divide 256 and be a multiple of 32");
@@ -557,7 +558,7 @@ cudaError_t prepare_h() {
 template <int H>
 cudaError_t launch_h(const CUtensorMap& tx, const CUtensorMap& tw, int grid, const MlpArgs& a,
                      cudaStream_t s) {
-  k_mlp_fitness<H><<<grid, kThreads, kSmemBytes, s>>>(tx, tw, a);
+  pdl_launch(k_mlp_fitness<H>, grid, kThreads, kSmemBytes, s, tx, tw, a);
   return cudaGetLastError();
 }
 
