@@ -41,11 +41,25 @@ WORKLOADS = {
     # configs[0]
     "c1": dict(desc="C1 sphere D=30, B=1, mu=5, lambda=30, M=3", kind="sphere", D=30, B=1, mu=5, lam=30, M=3,
                lo=-10.0, hi=10.0),
+    # configs[2]: LeNet-5 on 28x28 synthetic samples
+    "c3": dict(desc="C3 LeNet-5 (conv6-conv16-120-84-10), S=1024, B=1, mu=5, lambda=300, M=3", kind="lenet",
+               D=61706, B=1, mu=5, lam=300, M=3, lo=-1.0, hi=1.0, samples=1024),
+    # configs[4]: large population, MLP 784-256-10 (weak-scaling firework shards)
+    "c5": dict(desc="C5 MLP-weights 784-256-10, S=1024, B=1, mu=64, lambda=1024, M=3", kind="mlp", D=203530,
+               B=1, mu=64, lam=1024, M=3, lo=-1.0, hi=1.0, in_dim=784, hidden=256, out_dim=10, samples=1024),
     # configs[3]
     "c4": dict(desc="C4 Rastrigin D=1e5, B=1, mu=5, lambda=30, M=3", kind="rastrigin", D=100000, B=1, mu=5,
                lam=30, M=3, lo=-5.12, hi=5.12),
 }
 FLOP_PER_EVAL_C2 = 2 * 1024 * (784 * 32 + 32 * 10)  # 52,035,584
+LENET_FLOP_PER_SAMPLE = 833_040  # conv1 117,600 + conv2 240,000 + fc 58,920 MAC, x2
+
+
+def flop_per_eval(w):
+    """Algorithmic FLOP of one candidate evaluation."""
+    if w["kind"] == "lenet":
+        return LENET_FLOP_PER_SAMPLE * w["samples"]
+    return 2 * w["samples"] * (w["in_dim"] * w["hidden"] + w["hidden"] * w["out_dim"])
 
 
 def peaks():
@@ -80,6 +94,8 @@ def ncu_traffic(kernel_prefix: str):
 def make_objective(P, w):
     if w["kind"] == "mlp":
         return P.MlpWeights(w["in_dim"], w["hidden"], w["out_dim"], w["samples"], 1)
+    if w["kind"] == "lenet":
+        return P.LeNet(w["samples"], 1)
     return {"sphere": P.Sphere(), "rastrigin": P.Rastrigin(), "ackley": P.Ackley()}[w["kind"]]
 
 
@@ -144,22 +160,37 @@ def dist_env():
     return world, rank, local
 
 
+def _ref_desc(O, w):
+    kind = {"mlp": O.OBJ_MLP_WEIGHTS, "lenet": O.OBJ_LENET, "sphere": O.OBJ_SPHERE,
+            "rastrigin": O.OBJ_RASTRIGIN, "ackley": O.OBJ_ACKLEY}[w["kind"]]
+    return O.ObjectiveDesc(kind=kind, in_dim=w.get("in_dim", 784), hidden=w.get("hidden", 32),
+                           out_dim=w.get("out_dim", 10), samples=w.get("samples", 1024))
+
+
 def cpu_reference_generation(w, seed: int, workers: int):
-    """One full reference generation (run() with budget init + 1 wave) on the
-    host cores via the compiled reference; returns (evals, seconds)."""
+    """Reference CPU throughput on the host cores via the compiled reference
+    (oracle/_ref).  C1/C2/C4: one full generation, run() with budget
+    init + 1 wave.  C3/C5, whose CPU generations take minutes to hours
+    (SURVEY.md §8(d)): batched_apply() of a bounded sample of candidate rows
+    (fitness only, the dominant reference cost), extrapolated as evals/s.
+    Returns (evals, seconds, sample description)."""
     import oracle as O
 
     ref = O.Reference()
+    desc = _ref_desc(O, w)
+    if w["kind"] == "lenet" or w["D"] > 100000:
+        n = max(workers, 1) * (2 if w["kind"] == "lenet" else 1)
+        rows = np.random.default_rng(seed).uniform(w["lo"], w["hi"], size=(n, w["D"])) * 0.05
+        t = time.perf_counter()
+        ref.batched_apply(desc, rows[None], workers=workers)
+        return n, time.perf_counter() - t, f"batched_apply() of {n} candidate rows (fitness only)"
     cfg = O.Config(batches=w["B"], fireworks=w["mu"], sparks_per_firework=w["lam"], guides_per_firework=w["M"],
                    boosts=[1.0, 2.0, 4.0][: w["M"]],
                    max_evaluations=w["B"] * w["mu"] + w["B"] * w["mu"] * (w["lam"] + w["M"]))
-    kind = {"mlp": O.OBJ_MLP_WEIGHTS, "sphere": O.OBJ_SPHERE, "rastrigin": O.OBJ_RASTRIGIN}[w["kind"]]
-    desc = O.ObjectiveDesc(kind=kind, in_dim=w.get("in_dim", 784), hidden=w.get("hidden", 32),
-                           out_dim=w.get("out_dim", 10), samples=w.get("samples", 1024))
     lo, hi = np.full(w["D"], w["lo"]), np.full(w["D"], w["hi"])
     t = time.perf_counter()
     r = ref.run(cfg, lo, hi, desc, seed, workers=workers)
-    return r.evaluations_used, time.perf_counter() - t
+    return r.evaluations_used, time.perf_counter() - t, "mgfwa::run() of one generation (init + 1 wave)"
 
 
 def run_reference_arm(args, w):
@@ -169,13 +200,14 @@ def run_reference_arm(args, w):
     cores = os.cpu_count() or 1
     evals, secs, steps = 0, 0.0, 0
     t0 = time.perf_counter()
+    what = ""
     for _ in range(args.warmup):  # bounded warm-up
         cpu_reference_generation(w, 1000, cores)
         if time.perf_counter() - t0 > 30:
             break
     t1 = time.perf_counter()
     for k in range(args.steps):
-        e, s = cpu_reference_generation(w, k, cores)
+        e, s, what = cpu_reference_generation(w, k, cores)
         evals += e
         secs += s
         steps += 1
@@ -187,8 +219,7 @@ def run_reference_arm(args, w):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w["desc"], "budget_per_step": "init + 1 generation"}, "impl": "reference",
             "cpu_baseline": {"value": v, "unit": "evals/s", "cores": cores, "kind": "reference",
-                             "sample": f"{steps} x mgfwa::run() of one generation (init + 1 wave), "
-                                       f"EvalBackend::data_parallel({cores})"},
+                             "sample": f"{steps} x {what}, EvalBackend::data_parallel({cores})"},
             "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -271,15 +302,22 @@ def main():
     # dominant kernel: spark fitness (tcgen05 GEMM) timed alone, CUDA events
     fit_ms, units = eng.time_fitness(20)
     pk, pk_kind = peaks()
-    if w["kind"] == "mlp":
-        achieved = FLOP_PER_EVAL_C2 * units / (fit_ms * 1e-3) / 1e12
-        tr = ncu_traffic("k_mlp_fitness")
-        roof = {"kernel": "k_mlp_fitness<32> (tcgen05.mma kind::f16, TMA, TMEM)", "bound": "tensor",
+    if w["kind"] in ("mlp", "lenet"):
+        fpe = flop_per_eval(w)
+        achieved = fpe * units / (fit_ms * 1e-3) / 1e12
+        if w["kind"] == "mlp":
+            kname = f"k_mlp_fitness<{w['hidden']}> (tcgen05.mma kind::f16, TMA, TMEM)"
+            tr = ncu_traffic(f"k_mlp_fitness<{w['hidden']}>")
+            opb = units * w["D"] * 2 + w["samples"] * w["in_dim"] * 2
+        else:
+            kname = "k_lenet_fitness (mma.sync m16n8k16 bf16, weights staged in smem)"
+            tr = ncu_traffic("k_lenet_fitness")
+            opb = units * w["D"] * 2 + w["samples"] * 784 * 2
+        roof = {"kernel": kname, "bound": "tensor",
                 "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
                 "frac": achieved / pk["bf16_tflops"], "traffic": tr["bytes"] if tr else None,
                 "traffic_source": tr["source"] if tr else None,
-                "algorithmic_per_launch": f"{units} sparks x {FLOP_PER_EVAL_C2} FLOP; operand bytes "
-                                          f"{units * 25472 * 2 + 1024 * 784 * 2} (bf16 W + X)",
+                "algorithmic_per_launch": f"{units} candidates x {fpe} FLOP; operand bytes {opb} (bf16 W + X)",
                 "ms_per_launch": fit_ms, "peak_source": f"{pk_kind} bf16 burst (MEASURED_PEAKS.json)"}
     else:
         byts = units * w["D"] * 4 + w["B"] * w["mu"] * w["D"] * 4
@@ -291,7 +329,7 @@ def main():
     line = {"metric": "spark fitness evals/sec", "value": evals_total / (ms_max * 1e-3), "unit": "evals/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "bf16" if w["kind"] == "mlp" else "f32", "data": "synthetic",
+            "dtype": "bf16" if w["kind"] in ("mlp", "lenet") else "f32", "data": "synthetic",
             "config": {"workload": w["desc"], "D": w["D"], "fireworks_total": wn["mu"] * w["B"],
                        "parallelism": f"firework-sharded x{world}" + (" + NCCL all-gather/gen" if world > 1 else ""),
                        "l2": "inputs larger than L2: spark matrix fp32+bf16 229 MB/generation > 126 MB"
@@ -335,10 +373,10 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cores = os.cpu_count() or 1
-            e, s = cpu_reference_generation(w, 0, cores)
+            e, s, what = cpu_reference_generation(w, 0, cores)
             line["cpu_baseline"] = {"value": e / s, "unit": "evals/s", "cores": cores, "kind": "reference",
-                                    "sample": f"1 x mgfwa::run() of one generation (init + 1 wave) of the same "
-                                              f"workload, compiled reference, data_parallel({cores}), {s:.1f} s"}
+                                    "sample": f"1 x {what} of the same workload, compiled reference, "
+                                              f"data_parallel({cores}), {s:.1f} s"}
         except Exception as ex:  # the reference build travels in oracle/_ref
             line["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
     if rank == 0:

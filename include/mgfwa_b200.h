@@ -228,6 +228,19 @@ int mgfwa_shard_exchange(mgfwa_ctx_t dst, mgfwa_ctx_t src);
 int mgfwa_time_fitness(mgfwa_ctx_t ctx, uint64_t iters, double* ms,
                        uint64_t* units);
 
+/* Same, for one kernel of the generation (state-idempotent ones only):
+ * MGFWA_KERNEL_FITNESS (as above), _EXPLODE (explode + mapping (+ analytic
+ * fitness)), _RANK (spark fitness finalize + ranking), _GUIDES (guiding
+ * vector + guides + mapping), _GUIDE_FITNESS (NN fitness of the guides).
+ * Run on the state the context holds (e.g. after some generations). */
+#define MGFWA_KERNEL_FITNESS 0
+#define MGFWA_KERNEL_EXPLODE 1
+#define MGFWA_KERNEL_RANK 2
+#define MGFWA_KERNEL_GUIDES 3
+#define MGFWA_KERNEL_GUIDE_FITNESS 4
+int mgfwa_time_kernel(mgfwa_ctx_t ctx, int kernel, uint64_t iters, double* ms,
+                      uint64_t* units);
+
 /* ---- utilities ---------------------------------------------------------- */
 /* key_hash, rng.hpp:43-52, evaluated on the device for n keys [n][7]. */
 int mgfwa_key_hash(const uint64_t* keys, uint64_t n, uint64_t* out);

@@ -12,6 +12,7 @@ from .engine import (  # noqa: F401
     CudaError,
     Engine,
     FireworkState,
+    LeNet,
     MgfwaConfig,
     MlpWeights,
     Objective,

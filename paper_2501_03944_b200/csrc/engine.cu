@@ -21,6 +21,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "../../include/mgfwa_b200.h"
@@ -123,7 +124,34 @@ static Status validate_space(const mgfwa_space_t* s) {
   return ok();
 }
 
+// NN objectives (tensor-core fitness): the MLP-weights loss and LeNet-5.
+static bool nn_kind(int kind) { return kind == MGFWA_OBJ_MLP_WEIGHTS || kind == MGFWA_OBJ_LENET; }
+static uint32_t nn_in_dim(const mgfwa_objective_t* o) {
+  return o->kind == MGFWA_OBJ_LENET ? 784u : o->in_dim;
+}
+static uint32_t nn_out_dim(const mgfwa_objective_t* o) {
+  return o->kind == MGFWA_OBJ_LENET ? 10u : o->out_dim;
+}
+
+// One NN fitness plan: the MLP (tcgen05) or the LeNet (mma.sync) kernel.
+struct NnPlan {
+  MlpPlan* mlp = nullptr;
+  LenetPlan* lenet = nullptr;
+  void destroy() {
+    mlp_plan_destroy(mlp);
+    lenet_plan_destroy(lenet);
+    mlp = nullptr;
+    lenet = nullptr;
+  }
+};
+static cudaError_t nn_fitness_launch(const NnPlan& p, float* part, const int* gate,
+                                     cudaStream_t s) {
+  return p.lenet ? lenet_fitness_launch(p.lenet, part, gate, s)
+                 : mlp_fitness_launch(p.mlp, part, gate, s);
+}
+
 static uint64_t objective_dim(const mgfwa_objective_t* o) {
+  if (o->kind == MGFWA_OBJ_LENET) return lenet_dim();
   if (o->kind == MGFWA_OBJ_MLP_WEIGHTS)
     return (uint64_t)o->hidden * o->in_dim + o->hidden + (uint64_t)o->out_dim * o->hidden +
            o->out_dim;
@@ -144,7 +172,9 @@ static Status validate_objective(const mgfwa_objective_t* o, uint64_t D) {
         return invalid("forward: input dimension mismatch");
       return ok();
     case MGFWA_OBJ_LENET:
-      return invalid("mgfwa_b200: the LeNet objective is not available on the GPU engine yet");
+      if (o->samples == 0) return invalid("LeNet objective: samples must be positive");
+      if (objective_dim(o) != D) return invalid("forward: input dimension mismatch");
+      return ok();
     default:
       return invalid("unknown objective kind");
   }
@@ -204,16 +234,14 @@ struct Workspace {
   size_t arena_bytes = 0;
   __nv_bfloat16* X = nullptr;  // NN dataset
   int32_t* y = nullptr;
-  MlpPlan* plan_sparks = nullptr;
-  MlpPlan* plan_guides = nullptr;
-  MlpPlan* plan_fresh = nullptr;
+  NnPlan plan_sparks, plan_guides, plan_fresh;
   int nsm = 148;
   int device = 0;
 
   ~Workspace() {
-    mlp_plan_destroy(plan_sparks);
-    mlp_plan_destroy(plan_guides);
-    mlp_plan_destroy(plan_fresh);
+    plan_sparks.destroy();
+    plan_guides.destroy();
+    plan_fresh.destroy();
     if (arena) cudaFree(arena);
   }
 
@@ -226,7 +254,7 @@ struct Workspace {
                                         uint64_t rank = 0, uint64_t world = 1) {
     return {c.B, c.mu, c.lam, c.M, c.M > 0 ? c.top() : 0, space->dim, (uint64_t)obj->kind,
             obj->in_dim, obj->hidden, obj->out_dim, obj->samples,
-            obj->kind == MGFWA_OBJ_MLP_WEIGHTS ? obj->data_seed : 0, (uint64_t)dev, trace_cap,
+            nn_kind(obj->kind) ? obj->data_seed : 0, (uint64_t)dev, trace_cap,
             rank, world};
   }
 
@@ -270,6 +298,7 @@ struct Workspace {
     CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     CUDA_TRY(prepare_engine_kernels());
     const uint64_t D = space->dim;
+    v.mh = MulHi{4u, 32u, 2u};  // 2^(32-k) for the k = 30, 27, 31 shifts of splitmix64
     v.B = c.B;
     v.mu = c.mu;
     v.lam = c.lam;
@@ -284,9 +313,11 @@ struct Workspace {
     v.f_lo = rank * v.Fl;
     v.nch = (uint32_t)((D + kChunk - 1) / kChunk);
     v.obj_kind = obj->kind;
-    v.nn = obj->kind == MGFWA_OBJ_MLP_WEIGHTS;
+    v.nn = nn_kind(obj->kind);
     v.samples = v.nn ? obj->samples : 0;
-    v.nparts = v.nn ? mlp_num_parts(obj->samples) : v.nch;
+    v.nparts = !v.nn ? v.nch
+               : obj->kind == MGFWA_OBJ_LENET ? lenet_num_parts(obj->samples)
+                                              : mlp_num_parts(obj->samples);
     v.trace_cap = trace_cap;
 
     // ---- arena layout
@@ -334,7 +365,7 @@ struct Workspace {
     add(&v.tr_ns, trace_cap * c.B * 8);
     add(&v.ctl, sizeof(Ctl));
     if (v.nn) {
-      add(&X, (size_t)obj->samples * obj->in_dim * 2);
+      add(&X, (size_t)obj->samples * nn_in_dim(obj) * 2);
       add(&y, (size_t)obj->samples * 4);
     }
     size_t total = 0;
@@ -362,21 +393,24 @@ struct Workspace {
     if (v.nn) {
       std::vector<__nv_bfloat16> Xh;
       std::vector<int32_t> yh;
-      make_dataset(obj->samples, obj->in_dim, obj->out_dim, obj->data_seed, Xh, yh);
+      make_dataset(obj->samples, nn_in_dim(obj), nn_out_dim(obj), obj->data_seed, Xh, yh);
       CUDA_TRY(cudaMemcpy(X, Xh.data(), Xh.size() * 2, cudaMemcpyHostToDevice));
       CUDA_TRY(cudaMemcpy(y, yh.data(), yh.size() * 4, cudaMemcpyHostToDevice));
       char err[256] = {0};
-      plan_sparks = mlp_plan_create(X, y, obj->samples, obj->in_dim, obj->hidden, obj->out_dim,
-                                    v.sparks_h, P, Dp, nsm, err, sizeof err);
-      if (!plan_sparks) return invalid(err);
-      if (G > 0) {
-        plan_guides = mlp_plan_create(X, y, obj->samples, obj->in_dim, obj->hidden, obj->out_dim,
-                                      v.guides_h, G, Dp, nsm, err, sizeof err);
-        if (!plan_guides) return invalid(err);
-      }
-      plan_fresh = mlp_plan_create(X, y, obj->samples, obj->in_dim, obj->hidden, obj->out_dim,
-                                   v.fresh_h, F, Dp, nsm, err, sizeof err);
-      if (!plan_fresh) return invalid(err);
+      auto make = [&](NnPlan& pl, const __nv_bfloat16* W, uint64_t rows) -> Status {
+        if (obj->kind == MGFWA_OBJ_LENET) {
+          pl.lenet = lenet_plan_create(X, y, obj->samples, W, rows, Dp, nsm, err, sizeof err);
+          if (!pl.lenet) return invalid(err);
+        } else {
+          pl.mlp = mlp_plan_create(X, y, obj->samples, obj->in_dim, obj->hidden, obj->out_dim, W,
+                                   rows, Dp, nsm, err, sizeof err);
+          if (!pl.mlp) return invalid(err);
+        }
+        return ok();
+      };
+      STATUS_TRY(make(plan_sparks, v.sparks_h, P));
+      if (G > 0) STATUS_TRY(make(plan_guides, v.guides_h, G));
+      STATUS_TRY(make(plan_fresh, v.fresh_h, F));
     }
     return ok();
   }
@@ -420,19 +454,19 @@ class WorkspaceCache {
 // NN fitness hooks used inside the captured generation.
 static void hook_sparks(void* p, cudaStream_t s) {
   auto* w = static_cast<Workspace*>(p);
-  mlp_fitness_launch(w->plan_sparks, w->v.spart, &w->v.ctl->active, s);
+  nn_fitness_launch(w->plan_sparks, w->v.spart, &w->v.ctl->active, s);
 }
 static void hook_guides(void* p, cudaStream_t s) {
   auto* w = static_cast<Workspace*>(p);
-  mlp_fitness_launch(w->plan_guides, w->v.gpart, &w->v.ctl->active, s);
+  nn_fitness_launch(w->plan_guides, w->v.gpart, &w->v.ctl->active, s);
 }
 static void hook_fresh(void* p, cudaStream_t s) {
   auto* w = static_cast<Workspace*>(p);
-  mlp_fitness_launch(w->plan_fresh, w->v.fpart, &w->v.ctl->n_losers, s);
+  nn_fitness_launch(w->plan_fresh, w->v.fpart, &w->v.ctl->n_losers, s);
 }
 static void hook_fresh_all(void* p, cudaStream_t s) {
   auto* w = static_cast<Workspace*>(p);
-  mlp_fitness_launch(w->plan_fresh, w->v.fpart, nullptr, s);
+  nn_fitness_launch(w->plan_fresh, w->v.fpart, nullptr, s);
 }
 
 // ----------------------------------------------------------------- engine
@@ -1257,34 +1291,63 @@ int mgfwa_op_argmin_per_population(const double* fitness, uint64_t rows, uint64_
   return fail(nullptr, body());
 }
 
-int mgfwa_time_fitness(mgfwa_ctx_t ctx, uint64_t iters, double* ms, uint64_t* units) {
+int mgfwa_time_kernel(mgfwa_ctx_t ctx, int kernel, uint64_t iters, double* ms, uint64_t* units) {
   Engine& e = ctx->engine;
   auto body = [&]() -> Status {
     if (!e.initialized) return Status{MGFWA_ESTATE, "mgfwa: initialize() must precede timing"};
     Workspace& w = *e.ws;
+    const EngineView& v = w.v;
+    std::function<void()> launch;
+    switch (kernel) {
+      case MGFWA_KERNEL_FITNESS:  // the dominant kernel of the workload
+        if (v.nn)
+          launch = [&]() { nn_fitness_launch(w.plan_sparks, v.spart, nullptr, e.stream); };
+        else
+          launch = [&]() { launch_explode_map(v, w.nsm, e.stream); };
+        *units = v.Fl * v.lam;
+        break;
+      case MGFWA_KERNEL_EXPLODE:
+        launch = [&]() { launch_explode_map(v, w.nsm, e.stream); };
+        *units = v.Fl * v.lam;
+        break;
+      case MGFWA_KERNEL_RANK:
+        launch = [&]() { launch_rank(v, e.stream); };
+        *units = v.Fl * v.lam;
+        break;
+      case MGFWA_KERNEL_GUIDES:
+        if (v.M == 0) return invalid("mgfwa_time_kernel: no guides");
+        launch = [&]() { launch_guides(v, w.nsm, e.stream); };
+        *units = v.Fl * v.M;
+        break;
+      case MGFWA_KERNEL_GUIDE_FITNESS:
+        if (v.M == 0 || !v.nn) return invalid("mgfwa_time_kernel: no NN guide fitness");
+        launch = [&]() { nn_fitness_launch(w.plan_guides, v.gpart, nullptr, e.stream); };
+        *units = v.Fl * v.M;
+        break;
+      default:
+        return invalid("mgfwa_time_kernel: unknown kernel");
+    }
     cudaEvent_t a, b;
     CUDA_TRY(cudaEventCreate(&a));
     CUDA_TRY(cudaEventCreate(&b));
-    auto launch = [&]() {
-      if (w.v.nn)
-        mlp_fitness_launch(w.plan_sparks, w.v.spart, nullptr, e.stream);
-      else
-        launch_explode_map(w.v, w.nsm, e.stream);
-    };
     launch();
     CUDA_TRY(cudaEventRecord(a, e.stream));
     for (uint64_t i = 0; i < iters; ++i) launch();
     CUDA_TRY(cudaEventRecord(b, e.stream));
     CUDA_TRY(cudaEventSynchronize(b));
+    CUDA_TRY(cudaGetLastError());
     float t = 0.0f;
     CUDA_TRY(cudaEventElapsedTime(&t, a, b));
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     *ms = (double)t / (double)(iters ? iters : 1);
-    *units = w.v.F * w.v.lam;
     return ok();
   };
   return fail(ctx, body());
+}
+
+int mgfwa_time_fitness(mgfwa_ctx_t ctx, uint64_t iters, double* ms, uint64_t* units) {
+  return mgfwa_time_kernel(ctx, MGFWA_KERNEL_FITNESS, iters, ms, units);
 }
 
 int mgfwa_key_hash(const uint64_t* keys, uint64_t n, uint64_t* out) {

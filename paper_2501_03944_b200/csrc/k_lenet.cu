@@ -1,0 +1,508 @@
+// k_lenet.cu — LeNet-5 loss of every candidate (SURVEY.md §8(a) a10, config
+// C3): conv5x5 1->6 (pad 2) -> ReLU -> avgpool2 -> conv5x5 6->16 -> ReLU ->
+// avgpool2 -> fc 400->120 -> ReLU -> fc 120->84 -> ReLU -> fc 84->10 -> CE,
+// mean over the S synthetic samples.  Parameter layout and arithmetic follow
+// the fp64 restatement oracle/mgfwa_oracle.c f_lenet (PyTorch Conv2d/Linear
+// weight order: c1w[6][1][5][5], c1b, c2w[16][6][5][5], c2b, f1w[120][400],
+// f1b, f2w[84][120], f2b, f3w[10][84], f3b).
+//
+// Every candidate has its own weights, so the convolutions are per-candidate
+// implicit GEMMs with N = 6 (conv1) and N = 16 (conv2) output channels: far
+// below tcgen05's 128-row MMA tile, and each candidate's conv2 A operand
+// (pooled conv1 activations) is produced on chip.  They run on the warp-level
+// tensor-core MMA (mma.sync m16n8k16 bf16 -> fp32) instead:
+//   * one CTA = one candidate at a time, its 61,706 weights staged once into
+//     shared memory (bf16, re-laid-out for conflict-free fragment loads);
+//   * conv1: per warp one sample; M = 784 output pixels ordered by 2x2 pool
+//     window (4 consecutive rows = one window, so ReLU + pool is two warp
+//     shuffles in the accumulator layout), K = 5 rows x 6 taps (kx padded),
+//     A fragments read as 32-bit pairs from a "pair image" (x, x+1);
+//   * conv2: M = 100 pixels (pool order), K = 25 taps x 8 channels (6 + 2
+//     zero), N = 16; A fragments are 32-bit channel pairs of the pooled conv1
+//     map; the B fragments (conv2 weights) live in registers;
+//   * fc1/fc2/fc3 on a batch of 8 samples (one per warp): M = outputs (16-row
+//     tiles over the 8 warps), N = 8 samples, A via ldmatrix from the staged
+//     weights;
+//   * activations between layers are bf16, accumulation fp32, CE in fp32.
+// Output: part[(row * nparts + p) * 2] = sum of CE over sample chunk p (128
+// samples), slot 1 = 0 — the same partial-sum contract as k_mlp_fitness.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <new>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mgfwa_b200 {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarpsL = kThreads / 32;
+constexpr uint32_t kChunkS = 128;  // samples per work item (one partial)
+
+// parameter offsets in the candidate row (oracle f_lenet)
+constexpr int oC1W = 0, oC1B = 150, oC2W = 156, oC2B = 2556, oF1W = 2572, oF1B = 50572,
+              oF2W = 50692, oF2B = 60772, oF3W = 60856, oF3B = 61696;
+constexpr int kLenetDim = 61706;
+
+// shared-memory layout (bytes); strides chosen for conflict-free fragment
+// loads (32-bit) and 16-byte aligned ldmatrix rows.
+constexpr int kC1K = 32;    // conv1 K: 5 rows x 6 taps + 2 pad
+constexpr int kC2K = 208;   // conv2 K: 25 taps x 8 channels + 8 pad
+constexpr int kC2S = 216;   // conv2 weight row stride (bf16)
+constexpr int kF1S = 408;   // fc1 row stride (bf16), 128 rows, K = 400
+constexpr int kF2S = 136;   // fc2: 96 rows, K = 128 (120 + pad)
+constexpr int kF3S = 104;   // fc3: 16 rows, K = 96 (84 + pad)
+constexpr int kImgS = 33;   // pair-image row stride (32-bit words), 33 rows
+constexpr int kP2S = 408;   // pooled conv2 activations per sample (bf16)
+constexpr int kH1S = 136;
+constexpr int kH2S = 104;
+
+struct Smem {
+  static constexpr int wc1 = 0;                          // [8][32] bf16
+  static constexpr int wc2 = wc1 + 8 * kC1K * 2;         // [16][216] bf16
+  static constexpr int wf1 = wc2 + 16 * kC2S * 2;        // [128][408]
+  static constexpr int wf2 = wf1 + 128 * kF1S * 2;       // [96][136]
+  static constexpr int wf3 = wf2 + 96 * kF2S * 2;        // [16][104]
+  static constexpr int bc1 = wf3 + 16 * kF3S * 2;        // f32 [8]
+  static constexpr int bc2 = bc1 + 8 * 4;                // f32 [16]
+  static constexpr int bf1 = bc2 + 16 * 4;               // f32 [128]
+  static constexpr int bf2 = bf1 + 128 * 4;              // f32 [96]
+  static constexpr int bf3 = bf2 + 96 * 4;               // f32 [16]
+  static constexpr int img = bf3 + 16 * 4;               // per warp [33][33] u32
+  static constexpr int raw = img + kWarpsL * 33 * kImgS * 4;  // per warp 784 bf16
+  static constexpr int p1 = raw + kWarpsL * 784 * 2;     // per warp [14*14][4] u32
+  static constexpr int p2 = p1 + kWarpsL * 196 * 4 * 4;  // [8][408] bf16
+  static constexpr int h1 = p2 + 8 * kP2S * 2;           // [8][136] bf16
+  static constexpr int h2 = h1 + 8 * kH1S * 2;           // [8][104] bf16
+  static constexpr int logit = h2 + 8 * kH2S * 2;        // f32 [8][16]
+  static constexpr int total = logit + 8 * 16 * 4;
+};
+static_assert(Smem::total <= 227 * 1024, "LeNet shared memory");
+
+struct LenetArgs {
+  const __nv_bfloat16* X;  // [S][784]
+  const int32_t* y;        // [S]
+  const __nv_bfloat16* W;  // [rows][Dp]
+  uint64_t rows, Dp;
+  uint32_t S, nparts;
+  float* part;
+  const int* gate;
+};
+
+__device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void ldmatrix_x4(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 t = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&t);
+}
+
+__device__ __forceinline__ float bf(const __nv_bfloat16 x) { return __bfloat162float(x); }
+
+// Stage one candidate's weights into shared memory (all threads).
+__device__ void stage_weights(uint8_t* sm, const __nv_bfloat16* w) {
+  __nv_bfloat16* wc1 = reinterpret_cast<__nv_bfloat16*>(sm + Smem::wc1);
+  __nv_bfloat16* wc2 = reinterpret_cast<__nv_bfloat16*>(sm + Smem::wc2);
+  __nv_bfloat16* wf1 = reinterpret_cast<__nv_bfloat16*>(sm + Smem::wf1);
+  __nv_bfloat16* wf2 = reinterpret_cast<__nv_bfloat16*>(sm + Smem::wf2);
+  __nv_bfloat16* wf3 = reinterpret_cast<__nv_bfloat16*>(sm + Smem::wf3);
+  float* bc1 = reinterpret_cast<float*>(sm + Smem::bc1);
+  float* bc2 = reinterpret_cast<float*>(sm + Smem::bc2);
+  float* bf1 = reinterpret_cast<float*>(sm + Smem::bf1);
+  float* bf2 = reinterpret_cast<float*>(sm + Smem::bf2);
+  float* bf3 = reinterpret_cast<float*>(sm + Smem::bf3);
+  const int t = threadIdx.x;
+  // conv1 [c][ky*6+kx]
+  for (int i = t; i < 150; i += kThreads) {
+    const int c = i / 25, r = i % 25, ky = r / 5, kx = r % 5;
+    wc1[c * kC1K + ky * 6 + kx] = w[oC1W + i];
+  }
+  // conv2 [c][(ky*5+kx)*8 + ci]
+  for (int i = t; i < 2400; i += kThreads) {
+    const int c = i / 150, r = i % 150, ci = r / 25, tap = r % 25;
+    wc2[c * kC2S + tap * 8 + ci] = w[oC2W + i];
+  }
+  // fc1 rows (8-byte aligned in global: oF1W * 2 = 5144 = 8 mod 16)
+  for (int i = t; i < 120 * 100; i += kThreads) {
+    const int j = i / 100, q = i % 100;
+    *reinterpret_cast<uint2*>(wf1 + j * kF1S + q * 4) =
+        *reinterpret_cast<const uint2*>(w + oF1W + j * 400 + q * 4);
+  }
+  // fc2 rows (oF2W * 2 = 101384 = 8 mod 16; 120 = 30 x 4)
+  for (int i = t; i < 84 * 30; i += kThreads) {
+    const int j = i / 30, q = i % 30;
+    *reinterpret_cast<uint2*>(wf2 + j * kF2S + q * 4) =
+        *reinterpret_cast<const uint2*>(w + oF2W + j * 120 + q * 4);
+  }
+  // fc3 rows (oF3W * 2 = 121712 = 0 mod 16; 84 = 21 x 4)
+  for (int i = t; i < 10 * 21; i += kThreads) {
+    const int j = i / 21, q = i % 21;
+    *reinterpret_cast<uint2*>(wf3 + j * kF3S + q * 4) =
+        *reinterpret_cast<const uint2*>(w + oF3W + j * 84 + q * 4);
+  }
+  if (t < 6) bc1[t] = bf(w[oC1B + t]);
+  if (t < 16) bc2[t] = bf(w[oC2B + t]);
+  if (t < 120) bf1[t] = bf(w[oF1B + t]);
+  if (t < 84) bf2[t] = bf(w[oF2B + t]);
+  if (t < 10) bf3[t] = bf(w[oF3B + t]);
+}
+
+// Zero every padded region once (the staging never writes them).
+__device__ void zero_smem(uint8_t* sm) {
+  uint32_t* p = reinterpret_cast<uint32_t*>(sm);
+  for (int i = threadIdx.x; i < Smem::total / 4; i += kThreads) p[i] = 0u;
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kThreads, 1) k_lenet_fitness(LenetArgs args) {
+  pdl_enter();
+  if (args.gate != nullptr && *args.gate == 0) return;
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, c = lane & 3;
+
+  const __nv_bfloat16* wc1 = reinterpret_cast<const __nv_bfloat16*>(sm + Smem::wc1);
+  const __nv_bfloat16* wc2 = reinterpret_cast<const __nv_bfloat16*>(sm + Smem::wc2);
+  const float* bc1 = reinterpret_cast<const float*>(sm + Smem::bc1);
+  const float* bc2 = reinterpret_cast<const float*>(sm + Smem::bc2);
+  const float* bf1 = reinterpret_cast<const float*>(sm + Smem::bf1);
+  const float* bf2 = reinterpret_cast<const float*>(sm + Smem::bf2);
+  const float* bf3 = reinterpret_cast<const float*>(sm + Smem::bf3);
+  uint32_t* img = reinterpret_cast<uint32_t*>(sm + Smem::img) + warp * 33 * kImgS;
+  __nv_bfloat16* raw = reinterpret_cast<__nv_bfloat16*>(sm + Smem::raw) + warp * 784;
+  uint32_t* p1 = reinterpret_cast<uint32_t*>(sm + Smem::p1) + warp * 196 * 4;
+  __nv_bfloat16* p2 = reinterpret_cast<__nv_bfloat16*>(sm + Smem::p2);
+  __nv_bfloat16* h1 = reinterpret_cast<__nv_bfloat16*>(sm + Smem::h1);
+  __nv_bfloat16* h2 = reinterpret_cast<__nv_bfloat16*>(sm + Smem::h2);
+  float* logit = reinterpret_cast<float*>(sm + Smem::logit);
+
+  zero_smem(sm);
+  __syncthreads();
+
+  const uint64_t total = args.rows * args.nparts;
+  const uint64_t t_begin = total * blockIdx.x / gridDim.x;
+  const uint64_t t_end = total * (blockIdx.x + 1) / gridDim.x;
+  uint64_t staged = ~0ull;
+  uint32_t bw1[2][2];       // conv1 B fragments (k-step, reg)
+  uint32_t bw2[13][2][2];   // conv2 B fragments (k-step, n-tile, reg)
+
+  for (uint64_t item = t_begin; item < t_end; ++item) {
+    const uint64_t row = item / args.nparts;
+    const uint32_t part = (uint32_t)(item % args.nparts);
+    if (row != staged) {
+      __syncthreads();  // previous item's readers are done
+      stage_weights(sm, args.W + row * args.Dp);
+      __syncthreads();
+      staged = row;
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const __nv_bfloat16* b = wc1 + g * kC1K + 16 * s + 2 * c;
+        bw1[s][0] = *reinterpret_cast<const uint32_t*>(b);
+        bw1[s][1] = *reinterpret_cast<const uint32_t*>(b + 8);
+      }
+#pragma unroll
+      for (int s = 0; s < 13; ++s)
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+          const __nv_bfloat16* b = wc2 + (8 * n + g) * kC2S + 16 * s + 2 * c;
+          bw2[s][n][0] = *reinterpret_cast<const uint32_t*>(b);
+          bw2[s][n][1] = *reinterpret_cast<const uint32_t*>(b + 8);
+        }
+    }
+    const uint32_t s_lo = part * kChunkS;
+    const uint32_t s_hi = min(args.S, s_lo + kChunkS);
+    float loss = 0.0f;  // lanes 0..7 of warp 0: CE of their batch slot
+
+    for (uint32_t sb = s_lo; sb < s_hi; sb += kWarpsL) {
+      const uint32_t s = sb + warp;
+      const bool have = s < s_hi;
+      // ------------------------------------------------ conv1 (this warp)
+      if (have) {
+        const uint4* src = reinterpret_cast<const uint4*>(args.X + (uint64_t)s * 784);
+        for (int i = lane; i < 98; i += 32) reinterpret_cast<uint4*>(raw)[i] = src[i];
+        __syncwarp();
+        // pair image: padded (Y, X) -> (x[Y-2][X-2], x[Y-2][X-1]), 33 x 33
+        for (int i = lane; i < 33 * 33; i += 32) {
+          const int Y = i / 33, Xc = i % 33;
+          const int yy = Y - 2, x0 = Xc - 2, x1 = Xc - 1;
+          const bool iny = yy >= 0 && yy < 28;
+          const __nv_bfloat16 z = __float2bfloat16(0.0f);
+          const __nv_bfloat16 v0 = (iny && x0 >= 0 && x0 < 28) ? raw[yy * 28 + x0] : z;
+          const __nv_bfloat16 v1 = (iny && x1 >= 0 && x1 < 28) ? raw[yy * 28 + x1] : z;
+          __nv_bfloat162 pr;
+          pr.x = v0;
+          pr.y = v1;
+          img[Y * kImgS + Xc] = *reinterpret_cast<uint32_t*>(&pr);
+        }
+        __syncwarp();
+        // word offsets of the A fragment k pairs: k = ky * 6 + kx
+        int koff[2][2];
+#pragma unroll
+        for (int st = 0; st < 2; ++st)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int k = 16 * st + 8 * h + 2 * c;
+            koff[st][h] = (k / 6) * kImgS + (k % 6);
+          }
+        const float b0 = bc1[2 * c], b1 = bc1[2 * c + 1];
+        for (int t = 0; t < 49; ++t) {
+          // rows g and g + 8: window w = 4t + g/4 (+2), sub = g % 4
+          int base[2];
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int w = 4 * t + (g >> 2) + 2 * r, sub = g & 3;
+            const int py = w / 14, px = w % 14;
+            base[r] = (2 * py + (sub >> 1)) * kImgS + 2 * px + (sub & 1);
+          }
+          float d[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int st = 0; st < 2; ++st)
+            mma_bf16(d, img[base[0] + koff[st][0]], img[base[1] + koff[st][0]],
+                     img[base[0] + koff[st][1]], img[base[1] + koff[st][1]], bw1[st][0], bw1[st][1]);
+          // bias + ReLU, 2x2 average pool over lanes g..g+3 (lane bits 2, 3)
+          float v[4] = {fmaxf(d[0] + b0, 0.f), fmaxf(d[1] + b1, 0.f), fmaxf(d[2] + b0, 0.f),
+                        fmaxf(d[3] + b1, 0.f)};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            v[i] += __shfl_xor_sync(0xffffffffu, v[i], 4);
+            v[i] += __shfl_xor_sync(0xffffffffu, v[i], 8);
+          }
+          if ((g & 3) == 0) {
+            const int w0 = 4 * t + (g >> 2), w1 = w0 + 2;
+            p1[w0 * 4 + c] = pack_bf16(0.25f * v[0], 0.25f * v[1]);
+            p1[w1 * 4 + c] = pack_bf16(0.25f * v[2], 0.25f * v[3]);
+          }
+        }
+        __syncwarp();
+        // ---------------------------------------------- conv2 (this warp)
+        // p1 word layout [py*14 + px][cpair]; A k = tap * 8 + ci
+        int toff[13][2];
+#pragma unroll
+        for (int st = 0; st < 13; ++st)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int k = 16 * st + 8 * h + 2 * c;
+            const int tap = k >> 3, cp = (k & 7) >> 1;
+            toff[st][h] = tap < 25 ? ((tap / 5) * 14 + (tap % 5)) * 4 + cp : -1;
+          }
+        const float b2a = bc2[2 * c], b2b = bc2[2 * c + 1], b2c = bc2[8 + 2 * c],
+                    b2d = bc2[9 + 2 * c];
+        for (int t = 0; t < 7; ++t) {
+          int base[2];
+          bool valid[2];
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int m = 16 * t + g + 8 * r;  // pixel row in pool order
+            valid[r] = m < 100;
+            const int w = valid[r] ? (m >> 2) : 0, sub = m & 3;
+            const int py = w / 5, px = w % 5;
+            base[r] = ((2 * py + (sub >> 1)) * 14 + 2 * px + (sub & 1)) * 4;
+          }
+          float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int st = 0; st < 13; ++st) {
+            const uint32_t a0 = toff[st][0] >= 0 ? p1[base[0] + toff[st][0]] : 0u;
+            const uint32_t a1 = toff[st][0] >= 0 ? p1[base[1] + toff[st][0]] : 0u;
+            const uint32_t a2 = toff[st][1] >= 0 ? p1[base[0] + toff[st][1]] : 0u;
+            const uint32_t a3 = toff[st][1] >= 0 ? p1[base[1] + toff[st][1]] : 0u;
+            mma_bf16(d0, a0, a1, a2, a3, bw2[st][0][0], bw2[st][0][1]);
+            mma_bf16(d1, a0, a1, a2, a3, bw2[st][1][0], bw2[st][1][1]);
+          }
+          float v[8] = {fmaxf(d0[0] + b2a, 0.f), fmaxf(d0[1] + b2b, 0.f), fmaxf(d0[2] + b2a, 0.f),
+                        fmaxf(d0[3] + b2b, 0.f), fmaxf(d1[0] + b2c, 0.f), fmaxf(d1[1] + b2d, 0.f),
+                        fmaxf(d1[2] + b2c, 0.f), fmaxf(d1[3] + b2d, 0.f)};
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            v[i] += __shfl_xor_sync(0xffffffffu, v[i], 4);
+            v[i] += __shfl_xor_sync(0xffffffffu, v[i], 8);
+          }
+          if ((g & 3) == 0) {
+            __nv_bfloat16* o = p2 + warp * kP2S;
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+              const int m = 16 * t + g + 8 * r;
+              if (m < 100) {
+                const int w = m >> 2;
+                o[(2 * c) * 25 + w] = __float2bfloat16(0.25f * v[2 * r]);
+                o[(2 * c + 1) * 25 + w] = __float2bfloat16(0.25f * v[2 * r + 1]);
+                o[(8 + 2 * c) * 25 + w] = __float2bfloat16(0.25f * v[4 + 2 * r]);
+                o[(9 + 2 * c) * 25 + w] = __float2bfloat16(0.25f * v[4 + 2 * r + 1]);
+              }
+            }
+          }
+        }
+      } else {
+        // no sample in this batch slot: a zero activation row (finite)
+        for (int i = lane; i < 400; i += 32) p2[warp * kP2S + i] = __float2bfloat16(0.0f);
+      }
+      __syncthreads();
+      // ------------------------------------------------ fc1: 128 x 400 . 400 x 8
+      {
+        const int mt = warp;  // 16-row tile of the 128 (120) outputs
+        float d[4] = {0.f, 0.f, 0.f, 0.f};
+        const uint32_t a_base =
+            smem_addr(sm + Smem::wf1) +
+            (uint32_t)(((16 * mt + (lane & 7) + ((lane >> 3) & 1) * 8) * kF1S + (lane >> 4) * 8) * 2);
+        const __nv_bfloat16* bb = p2 + g * kP2S + 2 * c;
+#pragma unroll 5
+        for (int st = 0; st < 25; ++st) {
+          uint32_t a[4];
+          ldmatrix_x4(a, a_base + st * 32);
+          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(bb + 16 * st);
+          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(bb + 16 * st + 8);
+          mma_bf16(d, a[0], a[1], a[2], a[3], b0, b1);
+        }
+        // rows (outputs) 16mt + g (+8), cols (samples) 2c, 2c+1
+        const int j0 = 16 * mt + g, j1 = j0 + 8;
+        const float c0 = j0 < 120 ? bf1[j0] : 0.f, c1 = j1 < 120 ? bf1[j1] : 0.f;
+        h1[(2 * c) * kH1S + j0] = __float2bfloat16(j0 < 120 ? fmaxf(d[0] + c0, 0.f) : 0.f);
+        h1[(2 * c + 1) * kH1S + j0] = __float2bfloat16(j0 < 120 ? fmaxf(d[1] + c0, 0.f) : 0.f);
+        h1[(2 * c) * kH1S + j1] = __float2bfloat16(j1 < 120 ? fmaxf(d[2] + c1, 0.f) : 0.f);
+        h1[(2 * c + 1) * kH1S + j1] = __float2bfloat16(j1 < 120 ? fmaxf(d[3] + c1, 0.f) : 0.f);
+      }
+      __syncthreads();
+      // ------------------------------------------------ fc2: 96 x 128 . 128 x 8
+      if (warp < 6) {
+        const int mt = warp;
+        float d[4] = {0.f, 0.f, 0.f, 0.f};
+        const uint32_t a_base =
+            smem_addr(sm + Smem::wf2) +
+            (uint32_t)(((16 * mt + (lane & 7) + ((lane >> 3) & 1) * 8) * kF2S + (lane >> 4) * 8) * 2);
+        const __nv_bfloat16* bb = h1 + g * kH1S + 2 * c;
+#pragma unroll
+        for (int st = 0; st < 8; ++st) {
+          uint32_t a[4];
+          ldmatrix_x4(a, a_base + st * 32);
+          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(bb + 16 * st);
+          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(bb + 16 * st + 8);
+          mma_bf16(d, a[0], a[1], a[2], a[3], b0, b1);
+        }
+        const int j0 = 16 * mt + g, j1 = j0 + 8;
+        const float c0 = j0 < 84 ? bf2[j0] : 0.f, c1 = j1 < 84 ? bf2[j1] : 0.f;
+        h2[(2 * c) * kH2S + j0] = __float2bfloat16(j0 < 84 ? fmaxf(d[0] + c0, 0.f) : 0.f);
+        h2[(2 * c + 1) * kH2S + j0] = __float2bfloat16(j0 < 84 ? fmaxf(d[1] + c0, 0.f) : 0.f);
+        h2[(2 * c) * kH2S + j1] = __float2bfloat16(j1 < 84 ? fmaxf(d[2] + c1, 0.f) : 0.f);
+        h2[(2 * c + 1) * kH2S + j1] = __float2bfloat16(j1 < 84 ? fmaxf(d[3] + c1, 0.f) : 0.f);
+      }
+      __syncthreads();
+      // ------------------------------------- fc3 (16 x 96 . 96 x 8) + CE
+      if (warp == 0) {
+        float d[4] = {0.f, 0.f, 0.f, 0.f};
+        const uint32_t a_base =
+            smem_addr(sm + Smem::wf3) +
+            (uint32_t)((((lane & 7) + ((lane >> 3) & 1) * 8) * kF3S + (lane >> 4) * 8) * 2);
+        const __nv_bfloat16* bb = h2 + g * kH2S + 2 * c;
+#pragma unroll
+        for (int st = 0; st < 6; ++st) {
+          uint32_t a[4];
+          ldmatrix_x4(a, a_base + st * 32);
+          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(bb + 16 * st);
+          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(bb + 16 * st + 8);
+          mma_bf16(d, a[0], a[1], a[2], a[3], b0, b1);
+        }
+        // logits[sample][class]: rows = classes g (+8), cols = samples 2c, 2c+1
+        logit[(2 * c) * 16 + g] = d[0] + bf3[g];
+        logit[(2 * c + 1) * 16 + g] = d[1] + bf3[g];
+        if (g < 2) {
+          logit[(2 * c) * 16 + g + 8] = d[2] + bf3[g + 8];
+          logit[(2 * c + 1) * 16 + g + 8] = d[3] + bf3[g + 8];
+        }
+        __syncwarp();
+        if (lane < 8 && sb + lane < s_hi) {
+          const float* z = logit + lane * 16;
+          float m = z[0];
+#pragma unroll
+          for (int o = 1; o < 10; ++o) m = fmaxf(m, z[o]);
+          float se = 0.f;
+#pragma unroll
+          for (int o = 0; o < 10; ++o) se += expf(z[o] - m);
+          loss += (m + logf(se)) - z[args.y[sb + lane]];
+        }
+        __syncwarp();
+      }
+    }
+    if (warp == 0) {
+      // fixed-order sum of the 8 batch slots
+      float t = loss;
+      t += __shfl_xor_sync(0xffffffffu, t, 1);
+      t += __shfl_xor_sync(0xffffffffu, t, 2);
+      t += __shfl_xor_sync(0xffffffffu, t, 4);
+      if (lane == 0) {
+        args.part[(row * args.nparts + part) * 2] = t;
+        args.part[(row * args.nparts + part) * 2 + 1] = 0.0f;
+      }
+    }
+  }
+}
+
+struct LenetPlan {
+  LenetArgs args;
+  unsigned grid;
+};
+
+uint32_t lenet_num_parts(uint32_t S) { return (S + kChunkS - 1) / kChunkS; }
+uint64_t lenet_dim() { return kLenetDim; }
+
+LenetPlan* lenet_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t S,
+                             const __nv_bfloat16* W, uint64_t rows, uint64_t Dp, int nsm,
+                             char* err, size_t errlen) {
+  if (S == 0 || rows == 0) {
+    snprintf(err, errlen, "LeNet objective: samples and rows must be positive");
+    return nullptr;
+  }
+  if (Dp % 8 != 0 || Dp < (uint64_t)kLenetDim) {
+    snprintf(err, errlen, "LeNet objective: bad row stride");
+    return nullptr;
+  }
+  if (cudaFuncSetAttribute(k_lenet_fitness, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           Smem::total) != cudaSuccess) {
+    snprintf(err, errlen, "LeNet objective: shared memory opt-in failed");
+    return nullptr;
+  }
+  auto* p = new (std::nothrow) LenetPlan{};
+  if (!p) return nullptr;
+  p->args.X = X;
+  p->args.y = y;
+  p->args.W = W;
+  p->args.rows = rows;
+  p->args.Dp = Dp;
+  p->args.S = S;
+  p->args.nparts = lenet_num_parts(S);
+  const uint64_t items = rows * p->args.nparts;
+  p->grid = (unsigned)(items < (uint64_t)nsm ? items : (uint64_t)nsm);
+  return p;
+}
+
+void lenet_plan_destroy(LenetPlan* p) { delete p; }
+
+cudaError_t lenet_fitness_launch(const LenetPlan* p, float* part, const int* gate,
+                                 cudaStream_t s) {
+  LenetArgs a = p->args;
+  a.part = part;
+  a.gate = gate;
+  return pdl_launch(k_lenet_fitness, p->grid, kThreads, Smem::total, s, a);
+}
+
+}  // namespace mgfwa_b200

@@ -69,4 +69,17 @@ cudaError_t mlp_fitness_launch(const MlpPlan* p, float* part,
                                const int* gate, cudaStream_t s);
 uint32_t mlp_num_parts(uint32_t S);
 
+// ---- LeNet-5 fitness (k_lenet.cu, warp-level bf16 MMA) ----
+// W rows of stride Dp hold the 61,706 LeNet parameters (oracle f_lenet
+// order); X [S][784] bf16, y [S].  part[row][chunk of 128 samples][2].
+struct LenetPlan;
+LenetPlan* lenet_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t S,
+                             const __nv_bfloat16* W, uint64_t rows, uint64_t Dp, int nsm,
+                             char* err, size_t errlen);
+void lenet_plan_destroy(LenetPlan* p);
+cudaError_t lenet_fitness_launch(const LenetPlan* p, float* part, const int* gate,
+                                 cudaStream_t s);
+uint32_t lenet_num_parts(uint32_t S);
+uint64_t lenet_dim();
+
 }  // namespace mgfwa_b200

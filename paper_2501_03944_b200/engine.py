@@ -131,6 +131,8 @@ class Objective:
     def dim(self, analytic_dim: int = 0) -> int:
         if self.kind == A.OBJ_MLP_WEIGHTS:
             return self.hidden * self.in_dim + self.hidden + self.out_dim * self.hidden + self.out_dim
+        if self.kind == A.OBJ_LENET:
+            return LENET_DIM
         return analytic_dim
 
     def _c(self):
@@ -155,6 +157,17 @@ def MlpWeights(in_dim: int = 784, hidden: int = 32, out_dim: int = 10, samples: 
     """Mean CE of an I-H-O ReLU MLP whose weights (W1,b1,W2,b2 in reference
     Layer order) are the candidate; bf16 tensor-core evaluation."""
     return Objective(A.OBJ_MLP_WEIGHTS, in_dim, hidden, out_dim, samples, data_seed)
+
+
+LENET_DIM = (6 * 25 + 6) + (16 * 6 * 25 + 16) + (400 * 120 + 120) + (120 * 84 + 84) + (84 * 10 + 10)
+
+
+def LeNet(samples: int = 1024, data_seed: int = 1) -> Objective:
+    """Mean CE of LeNet-5 (conv5x5 1->6 pad 2, ReLU, avgpool2, conv5x5 6->16,
+    ReLU, avgpool2, fc 400-120-84-10) on S synthetic 28x28 samples; the
+    61,706 parameters (PyTorch order, oracle f_lenet) are the candidate;
+    bf16 tensor-core evaluation (config C3)."""
+    return Objective(A.OBJ_LENET, 784, 0, 10, samples, data_seed)
 
 
 # ------------------------------------------------------------------- state
@@ -263,6 +276,16 @@ class Engine:
         """(ms per launch, candidates per launch) of the dominant kernel."""
         ms, units = C.c_double(), C.c_uint64()
         _check(A.lib().mgfwa_time_fitness(self.h, iters, C.byref(ms), C.byref(units)), self.h)
+        return ms.value, int(units.value)
+
+    KERNELS = {"fitness": 0, "explode": 1, "rank": 2, "guides": 3, "guide_fitness": 4}
+
+    def time_kernel(self, kernel: str, iters: int = 10):
+        """(ms per launch, rows per launch) of one generation kernel on the
+        current state (mgfwa_time_kernel)."""
+        ms, units = C.c_double(), C.c_uint64()
+        _check(A.lib().mgfwa_time_kernel(self.h, self.KERNELS[kernel], iters, C.byref(ms), C.byref(units)),
+               self.h)
         return ms.value, int(units.value)
 
     def step(self, max_generations: int) -> int:

@@ -188,3 +188,69 @@ def test_mlp_nan_weights_become_inf(P):
     W[2, 5] = np.nan      # W1 entry: ReLU maps a NaN pre-activation to 0, as relu() does (nets.hpp:48)
     got, nan = P.batched_apply(P.MlpWeights(samples=128), W)
     assert np.isinf(got[1]) and nan == 1 and np.isfinite(got[0]) and np.isfinite(got[2])
+
+
+# ---------------------------------------------------------------- LeNet-5
+# Tolerances for the bf16 warp-MMA LeNet kernel (k_lenet.cu): weights and
+# the inter-layer activations (pooled conv maps, fc hiddens) are bf16,
+# accumulation fp32.  Against fp64 on the same bf16-rounded weights the
+# activation roundings remain: rel 1e-2 + abs 2e-3 (measured max well below,
+# see DESIGN.md); against fp64 on the unrounded weights: REL_BF16 / ABS_BF16.
+REL_LENET_ACT = 1e-2
+ABS_LENET_ACT = 2e-3
+
+
+def _bf16_image(W):
+    import torch
+
+    return torch.from_numpy(np.asarray(W, np.float32)).to(torch.bfloat16).to(torch.float64).numpy()
+
+
+def test_lenet_fitness_vs_reference_golden(P, golden):
+    g = golden("objectives.npz")
+    S = int(g["lenet__samples"])
+    got, nan = P.batched_apply(P.LeNet(samples=S), g["lenet__x"].astype(np.float64))
+    assert nan == 0
+    np.testing.assert_allclose(got, g["lenet__f"], rtol=REL_BF16, atol=ABS_BF16)
+
+
+def test_lenet_zero_weights_ln10(P):
+    got, nan = P.batched_apply(P.LeNet(samples=200), np.zeros((3, P.LeNet().dim())))
+    assert nan == 0
+    np.testing.assert_allclose(got, np.log(10.0), rtol=0, atol=1e-6)
+
+
+@pytest.mark.parametrize("S,scale", [(256, 0.1), (200, 0.3), (136, 0.05)])
+def test_lenet_fitness_vs_oracle(P, oracle, S, scale):
+    desc = O.ObjectiveDesc(kind=O.OBJ_LENET, samples=S)
+    rng = np.random.default_rng(S)
+    n = 6
+    W = f32(rng.uniform(-scale, scale, size=(n, desc.dim())))
+    got, nan = P.batched_apply(P.LeNet(samples=S), W)
+    assert nan == 0
+    want_bf16 = np.array([oracle.evaluate(desc, w) for w in _bf16_image(W)])
+    want = np.array([oracle.evaluate(desc, w) for w in W])
+    np.testing.assert_allclose(got, want_bf16, rtol=REL_LENET_ACT, atol=ABS_LENET_ACT)
+    np.testing.assert_allclose(got, want, rtol=REL_BF16, atol=ABS_BF16)
+
+
+def test_lenet_population_consistent(P, oracle):
+    """A 300-candidate batch (many CTAs, several rows per CTA): spot rows vs
+    the oracle, and a candidate's fitness does not depend on its position."""
+    desc = O.ObjectiveDesc(kind=O.OBJ_LENET, samples=128)
+    rng = np.random.default_rng(3)
+    W = f32(rng.uniform(-0.2, 0.2, size=(300, desc.dim())))
+    got, _ = P.batched_apply(P.LeNet(samples=128), W)
+    for i in (0, 149, 299):
+        want = oracle.evaluate(desc, _bf16_image(W[i:i + 1])[0])
+        assert abs(got[i] - want) <= REL_LENET_ACT * abs(want) + ABS_LENET_ACT
+    again, _ = P.batched_apply(P.LeNet(samples=128), W[[299, 0, 149]])
+    assert np.array_equal(again, got[[299, 0, 149]])
+
+
+def test_lenet_nan_weights_become_inf(P):
+    D = P.LeNet().dim()
+    W = np.zeros((2, D))
+    W[1, D - 1] = np.nan  # fc3 bias: NaN logit -> NaN loss -> +inf
+    got, nan = P.batched_apply(P.LeNet(samples=64), W)
+    assert np.isinf(got[1]) and nan == 1 and np.isfinite(got[0])
