@@ -13,13 +13,18 @@
 // tensor-core MMA (mma.sync m16n8k16 bf16 -> fp32) instead:
 //   * one CTA = one candidate at a time, its 61,706 weights staged once into
 //     shared memory (bf16, re-laid-out for conflict-free fragment loads);
-//   * conv1: per warp one sample; M = 784 output pixels ordered by 2x2 pool
-//     window (4 consecutive rows = one window, so ReLU + pool is two warp
-//     shuffles in the accumulator layout), K = 5 rows x 6 taps (kx padded),
-//     A fragments read as 32-bit pairs from a "pair image" (x, x+1);
-//   * conv2: M = 100 pixels (pool order), K = 25 taps x 8 channels (6 + 2
-//     zero), N = 16; A fragments are 32-bit channel pairs of the pooled conv1
-//     map; the B fragments (conv2 weights) live in registers;
+//   * conv1: per warp one sample; M = 784 output pixels in pool order: a
+//     16-row tile = 4 pool windows, rows r and r + 8 the two vertically
+//     adjacent pixels of a window, so in the accumulator layout a thread holds
+//     both rows of its window (vertical pool in-thread) and the horizontal
+//     pair is one shuffle; K = 5 rows x 6 taps (kx padded), A fragments read
+//     as 32-bit pairs from the sample's "pair image" (x, x+1), precomputed
+//     once per plan (the dataset never changes) and prefetched with cp.async;
+//   * conv2: M = 100 pixels (same pool order), K = 25 taps x 8 channels
+//     (6 + 2 zero), N = 16; A fragments are 32-bit channel pairs of the
+//     pooled conv1 map; the B fragments (conv2 weights) live in registers;
+//     the pooled output is stored window-major ([window][16 channels]) and
+//     fc1's columns are staged in that order;
 //   * fc1/fc2/fc3 on a batch of 8 samples (one per warp): M = outputs (16-row
 //     tiles over the 8 warps), N = 8 samples, A via ldmatrix from the staged
 //     weights;
@@ -52,13 +57,13 @@ constexpr int kLenetDim = 61706;
 // shared-memory layout (bytes); strides chosen for conflict-free fragment
 // loads (32-bit) and 16-byte aligned ldmatrix rows.
 constexpr int kC1K = 32;    // conv1 K: 5 rows x 6 taps + 2 pad
-constexpr int kC2K = 208;   // conv2 K: 25 taps x 8 channels + 8 pad
-constexpr int kC2S = 216;   // conv2 weight row stride (bf16)
-constexpr int kF1S = 408;   // fc1 row stride (bf16), 128 rows, K = 400
+constexpr int kC2S = 216;   // conv2 weight row stride (bf16), K = 25 taps x 8 + 8 pad
+constexpr int kF1S = 408;   // fc1 row stride (bf16), 128 rows, K = 400 (window-major)
 constexpr int kF2S = 136;   // fc2: 96 rows, K = 128 (120 + pad)
 constexpr int kF3S = 104;   // fc3: 16 rows, K = 96 (84 + pad)
-constexpr int kImgS = 33;   // pair-image row stride (32-bit words), 33 rows
-constexpr int kP2S = 408;   // pooled conv2 activations per sample (bf16)
+constexpr int kImgS = 40;   // pair-image row stride (32-bit words; = 8 mod 32), 33 rows
+constexpr int kImgWords = 33 * kImgS;  // 1320 words (16-byte multiple)
+constexpr int kP2S = 408;   // pooled conv2 activations per sample (bf16), [25][16]
 constexpr int kH1S = 136;
 constexpr int kH2S = 104;
 
@@ -73,19 +78,21 @@ struct Smem {
   static constexpr int bf1 = bc2 + 16 * 4;               // f32 [128]
   static constexpr int bf2 = bf1 + 128 * 4;              // f32 [96]
   static constexpr int bf3 = bf2 + 96 * 4;               // f32 [16]
-  static constexpr int img = bf3 + 16 * 4;               // per warp [33][33] u32
-  static constexpr int raw = img + kWarpsL * 33 * kImgS * 4;  // per warp 784 bf16
-  static constexpr int p1 = raw + kWarpsL * 784 * 2;     // per warp [14*14][4] u32
-  static constexpr int p2 = p1 + kWarpsL * 196 * 4 * 4;  // [8][408] bf16
+  static constexpr int img = bf3 + 16 * 4;               // per warp [33][40] u32
+  static constexpr int p1 = img + kWarpsL * kImgWords * 4;  // per warp [14*14 + 1][4] u32
+  static constexpr int p2 = p1 + kWarpsL * 197 * 4 * 4;  // [8][408] bf16
   static constexpr int h1 = p2 + 8 * kP2S * 2;           // [8][136] bf16
   static constexpr int h2 = h1 + 8 * kH1S * 2;           // [8][104] bf16
   static constexpr int logit = h2 + 8 * kH2S * 2;        // f32 [8][16]
   static constexpr int total = logit + 8 * 16 * 4;
 };
 static_assert(Smem::total <= 227 * 1024, "LeNet shared memory");
+static_assert(Smem::img % 16 == 0 && Smem::wf1 % 16 == 0 && Smem::wf2 % 16 == 0 &&
+                  Smem::wf3 % 16 == 0,
+              "16-byte aligned cp.async / ldmatrix regions");
 
 struct LenetArgs {
-  const __nv_bfloat16* X;  // [S][784]
+  const uint32_t* pimg;    // [S][1092] pair images of the samples
   const int32_t* y;        // [S]
   const __nv_bfloat16* W;  // [rows][Dp]
   uint64_t rows, Dp;
@@ -113,12 +120,32 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 t = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&t);
 }
 
 __device__ __forceinline__ float bf(const __nv_bfloat16 x) { return __bfloat162float(x); }
+
+// conv1 K order.  Pair q = 8 st + 4 h + c (the A-fragment k pair 2c[+8] of
+// k16-step st held by lane quad c) covers taps (ky, 2 kxp) and (ky, 2 kxp + 1):
+// q < 12: ky = c, kxp = q / 4; q = 12..14: ky = 4, kxp = c; q = 15: padding.
+// With the pair image's row stride = 8 mod 32 the four lane quads of one
+// A-fragment load hit banks 8 ky apart, and the 8 pixels of a tile row are
+// consecutive words: the loads are conflict-free.
+__host__ __device__ constexpr int conv1_k(int ky, int kx) {
+  return ky < 4 ? 2 * (4 * (kx >> 1) + ky) + (kx & 1) : 2 * (12 + (kx >> 1)) + (kx & 1);
+}
+__device__ __forceinline__ int conv1_koff(int q) {  // word offset of pair q in the pair image
+  const int c = q & 3, grp = q >> 2;
+  return grp < 3 ? c * kImgS + 2 * grp : 4 * kImgS + 2 * (c < 3 ? c : 2);
+}
 
 // Stage one candidate's weights into shared memory (all threads).
 __device__ void stage_weights(uint8_t* sm, const __nv_bfloat16* w) {
@@ -133,21 +160,20 @@ __device__ void stage_weights(uint8_t* sm, const __nv_bfloat16* w) {
   float* bf2 = reinterpret_cast<float*>(sm + Smem::bf2);
   float* bf3 = reinterpret_cast<float*>(sm + Smem::bf3);
   const int t = threadIdx.x;
-  // conv1 [c][ky*6+kx]
+  // conv1 [c][conv1_k(ky, kx)]
   for (int i = t; i < 150; i += kThreads) {
     const int c = i / 25, r = i % 25, ky = r / 5, kx = r % 5;
-    wc1[c * kC1K + ky * 6 + kx] = w[oC1W + i];
+    wc1[c * kC1K + conv1_k(ky, kx)] = w[oC1W + i];
   }
   // conv2 [c][(ky*5+kx)*8 + ci]
   for (int i = t; i < 2400; i += kThreads) {
     const int c = i / 150, r = i % 150, ci = r / 25, tap = r % 25;
     wc2[c * kC2S + tap * 8 + ci] = w[oC2W + i];
   }
-  // fc1 rows (8-byte aligned in global: oF1W * 2 = 5144 = 8 mod 16)
-  for (int i = t; i < 120 * 100; i += kThreads) {
-    const int j = i / 100, q = i % 100;
-    *reinterpret_cast<uint2*>(wf1 + j * kF1S + q * 4) =
-        *reinterpret_cast<const uint2*>(w + oF1W + j * 400 + q * 4);
+  // fc1 [j][window * 16 + channel]  <-  f1w[j][channel * 25 + window]
+  for (int i = t; i < 120 * 400; i += kThreads) {
+    const int j = i / 400, k = i % 400, ch = k / 25, win = k % 25;
+    wf1[j * kF1S + win * 16 + ch] = w[oF1W + i];
   }
   // fc2 rows (oF2W * 2 = 101384 = 8 mod 16; 120 = 30 x 4)
   for (int i = t; i < 84 * 30; i += kThreads) {
@@ -168,13 +194,31 @@ __device__ void stage_weights(uint8_t* sm, const __nv_bfloat16* w) {
   if (t < 10) bf3[t] = bf(w[oF3B + t]);
 }
 
-// Zero every padded region once (the staging never writes them).
-__device__ void zero_smem(uint8_t* sm) {
-  uint32_t* p = reinterpret_cast<uint32_t*>(sm);
-  for (int i = threadIdx.x; i < Smem::total / 4; i += kThreads) p[i] = 0u;
+// Prefetch one sample's pair image into this warp's buffer (cp.async).
+__device__ __forceinline__ void prefetch_img(uint32_t dst, const uint32_t* src, int lane) {
+  for (int i = lane; i < kImgWords / 4; i += 32) cp_async16(dst + 16 * i, src + 4 * i);
+  cp_async_commit();
 }
 
 }  // namespace
+
+// Pair images of the dataset: P[s][Y][X] = (x[s][Y-2][X-2], x[s][Y-2][X-1]),
+// zero outside the 28 x 28 image, 33 rows x 40 words.
+__global__ void k_lenet_pairs(const __nv_bfloat16* X, uint32_t S, uint32_t* P) {
+  const uint64_t n = (uint64_t)S * kImgWords;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = i / kImgWords;
+    const int r = (int)(i % kImgWords), Y = r / kImgS, Xc = r % kImgS;
+    const int yy = Y - 2, x0 = Xc - 2, x1 = Xc - 1;
+    const bool iny = yy >= 0 && yy < 28;
+    const __nv_bfloat16* img = X + s * 784;
+    __nv_bfloat162 pr;
+    pr.x = (iny && x0 >= 0 && x0 < 28) ? img[yy * 28 + x0] : __float2bfloat16(0.0f);
+    pr.y = (iny && x1 >= 0 && x1 < 28) ? img[yy * 28 + x1] : __float2bfloat16(0.0f);
+    P[i] = *reinterpret_cast<uint32_t*>(&pr);
+  }
+}
 
 __global__ void __launch_bounds__(kThreads, 1) k_lenet_fitness(LenetArgs args) {
   pdl_enter();
@@ -182,6 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lenet_fitness(LenetArgs args) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, c = lane & 3;
+  const int wi = g >> 1, dx = g & 1;  // window in the tile, column in the window
 
   const __nv_bfloat16* wc1 = reinterpret_cast<const __nv_bfloat16*>(sm + Smem::wc1);
   const __nv_bfloat16* wc2 = reinterpret_cast<const __nv_bfloat16*>(sm + Smem::wc2);
@@ -190,166 +235,161 @@ __global__ void __launch_bounds__(kThreads, 1) k_lenet_fitness(LenetArgs args) {
   const float* bf1 = reinterpret_cast<const float*>(sm + Smem::bf1);
   const float* bf2 = reinterpret_cast<const float*>(sm + Smem::bf2);
   const float* bf3 = reinterpret_cast<const float*>(sm + Smem::bf3);
-  uint32_t* img = reinterpret_cast<uint32_t*>(sm + Smem::img) + warp * 33 * kImgS;
-  __nv_bfloat16* raw = reinterpret_cast<__nv_bfloat16*>(sm + Smem::raw) + warp * 784;
-  uint32_t* p1 = reinterpret_cast<uint32_t*>(sm + Smem::p1) + warp * 196 * 4;
+  const uint32_t* img = reinterpret_cast<const uint32_t*>(sm + Smem::img) + warp * kImgWords;
+  const uint32_t img_s = smem_addr(img);
+  uint32_t* p1 = reinterpret_cast<uint32_t*>(sm + Smem::p1) + warp * 197 * 4;  // +1 zero pixel
   __nv_bfloat16* p2 = reinterpret_cast<__nv_bfloat16*>(sm + Smem::p2);
   __nv_bfloat16* h1 = reinterpret_cast<__nv_bfloat16*>(sm + Smem::h1);
   __nv_bfloat16* h2 = reinterpret_cast<__nv_bfloat16*>(sm + Smem::h2);
   float* logit = reinterpret_cast<float*>(sm + Smem::logit);
 
-  zero_smem(sm);
+  {  // zero everything once: the staging never writes the padded regions
+    uint32_t* p = reinterpret_cast<uint32_t*>(sm);
+    for (int i = threadIdx.x; i < Smem::total / 4; i += kThreads) p[i] = 0u;
+  }
   __syncthreads();
+
+  // A-fragment word offsets (k pairs 2c, 2c+1 and +8 of each k16 step)
+  int koff1[2][2];  // conv1 pair offsets (conv1_k order)
+#pragma unroll
+  for (int st = 0; st < 2; ++st)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) koff1[st][h] = conv1_koff(8 * st + 4 * h + c);
 
   const uint64_t total = args.rows * args.nparts;
   const uint64_t t_begin = total * blockIdx.x / gridDim.x;
   const uint64_t t_end = total * (blockIdx.x + 1) / gridDim.x;
   uint64_t staged = ~0ull;
-  uint32_t bw1[2][2];       // conv1 B fragments (k-step, reg)
-  uint32_t bw2[13][2][2];   // conv2 B fragments (k-step, n-tile, reg)
+  uint32_t bw1[2][2];      // conv1 B fragments (k-step, reg)
+  uint32_t bw2[13][2][2];  // conv2 B fragments (k-step, n-tile, reg)
+  float b1a = 0.f, b1b = 0.f, b2a = 0.f, b2b = 0.f, b2c = 0.f, b2d = 0.f;
 
   for (uint64_t item = t_begin; item < t_end; ++item) {
     const uint64_t row = item / args.nparts;
     const uint32_t part = (uint32_t)(item % args.nparts);
+    const uint32_t s_lo = part * kChunkS;
+    const uint32_t s_hi = min(args.S, s_lo + kChunkS);
     if (row != staged) {
       __syncthreads();  // previous item's readers are done
       stage_weights(sm, args.W + row * args.Dp);
       __syncthreads();
       staged = row;
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const __nv_bfloat16* b = wc1 + g * kC1K + 16 * s + 2 * c;
-        bw1[s][0] = *reinterpret_cast<const uint32_t*>(b);
-        bw1[s][1] = *reinterpret_cast<const uint32_t*>(b + 8);
+      for (int st = 0; st < 2; ++st) {
+        const __nv_bfloat16* b = wc1 + g * kC1K + 16 * st + 2 * c;
+        bw1[st][0] = *reinterpret_cast<const uint32_t*>(b);
+        bw1[st][1] = *reinterpret_cast<const uint32_t*>(b + 8);
       }
 #pragma unroll
-      for (int s = 0; s < 13; ++s)
+      for (int st = 0; st < 13; ++st)
 #pragma unroll
         for (int n = 0; n < 2; ++n) {
-          const __nv_bfloat16* b = wc2 + (8 * n + g) * kC2S + 16 * s + 2 * c;
-          bw2[s][n][0] = *reinterpret_cast<const uint32_t*>(b);
-          bw2[s][n][1] = *reinterpret_cast<const uint32_t*>(b + 8);
+          const __nv_bfloat16* b = wc2 + (8 * n + g) * kC2S + 16 * st + 2 * c;
+          bw2[st][n][0] = *reinterpret_cast<const uint32_t*>(b);
+          bw2[st][n][1] = *reinterpret_cast<const uint32_t*>(b + 8);
         }
+      b1a = bc1[2 * c];
+      b1b = bc1[2 * c + 1];
+      b2a = bc2[2 * c];
+      b2b = bc2[2 * c + 1];
+      b2c = bc2[8 + 2 * c];
+      b2d = bc2[9 + 2 * c];
     }
-    const uint32_t s_lo = part * kChunkS;
-    const uint32_t s_hi = min(args.S, s_lo + kChunkS);
+    if (s_lo + warp < s_hi) prefetch_img(img_s, args.pimg + (uint64_t)(s_lo + warp) * kImgWords, lane);
     float loss = 0.0f;  // lanes 0..7 of warp 0: CE of their batch slot
 
     for (uint32_t sb = s_lo; sb < s_hi; sb += kWarpsL) {
       const uint32_t s = sb + warp;
-      const bool have = s < s_hi;
-      // ------------------------------------------------ conv1 (this warp)
-      if (have) {
-        const uint4* src = reinterpret_cast<const uint4*>(args.X + (uint64_t)s * 784);
-        for (int i = lane; i < 98; i += 32) reinterpret_cast<uint4*>(raw)[i] = src[i];
+      if (s < s_hi) {
+        cp_async_wait_all();
         __syncwarp();
-        // pair image: padded (Y, X) -> (x[Y-2][X-2], x[Y-2][X-1]), 33 x 33
-        for (int i = lane; i < 33 * 33; i += 32) {
-          const int Y = i / 33, Xc = i % 33;
-          const int yy = Y - 2, x0 = Xc - 2, x1 = Xc - 1;
-          const bool iny = yy >= 0 && yy < 28;
-          const __nv_bfloat16 z = __float2bfloat16(0.0f);
-          const __nv_bfloat16 v0 = (iny && x0 >= 0 && x0 < 28) ? raw[yy * 28 + x0] : z;
-          const __nv_bfloat16 v1 = (iny && x1 >= 0 && x1 < 28) ? raw[yy * 28 + x1] : z;
-          __nv_bfloat162 pr;
-          pr.x = v0;
-          pr.y = v1;
-          img[Y * kImgS + Xc] = *reinterpret_cast<uint32_t*>(&pr);
-        }
-        __syncwarp();
-        // word offsets of the A fragment k pairs: k = ky * 6 + kx
-        int koff[2][2];
+        // ------------------------------------------------ conv1 (this warp)
+        // 49 tiles of 4 windows (window 4t + wi of the 14 x 14 pooled map),
+        // 4 tiles per step so that 4 independent MMA chains are in flight
+        for (int t0 = 0; t0 < 49; t0 += 4) {
+          int wpos[4];
+          float d[4][4];
 #pragma unroll
-        for (int st = 0; st < 2; ++st)
+          for (int u = 0; u < 4; ++u) {
+            const int w = 4 * (t0 + u) + wi;
+            wpos[u] = w < 196 ? w : -1;
+            const int wc = w < 196 ? w : 0;
+            const int py = wc / 14, px = wc - 14 * py;
+            const int base0 = (2 * py) * kImgS + 2 * px + dx, base1 = base0 + kImgS;
+            d[u][0] = b1a, d[u][1] = b1b, d[u][2] = b1a, d[u][3] = b1b;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int k = 16 * st + 8 * h + 2 * c;
-            koff[st][h] = (k / 6) * kImgS + (k % 6);
+            for (int st = 0; st < 2; ++st)
+              mma_bf16(d[u], img[base0 + koff1[st][0]], img[base1 + koff1[st][0]],
+                       img[base0 + koff1[st][1]], img[base1 + koff1[st][1]], bw1[st][0], bw1[st][1]);
           }
-        const float b0 = bc1[2 * c], b1 = bc1[2 * c + 1];
-        for (int t = 0; t < 49; ++t) {
-          // rows g and g + 8: window w = 4t + g/4 (+2), sub = g % 4
-          int base[2];
 #pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            const int w = 4 * t + (g >> 2) + 2 * r, sub = g & 3;
-            const int py = w / 14, px = w % 14;
-            base[r] = (2 * py + (sub >> 1)) * kImgS + 2 * px + (sub & 1);
-          }
-          float d[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-          for (int st = 0; st < 2; ++st)
-            mma_bf16(d, img[base[0] + koff[st][0]], img[base[1] + koff[st][0]],
-                     img[base[0] + koff[st][1]], img[base[1] + koff[st][1]], bw1[st][0], bw1[st][1]);
-          // bias + ReLU, 2x2 average pool over lanes g..g+3 (lane bits 2, 3)
-          float v[4] = {fmaxf(d[0] + b0, 0.f), fmaxf(d[1] + b1, 0.f), fmaxf(d[2] + b0, 0.f),
-                        fmaxf(d[3] + b1, 0.f)};
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            v[i] += __shfl_xor_sync(0xffffffffu, v[i], 4);
-            v[i] += __shfl_xor_sync(0xffffffffu, v[i], 8);
-          }
-          if ((g & 3) == 0) {
-            const int w0 = 4 * t + (g >> 2), w1 = w0 + 2;
-            p1[w0 * 4 + c] = pack_bf16(0.25f * v[0], 0.25f * v[1]);
-            p1[w1 * 4 + c] = pack_bf16(0.25f * v[2], 0.25f * v[3]);
+          for (int u = 0; u < 4; ++u) {
+            // ReLU, vertical pair in-thread (rows g, g+8), horizontal pair = lane ^ 4
+            float s0 = fmaxf(d[u][0], 0.f) + fmaxf(d[u][2], 0.f);
+            float s1 = fmaxf(d[u][1], 0.f) + fmaxf(d[u][3], 0.f);
+            s0 += __shfl_xor_sync(0xffffffffu, s0, 4);
+            s1 += __shfl_xor_sync(0xffffffffu, s1, 4);
+            if (dx == 0 && wpos[u] >= 0) p1[wpos[u] * 4 + c] = pack_bf16(0.25f * s0, 0.25f * s1);
           }
         }
         __syncwarp();
+        // the pair image is consumed: prefetch this warp's next sample
+        if (s + kWarpsL < s_hi) prefetch_img(img_s, args.pimg + (uint64_t)(s + kWarpsL) * kImgWords, lane);
         // ---------------------------------------------- conv2 (this warp)
         // p1 word layout [py*14 + px][cpair]; A k = tap * 8 + ci
-        int toff[13][2];
+        int toff[13][2];  // A-fragment word offsets: k = tap * 8 + ci
 #pragma unroll
         for (int st = 0; st < 13; ++st)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int k = 16 * st + 8 * h + 2 * c;
             const int tap = k >> 3, cp = (k & 7) >> 1;
-            toff[st][h] = tap < 25 ? ((tap / 5) * 14 + (tap % 5)) * 4 + cp : -1;
+            toff[st][h] = tap < 25 ? ((tap / 5) * 14 + (tap % 5)) * 4 + cp : 196 * 4;  // zero pixel
           }
-        const float b2a = bc2[2 * c], b2b = bc2[2 * c + 1], b2c = bc2[8 + 2 * c],
-                    b2d = bc2[9 + 2 * c];
-        for (int t = 0; t < 7; ++t) {
-          int base[2];
-          bool valid[2];
+        __nv_bfloat16* o = p2 + warp * kP2S;
+        // 7 tiles of 4 windows (window 4t + wi of the 5 x 5 pooled map), two
+        // tiles per step: 4 independent MMA chains (2 tiles x 2 n-tiles)
+        for (int t0 = 0; t0 < 7; t0 += 2) {
+          int wv[2], b0[2], b1[2];
+          float d[2][2][4];
 #pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            const int m = 16 * t + g + 8 * r;  // pixel row in pool order
-            valid[r] = m < 100;
-            const int w = valid[r] ? (m >> 2) : 0, sub = m & 3;
-            const int py = w / 5, px = w % 5;
-            base[r] = ((2 * py + (sub >> 1)) * 14 + 2 * px + (sub & 1)) * 4;
+          for (int u = 0; u < 2; ++u) {
+            const int w = 4 * (t0 + u) + wi;
+            wv[u] = w < 25 ? w : -1;
+            const int wc = w < 25 ? w : 0;
+            const int qy = wc / 5, qx = wc - 5 * qy;
+            b0[u] = ((2 * qy) * 14 + 2 * qx + dx) * 4;
+            b1[u] = b0[u] + 14 * 4;
+            d[u][0][0] = b2a, d[u][0][1] = b2b, d[u][0][2] = b2a, d[u][0][3] = b2b;
+            d[u][1][0] = b2c, d[u][1][1] = b2d, d[u][1][2] = b2c, d[u][1][3] = b2d;
           }
-          float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
           for (int st = 0; st < 13; ++st) {
-            const uint32_t a0 = toff[st][0] >= 0 ? p1[base[0] + toff[st][0]] : 0u;
-            const uint32_t a1 = toff[st][0] >= 0 ? p1[base[1] + toff[st][0]] : 0u;
-            const uint32_t a2 = toff[st][1] >= 0 ? p1[base[0] + toff[st][1]] : 0u;
-            const uint32_t a3 = toff[st][1] >= 0 ? p1[base[1] + toff[st][1]] : 0u;
-            mma_bf16(d0, a0, a1, a2, a3, bw2[st][0][0], bw2[st][0][1]);
-            mma_bf16(d1, a0, a1, a2, a3, bw2[st][1][0], bw2[st][1][1]);
-          }
-          float v[8] = {fmaxf(d0[0] + b2a, 0.f), fmaxf(d0[1] + b2b, 0.f), fmaxf(d0[2] + b2a, 0.f),
-                        fmaxf(d0[3] + b2b, 0.f), fmaxf(d1[0] + b2c, 0.f), fmaxf(d1[1] + b2d, 0.f),
-                        fmaxf(d1[2] + b2c, 0.f), fmaxf(d1[3] + b2d, 0.f)};
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            v[i] += __shfl_xor_sync(0xffffffffu, v[i], 4);
-            v[i] += __shfl_xor_sync(0xffffffffu, v[i], 8);
+            for (int u = 0; u < 2; ++u) {
+              const int z0 = st == 12 ? -b0[u] : 0, z1 = st == 12 ? -b1[u] : 0;  // tap 25: zero pixel
+              const uint32_t a0 = p1[b0[u] + toff[st][0]];
+              const uint32_t a1 = p1[b1[u] + toff[st][0]];
+              const uint32_t a2 = p1[b0[u] + z0 + toff[st][1]];
+              const uint32_t a3 = p1[b1[u] + z1 + toff[st][1]];
+              mma_bf16(d[u][0], a0, a1, a2, a3, bw2[st][0][0], bw2[st][0][1]);
+              mma_bf16(d[u][1], a0, a1, a2, a3, bw2[st][1][0], bw2[st][1][1]);
+            }
           }
-          if ((g & 3) == 0) {
-            __nv_bfloat16* o = p2 + warp * kP2S;
 #pragma unroll
-            for (int r = 0; r < 2; ++r) {
-              const int m = 16 * t + g + 8 * r;
-              if (m < 100) {
-                const int w = m >> 2;
-                o[(2 * c) * 25 + w] = __float2bfloat16(0.25f * v[2 * r]);
-                o[(2 * c + 1) * 25 + w] = __float2bfloat16(0.25f * v[2 * r + 1]);
-                o[(8 + 2 * c) * 25 + w] = __float2bfloat16(0.25f * v[4 + 2 * r]);
-                o[(9 + 2 * c) * 25 + w] = __float2bfloat16(0.25f * v[4 + 2 * r + 1]);
-              }
+          for (int u = 0; u < 2; ++u) {
+            float s0 = fmaxf(d[u][0][0], 0.f) + fmaxf(d[u][0][2], 0.f);
+            float s1 = fmaxf(d[u][0][1], 0.f) + fmaxf(d[u][0][3], 0.f);
+            float s2 = fmaxf(d[u][1][0], 0.f) + fmaxf(d[u][1][2], 0.f);
+            float s3 = fmaxf(d[u][1][1], 0.f) + fmaxf(d[u][1][3], 0.f);
+            s0 += __shfl_xor_sync(0xffffffffu, s0, 4);
+            s1 += __shfl_xor_sync(0xffffffffu, s1, 4);
+            s2 += __shfl_xor_sync(0xffffffffu, s2, 4);
+            s3 += __shfl_xor_sync(0xffffffffu, s3, 4);
+            if (dx == 0 && wv[u] >= 0) {
+              uint32_t* ow = reinterpret_cast<uint32_t*>(o + wv[u] * 16);
+              ow[c] = pack_bf16(0.25f * s0, 0.25f * s1);
+              ow[4 + c] = pack_bf16(0.25f * s2, 0.25f * s3);
             }
           }
         }
@@ -361,19 +401,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_lenet_fitness(LenetArgs args) {
       // ------------------------------------------------ fc1: 128 x 400 . 400 x 8
       {
         const int mt = warp;  // 16-row tile of the 128 (120) outputs
-        float d[4] = {0.f, 0.f, 0.f, 0.f};
+        float d[4] = {0.f, 0.f, 0.f, 0.f}, e[4] = {0.f, 0.f, 0.f, 0.f};
         const uint32_t a_base =
             smem_addr(sm + Smem::wf1) +
             (uint32_t)(((16 * mt + (lane & 7) + ((lane >> 3) & 1) * 8) * kF1S + (lane >> 4) * 8) * 2);
         const __nv_bfloat16* bb = p2 + g * kP2S + 2 * c;
-#pragma unroll 5
-        for (int st = 0; st < 25; ++st) {
-          uint32_t a[4];
+#pragma unroll 4
+        for (int st = 0; st < 24; st += 2) {  // two independent accumulator chains
+          uint32_t a[4], a2[4];
           ldmatrix_x4(a, a_base + st * 32);
-          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(bb + 16 * st);
-          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(bb + 16 * st + 8);
-          mma_bf16(d, a[0], a[1], a[2], a[3], b0, b1);
+          ldmatrix_x4(a2, a_base + st * 32 + 32);
+          mma_bf16(d, a[0], a[1], a[2], a[3], *reinterpret_cast<const uint32_t*>(bb + 16 * st),
+                   *reinterpret_cast<const uint32_t*>(bb + 16 * st + 8));
+          mma_bf16(e, a2[0], a2[1], a2[2], a2[3], *reinterpret_cast<const uint32_t*>(bb + 16 * st + 16),
+                   *reinterpret_cast<const uint32_t*>(bb + 16 * st + 24));
         }
+        {
+          uint32_t a[4];
+          ldmatrix_x4(a, a_base + 24 * 32);
+          mma_bf16(d, a[0], a[1], a[2], a[3], *reinterpret_cast<const uint32_t*>(bb + 16 * 24),
+                   *reinterpret_cast<const uint32_t*>(bb + 16 * 24 + 8));
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) d[i] += e[i];
         // rows (outputs) 16mt + g (+8), cols (samples) 2c, 2c+1
         const int j0 = 16 * mt + g, j1 = j0 + 8;
         const float c0 = j0 < 120 ? bf1[j0] : 0.f, c1 = j1 < 120 ? bf1[j1] : 0.f;
@@ -408,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lenet_fitness(LenetArgs args) {
       }
       __syncthreads();
       // ------------------------------------- fc3 (16 x 96 . 96 x 8) + CE
-      if (warp == 0) {
+      if (warp == kWarpsL - 1) {  // the warp with no fc2 tile
         float d[4] = {0.f, 0.f, 0.f, 0.f};
         const uint32_t a_base =
             smem_addr(sm + Smem::wf3) +
@@ -443,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lenet_fitness(LenetArgs args) {
         __syncwarp();
       }
     }
-    if (warp == 0) {
+    if (warp == kWarpsL - 1) {
       // fixed-order sum of the 8 batch slots
       float t = loss;
       t += __shfl_xor_sync(0xffffffffu, t, 1);
@@ -460,6 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lenet_fitness(LenetArgs args) {
 struct LenetPlan {
   LenetArgs args;
   unsigned grid;
+  uint32_t* pimg;  // owned
 };
 
 uint32_t lenet_num_parts(uint32_t S) { return (S + kChunkS - 1) / kChunkS; }
@@ -483,7 +534,20 @@ LenetPlan* lenet_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t 
   }
   auto* p = new (std::nothrow) LenetPlan{};
   if (!p) return nullptr;
-  p->args.X = X;
+  if (cudaMalloc(&p->pimg, (size_t)S * kImgWords * 4) != cudaSuccess) {
+    snprintf(err, errlen, "LeNet objective: cudaMalloc of the pair images failed");
+    delete p;
+    return nullptr;
+  }
+  const uint64_t n = (uint64_t)S * kImgWords;
+  k_lenet_pairs<<<(unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256>>>(X, S, p->pimg);
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    snprintf(err, errlen, "LeNet objective: pair-image kernel failed");
+    cudaFree(p->pimg);
+    delete p;
+    return nullptr;
+  }
+  p->args.pimg = p->pimg;
   p->args.y = y;
   p->args.W = W;
   p->args.rows = rows;
@@ -495,7 +559,11 @@ LenetPlan* lenet_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t 
   return p;
 }
 
-void lenet_plan_destroy(LenetPlan* p) { delete p; }
+void lenet_plan_destroy(LenetPlan* p) {
+  if (!p) return;
+  cudaFree(p->pimg);
+  delete p;
+}
 
 cudaError_t lenet_fitness_launch(const LenetPlan* p, float* part, const int* gate,
                                  cudaStream_t s) {
