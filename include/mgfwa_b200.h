@@ -242,6 +242,9 @@ int mgfwa_time_kernel(mgfwa_ctx_t ctx, int kernel, uint64_t iters, double* ms,
                       uint64_t* units);
 
 /* ---- utilities ---------------------------------------------------------- */
+/* MgfwaConfig::validate (config.cpp:42-79): MGFWA_OK, or MGFWA_EINVAL with
+ * the reference's message in mgfwa_last_error(NULL).  Host-only, no GPU. */
+int mgfwa_validate_config(const mgfwa_config_t* config);
 /* key_hash, rng.hpp:43-52, evaluated on the device for n keys [n][7]. */
 int mgfwa_key_hash(const uint64_t* keys, uint64_t n, uint64_t* out);
 const char* mgfwa_version(void);

@@ -81,6 +81,7 @@ SIGNATURES = {
     "mgfwa_op_batched_apply": (_int, [C.POINTER(mgfwa_objective_t), _pd, _u64, _u64, _pd, _pu64]),
     "mgfwa_op_argmin_per_population": (_int, [_pd, _u64, _u64, _pu64, _pd]),
     "mgfwa_key_hash": (_int, [_pu64, _u64, _pu64]),
+    "mgfwa_validate_config": (_int, [C.POINTER(mgfwa_config_t)]),
     "mgfwa_time_fitness": (_int, [_P, _u64, _pd, _pu64]),
     "mgfwa_time_kernel": (_int, [_P, _int, _u64, _pd, _pu64]),
     "mgfwa_create_shard": (_int, [C.POINTER(mgfwa_config_t), C.POINTER(mgfwa_space_t),

@@ -1350,6 +1350,11 @@ int mgfwa_time_fitness(mgfwa_ctx_t ctx, uint64_t iters, double* ms, uint64_t* un
   return mgfwa_time_kernel(ctx, MGFWA_KERNEL_FITNESS, iters, ms, units);
 }
 
+int mgfwa_validate_config(const mgfwa_config_t* config) {
+  if (config == nullptr) return fail(nullptr, invalid("mgfwa_validate_config: null config"));
+  return fail(nullptr, validate_config(to_host(config)));
+}
+
 int mgfwa_key_hash(const uint64_t* keys, uint64_t n, uint64_t* out) {
   auto body = [&]() -> Status {
     uint64_t *dk = nullptr, *dout = nullptr;

@@ -163,6 +163,12 @@ __global__ void k_pop_range(EngineView v) {
 #ifndef EXPLODE_MAPALL
 #define EXPLODE_MAPALL 0
 #endif
+#ifndef EXPLODE_NOMAP
+#define EXPLODE_NOMAP 0  // timing experiment only (wrong results)
+#endif
+#ifndef EXPLODE_ALWAYSMAP
+#define EXPLODE_ALWAYSMAP 0
+#endif
 constexpr int kSparkGroup = EXPLODE_KG;
 
 // t = -1 + u * 2 for u = (h >> 11) * 2^-53, exactly as the reference's
@@ -300,7 +306,13 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
     // Out-of-box / boundary coordinates of this spark: exact inclusive test
     // (config.hpp:22-24) and the kMapping draw U[pop_lo, pop_hi)
     // (engine.cpp:119-125), 4 independent chains, selected per lane.
+#if EXPLODE_NOMAP
+    if (false) {
+#elif EXPLODE_ALWAYSMAP
+    if (true) {
+#else
     if (__any_sync(0xffffffffu, slow != 0)) {
+#endif
       const double2 lo01 = *reinterpret_cast<const double2*>(&ch.lo[li0]);
       const double2 lo23 = *reinterpret_cast<const double2*>(&ch.lo[li0 + 2]);
       const double2 hi01 = *reinterpret_cast<const double2*>(&ch.hi[li0]);

@@ -69,6 +69,12 @@ class MgfwaConfig:
     max_evaluations: int = 0
     wall_clock_budget_ms: float = 0.0
 
+    def validate(self) -> None:
+        """MgfwaConfig::validate (config.cpp:42-79): raises ValueError with the
+        reference's message."""
+        c, _keep = self._c()
+        _check(A.lib().mgfwa_validate_config(C.byref(c)))
+
     def top_spark_count(self) -> int:  # config.cpp:37-40
         return int(math.ceil(self.guide_fraction * float(self.sparks_per_firework)))
 
