@@ -61,14 +61,21 @@ typedef struct {
 #define MGFWA_OBJ_ACKLEY 3      /* standard Ackley, unshifted               */
 #define MGFWA_OBJ_MLP_WEIGHTS 4 /* mean CE of an I-H-O ReLU MLP whose
                                    weights are the candidate (tensor cores) */
-#define MGFWA_OBJ_LENET 5       /* reserved: LeNet-5 loss (not yet on GPU) */
+#define MGFWA_OBJ_LENET 5       /* mean CE of LeNet-5 whose 61,706 parameters
+                                   are the candidate (28x28 samples)       */
+#define MGFWA_OBJ_NET 6         /* the reference's input-space benchmark
+                                   network net_id (nets.cpp:36-167): fixed
+                                   weights from weight_seed, the candidate
+                                   is the input vector; fp64 on the device */
 typedef struct {
   int kind;
   uint32_t in_dim;   /* MLP: I (e.g. 784)            */
   uint32_t hidden;   /* MLP: H (32, 64, 128, 256)    */
   uint32_t out_dim;  /* MLP: O (<= 10)               */
-  uint32_t samples;  /* MLP: S synthetic samples     */
+  uint32_t samples;  /* MLP / LeNet: S synthetic samples */
   uint64_t data_seed;
+  int net_id;            /* NET: 1..12 (net_registry, nets.cpp:36-55) */
+  uint64_t weight_seed;  /* NET: MlpBlackBox weight seed             */
 } mgfwa_objective_t;
 
 /* RunRecord counters, engine.hpp:63-66. */

@@ -51,12 +51,25 @@ struct Objective {
   int kind = MGFWA_OBJ_SPHERE;
   std::uint32_t in_dim = 0, hidden = 0, out_dim = 0, samples = 0;
   std::uint64_t data_seed = 0;
+  int net_id = 0;
+  std::uint64_t weight_seed = 0;
   static Objective sphere() { return Objective{MGFWA_OBJ_SPHERE}; }
   static Objective rastrigin() { return Objective{MGFWA_OBJ_RASTRIGIN}; }
   static Objective ackley() { return Objective{MGFWA_OBJ_ACKLEY}; }
   static Objective mlp_weights(std::uint32_t in = 784, std::uint32_t h = 32, std::uint32_t out = 10,
                                std::uint32_t s = 1024, std::uint64_t seed = 1) {
     return Objective{MGFWA_OBJ_MLP_WEIGHTS, in, h, out, s, seed};
+  }
+  static Objective lenet(std::uint32_t s = 1024, std::uint64_t seed = 1) {
+    return Objective{MGFWA_OBJ_LENET, 784, 0, 10, s, seed};
+  }
+  // The reference's benchmark network net_id (1..12) with its fixed weights
+  // (MlpBlackBox(net_spec(net_id), weight_seed), nets.cpp:36-167).
+  static Objective net(int net_id, std::uint64_t weight_seed = 1) {
+    Objective o{MGFWA_OBJ_NET};
+    o.net_id = net_id;
+    o.weight_seed = weight_seed;
+    return o;
   }
 };
 
@@ -105,8 +118,9 @@ class Engine {
       throw std::invalid_argument("SearchSpace: lower/upper must be non-empty and equal length");
     const mgfwa_config_t c = detail::to_c(config);
     const mgfwa_space_t s{space.lower.data(), space.upper.data(), space.lower.size()};
-    const mgfwa_objective_t o{objective.kind, objective.in_dim, objective.hidden,
-                              objective.out_dim, objective.samples, objective.data_seed};
+    const mgfwa_objective_t o{objective.kind,    objective.in_dim,    objective.hidden,
+                              objective.out_dim, objective.samples,   objective.data_seed,
+                              objective.net_id,  objective.weight_seed};
     detail::check(mgfwa_create(&c, &s, &o, seed, device, &ctx_));
   }
   Engine(const Engine&) = delete;

@@ -15,6 +15,8 @@ from .engine import (  # noqa: F401
     LeNet,
     MgfwaConfig,
     MlpWeights,
+    NET_REGISTRY,
+    Net,
     Objective,
     Rastrigin,
     RunRecord,
@@ -35,6 +37,7 @@ from .engine import (  # noqa: F401
     kReinit,
     key_hash,
     loser_out,
+    net_param_count,
     multi_guiding_sparks,
     random_mapping,
     run,

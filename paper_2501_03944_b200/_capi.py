@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libmgfwa_b200.so")
 
 MGFWA_OK, MGFWA_EINVAL, MGFWA_ECUDA, MGFWA_ENOMEM, MGFWA_ENCCL, MGFWA_ESTATE = range(6)
-OBJ_SPHERE, OBJ_RASTRIGIN, OBJ_ACKLEY, OBJ_MLP_WEIGHTS, OBJ_LENET = 1, 2, 3, 4, 5
+OBJ_SPHERE, OBJ_RASTRIGIN, OBJ_ACKLEY, OBJ_MLP_WEIGHTS, OBJ_LENET, OBJ_NET = 1, 2, 3, 4, 5, 6
 
 _u64, _dbl, _int = C.c_uint64, C.c_double, C.c_int
 _pd, _pu64 = C.POINTER(C.c_double), C.POINTER(C.c_uint64)
@@ -33,7 +33,8 @@ class mgfwa_space_t(C.Structure):
 
 class mgfwa_objective_t(C.Structure):
     _fields_ = [("kind", _int), ("in_dim", C.c_uint32), ("hidden", C.c_uint32),
-                ("out_dim", C.c_uint32), ("samples", C.c_uint32), ("data_seed", _u64)]
+                ("out_dim", C.c_uint32), ("samples", C.c_uint32), ("data_seed", _u64),
+                ("net_id", _int), ("weight_seed", _u64)]
 
 
 class mgfwa_counters_t(C.Structure):

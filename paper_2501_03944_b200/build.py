@@ -21,7 +21,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libmgfwa_b200.so")
 BUILD = os.path.join(HERE, "_build")
-SOURCES = ["k_engine.cu", "k_mlp_tc.cu", "k_lenet.cu", "engine.cu"]
+SOURCES = ["k_engine.cu", "k_mlp_tc.cu", "k_lenet.cu", "k_net.cu", "engine.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "-diag-suppress", "177"]

@@ -125,7 +125,13 @@ static Status validate_space(const mgfwa_space_t* s) {
 }
 
 // NN objectives (tensor-core fitness): the MLP-weights loss and LeNet-5.
-static bool nn_kind(int kind) { return kind == MGFWA_OBJ_MLP_WEIGHTS || kind == MGFWA_OBJ_LENET; }
+// NN fitness path (partials from a fitness kernel, not fused into explode):
+// the MLP-weights and LeNet losses (synthetic dataset) and the reference's
+// input-space benchmark networks (fixed weights).
+static bool nn_kind(int kind) {
+  return kind == MGFWA_OBJ_MLP_WEIGHTS || kind == MGFWA_OBJ_LENET || kind == MGFWA_OBJ_NET;
+}
+static bool has_dataset(int kind) { return kind == MGFWA_OBJ_MLP_WEIGHTS || kind == MGFWA_OBJ_LENET; }
 static uint32_t nn_in_dim(const mgfwa_objective_t* o) {
   return o->kind == MGFWA_OBJ_LENET ? 784u : o->in_dim;
 }
@@ -133,25 +139,35 @@ static uint32_t nn_out_dim(const mgfwa_objective_t* o) {
   return o->kind == MGFWA_OBJ_LENET ? 10u : o->out_dim;
 }
 
-// One NN fitness plan: the MLP (tcgen05) or the LeNet (mma.sync) kernel.
+// One NN fitness plan: the MLP (tcgen05), LeNet (mma.sync) or benchmark
+// network (fp64 GEMM chain) kernel.
 struct NnPlan {
   MlpPlan* mlp = nullptr;
   LenetPlan* lenet = nullptr;
+  NetPlan* net = nullptr;
   void destroy() {
     mlp_plan_destroy(mlp);
     lenet_plan_destroy(lenet);
+    net_plan_destroy(net);
     mlp = nullptr;
     lenet = nullptr;
+    net = nullptr;
   }
 };
 static cudaError_t nn_fitness_launch(const NnPlan& p, float* part, const int* gate,
                                      cudaStream_t s) {
+  if (p.net) return net_fitness_launch(p.net, part, gate, s);
   return p.lenet ? lenet_fitness_launch(p.lenet, part, gate, s)
                  : mlp_fitness_launch(p.mlp, part, gate, s);
 }
 
 static uint64_t objective_dim(const mgfwa_objective_t* o) {
   if (o->kind == MGFWA_OBJ_LENET) return lenet_dim();
+  if (o->kind == MGFWA_OBJ_NET) {
+    uint32_t d = 0;
+    net_spec_dims(o->net_id, &d, nullptr, nullptr, nullptr);
+    return d;
+  }
   if (o->kind == MGFWA_OBJ_MLP_WEIGHTS)
     return (uint64_t)o->hidden * o->in_dim + o->hidden + (uint64_t)o->out_dim * o->hidden +
            o->out_dim;
@@ -173,6 +189,10 @@ static Status validate_objective(const mgfwa_objective_t* o, uint64_t D) {
       return ok();
     case MGFWA_OBJ_LENET:
       if (o->samples == 0) return invalid("LeNet objective: samples must be positive");
+      if (objective_dim(o) != D) return invalid("forward: input dimension mismatch");
+      return ok();
+    case MGFWA_OBJ_NET:  // net_spec (nets.cpp:57-62), forward (nets.cpp:138-141)
+      if (o->net_id < 1 || o->net_id > 12) return invalid("net id must be in 1..12");
       if (objective_dim(o) != D) return invalid("forward: input dimension mismatch");
       return ok();
     default:
@@ -255,7 +275,8 @@ struct Workspace {
     return {c.B, c.mu, c.lam, c.M, c.M > 0 ? c.top() : 0, space->dim, (uint64_t)obj->kind,
             obj->in_dim, obj->hidden, obj->out_dim, obj->samples,
             nn_kind(obj->kind) ? obj->data_seed : 0, (uint64_t)dev, trace_cap,
-            rank, world};
+            rank, world, obj->kind == MGFWA_OBJ_NET ? (uint64_t)obj->net_id : 0,
+            obj->kind == MGFWA_OBJ_NET ? obj->weight_seed : 0};
   }
 
   // Run-specific scalars and the search box (cheap; H2D of 2 x D bounds).
@@ -314,8 +335,9 @@ struct Workspace {
     v.nch = (uint32_t)((D + kChunk - 1) / kChunk);
     v.obj_kind = obj->kind;
     v.nn = nn_kind(obj->kind);
-    v.samples = v.nn ? obj->samples : 0;
-    v.nparts = !v.nn ? v.nch
+    v.samples = !v.nn ? 0 : obj->kind == MGFWA_OBJ_NET ? 1 : obj->samples;
+    v.nparts = !v.nn                         ? v.nch
+               : obj->kind == MGFWA_OBJ_NET   ? 1
                : obj->kind == MGFWA_OBJ_LENET ? lenet_num_parts(obj->samples)
                                               : mlp_num_parts(obj->samples);
     v.trace_cap = trace_cap;
@@ -364,7 +386,7 @@ struct Workspace {
     add(&v.tr_best, trace_cap * c.B * 8);
     add(&v.tr_ns, trace_cap * c.B * 8);
     add(&v.ctl, sizeof(Ctl));
-    if (v.nn) {
+    if (has_dataset(obj->kind)) {
       add(&X, (size_t)obj->samples * nn_in_dim(obj) * 2);
       add(&y, (size_t)obj->samples * 4);
     }
@@ -390,7 +412,17 @@ struct Workspace {
     v.boosts = boosts;
     STATUS_TRY(configure(c, space, seed));
 
-    if (v.nn) {
+    if (obj->kind == MGFWA_OBJ_NET) {
+      char err[256] = {0};
+      auto make = [&](NnPlan& pl, const float* X32, uint64_t rows) -> Status {
+        pl.net = net_plan_create(obj->net_id, obj->weight_seed, X32, Dp, rows, err, sizeof err);
+        if (!pl.net) return invalid(err);
+        return ok();
+      };
+      STATUS_TRY(make(plan_sparks, v.sparks, P));
+      if (G > 0) STATUS_TRY(make(plan_guides, v.guides, G));
+      STATUS_TRY(make(plan_fresh, v.pos, F));
+    } else if (v.nn) {
       std::vector<__nv_bfloat16> Xh;
       std::vector<int32_t> yh;
       make_dataset(obj->samples, nn_in_dim(obj), nn_out_dim(obj), obj->data_seed, Xh, yh);

@@ -82,4 +82,14 @@ cudaError_t lenet_fitness_launch(const LenetPlan* p, float* part, const int* gat
 uint32_t lenet_num_parts(uint32_t S);
 uint64_t lenet_dim();
 
+// ---- reference benchmark networks (k_net.cu, fp64 layer GEMMs) ----
+// X: fp32 candidate rows of stride ldx; part[row][1][2] = network output.
+struct NetPlan;
+bool net_spec_dims(int net_id, uint32_t* input_dim, uint32_t* hidden_dim, uint32_t* layers,
+                   int* gelu);
+NetPlan* net_plan_create(int net_id, uint64_t weight_seed, const float* X, uint64_t ldx,
+                         uint64_t rows, char* err, size_t errlen);
+void net_plan_destroy(NetPlan* p);
+cudaError_t net_fitness_launch(const NetPlan* p, float* part, const int* gate, cudaStream_t s);
+
 }  // namespace mgfwa_b200

@@ -133,17 +133,21 @@ class Objective:
     out_dim: int = 0
     samples: int = 0
     data_seed: int = 0
+    net_id: int = 0
+    weight_seed: int = 0
 
     def dim(self, analytic_dim: int = 0) -> int:
         if self.kind == A.OBJ_MLP_WEIGHTS:
             return self.hidden * self.in_dim + self.hidden + self.out_dim * self.hidden + self.out_dim
         if self.kind == A.OBJ_LENET:
             return LENET_DIM
+        if self.kind == A.OBJ_NET:
+            return NET_REGISTRY[self.net_id][2]
         return analytic_dim
 
     def _c(self):
         return A.mgfwa_objective_t(self.kind, self.in_dim, self.hidden, self.out_dim, self.samples,
-                                   self.data_seed)
+                                   self.data_seed, self.net_id, self.weight_seed)
 
 
 def Sphere() -> Objective:  # nets.cpp:80-84
@@ -163,6 +167,33 @@ def MlpWeights(in_dim: int = 784, hidden: int = 32, out_dim: int = 10, samples: 
     """Mean CE of an I-H-O ReLU MLP whose weights (W1,b1,W2,b2 in reference
     Layer order) are the candidate; bf16 tensor-core evaluation."""
     return Objective(A.OBJ_MLP_WEIGHTS, in_dim, hidden, out_dim, samples, data_seed)
+
+
+# net_registry(), nets.cpp:36-55: id -> (scale, activation, input_dim,
+# hidden_dim, hidden_layers, reported_params)
+NET_REGISTRY = {
+    1: ("small", "relu", 10, 16, 2, 465), 2: ("small", "gelu", 10, 32, 5, 4609),
+    3: ("small", "relu", 20, 16, 5, 1441), 4: ("small", "gelu", 20, 32, 5, 4929),
+    5: ("medium", "relu", 100, 64, 8, 35649), 6: ("medium", "gelu", 100, 128, 8, 128641),
+    7: ("medium", "relu", 200, 64, 8, 42049), 8: ("medium", "gelu", 200, 128, 8, 141441),
+    9: ("large", "relu", 1000, 256, 11, 914433), 10: ("large", "gelu", 1000, 512, 11, 3137585),
+    11: ("large", "relu", 2000, 256, 11, 1173433), 12: ("large", "gelu", 2000, 512, 11, 3657585),
+}
+
+
+def Net(net_id: int, weight_seed: int = 1) -> Objective:
+    """The reference's benchmark network net_id (MlpBlackBox(net_spec(id),
+    weight_seed), nets.cpp:36-167): fixed weights, the candidate is the
+    network input, scalar output; fp64 evaluation on the device."""
+    if net_id not in NET_REGISTRY:
+        raise ValueError("net id must be in 1..12")
+    return Objective(A.OBJ_NET, net_id=net_id, weight_seed=weight_seed)
+
+
+def net_param_count(net_id: int) -> int:
+    """param_count(net_spec(id)), nets.cpp:64-72."""
+    _, _, d, h, lh, _ = NET_REGISTRY[net_id]
+    return (d * h + h) + (lh - 1) * (h * h + h) + (h + 1)
 
 
 LENET_DIM = (6 * 25 + 6) + (16 * 6 * 25 + 16) + (400 * 120 + 120) + (120 * 84 + 84) + (84 * 10 + 10)

@@ -17,10 +17,10 @@ Modes: the reference's ``serial`` (one population, one worker) and
 engine here; the mode rules are kept (serial forces ``batches = 1``), the
 worker count is meaningless on the device and is ignored.  ``compare`` thus
 reports the B-batch over single-batch throughput ratio of the engine.
-Objectives: ``net_id = 0`` is the sphere as in the reference; an explicit
-``objective`` (any device objective descriptor, e.g. ``MlpWeights()``) may
-be supplied instead.  The reference's input-space Nets 1-12 (§8(f) rank 2)
-are not available on the device yet and raise ``NotImplementedError``.
+Objectives: ``net_id = 0`` is the sphere and ``net_id`` 1..12 the
+reference's benchmark networks with ``weight_seed`` (``Net``, evaluated in
+fp64 on the device), as in the reference; an explicit ``objective`` (any
+device objective descriptor, e.g. ``MlpWeights()``) may be supplied instead.
 
 CLI:  python -m paper_2501_03944_b200.experiment run --net 0 --dim 30 \\
           --runs 8 --max-evals 20000 --out DIR      (trace.csv, summary.csv)
@@ -36,7 +36,7 @@ import sys
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence, TextIO
 
-from .engine import MgfwaConfig, Objective, RunRecord, SearchSpace, Sphere, run
+from .engine import NET_REGISTRY, MgfwaConfig, Net, Objective, RunRecord, SearchSpace, Sphere, run
 
 SERIAL, PARALLEL = "serial", "parallel"
 
@@ -99,8 +99,7 @@ def _objective(config: ExperimentConfig) -> Objective:
         return config.objective
     if config.net_id == 0:
         return Sphere()
-    raise NotImplementedError(
-        "mgfwa_b200: the input-space nets (Nets 1-12) are not available on the GPU engine yet")
+    return Net(config.net_id, config.weight_seed)
 
 
 def search_space_for(config: ExperimentConfig) -> SearchSpace:
@@ -110,10 +109,10 @@ def search_space_for(config: ExperimentConfig) -> SearchSpace:
         dim = obj.dim(config.dim)
         lo = config.lower if config.lower is not None else -1.0
         hi = config.upper if config.upper is not None else 1.0
-    else:
-        dim = config.sphere_dim
-        lo = config.lower if config.lower is not None else -10.0
-        hi = config.upper if config.upper is not None else 10.0
+    else:  # sphere(d) in [-10, 10], or net_spec(id).input_dim in [-5, 5]
+        dim = config.sphere_dim if config.net_id == 0 else NET_REGISTRY[config.net_id][2]
+        lo = config.lower if config.lower is not None else (-10.0 if config.net_id == 0 else -5.0)
+        hi = config.upper if config.upper is not None else (10.0 if config.net_id == 0 else 5.0)
     if dim <= 0:
         raise ValueError("sphere dimension must be positive")
     return SearchSpace.box(dim, lo, hi)

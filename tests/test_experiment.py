@@ -48,8 +48,9 @@ def test_mode_rules_and_space():
     sp = E.search_space_for(E.ExperimentConfig(sphere_dim=7))
     assert sp.dim() == 7 and sp.lower[0] == -10.0 and sp.upper[0] == 10.0
     assert E.objective_name(E.ExperimentConfig(sphere_dim=7)) == "sphere(d=7)"
-    with pytest.raises(NotImplementedError):
-        E.search_space_for(E.ExperimentConfig(net_id=3))
+    sp = E.search_space_for(E.ExperimentConfig(net_id=3))  # net_spec(3).input_dim, [-5, 5]
+    assert sp.dim() == 20 and sp.lower[0] == -5.0 and sp.upper[0] == 5.0
+    assert E.objective_name(E.ExperimentConfig(net_id=3)) == "net 3"
 
 
 def test_checkpoint_grid_matches_reference_formula():

@@ -254,3 +254,56 @@ def test_lenet_nan_weights_become_inf(P):
     W[1, D - 1] = np.nan  # fc3 bias: NaN logit -> NaN loss -> +inf
     got, nan = P.batched_apply(P.LeNet(samples=64), W)
     assert np.isinf(got[1]) and nan == 1 and np.isfinite(got[0])
+
+
+# ------------------------------------------------- reference benchmark nets
+# Nets 1-12 (nets.cpp:36-167) evaluated in fp64 with the reference's
+# operation order: ReLU nets are bit-identical to the reference's forward()
+# (then rounded once to the fp32 fitness); GELU nets differ only by the
+# device tanh (<= 2 ulp per activation), far below one fp32 ulp of the output.
+@pytest.mark.parametrize("net_id", list(range(1, 13)))
+def test_reference_nets_vs_compiled_reference(P, net_id):
+    ref = O.Reference()
+    gelu = P.NET_REGISTRY[net_id][1] == "gelu"
+    for wseed in (1, 7):
+        D = P.Net(net_id).dim()
+        rng = np.random.default_rng(net_id * 10 + wseed)
+        X = f32(rng.uniform(-5, 5, size=(37, D)))
+        got, nan = P.batched_apply(P.Net(net_id, wseed), X)
+        assert nan == 0
+        want = np.array([ref.evaluate(O.ObjectiveDesc(kind=O.OBJ_NET, net_id=net_id, weight_seed=wseed), x)
+                         for x in X])
+        if gelu:
+            np.testing.assert_allclose(got, want.astype(np.float32), rtol=2e-7, atol=1e-12)
+        else:
+            assert np.array_equal(got, want.astype(np.float32).astype(np.float64))
+
+
+def test_reference_net_golden(P, golden):
+    g = golden("objectives.npz")
+    got, _ = P.batched_apply(P.Net(1, 1), g["net1__x"])
+    np.testing.assert_allclose(got, g["net1__f"].astype(np.float32), rtol=2e-7)
+
+
+def test_reference_net_validation(P):
+    with pytest.raises(ValueError, match="forward: input dimension mismatch"):
+        P.batched_apply(P.Net(1), np.zeros((2, 11)))
+    with pytest.raises(ValueError, match="net id must be in 1..12"):
+        P.Net(13)
+
+
+def test_reference_net_run_statistical(P):
+    """A short MGFWA run on net 5 (the paper's medium ReLU net) on the device
+    against the compiled reference run(): final best over 6 seeds, MWU."""
+    from scipy.stats import mannwhitneyu
+
+    cfg = P.MgfwaConfig(batches=1, fireworks=5, sparks_per_firework=30, max_evaluations=5 + 165 * 40)
+    ocfg = O.Config(batches=1, fireworks=5, sparks_per_firework=30, guides_per_firework=3,
+                    boosts=[1.0, 2.0, 4.0], max_evaluations=5 + 165 * 40)
+    D = P.Net(5).dim()
+    space = P.SearchSpace.box(D, -5.0, 5.0)
+    ref = O.Reference()
+    g = [P.run(cfg, space, P.Net(5, 1), s).best_fitness[0] for s in range(6)]
+    r = [ref.run(ocfg, np.full(D, -5.0), np.full(D, 5.0), O.ObjectiveDesc(kind=O.OBJ_NET, net_id=5, weight_seed=1),
+                 s).best_fitness[0] for s in range(6)]
+    assert mannwhitneyu(g, r).pvalue > 0.01
