@@ -22,9 +22,12 @@ reference's benchmark networks with ``weight_seed`` (``Net``, evaluated in
 fp64 on the device), as in the reference; an explicit ``objective`` (any
 device objective descriptor, e.g. ``MlpWeights()``) may be supplied instead.
 
-CLI:  python -m paper_2501_03944_b200.experiment run --net 0 --dim 30 \\
-          --runs 8 --max-evals 20000 --out DIR      (trace.csv, summary.csv)
-      python -m paper_2501_03944_b200.experiment compare ... --out DIR
+CLI (cli.cpp's mgfwa_bench: subcommands run / compare / nets, the same
+flags, JSON config keys, messages and exit codes 0 / 2 / 3):
+      python -m paper_2501_03944_b200.experiment run --sphere 30 --runs 8 \\
+          --budget-evals 20000 --out DIR           (trace.csv, summary.csv)
+      python -m paper_2501_03944_b200.experiment compare --net 5 ... --out DIR
+      python -m paper_2501_03944_b200.experiment nets
 """
 from __future__ import annotations
 
@@ -56,7 +59,7 @@ class ExperimentConfig:
     sphere_dim: int = 10
     mode: str = PARALLEL
     workers: int = 0
-    algo: MgfwaConfig = field(default_factory=lambda: MgfwaConfig(max_evaluations=10000))
+    algo: MgfwaConfig = field(default_factory=MgfwaConfig)
     lower: Optional[float] = None
     upper: Optional[float] = None
     runs: int = 8
@@ -350,59 +353,236 @@ def write_compare_report(out: TextIO, rep: CompareReport) -> None:
 
 
 # ------------------------------------------------------------------- CLI
-def _config_from_args(a) -> ExperimentConfig:
-    algo = MgfwaConfig(batches=a.batches, fireworks=a.fireworks, sparks_per_firework=a.sparks,
-                       guides_per_firework=a.guides, boosts=[1.0, 2.0, 4.0, 8.0][: a.guides],
-                       max_evaluations=a.max_evals, wall_clock_budget_ms=a.wall_ms)
-    return ExperimentConfig(net_id=a.net, sphere_dim=a.dim, mode=a.mode, algo=algo, lower=a.lower,
-                            upper=a.upper, runs=a.runs, base_seed=a.seed, out_dir=a.out or "")
+# cli.cpp:22-380 (mgfwa_bench run / compare / nets) without CLI11: the same
+# subcommands, flags, JSON config keys, messages and exit codes.
+EXIT_OK, EXIT_INVALID_ARGS, EXIT_IO_FAILURE = 0, 2, 3  # cli.hpp:6-8
+
+_JSON_KEYS = {"net", "sphere", "mode", "workers", "batches", "mu", "lambda", "guides", "sigma", "beta", "ca",
+              "cr", "a0", "lower", "upper", "runs", "seed", "weight_seed", "budget_ms", "budget_evals", "out"}
+
+
+def apply_json_config(path: str, cfg: ExperimentConfig) -> bool:
+    """apply_json_config, cli.cpp:22-78; returns whether an objective was set."""
+    import json
+
+    try:
+        with open(path) as f:
+            doc = json.load(f)
+    except OSError:
+        raise ValueError("cannot read config file: " + path)
+    selected = False
+    for key, value in doc.items():
+        if key not in _JSON_KEYS:
+            raise ValueError("unknown config key: " + key)
+        selected |= _apply(cfg, key, value)
+    return selected
+
+
+def _apply(cfg: ExperimentConfig, key: str, value) -> bool:
+    a = cfg.algo
+    if key == "net":
+        cfg.net_id = int(value)
+        return True
+    if key == "sphere":
+        cfg.sphere_dim, cfg.net_id = int(value), 0
+        return True
+    setters = {
+        "mode": lambda v: setattr(cfg, "mode", mode_from_string(v)),
+        "workers": lambda v: setattr(cfg, "workers", int(v)),
+        "batches": lambda v: setattr(a, "batches", int(v)),
+        "mu": lambda v: setattr(a, "fireworks", int(v)),
+        "lambda": lambda v: setattr(a, "sparks_per_firework", int(v)),
+        "guides": lambda v: setattr(a, "guides_per_firework", int(v)),
+        "sigma": lambda v: setattr(a, "guide_fraction", float(v)),
+        "beta": lambda v: setattr(a, "boosts", [float(x) for x in v]),
+        "ca": lambda v: setattr(a, "amp_amplify", float(v)),
+        "cr": lambda v: setattr(a, "amp_reduce", float(v)),
+        "a0": lambda v: setattr(a, "initial_amplitude", float(v)),
+        "lower": lambda v: setattr(cfg, "lower", float(v)),
+        "upper": lambda v: setattr(cfg, "upper", float(v)),
+        "runs": lambda v: setattr(cfg, "runs", int(v)),
+        "seed": lambda v: setattr(cfg, "base_seed", int(v)),
+        "weight_seed": lambda v: setattr(cfg, "weight_seed", int(v)),
+        "budget_ms": lambda v: setattr(a, "wall_clock_budget_ms", float(v)),
+        "budget_evals": lambda v: setattr(a, "max_evaluations", int(v)),
+        "out": lambda v: setattr(cfg, "out_dir", str(v)),
+    }
+    setters[key](value)
+    return False
+
+
+def algorithm_params_match(x: ExperimentConfig, y: ExperimentConfig) -> bool:
+    """algorithm_params_match, bench.cpp:48-63."""
+    ax, ay = x.algo, y.algo
+    return (x.net_id == y.net_id and x.sphere_dim == y.sphere_dim and ax.fireworks == ay.fireworks
+            and ax.sparks_per_firework == ay.sparks_per_firework
+            and ax.guides_per_firework == ay.guides_per_firework and ax.guide_fraction == ay.guide_fraction
+            and list(ax.boosts) == list(ay.boosts) and ax.amp_amplify == ay.amp_amplify
+            and ax.amp_reduce == ay.amp_reduce and ax.initial_amplitude == ay.initial_amplitude
+            and ax.max_evaluations == ay.max_evaluations and ax.wall_clock_budget_ms == ay.wall_clock_budget_ms
+            and x.lower == y.lower and x.upper == y.upper and x.runs == y.runs and x.base_seed == y.base_seed
+            and x.weight_seed == y.weight_seed)
+
+
+_FLAG_KEYS = [("net", "net"), ("sphere", "sphere"), ("mode", "mode"), ("workers", "workers"),
+              ("batches", "batches"), ("mu", "mu"), ("lambda_", "lambda"), ("guides", "guides"),
+              ("sigma", "sigma"), ("beta", "beta"), ("ca", "ca"), ("cr", "cr"), ("a0", "a0"),
+              ("lower", "lower"), ("upper", "upper"), ("runs", "runs"), ("seed", "seed"),
+              ("weight_seed", "weight_seed"), ("budget_ms", "budget_ms"), ("budget_evals", "budget_evals"),
+              ("out", "out")]
+
+
+def resolve_config(args) -> tuple:
+    """resolve_config, cli.cpp:131-191: defaults, then the JSON file, then the
+    flags actually given; default boost ladder 1, 2, 4, ... when only the
+    guide count changed."""
+    cfg = ExperimentConfig(algo=MgfwaConfig())
+    selected = False
+    if args.config:
+        selected = apply_json_config(args.config, cfg)
+    for attr, key in _FLAG_KEYS:
+        v = getattr(args, attr, None)
+        if v is None:
+            continue
+        if key == "beta":
+            v = [float(x) for x in v.split(",")]
+        selected |= _apply(cfg, key, v)
+        if key == "guides" and cfg.algo.guides_per_firework == 0:
+            cfg.algo.boosts = []
+    a = cfg.algo
+    if a.guides_per_firework > 0 and len(a.boosts) != a.guides_per_firework and args.beta is None:
+        a.boosts = [2.0 ** i for i in range(a.guides_per_firework)]
+    return cfg, selected
+
+
+def do_run(cfg: ExperimentConfig) -> int:
+    """do_run, cli.cpp:209-245."""
+    if not cfg.out_dir:
+        raise ValueError("run requires --out DIR")
+    try:
+        os.makedirs(cfg.out_dir, exist_ok=True)
+    except OSError:
+        raise IOError("cannot create " + cfg.out_dir)
+    res = run_experiment(cfg)
+    trace_path = os.path.join(cfg.out_dir, "trace.csv")
+    summary_path = os.path.join(cfg.out_dir, "summary.csv")
+    with open(trace_path, "w") as f:
+        write_trace_csv(f, res)
+    with open(summary_path, "w") as f:
+        write_summary_csv(f, summarize(res, default_checkpoints(res)))
+    best = min(c.waves[-1].best for c in res.curves)
+    print(f"{objective_name(res.config)}, {res.config.mode} mode, {len(res.records)} runs: best fitness "
+          f"{format_double(best)}, {res.total_evaluations} evaluations total\n"
+          f"wrote {trace_path} and {summary_path}")
+    return EXIT_OK
+
+
+def do_compare(shared: ExperimentConfig) -> int:
+    """do_compare, cli.cpp:247-284 (curves as wall_ms,best_fitness)."""
+    if not shared.out_dir:
+        raise ValueError("compare requires --out DIR")
+    try:
+        os.makedirs(shared.out_dir, exist_ok=True)
+    except OSError:
+        raise IOError("cannot create " + shared.out_dir)
+    rep = compare(shared)
+    paths = []
+    for name, rows in (("compare_serial.csv", rep.serial_curve), ("compare_parallel.csv", rep.parallel_curve)):
+        path = os.path.join(shared.out_dir, name)
+        with open(path, "w") as f:
+            f.write("wall_ms,best_fitness\n")
+            for row in rows:
+                f.write(f"{format_double(row.checkpoint_ms)},{format_double(row.mean_best)}\n")
+        paths.append(path)
+    write_compare_report(sys.stdout, rep)
+    print(f"wrote {paths[0]} and {paths[1]}")
+    return EXIT_OK
+
+
+def do_nets() -> int:
+    """do_nets, cli.cpp:286-297."""
+    from .engine import net_param_count
+
+    print("id,scale,activation,input_dim,hidden_dim,output_dim,hidden_layers,params,reported_params")
+    for nid, (scale, act, d, h, lh, rep) in NET_REGISTRY.items():
+        print(f"{nid},{scale},{act},{d},{h},1,{lh},{net_param_count(nid)},{rep}")
+    return EXIT_OK
+
+
+def _parser():
+    ap = argparse.ArgumentParser(prog="python -m paper_2501_03944_b200.experiment",
+                                 description="Batched multi-guiding-spark fireworks optimizer benchmark (B200)")
+    sub = ap.add_subparsers(dest="command", required=True)
+
+    def common(p, with_mode):
+        p.add_argument("--config")
+        g = p.add_mutually_exclusive_group()
+        g.add_argument("--net", type=int, choices=range(1, 13), metavar="{1..12}")
+        g.add_argument("--sphere", type=int)
+        if with_mode:
+            p.add_argument("--mode")
+        p.add_argument("--workers", type=int)
+        p.add_argument("--batches", "-B", type=int)
+        p.add_argument("--mu", type=int)
+        p.add_argument("--lambda", dest="lambda_", type=int)
+        p.add_argument("--guides", "-M", type=int)
+        p.add_argument("--sigma", type=float)
+        p.add_argument("--beta")
+        p.add_argument("--ca", type=float)
+        p.add_argument("--cr", type=float)
+        p.add_argument("--a0", type=float)
+        p.add_argument("--lower", type=float)
+        p.add_argument("--upper", type=float)
+        p.add_argument("--runs", type=int)
+        p.add_argument("--seed", type=int)
+        p.add_argument("--weight-seed", dest="weight_seed", type=int)
+        p.add_argument("--budget-ms", dest="budget_ms", type=float)
+        p.add_argument("--budget-evals", dest="budget_evals", type=int)
+        p.add_argument("--out")
+
+    common(sub.add_parser("run", help="optimize one objective and write trace/summary CSVs"), True)
+    c = sub.add_parser("compare", help="run serial and parallel modes on shared parameters and seeds")
+    common(c, False)
+    c.add_argument("--serial-config", dest="serial_config")
+    c.add_argument("--parallel-config", dest="parallel_config")
+    sub.add_parser("nets", help="list the 12 benchmark networks")
+    return ap
 
 
 def main(argv=None) -> int:
-    ap = argparse.ArgumentParser(prog="python -m paper_2501_03944_b200.experiment")
-    ap.add_argument("command", choices=["run", "compare"])
-    ap.add_argument("--net", type=int, default=0)
-    ap.add_argument("--dim", type=int, default=10)
-    ap.add_argument("--mode", default=PARALLEL, type=mode_from_string)
-    ap.add_argument("--batches", type=int, default=1)
-    ap.add_argument("--fireworks", type=int, default=5)
-    ap.add_argument("--sparks", type=int, default=30)
-    ap.add_argument("--guides", type=int, default=3)
-    ap.add_argument("--max-evals", type=int, default=20000)
-    ap.add_argument("--wall-ms", type=float, default=0.0)
-    ap.add_argument("--lower", type=float, default=None)
-    ap.add_argument("--upper", type=float, default=None)
-    ap.add_argument("--runs", type=int, default=8)
-    ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--out", default="")
-    a = ap.parse_args(argv)
-    cfg = _config_from_args(a)
+    """cli_main, cli.cpp:301-380: exit codes 0 / 2 (invalid arguments) /
+    3 (I/O failure)."""
     try:
-        if a.command == "run":
-            res = run_experiment(cfg)
-            if not cfg.out_dir:
-                write_trace_csv(sys.stdout, res)
-                return 0
-            os.makedirs(cfg.out_dir, exist_ok=True)
-            with open(os.path.join(cfg.out_dir, "trace.csv"), "w") as f:
-                write_trace_csv(f, res)
-            with open(os.path.join(cfg.out_dir, "summary.csv"), "w") as f:
-                write_summary_csv(f, summarize(res, default_checkpoints(res)))
-            print(f"{objective_name(res.config)}: {res.total_evaluations} evaluations in "
-                  f"{format_double(res.total_wall_ms)} ms; wrote trace.csv and summary.csv")
-        else:
-            rep = compare(cfg)
-            write_compare_report(sys.stdout, rep)
-            if cfg.out_dir:
-                os.makedirs(cfg.out_dir, exist_ok=True)
-                for name, rows in (("compare_serial.csv", rep.serial_curve),
-                                   ("compare_parallel.csv", rep.parallel_curve)):
-                    with open(os.path.join(cfg.out_dir, name), "w") as f:
-                        write_summary_csv(f, rows)
-    except ValueError as e:
+        args = _parser().parse_args(argv)
+    except SystemExit as e:
+        return EXIT_OK if e.code == 0 else EXIT_INVALID_ARGS
+    try:
+        if args.command == "nets":
+            return do_nets()
+        cfg, selected = resolve_config(args)
+        if not selected:
+            raise ValueError("choose an objective: --net <1..12> or --sphere <D>")
+        if args.command == "run":
+            cfg.validate()
+            return do_run(cfg)
+        if args.serial_config or args.parallel_config:
+            s_cfg = dataclasses.replace(cfg, algo=dataclasses.replace(cfg.algo))
+            p_cfg = dataclasses.replace(cfg, algo=dataclasses.replace(cfg.algo))
+            if args.serial_config:
+                apply_json_config(args.serial_config, s_cfg)
+            if args.parallel_config:
+                apply_json_config(args.parallel_config, p_cfg)
+            if not algorithm_params_match(s_cfg, p_cfg):
+                raise ValueError("serial and parallel configs disagree on algorithm parameters")
+            cfg = p_cfg
+        cfg.validate()
+        return do_compare(cfg)
+    except (IOError, OSError) as e:
         print(f"error: {e}", file=sys.stderr)
-        return 2
-    return 0
+        return EXIT_IO_FAILURE
+    except (ValueError, KeyError, TypeError) as e:
+        print(f"error: {e}", file=sys.stderr)
+        return EXIT_INVALID_ARGS
 
 
 if __name__ == "__main__":
@@ -412,4 +592,5 @@ if __name__ == "__main__":
 __all__ = ["ExperimentConfig", "ExperimentResult", "RunCurve", "WavePoint", "SummaryRow", "CompareReport",
            "Crossing", "ModeStats", "mode_from_string", "normalized", "search_space_for", "objective_name",
            "run_experiment", "run_curve", "best_at", "checkpoint_grid", "default_checkpoints", "summarize",
-           "format_double", "write_trace_csv", "write_summary_csv", "compare", "write_compare_report"]
+           "format_double", "write_trace_csv", "write_summary_csv", "compare", "write_compare_report",
+           "apply_json_config", "algorithm_params_match", "resolve_config", "main"]

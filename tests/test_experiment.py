@@ -177,7 +177,46 @@ def test_compare_report_and_cli(tmp_path):
     out = io.StringIO()
     E.write_compare_report(out, rep)
     assert out.getvalue().startswith("serial  : ")
-    rc = E.main(["run", "--dim", "5", "--runs", "2", "--max-evals", "600", "--out", str(tmp_path)])
+    rc = E.main(["run", "--sphere", "5", "--runs", "2", "--budget-evals", "600", "--out", str(tmp_path)])
     assert rc == 0
     assert (tmp_path / "trace.csv").read_text().startswith("run_id,batch,evals,wall_ms,best_fitness\n")
     assert (tmp_path / "summary.csv").read_text().startswith("checkpoint_ms,mean_best,std_best,runs\n")
+    rc = E.main(["compare", "--net", "1", "-B", "2", "--lambda", "12", "--guides", "2", "--runs", "2",
+                 "--budget-evals", "2000", "--out", str(tmp_path / "cmp")])
+    assert rc == 0
+    assert (tmp_path / "cmp" / "compare_serial.csv").read_text().startswith("wall_ms,best_fitness\n")
+
+
+def test_cli_config_resolution_and_errors(tmp_path, capsys):
+    import json
+
+    conf = tmp_path / "c.json"
+    conf.write_text(json.dumps({"sphere": 12, "batches": 3, "guides": 4, "budget_evals": 1000, "seed": 9}))
+    args = E._parser().parse_args(["run", "--config", str(conf), "--mu", "7"])
+    cfg, selected = E.resolve_config(args)
+    assert selected and cfg.sphere_dim == 12 and cfg.algo.batches == 3 and cfg.algo.fireworks == 7
+    assert cfg.algo.boosts == [1.0, 2.0, 4.0, 8.0] and cfg.base_seed == 9  # default ladder (cli.cpp:180-189)
+    bad = tmp_path / "bad.json"
+    bad.write_text(json.dumps({"sphere": 3, "colour": 1}))
+    assert E.main(["run", "--config", str(bad), "--out", str(tmp_path)]) == E.EXIT_INVALID_ARGS
+    assert "unknown config key: colour" in capsys.readouterr().err
+    assert E.main(["run", "--budget-evals", "10", "--out", str(tmp_path)]) == E.EXIT_INVALID_ARGS
+    assert "choose an objective: --net <1..12> or --sphere <D>" in capsys.readouterr().err
+    assert E.main(["run", "--sphere", "4", "--budget-evals", "10"]) == E.EXIT_INVALID_ARGS
+    assert "run requires --out DIR" in capsys.readouterr().err
+    assert E.main(["run", "--net", "13"]) == E.EXIT_INVALID_ARGS
+    assert E.main(["run", "--config", str(tmp_path / "missing.json")]) == E.EXIT_INVALID_ARGS
+    assert "cannot read config file" in capsys.readouterr().err
+    s = tmp_path / "s.json"
+    s.write_text(json.dumps({"mu": 4}))
+    assert E.main(["compare", "--sphere", "3", "--budget-evals", "100", "--serial-config", str(s),
+                   "--out", str(tmp_path)]) == E.EXIT_INVALID_ARGS
+    assert "serial and parallel configs disagree on algorithm parameters" in capsys.readouterr().err
+
+
+def test_cli_nets_listing(capsys):
+    assert E.main(["nets"]) == 0
+    lines = capsys.readouterr().out.splitlines()
+    assert lines[0] == "id,scale,activation,input_dim,hidden_dim,output_dim,hidden_layers,params,reported_params"
+    assert lines[1] == "1,small,relu,10,16,1,2,465,465"
+    assert lines[10] == "10,large,gelu,1000,512,1,11,3139585,3137585"  # nets 10-12: nearest realizable
