@@ -500,7 +500,10 @@ __global__ void __launch_bounds__(kRankThreads) k_rank(EngineView v) {
   const uint32_t lam = (uint32_t)v.lam;
   unsigned nan_local = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  constexpr int R = 4;  // rows per warp step (loads of 4 rows in flight)
+#ifndef RANK_R
+#define RANK_R 4
+#endif
+  constexpr int R = RANK_R;  // rows per warp step (their loads in flight together)
   for (uint32_t k0 = warp * R; k0 < lam; k0 += nwarp * R) {
     int64_t rows[R];
     float x[R];
@@ -1131,11 +1134,16 @@ void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
     pdl_launch(k_select, (unsigned)v.Fl, kSelectThreads, 0, s, v);
   }
   if (phase != kGenA) {
+#ifndef GEN_SKIP  // timing experiments only (GEN_SKIP=1: loser..finalize, 2: whole phase B)
+#define GEN_SKIP 0
+#endif
+    if (GEN_SKIP == 0) {
     pdl_launch(k_loser, 1, 128, 0, s, v);
     pdl_launch(k_fresh_rows, capped((v.F * v.nch + kWarps - 1) / kWarps, nsm), 256, 0, s, v, 1);
     if (v.nn) hooks->eval_fresh(hooks->ctx, s);
     pdl_launch(k_finalize_record, 1, 256, 0, s, v, 1);
-    pdl_launch(k_record_copy, tail_blocks(v, nsm), 256, 0, s, v);
+    }
+    if (GEN_SKIP < 2) pdl_launch(k_record_copy, tail_blocks(v, nsm), 256, 0, s, v);
   }
 }
 

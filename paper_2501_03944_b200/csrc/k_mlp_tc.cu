@@ -44,19 +44,39 @@ namespace {
 constexpr int BM = 128;  // samples per tile (TMEM lanes)
 constexpr int BN = 256;  // (spark, hidden) columns per tile
 constexpr int BK = 64;   // K per pipeline stage (one 128-byte swizzle atom)
-constexpr int kStages = 4;
+#ifndef MLP_STAGES
+#define MLP_STAGES 4
+#endif
+#ifndef MLP_AHEAD
+#define MLP_AHEAD 0  // k-blocks the MMA issuer may run ahead of completion (0 = unbounded)
+#endif
+#ifndef MLP_PROBE
+#define MLP_PROBE 0  // 1: profiling probe, TMA + layer-1 MMA pipeline only (no epilogue math)
+#endif
+constexpr int kStages = MLP_STAGES;
 constexpr int kABytes = BM * BK * 2;  // 16 KB
-constexpr int kBBytes = BN * BK * 2;  // 32 KB
-constexpr int kStageBytes = kABytes + kBBytes;
+// CG = CTA group: 1 (one SM per tile, M = 128) or 2 (an SM pair per tile,
+// M = 256, cta_group::2: each CTA stages its own 128 A rows and HALF of B,
+// which halves the per-SM operand traffic through shared memory and L2).
+template <int CG>
+struct Cfg {
+  static constexpr int kBRows = BN / CG;                 // B rows staged per CTA
+  static constexpr int kBBytes = kBRows * BK * 2;        // 32 KB | 16 KB
+  static constexpr int kStageBytes = kABytes + kBBytes;  // 48 KB | 32 KB
+  static constexpr int kStages = CG == 2 ? 6 : MLP_STAGES;
+  static constexpr int kO2 = 16 / CG;                    // layer-2 B rows (outputs) per CTA
+};
 constexpr int kThreads = 384;
 constexpr int kEpiWarps = 8;
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kN2 = 16;  // layer-2 MMA N (outputs padded to 16)
 constexpr int kMaxO = 10;
 
-struct SmemLayout {
-  static constexpr int w2 = kStages * kStageBytes;       // bf16 W2^T, [spark][16][H] interleaved
-  static constexpr int b1 = w2 + kN2 * BN * 2;           // float[BN]
+template <int CG>
+struct SmemLayoutT {
+  static constexpr int kStages = Cfg<CG>::kStages;
+  static constexpr int w2 = kStages * Cfg<CG>::kStageBytes;  // bf16 W2^T, [spark][kO2][H] interleaved
+  static constexpr int b1 = w2 + Cfg<CG>::kO2 * BN * 2;  // float[BN]
   static constexpr int b2 = b1 + BN * 4;                 // float[8][kN2]
   static constexpr int red = b2 + 8 * kN2 * 4;           // float[kEpiWarps][8]
   static constexpr int bars = red + kEpiWarps * 8 * 4;   // u64 barriers
@@ -64,7 +84,8 @@ struct SmemLayout {
   static constexpr int tmem_slot = bars + nbars * 8;
   static constexpr int total = tmem_slot + 16;
 };
-constexpr int kSmemBytes = SmemLayout::total;
+template <int CG>
+constexpr int smem_bytes() { return SmemLayoutT<CG>::total; }
 
 struct MlpArgs {
   uint32_t S, I, H, O;
@@ -183,6 +204,88 @@ __device__ __forceinline__ void mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_
       "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
+// ---- CTA-pair (cta_group::2) variants
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on an mbarrier of (possibly) the peer CTA (shared::cluster address)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cbar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cbar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ bool mbar_test_cluster(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// 2-SM TMA: the completion bytes go to the leader CTA's mbarrier (cbar is a
+// shared::cluster address, possibly in the peer CTA).
+__device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const CUtensorMap* map, uint32_t cbar,
+                                                int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(cbar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_cg2(uint32_t dst, const CUtensorMap* map, uint32_t cbar,
+                                                int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(cbar), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+__device__ __forceinline__ void mma_ss2(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_ts2(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+// commit to the same barrier offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit2(uint32_t bar) {
+  const uint16_t mask = 3;
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(bar), "h"(mask)
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
@@ -262,7 +365,7 @@ __device__ __forceinline__ uint32_t d2_col(int j) {
 }
 
 // ------------------------------------------------------------------ kernel
-template <int H>
+template <int H, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     k_mlp_fitness(const __grid_constant__ CUtensorMap tmap_x,
                   const __grid_constant__ CUtensorMap tmap_w, MlpArgs args) {
@@ -270,6 +373,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (args.gate != nullptr && *args.gate == 0) return;
   constexpr int SPT = BN / H;  // sparks per N tile (1 when H == 256)
   static_assert(BN % H == 0 && H % 32 == 0, "H must divide 256 and be a multiple of 32");
+  using SmemLayout = SmemLayoutT<CG>;
+  constexpr int kStages = Cfg<CG>::kStages;
+  constexpr int kStageBytes = Cfg<CG>::kStageBytes;
+  constexpr int kO2 = Cfg<CG>::kO2;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0u;  // CTA rank in the pair
+  const bool leader = rank == 0;
 
   // 1024-byte aligned (SWIZZLE_128B atoms); no static shared memory is used,
   // so the dynamic window starts at the aligned base.
@@ -297,8 +406,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar_tfull + 8 * i, 1);
-      mbar_init(bar_tempty + 8 * i, kEpiWarps);
-      mbar_init(bar_a2full + 8 * i, kEpiWarps);
+      mbar_init(bar_tempty + 8 * i, kEpiWarps * CG);  // CG == 2: both CTAs' epilogues (leader's)
+      mbar_init(bar_a2full + 8 * i, kEpiWarps * CG);
       mbar_init(bar_d2full + 8 * i, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -306,94 +415,154 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_w)));
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-        smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+          smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+          smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync_all();  // peer barriers initialised, TMEM allocated on both SMs
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // the leader's copies of the pipeline barriers (TMA completion, epilogue arrivals)
+  const uint32_t c_full = CG == 2 ? mapa_rank(bar_full, 0) : bar_full;
+  const uint32_t c_tempty = CG == 2 ? mapa_rank(bar_tempty, 0) : bar_tempty;
+  const uint32_t c_a2full = CG == 2 ? mapa_rank(bar_a2full, 0) : bar_a2full;
 
   // Static contiguous tile range per CTA: tile t -> (n_tile = t / m_tiles,
   // m_tile = t % m_tiles), so one CTA walks all m-tiles of an N tile in turn
   // (its W1 tile stays hot in L2; X is L2-resident for everyone).
-  const uint32_t total = args.m_tiles * args.n_tiles;
-  const uint32_t t_begin = (uint32_t)(((uint64_t)total * blockIdx.x) / gridDim.x);
-  const uint32_t t_end = (uint32_t)(((uint64_t)total * (blockIdx.x + 1)) / gridDim.x);
+  // CG == 2: a unit is (n-tile, m-tile pair); CTA `rank` takes m-tile 2 mp + rank.
+  const uint32_t m_units = CG == 2 ? (args.m_tiles + 1) / 2 : args.m_tiles;
+  const uint32_t total = m_units * args.n_tiles;
+  const uint32_t groups = gridDim.x / CG, group = blockIdx.x / CG;
+  const uint32_t t_begin = (uint32_t)(((uint64_t)total * group) / groups);
+  const uint32_t t_end = (uint32_t)(((uint64_t)total * (group + 1)) / groups);
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer
       uint32_t stage = 0, phase = 0;
       for (uint32_t t = t_begin; t < t_end; ++t) {
-        const int m_tile = (int)(t % args.m_tiles), n_tile = (int)(t / args.m_tiles);
+        const int m_tile = (int)((t % m_units) * CG + rank), n_tile = (int)(t / m_units);
         for (uint32_t kb = 0; kb < args.k_blocks; ++kb) {
           mbar_wait(bar_empty + 8 * stage, phase ^ 1);
           const uint32_t sa = smem_u32(smem + stage * kStageBytes);
-          mbar_expect_tx(bar_full + 8 * stage, kStageBytes);
-          tma_load_2d(sa, &tmap_x, bar_full + 8 * stage, (int)(kb * BK), m_tile * BM);
-          tma_load_3d(sa + kABytes, &tmap_w, bar_full + 8 * stage, (int)(kb * BK), 0, n_tile * SPT);
+#if MLP_PROBE == 2  // profiling probe: no operand traffic after the first round of stages
+          if (t != t_begin || kb >= (uint32_t)kStages) {
+            mbar_arrive(bar_full + 8 * stage);
+            if (++stage == kStages) stage = 0, phase ^= 1;
+            continue;
+          }
+#endif
+          if (CG == 2) {
+            // both CTAs' halves complete on the leader's barrier
+            if (leader) mbar_expect_tx(bar_full + 8 * stage, 2 * kStageBytes);
+            const uint32_t cb = c_full + 8 * stage;
+            tma_load_2d_cg2(sa, &tmap_x, cb, (int)(kb * BK), m_tile * BM);
+            if (SPT >= 2)  // this CTA's half of the sparks of the N tile
+              tma_load_3d_cg2(sa + kABytes, &tmap_w, cb, (int)(kb * BK), 0,
+                              n_tile * SPT + (int)rank * (SPT / 2));
+            else  // H == 256: this CTA's half of the hidden rows
+              tma_load_3d_cg2(sa + kABytes, &tmap_w, cb, (int)(kb * BK), (int)rank * (H / 2), n_tile);
+          } else {
+            mbar_expect_tx(bar_full + 8 * stage, kStageBytes);
+            tma_load_2d(sa, &tmap_x, bar_full + 8 * stage, (int)(kb * BK), m_tile * BM);
+            tma_load_3d(sa + kABytes, &tmap_w, bar_full + 8 * stage, (int)(kb * BK), 0, n_tile * SPT);
+          }
           if (++stage == kStages) stage = 0, phase ^= 1;
         }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
-      constexpr uint32_t idesc1 = idesc_bf16(BM, BN);
-      constexpr uint32_t idesc2 = idesc_bf16(BM, kN2);
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer (the leader CTA of a pair)
+      constexpr uint32_t idesc1 = idesc_bf16(BM * CG, BN);
+      constexpr uint32_t idesc2 = idesc_bf16(BM * CG, kN2);
+      auto mma1 = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+        if (CG == 2) mma_ss2(d, a, b, idesc1, acc); else mma_ss(d, a, b, idesc1, acc);
+      };
+      auto commit = [&](uint32_t bar) {
+        if (CG == 2) mma_commit2(bar); else mma_commit(bar);
+      };
+      auto a2ready = [&](uint32_t b, uint32_t u) {
+        return CG == 2 ? mbar_test_cluster(bar_a2full + 8 * b, u) : mbar_test(bar_a2full + 8 * b, u);
+      };
+      auto a2wait = [&](uint32_t b, uint32_t u) {
+        if (CG == 2) mbar_wait_cluster(bar_a2full + 8 * b, u); else mbar_wait(bar_a2full + 8 * b, u);
+      };
       const uint32_t w2_base = smem_u32(s_w2);
       // layer-2 MMAs of the tile whose activations sit in buffer `b`
       auto issue_layer2 = [&](uint32_t b) {
         tc_fence_after();
         const uint32_t cb = tmem_base + b * BN;
 #pragma unroll
-        for (int j = 0; j < SPT; ++j) {
-          const uint32_t bj = w2_base + (uint32_t)(j * kN2 * H * 2);
+        for (int j = 0; j < (MLP_PROBE == 3 ? 0 : SPT); ++j) {
+          const uint32_t bj = w2_base + (uint32_t)(j * kO2 * H * 2);
 #pragma unroll
-          for (int kk = 0; kk < H / 16; ++kk)
-            mma_ts(cb + d2_col<H>(j), cb + a2_kcol<H>(j, kk),
-                   interleaved_desc(bj + kk * 512, 256, 128), idesc2, kk != 0);
+          for (int kk = 0; kk < H / 16; ++kk) {
+            // B: kO2 output rows x 16 K per step; core matrices 8 rows x 16 B,
+            // K-adjacent ones (kO2/8)*128 B apart, N-adjacent 128 B apart
+            const uint64_t bd = interleaved_desc(bj + kk * (kO2 / 8) * 256, (kO2 / 8) * 128, 128);
+            if (CG == 2)
+              mma_ts2(cb + d2_col<H>(j), cb + a2_kcol<H>(j, kk), bd, idesc2, kk != 0);
+            else
+              mma_ts(cb + d2_col<H>(j), cb + a2_kcol<H>(j, kk), bd, idesc2, kk != 0);
+          }
         }
-        mma_commit(bar_d2full + 8 * b);
+        commit(bar_d2full + 8 * b);
       };
       uint32_t stage = 0, phase = 0, i = 0;
+      uint32_t gk = 0;  // k-blocks issued so far (all tiles)
       bool pend = false;
       uint32_t pbuf = 0, puse = 0;
       for (uint32_t t = t_begin; t < t_end; ++t, ++i) {
         const uint32_t buf = i & 1, use = (i >> 1) & 1;
-        mbar_wait(bar_tempty + 8 * buf, use ^ 1);
+        if (CG == 2) mbar_wait_cluster(bar_tempty + 8 * buf, use ^ 1);
+        else mbar_wait(bar_tempty + 8 * buf, use ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * BN;
-        for (uint32_t kb = 0; kb < args.k_blocks; ++kb) {
+        for (uint32_t kb = 0; kb < args.k_blocks; ++kb, ++gk) {
+          // Keep at most MLP_AHEAD k-blocks queued in the tensor pipe, so the
+          // layer-2 MMAs slotted in below are not stuck behind a deep queue
+          // of layer-1 work (their completion releases the TMEM buffer).
+          if (MLP_AHEAD > 0 && gk >= (uint32_t)MLP_AHEAD) {
+            const uint32_t g0 = gk - MLP_AHEAD;
+            mbar_wait(bar_empty + 8 * (g0 % kStages), (g0 / kStages) & 1);
+          }
           mbar_wait(bar_full + 8 * stage, phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * kStageBytes);
           const uint64_t da = sw128_desc(sa), db = sw128_desc(sa + kABytes);
           const uint32_t rem = args.I - kb * BK;
           const uint32_t nk = rem >= BK ? BK / 16 : (rem + 15) / 16;
-          for (uint32_t kk = 0; kk < nk; ++kk)
-            mma_ss(d_tmem, da + 2 * kk, db + 2 * kk, idesc1, (kb | kk) != 0);
-          mma_commit(bar_empty + 8 * stage);
+          for (uint32_t kk = 0; kk < nk; ++kk) mma1(d_tmem, da + 2 * kk, db + 2 * kk, (kb | kk) != 0);
+          commit(bar_empty + 8 * stage);
           if (++stage == kStages) stage = 0, phase ^= 1;
-          if (pend && mbar_test(bar_a2full + 8 * pbuf, puse)) {
+          if (pend && a2ready(pbuf, puse)) {
             issue_layer2(pbuf);
             pend = false;
           }
         }
-        mma_commit(bar_tfull + 8 * buf);
+        commit(bar_tfull + 8 * buf);
+        if (MLP_PROBE == 1 || MLP_PROBE == 2) continue;
         if (pend) {
-          mbar_wait(bar_a2full + 8 * pbuf, puse);
+          a2wait(pbuf, puse);
           issue_layer2(pbuf);
         }
         pend = true;
         pbuf = buf;
         puse = use;
       }
-      if (pend) {
-        mbar_wait(bar_a2full + 8 * pbuf, puse);
+      if (pend && MLP_PROBE != 1 && MLP_PROBE != 2) {
+        a2wait(pbuf, puse);
         issue_layer2(pbuf);
       }
     }
@@ -410,12 +579,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t i = 0;
     uint32_t staged_n = 0xFFFFFFFFu;
     for (uint32_t t = t_begin; t < t_end; ++t, ++i) {
-      const uint32_t m_tile = t % args.m_tiles, n_tile = t / args.m_tiles;
+      const uint32_t m_tile = (t % m_units) * CG + rank, n_tile = t / m_units;
       const uint32_t buf = i & 1, use = (i >> 1) & 1;
       const uint32_t cb = tmem_base + buf * BN + lane_off;
       const uint32_t s = m_tile * BM + row;
       const bool valid = s < args.S;
       const int label = valid ? args.y[s] : 0;
+      if (MLP_PROBE == 1 || MLP_PROBE == 2) {
+        mbar_wait(bar_tfull + 8 * buf, use);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (CG == 2) mbar_arrive_cluster(c_tempty + 8 * buf); else mbar_arrive(bar_tempty + 8 * buf);
+        }
+        continue;
+      }
       // Stage b1 (fp32), b2 (fp32) and W2^T (bf16, interleaved core-matrix
       // layout: element (o, h) of spark j at j*16*H*2 + ((h/8)*2 + o/8)*128
       // + (o%8)*16 + (h%8)*2) when the N tile changes (every m_tiles tiles).
@@ -430,12 +608,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool ok = p < args.rows;
         const __nv_bfloat16* base = args.W + (ok ? p : 0) * args.Dp + (uint64_t)H * args.I;
         s_b1[idx] = ok ? __bfloat162float(base[h]) : 0.0f;
-        __nv_bfloat16* w2j = reinterpret_cast<__nv_bfloat16*>(s_w2 + j * kN2 * H * 2);
+        __nv_bfloat16* w2j = reinterpret_cast<__nv_bfloat16*>(s_w2 + j * kO2 * H * 2);
 #pragma unroll
-        for (int o = 0; o < kN2; ++o) {
+        for (int ol = 0; ol < kO2; ++ol) {  // this CTA's output rows o = rank * kO2 + ol
+          const int o = (int)rank * kO2 + ol;
           const __nv_bfloat16 wv =
               (ok && (uint32_t)o < O) ? base[H + o * H + h] : __float2bfloat16_rn(0.0f);
-          w2j[(((h >> 3) * 2 + (o >> 3)) * 128 + (o & 7) * 16 + (h & 7) * 2) / 2] = wv;
+          w2j[(((h >> 3) * (kO2 / 8) + (ol >> 3)) * 128 + (ol & 7) * 16 + (h & 7) * 2) / 2] = wv;
         }
       }
       for (int idx = et; idx < SPT * kN2; idx += kEpiThreads) {
@@ -471,7 +650,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar_a2full + 8 * buf);
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(c_a2full + 8 * buf); else mbar_arrive(bar_a2full + 8 * buf);
+      }
 
       // ---- logits (layer-2 MMA result) -> log-softmax CE
       mbar_wait(bar_d2full + 8 * buf, use);
@@ -504,7 +685,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // tile buffer consumed: hand it back to the MMA warp
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar_tempty + 8 * buf);
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(c_tempty + 8 * buf); else mbar_arrive(bar_tempty + 8 * buf);
+      }
       epi_bar();
       // deterministic per-(spark, m-tile) partial: the 4 lane quarters in order
       if (et < SPT) {
@@ -515,7 +698,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq) sum += s_red[(hh * 4 + qq) * 8 + jl];
         const uint64_t p = (uint64_t)n_tile * SPT + j;
-        if (p < args.rows) {
+        if (p < args.rows && m_tile < args.m_tiles) {
           args.part[(p * args.m_tiles + m_tile) * 2] = sum;
           args.part[(p * args.m_tiles + m_tile) * 2 + 1] = 0.0f;
         }
@@ -524,9 +707,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync_all();  // no MMA of the pair targets this TMEM any more
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+    if (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
   }
 }
 
@@ -549,17 +736,56 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-template <int H>
+template <int H, int CG>
 cudaError_t prepare_h() {
-  return cudaFuncSetAttribute(k_mlp_fitness<H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              kSmemBytes);
+  return cudaFuncSetAttribute(k_mlp_fitness<H, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              smem_bytes<CG>());
 }
 
-template <int H>
+template <int H, int CG>
 cudaError_t launch_h(const CUtensorMap& tx, const CUtensorMap& tw, int grid, const MlpArgs& a,
                      cudaStream_t s) {
-  pdl_launch(k_mlp_fitness<H>, grid, kThreads, kSmemBytes, s, tx, tw, a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem_bytes<CG>();
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (CG == 2) {  // the SM pair of a tile is a 2-CTA cluster
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = 2;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, k_mlp_fitness<H, CG>, tx, tw, a);
+}
+
+// CTA group of the plans (MGFWA_MLP_CG=1|2; default MLP_CG_DEFAULT).  The
+// pair variant is parity-green but measured slower on C2 (B200): 91 vs 75 us
+// per 1500 candidates.  Probes (MLP_PROBE): TMA + layer-1 MMA only 63.5 vs
+// 61.5 us; layer-1 MMA alone 62.9 vs 55.4 us; the epilogue chain, which for
+// a pair waits on both CTAs (remote mbarrier arrivals), adds 28 vs 14 us.
+// The single-SM kernel stays the default.
+#ifndef MLP_CG_DEFAULT
+#define MLP_CG_DEFAULT 1
+#endif
+int mlp_cg() {
+  static const int cg = [] {
+    const char* e = getenv("MGFWA_MLP_CG");
+    if (e && e[0] == '1') return 1;
+    if (e && e[0] == '2') return 2;
+    return MLP_CG_DEFAULT;
+  }();
+  return cg;
 }
 
 }  // namespace
@@ -570,6 +796,7 @@ struct MlpPlan {
   MlpArgs args;
   int grid;
   int H;
+  int cg;
 };
 
 uint32_t mlp_num_parts(uint32_t S) { return (S + BM - 1) / BM; }
@@ -603,10 +830,13 @@ MlpPlan* mlp_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t S, u
     }
   }
   const uint32_t spt = BN / H;
+  const int cg = mlp_cg();
   {
     cuuint64_t dims[3] = {I, H, rows};
     cuuint64_t strides[2] = {(cuuint64_t)I * 2, (cuuint64_t)Dp * 2};
-    cuuint32_t box[3] = {BK, H, spt};
+    // CG == 2: each CTA stages half of the N tile (half the sparks, or half
+    // the hidden rows of the one spark when H == 256)
+    cuuint32_t box[3] = {BK, cg == 2 && spt == 1 ? H / 2 : H, cg == 2 && spt >= 2 ? spt / 2 : spt};
     cuuint32_t es[3] = {1, 1, 1};
     if (enc(&p->tmap_w, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<__nv_bfloat16*>(W), dims,
             strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -628,12 +858,20 @@ MlpPlan* mlp_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t S, u
   p->args.spt = spt;
   p->args.W = W;
   p->args.y = y;
-  const uint32_t tiles = p->args.m_tiles * p->args.n_tiles;
-  p->grid = (int)(tiles < (uint32_t)nsm ? tiles : (uint32_t)nsm);
-  const cudaError_t e = H == 32    ? prepare_h<32>()
-                        : H == 64  ? prepare_h<64>()
-                        : H == 128 ? prepare_h<128>()
-                                   : prepare_h<256>();
+  p->cg = cg;
+  if (cg == 2) {
+    const uint32_t units = ((p->args.m_tiles + 1) / 2) * p->args.n_tiles;
+    const uint32_t pairs = (uint32_t)nsm / 2;
+    p->grid = 2 * (int)(units < pairs ? units : pairs);
+  } else {
+    const uint32_t tiles = p->args.m_tiles * p->args.n_tiles;
+    p->grid = (int)(tiles < (uint32_t)nsm ? tiles : (uint32_t)nsm);
+  }
+  const cudaError_t e =
+      cg == 2 ? (H == 32 ? prepare_h<32, 2>() : H == 64 ? prepare_h<64, 2>()
+                 : H == 128 ? prepare_h<128, 2>() : prepare_h<256, 2>())
+              : (H == 32 ? prepare_h<32, 1>() : H == 64 ? prepare_h<64, 1>()
+                 : H == 128 ? prepare_h<128, 1>() : prepare_h<256, 1>());
   if (e != cudaSuccess) {
     delete p;
     return fail(cudaGetErrorString(e));
@@ -647,11 +885,19 @@ cudaError_t mlp_fitness_launch(const MlpPlan* p, float* part, const int* gate, c
   MlpArgs a = p->args;
   a.part = part;
   a.gate = gate;
+  if (p->cg == 2) {
+    switch (p->H) {
+      case 32: return launch_h<32, 2>(p->tmap_x, p->tmap_w, p->grid, a, s);
+      case 64: return launch_h<64, 2>(p->tmap_x, p->tmap_w, p->grid, a, s);
+      case 128: return launch_h<128, 2>(p->tmap_x, p->tmap_w, p->grid, a, s);
+      case 256: return launch_h<256, 2>(p->tmap_x, p->tmap_w, p->grid, a, s);
+    }
+  }
   switch (p->H) {
-    case 32: return launch_h<32>(p->tmap_x, p->tmap_w, p->grid, a, s);
-    case 64: return launch_h<64>(p->tmap_x, p->tmap_w, p->grid, a, s);
-    case 128: return launch_h<128>(p->tmap_x, p->tmap_w, p->grid, a, s);
-    case 256: return launch_h<256>(p->tmap_x, p->tmap_w, p->grid, a, s);
+    case 32: return launch_h<32, 1>(p->tmap_x, p->tmap_w, p->grid, a, s);
+    case 64: return launch_h<64, 1>(p->tmap_x, p->tmap_w, p->grid, a, s);
+    case 128: return launch_h<128, 1>(p->tmap_x, p->tmap_w, p->grid, a, s);
+    case 256: return launch_h<256, 1>(p->tmap_x, p->tmap_w, p->grid, a, s);
   }
   return cudaErrorInvalidValue;
 }
