@@ -307,3 +307,26 @@ def test_reference_net_run_statistical(P):
     r = [ref.run(ocfg, np.full(D, -5.0), np.full(D, 5.0), O.ObjectiveDesc(kind=O.OBJ_NET, net_id=5, weight_seed=1),
                  s).best_fitness[0] for s in range(6)]
     assert mannwhitneyu(g, r).pvalue > 0.01
+
+
+def test_mlp_cta_pair_variant_matches(P, tmp_path):
+    """The cta_group::2 (SM-pair) MLP kernel (MGFWA_MLP_CG=2, off by
+    default) gives the same fitness as the single-SM kernel up to fp32
+    summation order, for every supported hidden width."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, paper_2501_03944_b200 as P\n"
+        "out = {}\n"
+        "for H in (32, 64, 128, 256):\n"
+        "    obj = P.MlpWeights(hidden=H, samples=300)\n"
+        "    W = np.random.default_rng(H).uniform(-0.05, 0.05, size=(21, obj.dim())).astype(np.float32)\n"
+        "    out[str(H)] = P.batched_apply(obj, W.astype(np.float64))[0]\n"
+        f"np.savez(r'{tmp_path}/' + __import__('os').environ['MGFWA_MLP_CG'] + '.npz', **out)\n")
+    for cg in ("1", "2"):
+        env = dict(__import__("os").environ, MGFWA_MLP_CG=cg)
+        subprocess.run([sys.executable, "-c", code], env=env, check=True, timeout=300)
+    a, b = np.load(tmp_path / "1.npz"), np.load(tmp_path / "2.npz")
+    for H in ("32", "64", "128", "256"):
+        np.testing.assert_allclose(a[H], b[H], rtol=1e-5, atol=1e-6)
