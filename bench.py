@@ -307,7 +307,7 @@ def main():
         achieved = fpe * units / (fit_ms * 1e-3) / 1e12
         if w["kind"] == "mlp":
             kname = f"k_mlp_fitness<{w['hidden']}> (tcgen05.mma kind::f16, TMA, TMEM)"
-            tr = ncu_traffic(f"k_mlp_fitness<{w['hidden']}>")
+            tr = ncu_traffic(f"k_mlp_fitness<{w['hidden']}")
             opb = units * w["D"] * 2 + w["samples"] * w["in_dim"] * 2
         else:
             kname = "k_lenet_fitness (mma.sync m16n8k16 bf16, weights staged in smem)"

@@ -1,6 +1,6 @@
 """Summarise ncu captures into profiles/ (text, committed).
 
-    python scripts/ncu_summarize.py launches <launches.csv> <out.md>
+    python scripts/ncu_summarize.py launches <launches.csv> <out.md> [first_n_launches]
     python scripts/ncu_summarize.py report <a.ncu-rep> [<b.ncu-rep> ...] <out.json>
 """
 import collections
@@ -29,7 +29,7 @@ METRICS = [
 ]
 
 
-def launches(path, out):
+def launches(path, out, first=None):
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     h, data = rows[hi], rows[hi + 1:]
@@ -37,9 +37,13 @@ def launches(path, out):
     tot = collections.OrderedDict()
     n = collections.Counter()
     scale = {"ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
+    seen = 0
     for r in data:
         if r[mi] != "gpu__time_duration.sum":
             continue
+        seen += 1
+        if first is not None and seen > first:
+            break
         name = r[ki].split("(")[0].replace("void ", "").replace("unnamed>::", "")
         t = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
         tot[name] = tot.get(name, 0.0) + t
@@ -47,6 +51,9 @@ def launches(path, out):
     total = sum(tot.values())
     with open(out, "w") as f:
         f.write(f"# ncu launch list summary ({path})\n\n")
+        if first is not None:
+            f.write(f"First {first} launches only (initialize + the bench's generations; the later\n"
+                    "roofline timing launches of the fitness kernel are excluded).\n\n")
         f.write("Cold-cache, serialised per-launch times (`--metrics gpu__time_duration.sum "
                 "--clock-control none`): compare SHARES, not absolutes.\n\n")
         f.write("| kernel | launches | total us | mean us | share |\n|---|---|---|---|---|\n")
@@ -74,6 +81,6 @@ def report(paths, out):
 
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
-        launches(sys.argv[2], sys.argv[3])
+        launches(sys.argv[2], sys.argv[3], int(sys.argv[4]) if len(sys.argv) > 4 else None)
     else:
         report(sys.argv[2:-1], sys.argv[-1])
