@@ -48,6 +48,14 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarpsL = kThreads / 32;
 constexpr uint32_t kChunkS = 128;  // samples per work item (one partial)
+#ifndef LENET_C1T
+#define LENET_C1T 8
+#endif
+#ifndef LENET_C2T
+#define LENET_C2T 4
+#endif
+constexpr int kC1T = LENET_C1T;  // conv1 tiles in flight per warp (independent MMA chains)
+constexpr int kC2T = LENET_C2T;  // conv2 tiles in flight per warp (x 2 n-tiles)
 
 // parameter offsets in the candidate row (oracle f_lenet)
 constexpr int oC1W = 0, oC1B = 150, oC2W = 156, oC2B = 2556, oF1W = 2572, oF1B = 50572,
@@ -305,12 +313,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_lenet_fitness(LenetArgs args) {
         __syncwarp();
         // ------------------------------------------------ conv1 (this warp)
         // 49 tiles of 4 windows (window 4t + wi of the 14 x 14 pooled map),
-        // 4 tiles per step so that 4 independent MMA chains are in flight
-        for (int t0 = 0; t0 < 49; t0 += 4) {
-          int wpos[4];
-          float d[4][4];
+        // kC1T tiles per step so that kC1T independent MMA chains are in flight
+        for (int t0 = 0; t0 < 49; t0 += kC1T) {
+          int wpos[kC1T];
+          float d[kC1T][4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < kC1T; ++u) {
             const int w = 4 * (t0 + u) + wi;
             wpos[u] = w < 196 ? w : -1;
             const int wc = w < 196 ? w : 0;
@@ -323,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lenet_fitness(LenetArgs args) {
                        img[base0 + koff1[st][1]], img[base1 + koff1[st][1]], bw1[st][0], bw1[st][1]);
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < kC1T; ++u) {
             // ReLU, vertical pair in-thread (rows g, g+8), horizontal pair = lane ^ 4
             float s0 = fmaxf(d[u][0], 0.f) + fmaxf(d[u][2], 0.f);
             float s1 = fmaxf(d[u][1], 0.f) + fmaxf(d[u][3], 0.f);
@@ -348,12 +356,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_lenet_fitness(LenetArgs args) {
           }
         __nv_bfloat16* o = p2 + warp * kP2S;
         // 7 tiles of 4 windows (window 4t + wi of the 5 x 5 pooled map), two
-        // tiles per step: 4 independent MMA chains (2 tiles x 2 n-tiles)
-        for (int t0 = 0; t0 < 7; t0 += 2) {
-          int wv[2], b0[2], b1[2];
-          float d[2][2][4];
+        // tiles per step: 2 kC2T independent MMA chains (kC2T tiles x 2 n-tiles)
+        for (int t0 = 0; t0 < 7; t0 += kC2T) {
+          int wv[kC2T], b0[kC2T], b1[kC2T];
+          float d[kC2T][2][4];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
+          for (int u = 0; u < kC2T; ++u) {
             const int w = 4 * (t0 + u) + wi;
             wv[u] = w < 25 ? w : -1;
             const int wc = w < 25 ? w : 0;
@@ -366,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lenet_fitness(LenetArgs args) {
 #pragma unroll
           for (int st = 0; st < 13; ++st) {
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < kC2T; ++u) {
               const int z0 = st == 12 ? -b0[u] : 0, z1 = st == 12 ? -b1[u] : 0;  // tap 25: zero pixel
               const uint32_t a0 = p1[b0[u] + toff[st][0]];
               const uint32_t a1 = p1[b1[u] + toff[st][0]];
@@ -377,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_lenet_fitness(LenetArgs args) {
             }
           }
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
+          for (int u = 0; u < kC2T; ++u) {
             float s0 = fmaxf(d[u][0][0], 0.f) + fmaxf(d[u][0][2], 0.f);
             float s1 = fmaxf(d[u][0][1], 0.f) + fmaxf(d[u][0][3], 0.f);
             float s2 = fmaxf(d[u][1][0], 0.f) + fmaxf(d[u][1][2], 0.f);

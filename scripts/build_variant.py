@@ -19,7 +19,7 @@ B.build()
 objs = []
 for src in B.SOURCES:
     o = os.path.join(B.BUILD, src.replace(".cu", ".o"))
-    if src in ("k_engine.cu", "k_mlp_tc.cu") and defs:
+    if src != "engine.cu" and defs:
         o = os.path.join(out_dir, f"{name}_{src[:-3]}.o")
         cmd = [B.nvcc()] + B.ARCH + B.FLAGS + defs + ["-c", os.path.join(B.CSRC, src), "-o", o]
         r = subprocess.run(cmd, capture_output=True, text=True)
