@@ -51,13 +51,21 @@ def _sharded(P, cfg, space, obj, seed, world):
     return recs, states
 
 
-@pytest.mark.parametrize("kind", ["sphere", "rastrigin", "mlp"])
+@pytest.mark.parametrize("kind", ["sphere", "rastrigin", "mlp", "lenet", "net"])
 @pytest.mark.parametrize("world", [2, 5])
 def test_sharded_run_bit_identical(P, kind, world):
     if kind == "mlp":
         obj = P.MlpWeights(samples=128)
         space = P.SearchSpace.box(obj.dim(), -0.5, 0.5)
         budget = 10 + 6 * 2 * 5 * 13
+    elif kind == "lenet":
+        obj = P.LeNet(samples=64)
+        space = P.SearchSpace.box(obj.dim(), -0.3, 0.3)
+        budget = 10 + 3 * 2 * 5 * 13
+    elif kind == "net":
+        obj = P.Net(3, 2)
+        space = P.SearchSpace.box(obj.dim(), -5.0, 5.0)
+        budget = 10 + 30 * 2 * 5 * 13
     else:
         obj = P.Sphere() if kind == "sphere" else P.Rastrigin()
         space = P.SearchSpace.box(37, -5.12, 5.12)
