@@ -4,17 +4,18 @@ MGFWA engine on BASELINE.json's configs[1] (C2: MLP-weights black box
 sparks, M = 3 guides).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c2|c1|c4]
+                    [--workload c1|c2|c3|c4|c5] [--scaling weak|strong]
 
 A "step" is one MGFWA generation (the body of run()'s loop,
 engine.cpp:359-417) on synthetic data.  value = whole-job evaluations per
 second, device-timed with CUDA events on the engine's stream over exactly K
 generations (max over ranks).  e2e = the same metric through the one-shot
 C-ABI run() drop-in (mgfwa_run_once) with host buffers in and out.
-Multi-GPU (torchrun, N ranks): weak scaling — the population grows to N x mu
-fireworks, each rank owns mu of them, and one in-place NCCL all-gather of the
-selected fireworks per generation keeps the population state replicated
-(DESIGN.md §5).  ``--impl reference`` times the compiled reference
+Multi-GPU (torchrun, N ranks): weak scaling by default — the population grows
+to N x mu fireworks, each rank owns mu of them, and one in-place NCCL
+all-gather of the selected fireworks per generation keeps the population
+state replicated; ``--scaling strong`` splits the workload's
+own mu fireworks over the ranks instead (C5: 64 fireworks, 8 per GPU at N=8).  ``--impl reference`` times the compiled reference
 (oracle/_ref, /root/reference/proj/src/engine.cpp run()) on the host cores.
 """
 from __future__ import annotations
@@ -231,6 +232,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak = mu fireworks per rank (default); strong = the workload's mu "
+                         "fireworks split over the ranks (e.g. C5: 64 fireworks, 8 per GPU at N=8)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -261,7 +265,10 @@ def main():
     # rank owns mu of them (firework sharding), one in-place NCCL all-gather
     # of the selected fireworks per generation.
     wn = dict(w)
-    wn["mu"] = w["mu"] * world
+    if args.scaling == "weak":
+        wn["mu"] = w["mu"] * world
+    elif (w["B"] * w["mu"]) % world != 0:
+        raise SystemExit(f"--scaling strong needs B*mu divisible by the rank count ({w['B'] * w['mu']} % {world})")
     eng = P.Engine(make_config(P, wn, 1 << 62), space, obj, seed=0, device=dev, rank=rank, world=world)
     if world > 1:
         uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
@@ -328,7 +335,7 @@ def main():
 
     line = {"metric": "spark fitness evals/sec", "value": evals_total / (ms_max * 1e-3), "unit": "evals/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "bf16" if w["kind"] in ("mlp", "lenet") else "f32", "data": "synthetic",
             "config": {"workload": w["desc"], "D": w["D"], "fireworks_total": wn["mu"] * w["B"],
                        "parallelism": f"firework-sharded x{world}" + (" + NCCL all-gather/gen" if world > 1 else ""),
