@@ -32,6 +32,7 @@ struct Ctl {
   double iters_rem;       // iterations_remaining of the current generation
   int active;             // 1 while the loop body must run
   int n_losers;           // losers of the current generation
+  unsigned small_done;    // blocks of k_small_b done in this generation
 };
 
 // Run-time multipliers 2^(32-k) for the splitmix64 right shifts done on the

@@ -641,14 +641,16 @@ __global__ void __launch_bounds__(256) k_guides(EngineView v) {
 // (engine.cpp:388-390) and the winner row copy (engine.cpp:232-233).  One
 // block per firework.
 constexpr int kSelectThreads = 512;
+// select_best + update_amplitudes + wave accounting + winner copy for local
+// firework fl, given the guide fitness gs[M] (all threads of the block;
+// any block size that is a multiple of 32, at most 1024).
+__device__ void select_core(const EngineView& v, uint64_t fl, const float* gs, unsigned nan_local);
+
 __global__ void __launch_bounds__(kSelectThreads) k_select(EngineView v) {
   pdl_enter<true>();
   if (gen_inactive(v)) return;
-  const uint64_t fl = blockIdx.x, f = v.f_lo + fl;  // local / global firework
-  __shared__ double sv[kSelectThreads / 32];
-  __shared__ int so[kSelectThreads / 32];
+  const uint64_t fl = blockIdx.x;  // local firework
   __shared__ float gs[16];
-  __shared__ int s_win;
   unsigned nan_local = 0;
   // guide fitness: one warp per guide row (warp-cooperative finalize)
   for (uint64_t m = threadIdx.x >> 5; m < v.M; m += blockDim.x >> 5) {
@@ -658,12 +660,20 @@ __global__ void __launch_bounds__(kSelectThreads) k_select(EngineView v) {
     } else {
       bool nan;
       g = finalize_row(v, v.gpart, fl * v.M + m, &nan);
-      nan_local += nan;
+      nan_local += nan && (threadIdx.x & 31) == 0;  // once per row (select_core sums lanes)
       if ((threadIdx.x & 31) == 0) v.gfit[fl * v.M + m] = g;
     }
     if ((threadIdx.x & 31) == 0) gs[m] = g;
   }
   __syncthreads();
+  select_core(v, fl, gs, nan_local);
+}
+
+__device__ void select_core(const EngineView& v, uint64_t fl, const float* gs, unsigned nan_local) {
+  const uint64_t f = v.f_lo + fl;  // global firework
+  __shared__ double sv[32];
+  __shared__ int so[32];
+  __shared__ int s_win;
   double best_v = v.fit[f];
   int best_o = 0;
   if (threadIdx.x != 0) best_v = __longlong_as_double(0x7ff0000000000000ll), best_o = 0x7fffffff;
@@ -723,29 +733,21 @@ __global__ void __launch_bounds__(kSelectThreads) k_select(EngineView v) {
                              : v.guides + (fl * v.M + (win - 1 - v.lam)) * v.Dp);
   float4* dst = reinterpret_cast<float4*>(v.pos + f * v.Dp);
   const uint64_t n4 = (v.D + 3) / 4;
+  const uint32_t nt = blockDim.x;
   uint64_t i = threadIdx.x;
-  for (; i + 3 * kSelectThreads < n4; i += 4 * kSelectThreads) {
+  for (; i + 3 * nt < n4; i += 4 * nt) {
     float4 t[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) t[u] = src[i + u * kSelectThreads];
+    for (int u = 0; u < 4; ++u) t[u] = src[i + u * nt];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) dst[i + u * kSelectThreads] = t[u];
+    for (int u = 0; u < 4; ++u) dst[i + u * nt] = t[u];
   }
-  for (; i < n4; i += kSelectThreads) dst[i] = src[i];
+  for (; i < n4; i += nt) dst[i] = src[i];
 }
 
 // ------------------------------------------------------------------ loser
-// loser_out decision (engine.cpp:258-286) with iterations_remaining from
-// engine.cpp:394-410 (device clock for the wall-clock budget).  One block.
-__global__ void k_loser(EngineView v) {
-  pdl_enter<true>();
-  __shared__ int count;
-  if (threadIdx.x == 0) count = 0;
-  __syncthreads();
-  if (gen_inactive(v)) {
-    if (threadIdx.x == 0) v.ctl->n_losers = 0;
-    return;
-  }
+// iterations_remaining of the current generation, engine.cpp:394-410.
+__device__ double iters_remaining(const EngineView& v) {
   double iters_rem = 0.0;
   if (v.has_iters_override) {
     iters_rem = v.iters_override;
@@ -761,6 +763,21 @@ __global__ void k_loser(EngineView v) {
       iters_rem = (rem > 0.0 ? rem : 0.0) / avg;
     }
   }
+  return iters_rem;
+}
+
+// loser_out decision (engine.cpp:258-286) with iterations_remaining from
+// engine.cpp:394-410 (device clock for the wall-clock budget).  One block.
+__global__ void k_loser(EngineView v) {
+  pdl_enter<true>();
+  __shared__ int count;
+  if (threadIdx.x == 0) count = 0;
+  __syncthreads();
+  if (gen_inactive(v)) {
+    if (threadIdx.x == 0) v.ctl->n_losers = 0;
+    return;
+  }
+  const double iters_rem = iters_remaining(v);
   for (uint64_t b = threadIdx.x; b < v.B; b += blockDim.x) {
     // argmin_per_population (backend.cpp:69-83)
     uint64_t bi = 0;
@@ -772,7 +789,8 @@ __global__ void k_loser(EngineView v) {
       const uint64_t f = b * v.mu + n;
       int is_loser = 0;
       if (iters_rem > 0.0 && n != bi) {
-        const double projected = v.fit[f] - v.li[f] * iters_rem;
+        // projected = f - li * iters_rem, rounded like the reference (no FMA)
+        const double projected = __dsub_rn(v.fit[f], __dmul_rn(v.li[f], iters_rem));
         is_loser = projected > bv;
       }
       v.loser[f] = is_loser;
@@ -977,6 +995,275 @@ static unsigned tail_blocks(const EngineView& v, int nsm) {
   return (unsigned)(g == 0 ? 1 : (g < cap ? g : cap));
 }
 
+// ------------------------------------------------------ small problems
+// One context, analytic objective, D <= kChunk: the post-explode part of a
+// generation as two kernels instead of eight (the launch latency dominates
+// at these sizes, e.g. C1: D = 30, 165 evaluations per generation).  Every
+// value is computed with the same operation order as the general kernels
+// (tests compare the two paths bit for bit through the sharded runs).
+//
+// k_small_a, one block per firework: spark-fitness finalize + ranking
+// (k_rank), guiding vector + guides + kGuide mapping (k_guides), guide
+// fitness (k_analytic_partials + the finalize of k_select), selection,
+// amplitudes, wave accounting and winner copy (k_select); block 0 also
+// fixes iterations_remaining for the loser decision (k_loser's value).
+constexpr int kSmallThreads = 256;
+
+// Analytic partial sums of one <= kChunk row, exactly as k_analytic_partials
+// (per-4 groups, lane-strided, warp butterfly), finalized as finalize_rows
+// (lane 0's value).  Whole warp.
+__device__ __forceinline__ float small_row_fitness(const EngineView& v, const float* row,
+                                                   float* part, bool* was_nan) {
+  const int lane = threadIdx.x & 31;
+  float s0 = 0.0f, s1 = 0.0f;
+  for (int q = 0; q < 4; ++q) {
+    const uint64_t d0 = q * 128 + lane * 4;
+    if (d0 >= v.D) break;
+    const float4 x4 = *reinterpret_cast<const float4*>(row + d0);
+    const float xs[4] = {x4.x, x4.y, x4.z, x4.w};
+    float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (d0 + e < v.D) analytic_terms(v.obj_kind, xs[e], a0, a1);
+    s0 += a0;
+    s1 += a1;
+  }
+  s0 = warp_sum(s0);
+  s1 = warp_sum(s1);
+  if (lane == 0 && part != nullptr) {
+    part[0] = s0;
+    part[1] = s1;
+  }
+  // finalize_rows with nparts == 1: lane 0's partial plus zeros
+  const float a = __shfl_sync(0xffffffffu, warp_sum(lane == 0 ? s0 : 0.0f), 0);
+  const float b = __shfl_sync(0xffffffffu, warp_sum(lane == 0 ? s1 : 0.0f), 0);
+  const float f = analytic_finalize(v.obj_kind, a, b, v.D);
+  *was_nan = isnan(f);
+  return isnan(f) ? __int_as_float(0x7f800000) : f;
+}
+
+__global__ void __launch_bounds__(kSmallThreads) k_small_a(EngineView v) {
+  pdl_enter<true>();
+  if (gen_inactive(v)) return;
+  extern __shared__ uint64_t sa_keys[];  // [lam] rank keys
+  __shared__ int s_idx[2 * 1024];        // top / bottom spark indices (top <= 1024)
+  __shared__ float gs[16];
+  const uint64_t fl = blockIdx.x, f = v.f_lo + fl;
+  const uint32_t lam = (uint32_t)v.lam, top = (uint32_t)v.top;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const uint64_t it = v.ctl->iteration;
+  unsigned nan_local = 0;
+  // ---- spark fitness (finalize) + keys
+  constexpr int R = 4;
+  for (uint32_t k0 = warp * R; k0 < lam; k0 += nwarp * R) {
+    int64_t rows[R];
+    float x[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) rows[r] = (k0 + r < lam) ? (int64_t)(fl * lam + k0 + r) : -1;
+    finalize_rows<R>(v, v.spart, rows, x, nan_local);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (lane == r && rows[r] >= 0) {
+        v.sfit[rows[r]] = x[r];
+        sa_keys[k0 + r] = rank_key(x[r], k0 + r);
+      }
+  }
+  __syncthreads();
+  if (v.M > 0) {
+    // ---- counting rank (k_rank)
+    for (uint32_t k = threadIdx.x; k < lam; k += blockDim.x) {
+      const uint64_t kk = sa_keys[k];
+      uint32_t r = 0;
+      for (uint32_t j = 0; j < lam; ++j) r += sa_keys[j] < kk;
+      if (r < top) s_idx[r] = (int)k;
+      if (r >= lam - top) s_idx[top + (r - (lam - top))] = (int)k;
+    }
+    __syncthreads();
+    // ---- guiding vector + guides + kGuide mapping (k_guides)
+    const uint64_t b = f / v.mu, n = f % v.mu;
+    const float* sb = v.sparks + fl * v.lam * v.Dp;
+    const float* plo = v.pop_lo + b * v.Dp;
+    const float* phi = v.pop_hi + b * v.Dp;
+    const uint64_t d4 = (v.D + 3) & ~3ull;
+    for (uint64_t d = threadIdx.x; d < d4; d += blockDim.x) {
+      if (d >= v.D) {
+        for (uint64_t m = 0; m < v.M; ++m) v.guides[(fl * v.M + m) * v.Dp + d] = 0.0f;
+        continue;
+      }
+      double acc = 0.0;
+      for (uint32_t t = 0; t < top; ++t)
+        acc = __dadd_rn(acc, __dsub_rn((double)sb[(uint64_t)s_idx[t] * v.Dp + d],
+                                       (double)sb[(uint64_t)s_idx[top + t] * v.Dp + d]));
+      const double delta = __ddiv_rn(acc, (double)top);
+      const double pv = (double)v.pos[f * v.Dp + d];
+      for (uint64_t m = 0; m < v.M; ++m) {
+        const uint64_t pg = key_prefix(v.seed, kGuide, it, b, n, m);
+        const double gx = __dadd_rn(pv, __dmul_rn(v.boosts[m], delta));
+        v.guides[(fl * v.M + m) * v.Dp + d] = map_coord(v, gx, d, pg, plo, phi);
+      }
+    }
+    __syncthreads();
+    // ---- guide fitness, one warp per guide
+    for (uint64_t m = warp; m < v.M; m += nwarp) {
+      bool nan;
+      const uint64_t row = fl * v.M + m;
+      const float g = small_row_fitness(v, v.guides + row * v.Dp, v.gpart + row * 2, &nan);
+      nan_local += nan && lane == 0;
+      if (lane == 0) {
+        v.gfit[row] = g;
+        gs[m] = g;
+      }
+    }
+    __syncthreads();
+  }
+  select_core(v, fl, gs, nan_local);
+  if (fl == 0 && threadIdx.x == 0) v.ctl->iters_rem = iters_remaining(v);  // after the wave
+}
+
+// k_small_b, one block per batch: loser-out (k_loser), reinit + fitness of
+// the losers (k_fresh_rows + k_finalize_record), record_wave, best copy and
+// population_range of the next generation (k_record_copy); the last block
+// to finish completes the trace point and the loop-top termination test.
+__global__ void __launch_bounds__(kSmallThreads) k_small_b(EngineView v) {
+  pdl_enter<true>();
+  if (gen_inactive(v)) {
+    if (threadIdx.x == 0) v.rec_flag[blockIdx.x] = 0;
+    return;
+  }
+  Ctl* ctl = v.ctl;
+  const uint64_t b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const uint64_t it = ctl->iteration;
+  const uint64_t slot = ctl->trace_n % v.trace_cap;
+  __shared__ int s_count;
+  unsigned nan_local = 0;
+  // ---- loser decision for batch b (k_loser, engine.cpp:258-286)
+  if (threadIdx.x == 0) {
+    const double iters_rem = ctl->iters_rem;
+    uint64_t bi = 0;
+    double bv = v.fit[b * v.mu];
+    for (uint64_t n = 1; n < v.mu; ++n)
+      if (v.fit[b * v.mu + n] < bv) bv = v.fit[b * v.mu + n], bi = n;
+    int cnt = 0;
+    for (uint64_t n = 0; n < v.mu; ++n) {
+      const uint64_t f = b * v.mu + n;
+      int is_loser = 0;
+      if (iters_rem > 0.0 && n != bi)
+        is_loser = __dsub_rn(v.fit[f], __dmul_rn(v.li[f], iters_rem)) > bv;
+      v.loser[f] = is_loser;
+      if (is_loser) {
+        v.amp[f] = v.a0;
+        v.li[f] = 0.0;
+        ++cnt;
+      }
+    }
+    s_count = cnt;
+    if (cnt) {
+      atomicAdd((unsigned long long*)&ctl->used, (unsigned long long)cnt);
+      atomicAdd((unsigned long long*)&ctl->losers_total, (unsigned long long)cnt);
+    }
+  }
+  __syncthreads();
+  // ---- losers: kReinit rows + fitness (k_fresh_rows mode 1, k_finalize_record)
+  if (s_count) {
+    for (uint64_t n = warp; n < v.mu; n += nwarp) {
+      const uint64_t f = b * v.mu + n;
+      if (!v.loser[f]) continue;
+      const uint64_t pk = key_prefix(v.seed, kReinit, it, b, n, 0);
+      for (int q = 0; q < 4; ++q) {
+        const uint64_t d0 = q * 128 + lane * 4;
+        if (d0 >= v.D) break;
+        float x[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint64_t d = d0 + e;
+          x[e] = d < v.D ? to_f32_in_box(uniform_draw(splitmix64(pk ^ d), v.lower[d], v.upper[d]),
+                                         v.lower_f[d], v.upper_f[d])
+                         : 0.0f;
+        }
+        *reinterpret_cast<float4*>(v.pos + f * v.Dp + d0) = make_float4(x[0], x[1], x[2], x[3]);
+      }
+      __syncwarp();
+      bool nan;
+      const float x = small_row_fitness(v, v.pos + f * v.Dp, v.fpart + f * v.nparts * 2, &nan);
+      nan_local += nan && lane == 0;
+      if (lane == 0) v.fit[f] = (double)x;
+    }
+    if (lane == 0 && nan_local)
+      atomicAdd((unsigned long long*)&ctl->nan_count, (unsigned long long)nan_local);
+    __syncthreads();
+  }
+  // ---- record_wave for batch b (engine.cpp:340-351)
+  __shared__ int s_flag, s_best;
+  const uint64_t now = global_ns();
+  if (threadIdx.x == 0) {
+    uint64_t bi = 0;
+    double bv = v.fit[b * v.mu];
+    for (uint64_t n = 1; n < v.mu; ++n)
+      if (v.fit[b * v.mu + n] < bv) bv = v.fit[b * v.mu + n], bi = n;
+    double cur = v.best_fit[b];
+    int flag = 0;
+    if (bv < cur) {
+      cur = bv;
+      v.best_idx[b] = (int)bi;
+      flag = 1;
+    }
+    v.best_fit[b] = cur;
+    v.rec_flag[b] = flag;
+    v.tr_best[slot * v.B + b] = cur;
+    v.tr_ns[slot * v.B + b] = now - ctl->start_ns;
+    s_flag = flag;
+    s_best = (int)bi;
+  }
+  __syncthreads();
+  // ---- best copy + population_range (k_record_copy)
+  const float* pb = v.pos + b * v.mu * v.Dp;
+  const uint64_t d4 = (v.D + 3) & ~3ull;
+  for (uint64_t d = threadIdx.x; d < d4; d += blockDim.x) {
+    if (s_flag) v.best_pos[b * v.Dp + d] = pb[(uint64_t)s_best * v.Dp + d];
+    float mn = pb[d], mx = mn;
+    for (uint64_t n = 1; n < v.mu; ++n) {
+      const float x = pb[n * v.Dp + d];
+      mn = x < mn ? x : mn;
+      mx = mx < x ? x : mx;
+    }
+    v.pop_lo[b * v.Dp + d] = mn;
+    v.pop_hi[b * v.Dp + d] = mx;
+  }
+  // ---- the last block: trace evaluations, termination (k_finalize_record)
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned done = atomicAdd(&ctl->small_done, 1u);
+    if (done == gridDim.x - 1) {
+      __threadfence();
+      const uint64_t used = *(volatile uint64_t*)&ctl->used;
+      for (uint64_t bb = 0; bb < v.B; ++bb) v.tr_evals[slot * v.B + bb] = used;
+      ctl->small_done = 0;
+      ctl->trace_n += 1;
+      ctl->gens_run += 1;
+      const double now_ms = (double)(now - ctl->start_ns) * 1e-6;
+      int active = 1;
+      if (v.max_evals > 0 && used >= v.max_evals) active = 0;
+      if (v.wall_budget_ms > 0.0 && now_ms >= v.wall_budget_ms) active = 0;
+      ctl->active = active;
+      if (active) ctl->iteration += 1;
+    }
+  }
+}
+
+static bool small_path_disabled() {  // MGFWA_SMALL_PATH=0: always the general kernels
+  static const bool off = [] {
+    const char* e = getenv("MGFWA_SMALL_PATH");
+    return e != nullptr && e[0] == '0';
+  }();
+  return off;
+}
+
+bool small_path(const EngineView& v) {
+  return !v.nn && v.Fl == v.F && v.D <= (uint64_t)kChunk && v.lam <= 2048 && v.top <= 1024 &&
+         v.M <= 16 && v.mu <= 1024;
+}
+
 // ------------------------------------------------------- operator seams
 // Analytic partial sums of arbitrary fp32 rows (batched_apply seam).
 __global__ void __launch_bounds__(256) k_analytic_partials(const float* rows,
@@ -1118,6 +1405,12 @@ static unsigned capped(uint64_t g, int nsm) {
 // per-generation all-gather of the selected fireworks).
 void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
                                GenerationHooks* hooks, int phase) {
+  if (phase == kGenAll && small_path(v) && !small_path_disabled()) {
+    launch_explode_map_impl(v, nsm, s);
+    pdl_launch(k_small_a, (unsigned)v.Fl, kSmallThreads, v.lam * sizeof(uint64_t), s, v);
+    pdl_launch(k_small_b, (unsigned)v.B, kSmallThreads, 0, s, v);
+    return;
+  }
   if (phase != kGenB) {
     // population_range of this generation was computed by the previous
     // generation's (or initialize's) tail kernel, k_record_copy.
