@@ -138,3 +138,28 @@ def test_mlp_run_statistical(P, oracle):
     p = _mwu(np.array(gpu), np.array(cpu))
     print("mlp gpu", np.median(gpu), "cpu", np.median(cpu), "p", p)
     assert p > ALPHA
+
+
+def test_wall_clock_budget_terminates(P):
+    """A wall-clock-only budget (engine.cpp:360-367, 394-410 with the device
+    clock): the loop stops at the first loop top past the budget; trace time
+    stamps are non-decreasing and the last wave is at or past the budget."""
+    cfg = P.MgfwaConfig(batches=2, fireworks=5, sparks_per_firework=30, wall_clock_budget_ms=40.0)
+    r = P.run(cfg, P.SearchSpace.box(30, -10.0, 10.0), P.Sphere(), 5)
+    assert r.iterations > 10
+    assert r.evaluations_used >= 10 + r.iterations * cfg.evaluations_per_wave()
+    w = r.trace_wall_ms[0]
+    assert np.all(np.diff(w) >= 0) and w[-1] >= 40.0 and w[-2] < 40.0
+    assert np.all(np.diff(r.trace_best, axis=1) <= 0)
+
+
+@pytest.mark.parametrize("kind", ["sphere", "rastrigin"])
+def test_one_dimensional_problem(P, kind):
+    obj = P.Sphere() if kind == "sphere" else P.Rastrigin()
+    cfg = P.MgfwaConfig(batches=3, fireworks=4, sparks_per_firework=10, max_evaluations=12 + 39 * 40)
+    r = P.run(cfg, P.SearchSpace.box(1, -5.0, 5.0), obj, 2)
+    assert r.best_position.shape == (3, 1) and np.all(np.abs(r.best_position) <= 5.0)
+    assert np.all(r.best_fitness >= 0.0) and np.all(r.best_fitness < 0.1)
+    assert np.all(r.best_fitness <= r.trace_best[:, 0])
+    fit, _ = P.batched_apply(obj, r.best_position)  # cached == re-evaluated (D = 1 row padding)
+    assert np.array_equal(fit, r.best_fitness)
