@@ -41,29 +41,6 @@ __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
-// splitmix64 with the pipes balanced for throughput-bound kernels: the
-// high-word right shifts are IMAD.HI on the FMA pipe (m = 2^(32-k), a
-// run-time value), the rest stays on the ALU pipe.  Bit-identical to
-// splitmix64.
-__device__ __forceinline__ uint32_t mulhi_fma(uint32_t a, uint32_t m) {
-  uint32_t r;
-  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(m));
-  return r;
-}
-__device__ __forceinline__ uint64_t xorshift_bal(uint64_t x, int k, uint32_t m) {
-  const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
-  const uint32_t nlo = lo ^ __funnelshift_r(lo, hi, k);
-  const uint32_t nhi = hi ^ mulhi_fma(hi, m);
-  return ((uint64_t)nhi << 32) | nlo;
-}
-template <typename MH>
-__device__ __forceinline__ uint64_t splitmix64_bal(uint64_t x, const MH& mh) {
-  x += 0x9E3779B97F4A7C15ull;
-  x = xorshift_bal(x, 30, mh.s30) * 0xBF58476D1CE4E5B9ull;
-  x = xorshift_bal(x, 27, mh.s27) * 0x94D049BB133111EBull;
-  return xorshift_bal(x, 31, mh.s31);
-}
-
 // rng.hpp:43-52 absorbed up to and including field k; the per-coordinate
 // hash is then splitmix64(prefix ^ d) — one mixer round per draw.
 __host__ __device__ __forceinline__ uint64_t key_prefix(uint64_t seed,

@@ -319,7 +319,6 @@ struct Workspace {
     CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     CUDA_TRY(prepare_engine_kernels());
     const uint64_t D = space->dim;
-    v.mh = MulHi{4u, 32u, 2u};  // 2^(32-k) for the k = 30, 27, 31 shifts of splitmix64
     v.B = c.B;
     v.mu = c.mu;
     v.lam = c.lam;

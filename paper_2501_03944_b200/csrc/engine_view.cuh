@@ -35,13 +35,6 @@ struct Ctl {
   unsigned small_done;    // blocks of k_small_b done in this generation
 };
 
-// Run-time multipliers 2^(32-k) for the splitmix64 right shifts done on the
-// FMA pipe (IMAD.HI) instead of the ALU pipe (see splitmix64_bal): run-time
-// values so the compiler cannot strength-reduce them back into shifts.
-struct MulHi {
-  uint32_t s30, s27, s31;
-};
-
 struct EngineView {
   // shape.  F = B * mu fireworks in total; this context owns the contiguous
   // range [f_lo, f_lo + Fl) (firework sharding across ranks).
@@ -58,7 +51,6 @@ struct EngineView {
   int nn;              // 1 when fitness runs on the tensor cores
   uint32_t samples;    // NN: S
   uint64_t seed;
-  MulHi mh;
   // algorithm parameters (MgfwaConfig)
   double amp_amplify, amp_reduce, a0, max_range, amp_floor;
   uint64_t max_evals;

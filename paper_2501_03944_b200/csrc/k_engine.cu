@@ -154,22 +154,7 @@ __global__ void k_pop_range(EngineView v) {
 // kMapping draw for those 4 coordinates as 4 independent chains and selects
 // per lane.  Out-of-box coordinates are common (C2: about half of them once
 // the amplitudes reach the range), so this dense form beats compaction.
-#ifndef EXPLODE_KG
-#define EXPLODE_KG 4
-#endif
-#ifndef EXPLODE_MINB
-#define EXPLODE_MINB 2
-#endif
-#ifndef EXPLODE_MAPALL
-#define EXPLODE_MAPALL 0
-#endif
-#ifndef EXPLODE_NOMAP
-#define EXPLODE_NOMAP 0  // timing experiment only (wrong results)
-#endif
-#ifndef EXPLODE_ALWAYSMAP
-#define EXPLODE_ALWAYSMAP 0
-#endif
-constexpr int kSparkGroup = EXPLODE_KG;
+constexpr int kSparkGroup = 4;
 
 // t = -1 + u * 2 for u = (h >> 11) * 2^-53, exactly as the reference's
 // uniform_sample(key, -1, 1) (rng.hpp:55-65): with m = h >> 11 and
@@ -225,70 +210,6 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
   const double pd[4] = {(double)p4.x, (double)p4.y, (double)p4.z, (double)p4.w};
   const float lf[4] = {lf4.x, lf4.y, lf4.z, lf4.w};
   const float uf[4] = {uf4.x, uf4.y, uf4.z, uf4.w};
-#if EXPLODE_MAPALL
-  float x[KG][4];
-  double sv[KG][4];
-  unsigned slow = 0;
-#pragma unroll
-  for (int kk = 0; kk < KG; ++kk) {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const uint64_t h = splitmix64(pe[kk] ^ (uint64_t)(d0 + e));
-      sv[kk][e] = __dadd_rn(pd[e], __dmul_rn(unit_pm1(h), a));
-      x[kk][e] = __double2float_rn(sv[kk][e]);
-      const bool need = !in_box_fast(x[kk][e], lf[e], uf[e]);
-      if (FULL ? need : (kk < kn && e < nvalid && need)) slow |= 1u << (kk * 4 + e);
-    }
-  }
-  if (__any_sync(0xffffffffu, slow != 0)) {
-    const double2 lo01 = *reinterpret_cast<const double2*>(&ch.lo[li0]);
-    const double2 lo23 = *reinterpret_cast<const double2*>(&ch.lo[li0 + 2]);
-    const double2 hi01 = *reinterpret_cast<const double2*>(&ch.hi[li0]);
-    const double2 hi23 = *reinterpret_cast<const double2*>(&ch.hi[li0 + 2]);
-    const double2 pl01 = *reinterpret_cast<const double2*>(&ch.plo[li0]);
-    const double2 pl23 = *reinterpret_cast<const double2*>(&ch.plo[li0 + 2]);
-    const double2 pw01 = *reinterpret_cast<const double2*>(&ch.pw[li0]);
-    const double2 pw23 = *reinterpret_cast<const double2*>(&ch.pw[li0 + 2]);
-    const double lo[4] = {lo01.x, lo01.y, lo23.x, lo23.y};
-    const double hi[4] = {hi01.x, hi01.y, hi23.x, hi23.y};
-    const double pl[4] = {pl01.x, pl01.y, pl23.x, pl23.y};
-    const double pw[4] = {pw01.x, pw01.y, pw23.x, pw23.y};
-#pragma unroll
-    for (int kk = 0; kk < KG; ++kk) {
-      if (!__any_sync(0xffffffffu, ((slow >> (kk * 4)) & 15u) != 0)) continue;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const uint64_t h = splitmix64(pm[kk] ^ (uint64_t)(d0 + e));
-        const float m = __double2float_rn(__dadd_rn(pl[e], __dmul_rn(unit_u53(h), pw[e])));
-        const float r = (sv[kk][e] >= lo[e] && sv[kk][e] <= hi[e]) ? x[kk][e] : m;
-        x[kk][e] = ((slow >> (kk * 4 + e)) & 1u) ? fminf(fmaxf(r, lf[e]), uf[e]) : x[kk][e];
-      }
-    }
-  }
-#pragma unroll
-  for (int kk = 0; kk < KG; ++kk) {
-    if (!FULL && kk >= kn) break;
-    if (on) {
-      if (!FULL) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (e >= nvalid) x[kk][e] = 0.0f;
-      }
-      if (KIND != 0) {
-        float a0 = 0.0f, a1 = 0.0f;
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if (FULL || e < nvalid) analytic_terms(KIND, x[kk][e], a0, a1);
-        s0[kk] += a0;
-        s1[kk] += a1;
-      }
-      const uint64_t off = ((f - v.f_lo) * v.lam + k0 + kk) * v.Dp + d0;  // local spark row
-      *reinterpret_cast<float4*>(v.sparks + off) = make_float4(x[kk][0], x[kk][1], x[kk][2], x[kk][3]);
-      if (KIND == 0) store_bf16x4(v.sparks_h, off, x[kk]);
-    }
-  }
-}
-#else
 #pragma unroll
   for (int kk = 0; kk < KG; ++kk) {
     if (!FULL && kk >= kn) break;
@@ -306,13 +227,7 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
     // Out-of-box / boundary coordinates of this spark: exact inclusive test
     // (config.hpp:22-24) and the kMapping draw U[pop_lo, pop_hi)
     // (engine.cpp:119-125), 4 independent chains, selected per lane.
-#if EXPLODE_NOMAP
-    if (false) {
-#elif EXPLODE_ALWAYSMAP
-    if (true) {
-#else
     if (__any_sync(0xffffffffu, slow != 0)) {
-#endif
       const double2 lo01 = *reinterpret_cast<const double2*>(&ch.lo[li0]);
       const double2 lo23 = *reinterpret_cast<const double2*>(&ch.lo[li0 + 2]);
       const double2 hi01 = *reinterpret_cast<const double2*>(&ch.hi[li0]);
@@ -353,7 +268,6 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
     }
   }
 }
-#endif
 
 // Work item = (firework f, 512-coordinate chunk c, 8 consecutive spark
 // groups): the block stages the chunk's box / population range once; warp w
@@ -361,7 +275,7 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
 // KIND == 0: NN objective (bf16 shadow, no analytic partials); otherwise the
 // analytic objective kind whose partial sums are fused in.
 template <int KIND>
-__global__ void __launch_bounds__(256, EXPLODE_MINB) k_explode_map(EngineView v) {
+__global__ void __launch_bounds__(256, 2) k_explode_map(EngineView v) {
   pdl_enter();
   if (gen_inactive(v)) return;
   constexpr int KG = kSparkGroup;
@@ -500,10 +414,7 @@ __global__ void __launch_bounds__(kRankThreads) k_rank(EngineView v) {
   const uint32_t lam = (uint32_t)v.lam;
   unsigned nan_local = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-#ifndef RANK_R
-#define RANK_R 4
-#endif
-  constexpr int R = RANK_R;  // rows per warp step (their loads in flight together)
+  constexpr int R = 4;  // rows per warp step (their loads in flight together)
   for (uint32_t k0 = warp * R; k0 < lam; k0 += nwarp * R) {
     int64_t rows[R];
     float x[R];
@@ -1427,16 +1338,11 @@ void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
     pdl_launch(k_select, (unsigned)v.Fl, kSelectThreads, 0, s, v);
   }
   if (phase != kGenA) {
-#ifndef GEN_SKIP  // timing experiments only (GEN_SKIP=1: loser..finalize, 2: whole phase B)
-#define GEN_SKIP 0
-#endif
-    if (GEN_SKIP == 0) {
     pdl_launch(k_loser, 1, 128, 0, s, v);
     pdl_launch(k_fresh_rows, capped((v.F * v.nch + kWarps - 1) / kWarps, nsm), 256, 0, s, v, 1);
     if (v.nn) hooks->eval_fresh(hooks->ctx, s);
     pdl_launch(k_finalize_record, 1, 256, 0, s, v, 1);
-    }
-    if (GEN_SKIP < 2) pdl_launch(k_record_copy, tail_blocks(v, nsm), 256, 0, s, v);
+    pdl_launch(k_record_copy, tail_blocks(v, nsm), 256, 0, s, v);
   }
 }
 

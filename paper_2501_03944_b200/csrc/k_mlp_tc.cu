@@ -47,9 +47,6 @@ constexpr int BK = 64;   // K per pipeline stage (one 128-byte swizzle atom)
 #ifndef MLP_STAGES
 #define MLP_STAGES 4
 #endif
-#ifndef MLP_AHEAD
-#define MLP_AHEAD 0  // k-blocks the MMA issuer may run ahead of completion (0 = unbounded)
-#endif
 #ifndef MLP_PROBE
 #define MLP_PROBE 0  // 1: profiling probe, TMA + layer-1 MMA pipeline only (no epilogue math)
 #endif
@@ -520,7 +517,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         commit(bar_d2full + 8 * b);
       };
       uint32_t stage = 0, phase = 0, i = 0;
-      uint32_t gk = 0;  // k-blocks issued so far (all tiles)
       bool pend = false;
       uint32_t pbuf = 0, puse = 0;
       for (uint32_t t = t_begin; t < t_end; ++t, ++i) {
@@ -529,14 +525,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         else mbar_wait(bar_tempty + 8 * buf, use ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * BN;
-        for (uint32_t kb = 0; kb < args.k_blocks; ++kb, ++gk) {
-          // Keep at most MLP_AHEAD k-blocks queued in the tensor pipe, so the
-          // layer-2 MMAs slotted in below are not stuck behind a deep queue
-          // of layer-1 work (their completion releases the TMEM buffer).
-          if (MLP_AHEAD > 0 && gk >= (uint32_t)MLP_AHEAD) {
-            const uint32_t g0 = gk - MLP_AHEAD;
-            mbar_wait(bar_empty + 8 * (g0 % kStages), (g0 / kStages) & 1);
-          }
+        for (uint32_t kb = 0; kb < args.k_blocks; ++kb) {
           mbar_wait(bar_full + 8 * stage, phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * kStageBytes);
