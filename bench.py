@@ -343,6 +343,31 @@ def main():
                        if args.workload == "c2" else "n/a"},
             "gpu_launches": kpg * args.steps, "roofline": roof}
     line["clocks"] = clk.summary()
+    # per-kernel device times of the generation's idempotent kernels on the
+    # steady-state engine (CUDA events, back-to-back launches) with their
+    # achieved HBM bandwidth against algorithmic bytes (GB/s
+    # for generation and guiding); per rank's own fireworks.
+    try:
+        Fl = wn["B"] * wn["mu"] // world
+        Dp4, nn = w["D"] * 4, w["kind"] in ("mlp", "lenet")
+        top = -(-w["lam"] // 5)  # ceil(0.2 * lambda), the default guide fraction
+        algo = {"explode": Fl * w["lam"] * w["D"] * (6 if nn else 4) + Fl * w["D"] * 4,
+                "guides": Fl * (2 * top * Dp4 + w["M"] * w["D"] * (6 if nn else 4) + Dp4),
+                "rank": Fl * w["lam"] * (4 if nn else 8) * 2}
+        kb = {}
+        for name in ("explode", "rank", "guides"):
+            kms, _ = eng.time_kernel(name, 10)
+            kb[name] = {"us": 1e3 * kms, "algorithmic_bytes": algo[name],
+                        "achieved_GBs": algo[name] / (kms * 1e-3) / 1e9,
+                        "frac_hbm": algo[name] / (kms * 1e-3) / 1e9 / pk["hbm_gbs"]}
+        if nn:
+            for name in ("fitness", "guide_fitness"):
+                kms, units_k = eng.time_kernel(name, 10)
+                kb[name] = {"us": 1e3 * kms, "rows": units_k,
+                            "achieved_TFLOPs": flop_per_eval(w) * units_k / (kms * 1e-3) / 1e12}
+        line["kernel_breakdown"] = kb
+    except Exception as ex:
+        line["kernel_breakdown"] = {"error": str(ex)[:200]}
 
     if world > 1 and not args.no_e2e:
         # e2e at N GPUs through the public API: every rank creates its shard
