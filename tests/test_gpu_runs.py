@@ -163,3 +163,18 @@ def test_one_dimensional_problem(P, kind):
     assert np.all(r.best_fitness <= r.trace_best[:, 0])
     fit, _ = P.batched_apply(obj, r.best_position)  # cached == re-evaluated (D = 1 row padding)
     assert np.array_equal(fit, r.best_fitness)
+
+
+@pytest.mark.parametrize("obj_name", ["mlp", "lenet", "net"])
+def test_nn_run_no_guides_odd_lambda(P, obj_name):
+    """NN objectives without guiding sparks (M = 0), an odd lambda (partial
+    spark groups, partial N tiles) and B = 3: the run completes, the trace is
+    monotone and the cached best equals its re-evaluation."""
+    obj = {"mlp": P.MlpWeights(samples=200), "lenet": P.LeNet(samples=40), "net": P.Net(4, 3)}[obj_name]
+    D = obj.dim()
+    cfg = P.MgfwaConfig(batches=3, fireworks=3, sparks_per_firework=7, guides_per_firework=0, boosts=[],
+                        max_evaluations=9 + 63 * 6)
+    r = P.run(cfg, P.SearchSpace.box(D, -0.5, 0.5), obj, 11)
+    assert r.iterations == 6 and np.all(np.diff(r.trace_best, axis=1) <= 0)
+    fit, _ = P.batched_apply(obj, r.best_position)
+    assert np.array_equal(fit, r.best_fitness)
