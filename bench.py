@@ -350,7 +350,8 @@ def main():
                        "parallelism": f"firework-sharded x{world}" + (" + NCCL all-gather/gen" if world > 1 else ""),
                        "l2": "inputs larger than L2: spark matrix fp32+bf16 229 MB/generation > 126 MB"
                        if args.workload == "c2" else "n/a"},
-            "gpu_launches": kpg * args.steps, "roofline": roof}
+            "gpu_launches": kpg * args.steps if kpg else 1,  # 1: the persistent small-problem loop
+            "roofline": roof}
     line["clocks"] = clk.summary()
     # per-kernel device times of the generation's idempotent kernels on the
     # steady-state engine (CUDA events, back-to-back launches) with their

@@ -102,7 +102,10 @@ int mgfwa_destroy(mgfwa_ctx_t ctx);
 const char* mgfwa_last_error(mgfwa_ctx_t ctx);
 /* Run subsequent work on an external stream (cudaStream_t as void*). */
 int mgfwa_set_stream(mgfwa_ctx_t ctx, void* cuda_stream);
-/* Number of graph-replayed kernels one generation launches. */
+/* Number of graph-replayed kernels one generation launches; 0 when the
+ * context runs the persistent small-problem loop (analytic objective,
+ * D <= 512, one context), which executes any number of generations in one
+ * kernel launch per enqueue. */
 int mgfwa_kernels_per_generation(mgfwa_ctx_t ctx, uint64_t* n);
 
 /* ---- the generation loop (engine.hpp:71-132) --------------------------- */

@@ -630,7 +630,15 @@ class Engine {
   // exercises the exchange path on a single GPU).
   bool sharded() const { return world > 1 || comm != nullptr; }
 
+  // Small analytic problems on one context: the whole loop is one persistent
+  // cooperative kernel per enqueue (no graph, no launch per generation).
+  bool persistent() const { return !sharded() && small_run_ok(ws->v, ws->nsm); }
+
   Status capture() {
+    if (persistent()) {
+      kernels_per_gen = 0;  // one launch per enqueue, any number of generations
+      return ok();
+    }
     if (!sharded()) {
       if (gen_exec) return ok();
       size_t n = 0;
@@ -737,6 +745,10 @@ class Engine {
 
   Status enqueue(uint64_t n) {
     if (!initialized) return Status{MGFWA_ESTATE, "mgfwa: initialize() must precede the loop"};
+    if (persistent()) {
+      if (n > 0) CUDA_TRY(launch_small_run(ws->v, n, stream));
+      return ok();
+    }
     if (!sharded()) {
       for (uint64_t i = 0; i < n; ++i) CUDA_TRY(cudaGraphLaunch(gen_exec, stream));
       return ok();

@@ -33,6 +33,8 @@ struct Ctl {
   int active;             // 1 while the loop body must run
   int n_losers;           // losers of the current generation
   unsigned small_done;    // blocks of k_small_b done in this generation
+  unsigned bar_count;     // grid barrier of the persistent small-problem loop
+  unsigned bar_gen;
 };
 
 struct EngineView {

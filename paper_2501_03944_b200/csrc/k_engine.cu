@@ -269,6 +269,81 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
   }
 }
 
+// One warp: spark group g (kSparkGroup sparks) of local firework fl over the
+// staged chunk c (box images + population range of the firework's batch).
+template <int KIND>
+__device__ __forceinline__ void explode_group(const EngineView& v, const ExplodeChunk& ch,
+                                              ExplodeWarp& wq, int lane, uint32_t c, uint64_t fl,
+                                              uint64_t g) {
+  constexpr int KG = kSparkGroup;
+  const uint32_t D = (uint32_t)v.D;
+  const uint64_t it = v.ctl->iteration;
+  const uint64_t f = v.f_lo + fl;
+  const uint64_t b = f / v.mu, n = f % v.mu;
+  const uint32_t cbase = c * kChunk;
+  const uint64_t k0 = g * KG;
+  const int kn = (int)(v.lam - k0 < (uint64_t)KG ? v.lam - k0 : KG);
+  // key prefixes: lanes [0, KG) explode, [KG, 2KG) mapping (hoisted
+  // rng.hpp:43-51 up to field k; each draw is then one splitmix64 round)
+  if (lane < kn)
+    wq.pre[lane] = key_prefix(v.seed, kExplode, it, b, n, k0 + lane);
+  else if (lane >= KG && lane < KG + kn)
+    wq.pre[lane] = key_prefix(v.seed, kMapping, it, b, n, k0 + lane - KG);
+  __syncwarp();
+  uint64_t pe[KG], pm[KG];
+#pragma unroll
+  for (int kk = 0; kk < KG; ++kk) {
+    pe[kk] = wq.pre[kk];
+    pm[kk] = wq.pre[KG + kk];
+  }
+  __syncwarp();  // wq.pre is reused by this warp's next group
+  const double a = v.amp[f];
+  float s0[KG], s1[KG];
+#pragma unroll
+  for (int kk = 0; kk < KG; ++kk) s0[kk] = s1[kk] = 0.0f;
+#pragma unroll 1
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t qoff = q * 128;
+    if (cbase + qoff >= D) break;  // warp-uniform
+    if (kn == KG && cbase + qoff + 128 <= D)
+      explode_slice<KIND, true>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, s0, s1);
+    else
+      explode_slice<KIND, false>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, s0, s1);
+  }
+  if (KIND != 0) {
+#pragma unroll
+    for (int kk = 0; kk < KG; ++kk) {
+      if (kk >= kn) break;
+      const float t0 = warp_sum(s0[kk]);
+      const float t1 = warp_sum(s1[kk]);
+      if (lane == 0) {
+        const uint64_t r = fl * v.lam + k0 + kk;
+        v.spart[(r * v.nparts + c) * 2] = t0;
+        v.spart[(r * v.nparts + c) * 2 + 1] = t1;
+      }
+    }
+  }
+}
+
+// Stage chunk c of batch b: box (fp64 and fp32 images) and population range.
+__device__ __forceinline__ void stage_explode_chunk(const EngineView& v, ExplodeChunk& ch,
+                                                    uint64_t b, uint32_t c) {
+  const uint32_t D = (uint32_t)v.D;
+  const uint32_t cbase = c * kChunk;
+  for (uint32_t i = threadIdx.x; i < kChunk; i += blockDim.x) {
+    const uint32_t d = cbase + i;
+    const bool in = d < D;
+    ch.lo[i] = in ? v.lower[d] : 0.0;
+    ch.hi[i] = in ? v.upper[d] : 0.0;
+    ch.lof[i] = in ? v.lower_f[d] : 0.0f;
+    ch.hif[i] = in ? v.upper_f[d] : 0.0f;
+    const double pl = in ? (double)v.pop_lo[b * v.Dp + d] : 0.0;
+    const double ph = in ? (double)v.pop_hi[b * v.Dp + d] : 0.0;
+    ch.plo[i] = pl;
+    ch.pw[i] = __dsub_rn(ph, pl);
+  }
+}
+
 // Work item = (firework f, 512-coordinate chunk c, 8 consecutive spark
 // groups): the block stages the chunk's box / population range once; warp w
 // takes spark group 8*item_group + w.
@@ -284,74 +359,19 @@ __global__ void __launch_bounds__(256, 2) k_explode_map(EngineView v) {
   ExplodeWarp* wqs = reinterpret_cast<ExplodeWarp*>(ex_smem + sizeof(ExplodeChunk));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   ExplodeWarp& wq = wqs[warp];
-  const uint64_t it = v.ctl->iteration;
   const uint64_t ngrp = (v.lam + KG - 1) / KG;
   const uint64_t nsup = (ngrp + kWarps - 1) / kWarps;  // groups of 8 spark groups
   const uint64_t items = v.Fl * v.nch * nsup;
-  const uint32_t D = (uint32_t)v.D;
   for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
     const uint64_t sup = item % nsup, rest = item / nsup;
     const uint32_t c = (uint32_t)(rest % v.nch);
-    const uint64_t fl = rest / v.nch, f = v.f_lo + fl;
-    const uint64_t b = f / v.mu, n = f % v.mu;
-    const uint32_t cbase = c * kChunk;
+    const uint64_t fl = rest / v.nch, b = (v.f_lo + fl) / v.mu;
     __syncthreads();  // previous item's readers are done with the chunk
-    for (uint32_t i = threadIdx.x; i < kChunk; i += blockDim.x) {
-      const uint32_t d = cbase + i;
-      const bool in = d < D;
-      ch.lo[i] = in ? v.lower[d] : 0.0;
-      ch.hi[i] = in ? v.upper[d] : 0.0;
-      ch.lof[i] = in ? v.lower_f[d] : 0.0f;
-      ch.hif[i] = in ? v.upper_f[d] : 0.0f;
-      const double pl = in ? (double)v.pop_lo[b * v.Dp + d] : 0.0;
-      const double ph = in ? (double)v.pop_hi[b * v.Dp + d] : 0.0;
-      ch.plo[i] = pl;
-      ch.pw[i] = __dsub_rn(ph, pl);
-    }
+    stage_explode_chunk(v, ch, b, c);
     __syncthreads();
     const uint64_t g = sup * kWarps + warp;
     if (g >= ngrp) continue;  // warp-uniform
-    const uint64_t k0 = g * KG;
-    const int kn = (int)(v.lam - k0 < (uint64_t)KG ? v.lam - k0 : KG);
-    // key prefixes: lanes [0, KG) explode, [KG, 2KG) mapping (hoisted
-    // rng.hpp:43-51 up to field k; each draw is then one splitmix64 round)
-    if (lane < kn)
-      wq.pre[lane] = key_prefix(v.seed, kExplode, it, b, n, k0 + lane);
-    else if (lane >= KG && lane < KG + kn)
-      wq.pre[lane] = key_prefix(v.seed, kMapping, it, b, n, k0 + lane - KG);
-    __syncwarp();
-    uint64_t pe[KG], pm[KG];
-#pragma unroll
-    for (int kk = 0; kk < KG; ++kk) {
-      pe[kk] = wq.pre[kk];
-      pm[kk] = wq.pre[KG + kk];
-    }
-    const double a = v.amp[f];
-    float s0[KG], s1[KG];
-#pragma unroll
-    for (int kk = 0; kk < KG; ++kk) s0[kk] = s1[kk] = 0.0f;
-#pragma unroll 1
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t qoff = q * 128;
-      if (cbase + qoff >= D) break;  // warp-uniform
-      if (kn == KG && cbase + qoff + 128 <= D)
-        explode_slice<KIND, true>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, s0, s1);
-      else
-        explode_slice<KIND, false>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, s0, s1);
-    }
-    if (KIND != 0) {
-#pragma unroll
-      for (int kk = 0; kk < KG; ++kk) {
-        if (kk >= kn) break;
-        const float t0 = warp_sum(s0[kk]);
-        const float t1 = warp_sum(s1[kk]);
-        if (lane == 0) {
-          const uint64_t r = fl * v.lam + k0 + kk;
-          v.spart[(r * v.nparts + c) * 2] = t0;
-          v.spart[(r * v.nparts + c) * 2 + 1] = t1;
-        }
-      }
-    }
+    explode_group<KIND>(v, ch, wq, lane, c, fl, g);
   }
 }
 
@@ -953,13 +973,12 @@ __device__ __forceinline__ float small_row_fitness(const EngineView& v, const fl
   return isnan(f) ? __int_as_float(0x7f800000) : f;
 }
 
-__global__ void __launch_bounds__(kSmallThreads) k_small_a(EngineView v) {
-  pdl_enter<true>();
-  if (gen_inactive(v)) return;
-  extern __shared__ uint64_t sa_keys[];  // [lam] rank keys
+// Phase A of local firework fl (all threads of the block; sa_keys: lam
+// uint64 of shared memory).
+__device__ void small_a_body(const EngineView& v, uint64_t fl, uint64_t* sa_keys) {
   __shared__ int s_idx[2 * 1024];        // top / bottom spark indices (top <= 1024)
   __shared__ float gs[16];
-  const uint64_t fl = blockIdx.x, f = v.f_lo + fl;
+  const uint64_t f = v.f_lo + fl;
   const uint32_t lam = (uint32_t)v.lam, top = (uint32_t)v.top;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const uint64_t it = v.ctl->iteration;
@@ -1029,20 +1048,24 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_a(EngineView v) {
   }
   select_core(v, fl, gs, nan_local);
   if (fl == 0 && threadIdx.x == 0) v.ctl->iters_rem = iters_remaining(v);  // after the wave
+  __syncthreads();  // shared state (s_idx, gs, keys) free for the next firework
+}
+
+__global__ void __launch_bounds__(kSmallThreads) k_small_a(EngineView v) {
+  pdl_enter<true>();
+  if (gen_inactive(v)) return;
+  extern __shared__ uint64_t sa_keys[];  // [lam] rank keys
+  small_a_body(v, blockIdx.x, sa_keys);
 }
 
 // k_small_b, one block per batch: loser-out (k_loser), reinit + fitness of
 // the losers (k_fresh_rows + k_finalize_record), record_wave, best copy and
 // population_range of the next generation (k_record_copy); the last block
 // to finish completes the trace point and the loop-top termination test.
-__global__ void __launch_bounds__(kSmallThreads) k_small_b(EngineView v) {
-  pdl_enter<true>();
-  if (gen_inactive(v)) {
-    if (threadIdx.x == 0) v.rec_flag[blockIdx.x] = 0;
-    return;
-  }
+// Phase B of batch b (all threads of the block); the last of the `nblocks`
+// callers of a generation completes the trace point and the termination test.
+__device__ void small_b_body(const EngineView& v, uint64_t b, unsigned nblocks) {
   Ctl* ctl = v.ctl;
-  const uint64_t b = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const uint64_t it = ctl->iteration;
   const uint64_t slot = ctl->trace_n % v.trace_cap;
@@ -1145,7 +1168,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_b(EngineView v) {
   if (threadIdx.x == 0) {
     __threadfence();
     const unsigned done = atomicAdd(&ctl->small_done, 1u);
-    if (done == gridDim.x - 1) {
+    if (done == nblocks - 1) {
       __threadfence();
       const uint64_t used = *(volatile uint64_t*)&ctl->used;
       for (uint64_t bb = 0; bb < v.B; ++bb) v.tr_evals[slot * v.B + bb] = used;
@@ -1159,6 +1182,101 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_b(EngineView v) {
       ctl->active = active;
       if (active) ctl->iteration += 1;
     }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSmallThreads) k_small_b(EngineView v) {
+  pdl_enter<true>();
+  if (gen_inactive(v)) {
+    if (threadIdx.x == 0) v.rec_flag[blockIdx.x] = 0;
+    return;
+  }
+  small_b_body(v, blockIdx.x, gridDim.x);
+}
+
+// Grid-wide barrier of a cooperative launch (all blocks co-resident).
+__device__ void grid_barrier(Ctl* ctl, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = &ctl->bar_gen;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(&ctl->bar_count, 1u) == nblocks - 1) {
+      ctl->bar_count = 0;
+      __threadfence();
+      *gen = g + 1;
+    } else {
+      while (*gen == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// The whole generation loop of a small problem in one persistent launch:
+// one block per firework, up to max_gens generations: explode + mapping +
+// fitness and phase A of the block's firework, a grid barrier
+// (iterations_remaining after the global wave), phase B of the batch by its
+// first firework's block, a grid barrier (termination test).  No launch
+// latency between phases; every value is computed with the same device
+// functions, in the same order, as the multi-kernel path.
+template <int KIND>
+__global__ void __launch_bounds__(kSmallThreads) k_small_run(EngineView v, uint64_t max_gens) {
+  extern __shared__ __align__(16) uint8_t run_smem[];
+  ExplodeChunk& ch = *reinterpret_cast<ExplodeChunk*>(run_smem);
+  ExplodeWarp* wqs = reinterpret_cast<ExplodeWarp*>(run_smem + sizeof(ExplodeChunk));
+  uint64_t* keys =
+      reinterpret_cast<uint64_t*>(run_smem + sizeof(ExplodeChunk) + kWarps * sizeof(ExplodeWarp));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t f = blockIdx.x, b = f / v.mu;
+  const uint64_t ngrp = (v.lam + kSparkGroup - 1) / kSparkGroup;
+  for (uint64_t gen = 0; gen < max_gens; ++gen) {
+    if (*(volatile int*)&v.ctl->active == 0) break;  // uniform: set before the last barrier
+    // explode + mapping + fused fitness partials of firework f (one chunk: D <= kChunk)
+    stage_explode_chunk(v, ch, b, 0);
+    __syncthreads();
+    for (uint64_t g = warp; g < ngrp; g += kWarps) explode_group<KIND>(v, ch, wqs[warp], lane, 0, f, g);
+    __syncthreads();
+    small_a_body(v, f, keys);
+    grid_barrier(v.ctl, gridDim.x);  // iterations_remaining (block 0) is final
+    if (f % v.mu == 0) small_b_body(v, b, (unsigned)v.B);
+    grid_barrier(v.ctl, gridDim.x);  // termination / iteration of the next generation
+  }
+}
+
+static bool small_path_disabled();
+
+bool small_run_ok(const EngineView& v, int nsm) {
+  static const bool off = [] {  // MGFWA_SMALL_RUN=0: the graph-replayed kernels instead
+    const char* e = getenv("MGFWA_SMALL_RUN");
+    return e != nullptr && e[0] == '0';
+  }();
+  if (off || small_path_disabled()) return false;
+  return !v.nn && v.Fl == v.F && v.D <= (uint64_t)kChunk && v.lam <= 2048 && v.top <= 1024 &&
+         v.M <= 16 && v.F <= (uint64_t)nsm;
+}
+
+static size_t small_run_smem(const EngineView& v) {
+  return sizeof(ExplodeChunk) + kWarps * sizeof(ExplodeWarp) + v.lam * sizeof(uint64_t);
+}
+
+cudaError_t launch_small_run(const EngineView& v, uint64_t max_gens, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)v.F);
+  cfg.blockDim = dim3(kSmallThreads);
+  cfg.dynamicSmemBytes = small_run_smem(v);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for the grid barrier
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  switch (v.obj_kind) {
+    case OBJ_SPHERE: return cudaLaunchKernelEx(&cfg, k_small_run<OBJ_SPHERE>, v, max_gens);
+    case OBJ_RASTRIGIN: return cudaLaunchKernelEx(&cfg, k_small_run<OBJ_RASTRIGIN>, v, max_gens);
+    default: return cudaLaunchKernelEx(&cfg, k_small_run<OBJ_ACKLEY>, v, max_gens);
   }
 }
 

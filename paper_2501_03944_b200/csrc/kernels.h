@@ -28,6 +28,11 @@ void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
 void launch_initialize_kernels(const EngineView& v, int nsm, cudaStream_t s,
                                GenerationHooks* hooks);
 
+// Persistent whole-loop kernel for small analytic problems (one context,
+// D <= 512, B * mu <= #SMs): up to max_gens generations in one cooperative launch.
+bool small_run_ok(const EngineView& v, int nsm);
+cudaError_t launch_small_run(const EngineView& v, uint64_t max_gens, cudaStream_t s);
+
 // operator seams
 void launch_pop_range(const EngineView& v, int nsm, cudaStream_t s);
 void launch_explode_map(const EngineView& v, int nsm, cudaStream_t s);
