@@ -150,10 +150,9 @@ __device__ __forceinline__ float bf(const __nv_bfloat16 x) { return __bfloat162f
 __host__ __device__ constexpr int conv1_k(int ky, int kx) {
   return ky < 4 ? 2 * (4 * (kx >> 1) + ky) + (kx & 1) : 2 * (12 + (kx >> 1)) + (kx & 1);
 }
-__device__ __forceinline__ int conv1_koff(int q) {  // word offset of pair q in the pair image
-  const int c = q & 3, grp = q >> 2;
-  return grp < 3 ? c * kImgS + 2 * grp : 4 * kImgS + 2 * (c < 3 ? c : 2);
-}
+// conv2 tap t = ky * 5 + kx -> word offset in the pooled conv1 map [14][14][4 words]
+__host__ __device__ constexpr int tap_off(int t) { return ((t / 5) * 14 + (t % 5)) * 4; }
+
 
 // Stage one candidate's weights into shared memory (all threads).
 __device__ void stage_weights(uint8_t* sm, const __nv_bfloat16* w) {
@@ -258,11 +257,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_lenet_fitness(LenetArgs args) {
   __syncthreads();
 
   // A-fragment word offsets (k pairs 2c, 2c+1 and +8 of each k16 step)
-  int koff1[2][2];  // conv1 pair offsets (conv1_k order)
-#pragma unroll
-  for (int st = 0; st < 2; ++st)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) koff1[st][h] = conv1_koff(8 * st + 4 * h + c);
+  // conv1 pair offsets (conv1_k order): groups 0..2 are (ky = c, kxp = group),
+  // group 3 is (ky = 4, kxp = min(c, 2)); the lane part goes into two base
+  // pointers so the per-group offsets are immediates
+  const uint32_t* imgc = img + c * kImgS;
+  const uint32_t* imgd = img + 4 * kImgS + 2 * (c < 3 ? c : 2);
 
   const uint64_t total = args.rows * args.nparts;
   const uint64_t t_begin = total * blockIdx.x / gridDim.x;
@@ -325,10 +324,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_lenet_fitness(LenetArgs args) {
             const int py = wc / 14, px = wc - 14 * py;
             const int base0 = (2 * py) * kImgS + 2 * px + dx, base1 = base0 + kImgS;
             d[u][0] = b1a, d[u][1] = b1b, d[u][2] = b1a, d[u][3] = b1b;
-#pragma unroll
-            for (int st = 0; st < 2; ++st)
-              mma_bf16(d[u], img[base0 + koff1[st][0]], img[base1 + koff1[st][0]],
-                       img[base0 + koff1[st][1]], img[base1 + koff1[st][1]], bw1[st][0], bw1[st][1]);
+            mma_bf16(d[u], imgc[base0], imgc[base1], imgc[base0 + 2], imgc[base1 + 2], bw1[0][0], bw1[0][1]);
+            mma_bf16(d[u], imgc[base0 + 4], imgc[base1 + 4], imgd[base0], imgd[base1], bw1[1][0], bw1[1][1]);
           }
 #pragma unroll
           for (int u = 0; u < kC1T; ++u) {
@@ -345,15 +342,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_lenet_fitness(LenetArgs args) {
         if (s + kWarpsL < s_hi) prefetch_img(img_s, args.pimg + (uint64_t)(s + kWarpsL) * kImgWords, lane);
         // ---------------------------------------------- conv2 (this warp)
         // p1 word layout [py*14 + px][cpair]; A k = tap * 8 + ci
-        int toff[13][2];  // A-fragment word offsets: k = tap * 8 + ci
-#pragma unroll
-        for (int st = 0; st < 13; ++st)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int k = 16 * st + 8 * h + 2 * c;
-            const int tap = k >> 3, cp = (k & 7) >> 1;
-            toff[st][h] = tap < 25 ? ((tap / 5) * 14 + (tap % 5)) * 4 + cp : 196 * 4;  // zero pixel
-          }
+        // A-fragment k = tap * 8 + ci: the lane's channel pair c is folded into
+        // the base pointer, the tap offsets are compile-time immediates
+        const uint32_t* p1c = p1 + c;
         __nv_bfloat16* o = p2 + warp * kP2S;
         // 7 tiles of 4 windows (window 4t + wi of the 5 x 5 pooled map), two
         // tiles per step: 2 kC2T independent MMA chains (kC2T tiles x 2 n-tiles)
@@ -375,11 +366,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_lenet_fitness(LenetArgs args) {
           for (int st = 0; st < 13; ++st) {
 #pragma unroll
             for (int u = 0; u < kC2T; ++u) {
-              const int z0 = st == 12 ? -b0[u] : 0, z1 = st == 12 ? -b1[u] : 0;  // tap 25: zero pixel
-              const uint32_t a0 = p1[b0[u] + toff[st][0]];
-              const uint32_t a1 = p1[b1[u] + toff[st][0]];
-              const uint32_t a2 = p1[b0[u] + z0 + toff[st][1]];
-              const uint32_t a3 = p1[b1[u] + z1 + toff[st][1]];
+              const uint32_t a0 = p1c[b0[u] + tap_off(2 * st)];
+              const uint32_t a1 = p1c[b1[u] + tap_off(2 * st)];
+              const uint32_t a2 = st < 12 ? p1c[b0[u] + tap_off(2 * st + 1)] : 0u;  // tap 25: K padding
+              const uint32_t a3 = st < 12 ? p1c[b1[u] + tap_off(2 * st + 1)] : 0u;
               mma_bf16(d[u][0], a0, a1, a2, a3, bw2[st][0][0], bw2[st][0][1]);
               mma_bf16(d[u][1], a0, a1, a2, a3, bw2[st][1][0], bw2[st][1][1]);
             }
