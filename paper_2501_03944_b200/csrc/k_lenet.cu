@@ -505,10 +505,436 @@ __global__ void __launch_bounds__(kThreads, 1) k_lenet_fitness(LenetArgs args) {
   }
 }
 
+// ------------------------------------------------------------ split path
+// Two kernels instead of one: k_lenet_conv (conv1 + conv2 of every sample,
+// one sample per warp, no block-wide synchronisation, only the conv weights
+// staged, 12 warps per SM) writes the pooled conv2 activations (window-major
+// bf16 [400]) to a per-plan scratch; k_lenet_fc (fc1/fc2/fc3 + CE on batches
+// of 16 samples, fc weights staged) reads them back.  Same arithmetic as the
+// fused kernel except the loss summation order (16 batch slots).
+namespace {
+
+#ifndef LENET_CV_WARPS
+#define LENET_CV_WARPS 12
+#endif
+#ifndef LENET_CV_C1T
+#define LENET_CV_C1T 4
+#endif
+#ifndef LENET_CV_C2T
+#define LENET_CV_C2T 2
+#endif
+constexpr int kConvWarps = LENET_CV_WARPS;
+constexpr int kCvC1T = LENET_CV_C1T;  // conv1 tiles in flight per warp
+constexpr int kCvC2T = LENET_CV_C2T;  // conv2 tiles in flight per warp (x 2 n-tiles)
+constexpr int kConvThreads = kConvWarps * 32;
+constexpr int kP2Row = 400;  // bf16 per sample in the scratch
+
+struct ConvSmem {
+  static constexpr int wc1 = 0;                                // [8][32] bf16
+  static constexpr int wc2 = wc1 + 8 * kC1K * 2;               // [16][216] bf16
+  static constexpr int bc1 = wc2 + 16 * kC2S * 2;              // f32 [8]
+  static constexpr int bc2 = bc1 + 8 * 4;                      // f32 [16]
+  static constexpr int img = bc2 + 16 * 4;                     // per warp [33][40] u32
+  static constexpr int p1 = img + kConvWarps * kImgWords * 4;  // per warp [197][4] u32
+  static constexpr int p2 = p1 + kConvWarps * 197 * 4 * 4;     // per warp [400] bf16
+  static constexpr int total = p2 + kConvWarps * kP2Row * 2;
+};
+static_assert(ConvSmem::img % 16 == 0 && ConvSmem::p2 % 16 == 0, "aligned cp.async / uint4 regions");
+
+constexpr int kFcWarps = 8;
+constexpr int kFcThreads = kFcWarps * 32;
+struct FcSmem {
+  static constexpr int r = 0;                            // [128][408] bf16: wf1 staging | p2 chunk
+  static constexpr int wf2 = r + 128 * kF1S * 2;         // [96][136]
+  static constexpr int wf3 = wf2 + 96 * kF2S * 2;        // [16][104]
+  static constexpr int bf1 = wf3 + 16 * kF3S * 2;        // f32 [128]
+  static constexpr int bf2 = bf1 + 128 * 4;              // f32 [96]
+  static constexpr int bf3 = bf2 + 96 * 4;               // f32 [16]
+  static constexpr int wsum = bf3 + 16 * 4;              // f32 [8]
+  static constexpr int h1 = wsum + 8 * 4;                // [128][136] bf16 (then f32 logits [128][16])
+  static constexpr int h2 = h1 + 128 * kH1S * 2;         // [128][104] bf16
+  static constexpr int total = h2 + 128 * kH2S * 2;
+};
+static_assert(FcSmem::total <= 227 * 1024 && FcSmem::h1 % 16 == 0 && FcSmem::h2 % 16 == 0 &&
+                  FcSmem::wf2 % 16 == 0 && FcSmem::wf3 % 16 == 0,
+              "LeNet fc shared memory");
+static_assert(kF1S == kP2S && kChunkS == 128, "the staging region doubles as the p2 chunk");
+
+struct LenetSplitArgs {
+  LenetArgs base;
+  __nv_bfloat16* p2;  // [rows][S][400] scratch
+};
+
+}  // namespace
+
+__global__ void __launch_bounds__(kConvThreads, 1) k_lenet_conv(LenetSplitArgs sa) {
+  pdl_enter();
+  const LenetArgs& args = sa.base;
+  if (args.gate != nullptr && *args.gate == 0) return;
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, c = lane & 3;
+  const int wi = g >> 1, dx = g & 1;
+  __nv_bfloat16* wc1 = reinterpret_cast<__nv_bfloat16*>(sm + ConvSmem::wc1);
+  __nv_bfloat16* wc2 = reinterpret_cast<__nv_bfloat16*>(sm + ConvSmem::wc2);
+  float* bc1 = reinterpret_cast<float*>(sm + ConvSmem::bc1);
+  float* bc2 = reinterpret_cast<float*>(sm + ConvSmem::bc2);
+  const uint32_t* img = reinterpret_cast<const uint32_t*>(sm + ConvSmem::img) + warp * kImgWords;
+  const uint32_t img_s = smem_addr(img);
+  uint32_t* p1 = reinterpret_cast<uint32_t*>(sm + ConvSmem::p1) + warp * 197 * 4;  // +1 zero pixel
+  __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(sm + ConvSmem::p2) + warp * kP2Row;
+  {
+    uint32_t* p = reinterpret_cast<uint32_t*>(sm);
+    for (int i = threadIdx.x; i < ConvSmem::total / 4; i += kConvThreads) p[i] = 0u;
+  }
+  __syncthreads();
+  const uint32_t* imgc = img + c * kImgS;
+  const uint32_t* imgd = img + 4 * kImgS + 2 * (c < 3 ? c : 2);
+  const uint32_t* p1c = p1 + c;
+
+  const uint64_t total = args.rows * args.nparts;
+  const uint64_t t_begin = total * blockIdx.x / gridDim.x;
+  const uint64_t t_end = total * (blockIdx.x + 1) / gridDim.x;
+  uint64_t staged = ~0ull;
+  uint32_t bw1[2][2], bw2[13][2][2];
+  float b1a = 0.f, b1b = 0.f, b2a = 0.f, b2b = 0.f, b2c = 0.f, b2d = 0.f;
+  for (uint64_t item = t_begin; item < t_end; ++item) {
+    const uint64_t row = item / args.nparts;
+    const uint32_t part = (uint32_t)(item % args.nparts);
+    const uint32_t s_lo = part * kChunkS, s_hi = min(args.S, s_lo + kChunkS);
+    if (row != staged) {
+      __syncthreads();
+      const __nv_bfloat16* w = args.W + row * args.Dp;
+      for (int i = threadIdx.x; i < 150; i += kConvThreads) {
+        const int ch = i / 25, r = i % 25, ky = r / 5, kx = r % 5;
+        wc1[ch * kC1K + conv1_k(ky, kx)] = w[oC1W + i];
+      }
+      for (int i = threadIdx.x; i < 2400; i += kConvThreads) {
+        const int ch = i / 150, r = i % 150, ci = r / 25, tap = r % 25;
+        wc2[ch * kC2S + tap * 8 + ci] = w[oC2W + i];
+      }
+      if (threadIdx.x < 6) bc1[threadIdx.x] = bf(w[oC1B + threadIdx.x]);
+      if (threadIdx.x < 16) bc2[threadIdx.x] = bf(w[oC2B + threadIdx.x]);
+      __syncthreads();
+      staged = row;
+#pragma unroll
+      for (int st = 0; st < 2; ++st) {
+        const __nv_bfloat16* b = wc1 + g * kC1K + 16 * st + 2 * c;
+        bw1[st][0] = *reinterpret_cast<const uint32_t*>(b);
+        bw1[st][1] = *reinterpret_cast<const uint32_t*>(b + 8);
+      }
+#pragma unroll
+      for (int st = 0; st < 13; ++st)
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+          const __nv_bfloat16* b = wc2 + (8 * n + g) * kC2S + 16 * st + 2 * c;
+          bw2[st][n][0] = *reinterpret_cast<const uint32_t*>(b);
+          bw2[st][n][1] = *reinterpret_cast<const uint32_t*>(b + 8);
+        }
+      b1a = bc1[2 * c], b1b = bc1[2 * c + 1];
+      b2a = bc2[2 * c], b2b = bc2[2 * c + 1], b2c = bc2[8 + 2 * c], b2d = bc2[9 + 2 * c];
+    }
+    if (s_lo + warp < s_hi) prefetch_img(img_s, args.pimg + (uint64_t)(s_lo + warp) * kImgWords, lane);
+    for (uint32_t s = s_lo + warp; s < s_hi; s += kConvWarps) {
+      cp_async_wait_all();
+      __syncwarp();
+      // ---- conv1 + ReLU + pool -> p1 (as k_lenet_fitness)
+      for (int t0 = 0; t0 < 49; t0 += kCvC1T) {
+        int wpos[kCvC1T];
+        float d[kCvC1T][4];
+#pragma unroll
+        for (int u = 0; u < kCvC1T; ++u) {
+          const int w = 4 * (t0 + u) + wi;
+          wpos[u] = w < 196 ? w : -1;
+          const int wc = w < 196 ? w : 0;
+          const int py = wc / 14, px = wc - 14 * py;
+          const int base0 = (2 * py) * kImgS + 2 * px + dx, base1 = base0 + kImgS;
+          d[u][0] = b1a, d[u][1] = b1b, d[u][2] = b1a, d[u][3] = b1b;
+          mma_bf16(d[u], imgc[base0], imgc[base1], imgc[base0 + 2], imgc[base1 + 2], bw1[0][0], bw1[0][1]);
+          mma_bf16(d[u], imgc[base0 + 4], imgc[base1 + 4], imgd[base0], imgd[base1], bw1[1][0], bw1[1][1]);
+        }
+#pragma unroll
+        for (int u = 0; u < kCvC1T; ++u) {
+          float s0 = fmaxf(d[u][0], 0.f) + fmaxf(d[u][2], 0.f);
+          float s1 = fmaxf(d[u][1], 0.f) + fmaxf(d[u][3], 0.f);
+          s0 += __shfl_xor_sync(0xffffffffu, s0, 4);
+          s1 += __shfl_xor_sync(0xffffffffu, s1, 4);
+          if (dx == 0 && wpos[u] >= 0) p1[wpos[u] * 4 + c] = pack_bf16(0.25f * s0, 0.25f * s1);
+        }
+      }
+      __syncwarp();
+      if (s + kConvWarps < s_hi)
+        prefetch_img(img_s, args.pimg + (uint64_t)(s + kConvWarps) * kImgWords, lane);
+      // ---- conv2 + ReLU + pool -> o (window-major [25][16])
+      for (int t0 = 0; t0 < 7; t0 += kCvC2T) {
+        int wv[kCvC2T], b0[kCvC2T], b1[kCvC2T];
+        float d[kCvC2T][2][4];
+#pragma unroll
+        for (int u = 0; u < kCvC2T; ++u) {
+          const int w = 4 * (t0 + u) + wi;
+          wv[u] = w < 25 ? w : -1;
+          const int wc = w < 25 ? w : 0;
+          const int qy = wc / 5, qx = wc - 5 * qy;
+          b0[u] = ((2 * qy) * 14 + 2 * qx + dx) * 4;
+          b1[u] = b0[u] + 14 * 4;
+          d[u][0][0] = b2a, d[u][0][1] = b2b, d[u][0][2] = b2a, d[u][0][3] = b2b;
+          d[u][1][0] = b2c, d[u][1][1] = b2d, d[u][1][2] = b2c, d[u][1][3] = b2d;
+        }
+#pragma unroll
+        for (int st = 0; st < 13; ++st) {
+#pragma unroll
+          for (int u = 0; u < kCvC2T; ++u) {
+            const uint32_t a0 = p1c[b0[u] + tap_off(2 * st)];
+            const uint32_t a1 = p1c[b1[u] + tap_off(2 * st)];
+            const uint32_t a2 = st < 12 ? p1c[b0[u] + tap_off(2 * st + 1)] : 0u;
+            const uint32_t a3 = st < 12 ? p1c[b1[u] + tap_off(2 * st + 1)] : 0u;
+            mma_bf16(d[u][0], a0, a1, a2, a3, bw2[st][0][0], bw2[st][0][1]);
+            mma_bf16(d[u][1], a0, a1, a2, a3, bw2[st][1][0], bw2[st][1][1]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kCvC2T; ++u) {
+          float s0 = fmaxf(d[u][0][0], 0.f) + fmaxf(d[u][0][2], 0.f);
+          float s1 = fmaxf(d[u][0][1], 0.f) + fmaxf(d[u][0][3], 0.f);
+          float s2 = fmaxf(d[u][1][0], 0.f) + fmaxf(d[u][1][2], 0.f);
+          float s3 = fmaxf(d[u][1][1], 0.f) + fmaxf(d[u][1][3], 0.f);
+          s0 += __shfl_xor_sync(0xffffffffu, s0, 4);
+          s1 += __shfl_xor_sync(0xffffffffu, s1, 4);
+          s2 += __shfl_xor_sync(0xffffffffu, s2, 4);
+          s3 += __shfl_xor_sync(0xffffffffu, s3, 4);
+          if (dx == 0 && wv[u] >= 0) {
+            uint32_t* ow = reinterpret_cast<uint32_t*>(o + wv[u] * 16);
+            ow[c] = pack_bf16(0.25f * s0, 0.25f * s1);
+            ow[4 + c] = pack_bf16(0.25f * s2, 0.25f * s3);
+          }
+        }
+      }
+      __syncwarp();
+      // ---- p2 row -> scratch (800 B, coalesced 16-byte stores)
+      uint4* dst = reinterpret_cast<uint4*>(sa.p2 + (row * args.S + s) * (uint64_t)kP2Row);
+      const uint4* srcv = reinterpret_cast<const uint4*>(o);
+      for (int i = lane; i < kP2Row * 2 / 16; i += 32) dst[i] = srcv[i];
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kFcThreads, 1) k_lenet_fc(LenetSplitArgs sa) {
+  pdl_enter();
+  const LenetArgs& args = sa.base;
+  if (args.gate != nullptr && *args.gate == 0) return;
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, c = lane & 3;
+  __nv_bfloat16* rg = reinterpret_cast<__nv_bfloat16*>(sm + FcSmem::r);  // wf1 staging | p2 chunk
+  __nv_bfloat16* wf2 = reinterpret_cast<__nv_bfloat16*>(sm + FcSmem::wf2);
+  __nv_bfloat16* wf3 = reinterpret_cast<__nv_bfloat16*>(sm + FcSmem::wf3);
+  float* bf1 = reinterpret_cast<float*>(sm + FcSmem::bf1);
+  float* bf2 = reinterpret_cast<float*>(sm + FcSmem::bf2);
+  float* bf3 = reinterpret_cast<float*>(sm + FcSmem::bf3);
+  __nv_bfloat16* h1 = reinterpret_cast<__nv_bfloat16*>(sm + FcSmem::h1);
+  __nv_bfloat16* h2 = reinterpret_cast<__nv_bfloat16*>(sm + FcSmem::h2);
+  float* logit = reinterpret_cast<float*>(sm + FcSmem::h1);  // [128][16], h1 is dead by then
+  float* wsum = reinterpret_cast<float*>(sm + FcSmem::wsum);
+  {
+    uint32_t* p = reinterpret_cast<uint32_t*>(sm);
+    for (int i = threadIdx.x; i < FcSmem::total / 4; i += kFcThreads) p[i] = 0u;
+  }
+  __syncthreads();
+  // ldmatrix lane addressing: matrices {rows 0-7, k lo}, {rows 8-15, k lo},
+  // {rows 0-7, k hi}, {rows 8-15, k hi} for A; {n 0-7, k lo}, {n 0-7, k hi},
+  // {n 8-15, k lo}, {n 8-15, k hi} for two B n-tiles.
+  const int a_row = (lane & 7) + ((lane >> 3) & 1) * 8, a_col = (lane >> 4) * 8;
+  const int b_row = (lane & 7) + (lane >> 4) * 8, b_col = ((lane >> 3) & 1) * 8;
+  const uint32_t r_s = smem_addr(rg), h1_s = smem_addr(h1), h2_s = smem_addr(h2);
+  const uint32_t wf2_s = smem_addr(wf2), wf3_s = smem_addr(wf3);
+
+  const uint64_t total = args.rows * args.nparts;
+  const uint64_t t_begin = total * blockIdx.x / gridDim.x;
+  const uint64_t t_end = total * (blockIdx.x + 1) / gridDim.x;
+  uint64_t staged = ~0ull;
+  uint32_t af1[25][4];  // this warp's fc1 A fragments (outputs 16 warp .. +15, K = 400)
+  float bias1[2] = {0.f, 0.f};
+  for (uint64_t item = t_begin; item < t_end; ++item) {
+    const uint64_t row = item / args.nparts;
+    const uint32_t part = (uint32_t)(item % args.nparts);
+    const uint32_t s_lo = part * kChunkS, s_hi = min(args.S, s_lo + kChunkS);
+    __syncthreads();  // previous item: readers of the region / h1 / logits are done
+    if (row != staged) {
+      const __nv_bfloat16* w = args.W + row * args.Dp;
+      for (int i = threadIdx.x; i < 120 * 400; i += kFcThreads) {  // window-major columns
+        const int j = i / 400, k = i % 400, ch = k / 25, win = k % 25;
+        rg[j * kF1S + win * 16 + ch] = w[oF1W + i];
+      }
+      for (int i = threadIdx.x; i < 8 * kF1S / 2; i += kFcThreads)  // rows 120..127 = 0
+        reinterpret_cast<uint32_t*>(rg + 120 * kF1S)[i] = 0u;
+      for (int i = threadIdx.x; i < 84 * 30; i += kFcThreads) {
+        const int j = i / 30, q = i % 30;
+        *reinterpret_cast<uint2*>(wf2 + j * kF2S + q * 4) =
+            *reinterpret_cast<const uint2*>(w + oF2W + j * 120 + q * 4);
+      }
+      for (int i = threadIdx.x; i < 10 * 21; i += kFcThreads) {
+        const int j = i / 21, q = i % 21;
+        *reinterpret_cast<uint2*>(wf3 + j * kF3S + q * 4) =
+            *reinterpret_cast<const uint2*>(w + oF3W + j * 84 + q * 4);
+      }
+      if (threadIdx.x < 120) bf1[threadIdx.x] = bf(w[oF1B + threadIdx.x]);
+      if (threadIdx.x < 84) bf2[threadIdx.x] = bf(w[oF2B + threadIdx.x]);
+      if (threadIdx.x < 10) bf3[threadIdx.x] = bf(w[oF3B + threadIdx.x]);
+      __syncthreads();
+      const uint32_t a_base = r_s + (uint32_t)(((16 * warp + a_row) * kF1S + a_col) * 2);
+#pragma unroll
+      for (int st = 0; st < 25; ++st) ldmatrix_x4(af1[st], a_base + st * 32);
+      {
+        const int j0 = 16 * warp + g, j1 = j0 + 8;
+        bias1[0] = j0 < 120 ? bf1[j0] : 0.f;
+        bias1[1] = j1 < 120 ? bf1[j1] : 0.f;
+      }
+      staged = row;
+      __syncthreads();  // the region is about to hold activations
+    }
+    // ---- p2 rows of the chunk (cp.async, zero rows past s_hi)
+    for (int i = threadIdx.x; i < (int)kChunkS * 50; i += kFcThreads) {
+      const int r = i / 50, q = i % 50;
+      const uint32_t dst = r_s + (uint32_t)(r * kP2S * 2 + q * 16);
+      if (s_lo + r < s_hi)
+        cp_async16(dst, sa.p2 + (row * args.S + s_lo + r) * (uint64_t)kP2Row + q * 8);
+      else
+        *reinterpret_cast<uint4*>(rg + r * kP2S + q * 8) = make_uint4(0u, 0u, 0u, 0u);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    // ---- fc1: outputs 16 warp .. +15 for all 128 samples, 4 n-tiles at a time
+#pragma unroll 1
+    for (int ng = 0; ng < 16; ng += 4) {
+      float d[4][4] = {};
+      const uint32_t b_base = r_s + (uint32_t)(((8 * ng + b_row) * kP2S + b_col) * 2);
+#pragma unroll
+      for (int st = 0; st < 25; ++st) {
+        uint32_t b[2][4];
+        ldmatrix_x4(b[0], b_base + st * 32);
+        ldmatrix_x4(b[1], b_base + 16 * kP2S * 2 + st * 32);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          mma_bf16(d[j], af1[st][0], af1[st][1], af1[st][2], af1[st][3], b[j >> 1][(j & 1) * 2],
+                   b[j >> 1][(j & 1) * 2 + 1]);
+      }
+      const int j0 = 16 * warp + g, j1 = j0 + 8;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int s0 = 8 * (ng + j) + 2 * c;
+        h1[s0 * kH1S + j0] = __float2bfloat16(j0 < 120 ? fmaxf(d[j][0] + bias1[0], 0.f) : 0.f);
+        h1[(s0 + 1) * kH1S + j0] = __float2bfloat16(j0 < 120 ? fmaxf(d[j][1] + bias1[0], 0.f) : 0.f);
+        h1[s0 * kH1S + j1] = __float2bfloat16(j1 < 120 ? fmaxf(d[j][2] + bias1[1], 0.f) : 0.f);
+        h1[(s0 + 1) * kH1S + j1] = __float2bfloat16(j1 < 120 ? fmaxf(d[j][3] + bias1[1], 0.f) : 0.f);
+      }
+    }
+    __syncthreads();
+    // ---- fc2: samples 16 warp .. +15 (two n-tiles), all 6 output tiles
+    {
+      uint32_t b[8][4];
+      const uint32_t b_base = h1_s + (uint32_t)(((16 * warp + b_row) * kH1S + b_col) * 2);
+#pragma unroll
+      for (int st = 0; st < 8; ++st) ldmatrix_x4(b[st], b_base + st * 32);
+#pragma unroll
+      for (int mt = 0; mt < 6; ++mt) {
+        float d[2][4] = {};
+        const uint32_t a_base = wf2_s + (uint32_t)(((16 * mt + a_row) * kF2S + a_col) * 2);
+#pragma unroll
+        for (int st = 0; st < 8; ++st) {
+          uint32_t a[4];
+          ldmatrix_x4(a, a_base + st * 32);
+          mma_bf16(d[0], a[0], a[1], a[2], a[3], b[st][0], b[st][1]);
+          mma_bf16(d[1], a[0], a[1], a[2], a[3], b[st][2], b[st][3]);
+        }
+        const int j0 = 16 * mt + g, j1 = j0 + 8;
+        const float c0 = j0 < 84 ? bf2[j0] : 0.f, c1 = j1 < 84 ? bf2[j1] : 0.f;
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+          const int s0 = 16 * warp + 8 * n + 2 * c;
+          h2[s0 * kH2S + j0] = __float2bfloat16(j0 < 84 ? fmaxf(d[n][0] + c0, 0.f) : 0.f);
+          h2[(s0 + 1) * kH2S + j0] = __float2bfloat16(j0 < 84 ? fmaxf(d[n][1] + c0, 0.f) : 0.f);
+          h2[s0 * kH2S + j1] = __float2bfloat16(j1 < 84 ? fmaxf(d[n][2] + c1, 0.f) : 0.f);
+          h2[(s0 + 1) * kH2S + j1] = __float2bfloat16(j1 < 84 ? fmaxf(d[n][3] + c1, 0.f) : 0.f);
+        }
+      }
+    }
+    // fc3 reads only this warp's own h2 rows (samples 16 warp .. +15)
+    __syncwarp();
+    float loss;
+    {
+      float d[2][4] = {};
+      const uint32_t b_base = h2_s + (uint32_t)(((16 * warp + b_row) * kH2S + b_col) * 2);
+      const uint32_t a_base = wf3_s + (uint32_t)((a_row * kF3S + a_col) * 2);
+#pragma unroll
+      for (int st = 0; st < 6; ++st) {
+        uint32_t a[4], b[4];
+        ldmatrix_x4(a, a_base + st * 32);
+        ldmatrix_x4(b, b_base + st * 32);
+        mma_bf16(d[0], a[0], a[1], a[2], a[3], b[0], b[1]);
+        mma_bf16(d[1], a[0], a[1], a[2], a[3], b[2], b[3]);
+      }
+      // logits[sample][class]; h1 is dead once every warp has passed fc2
+      __syncthreads();
+#pragma unroll
+      for (int n = 0; n < 2; ++n) {
+        const int s0 = 16 * warp + 8 * n + 2 * c;
+        logit[s0 * 16 + g] = d[n][0] + bf3[g];
+        logit[(s0 + 1) * 16 + g] = d[n][1] + bf3[g];
+        if (g < 2) {
+          logit[s0 * 16 + g + 8] = d[n][2] + bf3[g + 8];
+          logit[(s0 + 1) * 16 + g + 8] = d[n][3] + bf3[g + 8];
+        }
+      }
+      __syncwarp();
+      loss = 0.f;
+      const uint32_t s = s_lo + 16 * warp + lane;
+      if (lane < 16 && s < s_hi) {
+        const float* z = logit + (16 * warp + lane) * 16;
+        float m = z[0];
+#pragma unroll
+        for (int q = 1; q < 10; ++q) m = fmaxf(m, z[q]);
+        float se = 0.f;
+#pragma unroll
+        for (int q = 0; q < 10; ++q) se += expf(z[q] - m);
+        loss = (m + logf(se)) - z[args.y[s]];
+      }
+    }
+    // fixed-order reduction: 16 lanes per warp, then the 8 warps in order
+    loss += __shfl_xor_sync(0xffffffffu, loss, 1);
+    loss += __shfl_xor_sync(0xffffffffu, loss, 2);
+    loss += __shfl_xor_sync(0xffffffffu, loss, 4);
+    loss += __shfl_xor_sync(0xffffffffu, loss, 8);
+    if (lane == 0) wsum[warp] = loss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float t = 0.f;
+      for (int w = 0; w < kFcWarps; ++w) t += wsum[w];
+      args.part[(row * args.nparts + part) * 2] = t;
+      args.part[(row * args.nparts + part) * 2 + 1] = 0.0f;
+    }
+  }
+}
+
+#ifndef LENET_SPLIT_DEFAULT
+#define LENET_SPLIT_DEFAULT 1
+#endif
+static bool lenet_split() {  // MGFWA_LENET_SPLIT=0|1 (default LENET_SPLIT_DEFAULT)
+  static const bool on = [] {
+    const char* e = getenv("MGFWA_LENET_SPLIT");
+    if (e && (e[0] == '0' || e[0] == '1')) return e[0] == '1';
+    return LENET_SPLIT_DEFAULT != 0;
+  }();
+  return on;
+}
+
 struct LenetPlan {
   LenetArgs args;
   unsigned grid;
-  uint32_t* pimg;  // owned
+  uint32_t* pimg;      // owned
+  __nv_bfloat16* p2;   // owned scratch (split path)
+  bool split;
 };
 
 uint32_t lenet_num_parts(uint32_t S) { return (S + kChunkS - 1) / kChunkS; }
@@ -526,7 +952,11 @@ LenetPlan* lenet_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t 
     return nullptr;
   }
   if (cudaFuncSetAttribute(k_lenet_fitness, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           Smem::total) != cudaSuccess) {
+                           Smem::total) != cudaSuccess ||
+      cudaFuncSetAttribute(k_lenet_conv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           ConvSmem::total) != cudaSuccess ||
+      cudaFuncSetAttribute(k_lenet_fc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           FcSmem::total) != cudaSuccess) {
     snprintf(err, errlen, "LeNet objective: shared memory opt-in failed");
     return nullptr;
   }
@@ -541,6 +971,13 @@ LenetPlan* lenet_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t 
   k_lenet_pairs<<<(unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256>>>(X, S, p->pimg);
   if (cudaDeviceSynchronize() != cudaSuccess) {
     snprintf(err, errlen, "LeNet objective: pair-image kernel failed");
+    cudaFree(p->pimg);
+    delete p;
+    return nullptr;
+  }
+  p->split = lenet_split();
+  if (p->split && cudaMalloc(&p->p2, (size_t)rows * S * kP2Row * 2) != cudaSuccess) {
+    snprintf(err, errlen, "LeNet objective: cudaMalloc of the activation scratch failed");
     cudaFree(p->pimg);
     delete p;
     return nullptr;
@@ -560,6 +997,7 @@ LenetPlan* lenet_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t 
 void lenet_plan_destroy(LenetPlan* p) {
   if (!p) return;
   cudaFree(p->pimg);
+  cudaFree(p->p2);
   delete p;
 }
 
@@ -568,6 +1006,12 @@ cudaError_t lenet_fitness_launch(const LenetPlan* p, float* part, const int* gat
   LenetArgs a = p->args;
   a.part = part;
   a.gate = gate;
+  if (p->split) {
+    const LenetSplitArgs sa{a, p->p2};
+    cudaError_t e = pdl_launch(k_lenet_conv, p->grid, kConvThreads, ConvSmem::total, s, sa);
+    if (e != cudaSuccess) return e;
+    return pdl_launch(k_lenet_fc, p->grid, kFcThreads, FcSmem::total, s, sa);
+  }
   return pdl_launch(k_lenet_fitness, p->grid, kThreads, Smem::total, s, a);
 }
 
