@@ -326,9 +326,11 @@ def main():
             tr = ncu_traffic(f"k_mlp_fitness<{w['hidden']}")
             opb = units * w["D"] * 2 + w["samples"] * w["in_dim"] * 2
         else:
-            kname = "k_lenet_fitness (mma.sync m16n8k16 bf16, weights staged in smem)"
-            tr = ncu_traffic("k_lenet_fitness")
-            opb = units * w["D"] * 2 + w["samples"] * 784 * 2
+            kname = "k_lenet_conv + k_lenet_fc (mma.sync m16n8k16 bf16, weights staged in smem)"
+            tc, tf = ncu_traffic("k_lenet_conv"), ncu_traffic("k_lenet_fc")
+            tr = {"bytes": tc["bytes"] + tf["bytes"], "source": tc["source"]} if tc and tf else None
+            # + the pooled conv2 activations through the HBM scratch (bf16 x 400, written + read)
+            opb = units * w["D"] * 2 + w["samples"] * 784 * 2 + 2 * units * w["samples"] * 800
         roof = {"kernel": kname, "bound": "tensor",
                 "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
                 "frac": achieved / pk["bf16_tflops"], "traffic": tr["bytes"] if tr else None,

@@ -10,25 +10,31 @@
 // implicit GEMMs with N = 6 (conv1) and N = 16 (conv2) output channels: far
 // below tcgen05's 128-row MMA tile, and each candidate's conv2 A operand
 // (pooled conv1 activations) is produced on chip.  They run on the warp-level
-// tensor-core MMA (mma.sync m16n8k16 bf16 -> fp32) instead:
-//   * one CTA = one candidate at a time, its 61,706 weights staged once into
-//     shared memory (bf16, re-laid-out for conflict-free fragment loads);
-//   * conv1: per warp one sample; M = 784 output pixels in pool order: a
-//     16-row tile = 4 pool windows, rows r and r + 8 the two vertically
-//     adjacent pixels of a window, so in the accumulator layout a thread holds
-//     both rows of its window (vertical pool in-thread) and the horizontal
-//     pair is one shuffle; K = 5 rows x 6 taps (kx padded), A fragments read
-//     as 32-bit pairs from the sample's "pair image" (x, x+1), precomputed
-//     once per plan (the dataset never changes) and prefetched with cp.async;
-//   * conv2: M = 100 pixels (same pool order), K = 25 taps x 8 channels
-//     (6 + 2 zero), N = 16; A fragments are 32-bit channel pairs of the
-//     pooled conv1 map; the B fragments (conv2 weights) live in registers;
-//     the pooled output is stored window-major ([window][16 channels]) and
-//     fc1's columns are staged in that order;
-//   * fc1/fc2/fc3 on a batch of 8 samples (one per warp): M = outputs (16-row
-//     tiles over the 8 warps), N = 8 samples, A via ldmatrix from the staged
-//     weights;
-//   * activations between layers are bf16, accumulation fp32, CE in fp32.
+// tensor-core MMA (mma.sync m16n8k16 bf16 -> fp32) in two kernels per
+// evaluation:
+//
+// k_lenet_conv — one sample per warp, 12 warps per SM, no block-wide
+// synchronisation inside a work item (candidate x 128-sample chunk); only the
+// candidate's conv weights are staged (B fragments then live in registers):
+//   * conv1: M = 784 output pixels in pool order: a 16-row tile = 4 pool
+//     windows, rows r and r + 8 the two vertically adjacent pixels of a window,
+//     so in the accumulator layout a thread holds both rows of its window
+//     (vertical pool in-thread) and the horizontal pair is one shuffle;
+//     K = 5 rows x 6 taps (kx padded), A fragments read as 32-bit pairs from the
+//     sample's "pair image" (x, x+1), precomputed once per plan (the dataset
+//     never changes) and prefetched with cp.async;
+//   * conv2: M = 100 pixels (same pool order), K = 25 taps x 8 channels (6 + 2
+//     zero), N = 16, taps ordered so that a fragment's row-(g+8) word equals
+//     its second tap's row-g word (conv2_k): 30 shared-memory loads per tile
+//     feed 26 MMAs;
+//   * the pooled output ([window][16 channels] bf16, 800 B per sample) goes to
+//     a scratch buffer in HBM (at most kScratchBytes; candidates are processed
+//     in groups that fit).
+// k_lenet_fc — one work item = (candidate, 128-sample chunk): fc1 (M = 128
+//   outputs: one 16-row tile per warp, whose A fragments stay in registers for
+//   all the candidate's chunks) x N = 128 samples, fc2 and fc3 with B via
+//   ldmatrix from the chunk's activations, CE per sample, fixed-order sums.
+// Activations between layers are bf16, accumulation fp32, CE in fp32.
 // Output: part[(row * nparts + p) * 2] = sum of CE over sample chunk p (128
 // samples), slot 1 = 0 — the same partial-sum contract as k_mlp_fitness.
 #include <cuda_bf16.h>
@@ -45,17 +51,7 @@ namespace mgfwa_b200 {
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarpsL = kThreads / 32;
 constexpr uint32_t kChunkS = 128;  // samples per work item (one partial)
-#ifndef LENET_C1T
-#define LENET_C1T 8
-#endif
-#ifndef LENET_C2T
-#define LENET_C2T 4
-#endif
-constexpr int kC1T = LENET_C1T;  // conv1 tiles in flight per warp (independent MMA chains)
-constexpr int kC2T = LENET_C2T;  // conv2 tiles in flight per warp (x 2 n-tiles)
 
 // parameter offsets in the candidate row (oracle f_lenet)
 constexpr int oC1W = 0, oC1B = 150, oC2W = 156, oC2B = 2556, oF1W = 2572, oF1B = 50572,
@@ -74,30 +70,6 @@ constexpr int kImgWords = 33 * kImgS;  // 1320 words (16-byte multiple)
 constexpr int kP2S = 408;   // pooled conv2 activations per sample (bf16), [25][16]
 constexpr int kH1S = 136;
 constexpr int kH2S = 104;
-
-struct Smem {
-  static constexpr int wc1 = 0;                          // [8][32] bf16
-  static constexpr int wc2 = wc1 + 8 * kC1K * 2;         // [16][216] bf16
-  static constexpr int wf1 = wc2 + 16 * kC2S * 2;        // [128][408]
-  static constexpr int wf2 = wf1 + 128 * kF1S * 2;       // [96][136]
-  static constexpr int wf3 = wf2 + 96 * kF2S * 2;        // [16][104]
-  static constexpr int bc1 = wf3 + 16 * kF3S * 2;        // f32 [8]
-  static constexpr int bc2 = bc1 + 8 * 4;                // f32 [16]
-  static constexpr int bf1 = bc2 + 16 * 4;               // f32 [128]
-  static constexpr int bf2 = bf1 + 128 * 4;              // f32 [96]
-  static constexpr int bf3 = bf2 + 96 * 4;               // f32 [16]
-  static constexpr int img = bf3 + 16 * 4;               // per warp [33][40] u32
-  static constexpr int p1 = img + kWarpsL * kImgWords * 4;  // per warp [14*14 + 1][4] u32
-  static constexpr int p2 = p1 + kWarpsL * 197 * 4 * 4;  // [8][408] bf16
-  static constexpr int h1 = p2 + 8 * kP2S * 2;           // [8][136] bf16
-  static constexpr int h2 = h1 + 8 * kH1S * 2;           // [8][104] bf16
-  static constexpr int logit = h2 + 8 * kH2S * 2;        // f32 [8][16]
-  static constexpr int total = logit + 8 * 16 * 4;
-};
-static_assert(Smem::total <= 227 * 1024, "LeNet shared memory");
-static_assert(Smem::img % 16 == 0 && Smem::wf1 % 16 == 0 && Smem::wf2 % 16 == 0 &&
-                  Smem::wf3 % 16 == 0,
-              "16-byte aligned cp.async / ldmatrix regions");
 
 struct LenetArgs {
   const uint32_t* pimg;    // [S][1092] pair images of the samples
@@ -154,53 +126,6 @@ __host__ __device__ constexpr int conv1_k(int ky, int kx) {
 __host__ __device__ constexpr int tap_off(int t) { return ((t / 5) * 14 + (t % 5)) * 4; }
 
 
-// Stage one candidate's weights into shared memory (all threads).
-__device__ void stage_weights(uint8_t* sm, const __nv_bfloat16* w) {
-  __nv_bfloat16* wc1 = reinterpret_cast<__nv_bfloat16*>(sm + Smem::wc1);
-  __nv_bfloat16* wc2 = reinterpret_cast<__nv_bfloat16*>(sm + Smem::wc2);
-  __nv_bfloat16* wf1 = reinterpret_cast<__nv_bfloat16*>(sm + Smem::wf1);
-  __nv_bfloat16* wf2 = reinterpret_cast<__nv_bfloat16*>(sm + Smem::wf2);
-  __nv_bfloat16* wf3 = reinterpret_cast<__nv_bfloat16*>(sm + Smem::wf3);
-  float* bc1 = reinterpret_cast<float*>(sm + Smem::bc1);
-  float* bc2 = reinterpret_cast<float*>(sm + Smem::bc2);
-  float* bf1 = reinterpret_cast<float*>(sm + Smem::bf1);
-  float* bf2 = reinterpret_cast<float*>(sm + Smem::bf2);
-  float* bf3 = reinterpret_cast<float*>(sm + Smem::bf3);
-  const int t = threadIdx.x;
-  // conv1 [c][conv1_k(ky, kx)]
-  for (int i = t; i < 150; i += kThreads) {
-    const int c = i / 25, r = i % 25, ky = r / 5, kx = r % 5;
-    wc1[c * kC1K + conv1_k(ky, kx)] = w[oC1W + i];
-  }
-  // conv2 [c][(ky*5+kx)*8 + ci]
-  for (int i = t; i < 2400; i += kThreads) {
-    const int c = i / 150, r = i % 150, ci = r / 25, tap = r % 25;
-    wc2[c * kC2S + tap * 8 + ci] = w[oC2W + i];
-  }
-  // fc1 [j][window * 16 + channel]  <-  f1w[j][channel * 25 + window]
-  for (int i = t; i < 120 * 400; i += kThreads) {
-    const int j = i / 400, k = i % 400, ch = k / 25, win = k % 25;
-    wf1[j * kF1S + win * 16 + ch] = w[oF1W + i];
-  }
-  // fc2 rows (oF2W * 2 = 101384 = 8 mod 16; 120 = 30 x 4)
-  for (int i = t; i < 84 * 30; i += kThreads) {
-    const int j = i / 30, q = i % 30;
-    *reinterpret_cast<uint2*>(wf2 + j * kF2S + q * 4) =
-        *reinterpret_cast<const uint2*>(w + oF2W + j * 120 + q * 4);
-  }
-  // fc3 rows (oF3W * 2 = 121712 = 0 mod 16; 84 = 21 x 4)
-  for (int i = t; i < 10 * 21; i += kThreads) {
-    const int j = i / 21, q = i % 21;
-    *reinterpret_cast<uint2*>(wf3 + j * kF3S + q * 4) =
-        *reinterpret_cast<const uint2*>(w + oF3W + j * 84 + q * 4);
-  }
-  if (t < 6) bc1[t] = bf(w[oC1B + t]);
-  if (t < 16) bc2[t] = bf(w[oC2B + t]);
-  if (t < 120) bf1[t] = bf(w[oF1B + t]);
-  if (t < 84) bf2[t] = bf(w[oF2B + t]);
-  if (t < 10) bf3[t] = bf(w[oF3B + t]);
-}
-
 // Prefetch one sample's pair image into this warp's buffer (cp.async).
 __device__ __forceinline__ void prefetch_img(uint32_t dst, const uint32_t* src, int lane) {
   for (int i = lane; i < kImgWords / 4; i += 32) cp_async16(dst + 16 * i, src + 4 * i);
@@ -227,298 +152,13 @@ __global__ void k_lenet_pairs(const __nv_bfloat16* X, uint32_t S, uint32_t* P) {
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_lenet_fitness(LenetArgs args) {
-  pdl_enter();
-  if (args.gate != nullptr && *args.gate == 0) return;
-  extern __shared__ __align__(16) uint8_t sm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, c = lane & 3;
-  const int wi = g >> 1, dx = g & 1;  // window in the tile, column in the window
-
-  const __nv_bfloat16* wc1 = reinterpret_cast<const __nv_bfloat16*>(sm + Smem::wc1);
-  const __nv_bfloat16* wc2 = reinterpret_cast<const __nv_bfloat16*>(sm + Smem::wc2);
-  const float* bc1 = reinterpret_cast<const float*>(sm + Smem::bc1);
-  const float* bc2 = reinterpret_cast<const float*>(sm + Smem::bc2);
-  const float* bf1 = reinterpret_cast<const float*>(sm + Smem::bf1);
-  const float* bf2 = reinterpret_cast<const float*>(sm + Smem::bf2);
-  const float* bf3 = reinterpret_cast<const float*>(sm + Smem::bf3);
-  const uint32_t* img = reinterpret_cast<const uint32_t*>(sm + Smem::img) + warp * kImgWords;
-  const uint32_t img_s = smem_addr(img);
-  uint32_t* p1 = reinterpret_cast<uint32_t*>(sm + Smem::p1) + warp * 197 * 4;  // +1 zero pixel
-  __nv_bfloat16* p2 = reinterpret_cast<__nv_bfloat16*>(sm + Smem::p2);
-  __nv_bfloat16* h1 = reinterpret_cast<__nv_bfloat16*>(sm + Smem::h1);
-  __nv_bfloat16* h2 = reinterpret_cast<__nv_bfloat16*>(sm + Smem::h2);
-  float* logit = reinterpret_cast<float*>(sm + Smem::logit);
-
-  {  // zero everything once: the staging never writes the padded regions
-    uint32_t* p = reinterpret_cast<uint32_t*>(sm);
-    for (int i = threadIdx.x; i < Smem::total / 4; i += kThreads) p[i] = 0u;
-  }
-  __syncthreads();
-
-  // A-fragment word offsets (k pairs 2c, 2c+1 and +8 of each k16 step)
-  // conv1 pair offsets (conv1_k order): groups 0..2 are (ky = c, kxp = group),
-  // group 3 is (ky = 4, kxp = min(c, 2)); the lane part goes into two base
-  // pointers so the per-group offsets are immediates
-  const uint32_t* imgc = img + c * kImgS;
-  const uint32_t* imgd = img + 4 * kImgS + 2 * (c < 3 ? c : 2);
-
-  const uint64_t total = args.rows * args.nparts;
-  const uint64_t t_begin = total * blockIdx.x / gridDim.x;
-  const uint64_t t_end = total * (blockIdx.x + 1) / gridDim.x;
-  uint64_t staged = ~0ull;
-  uint32_t bw1[2][2];      // conv1 B fragments (k-step, reg)
-  uint32_t bw2[13][2][2];  // conv2 B fragments (k-step, n-tile, reg)
-  float b1a = 0.f, b1b = 0.f, b2a = 0.f, b2b = 0.f, b2c = 0.f, b2d = 0.f;
-
-  for (uint64_t item = t_begin; item < t_end; ++item) {
-    const uint64_t row = item / args.nparts;
-    const uint32_t part = (uint32_t)(item % args.nparts);
-    const uint32_t s_lo = part * kChunkS;
-    const uint32_t s_hi = min(args.S, s_lo + kChunkS);
-    if (row != staged) {
-      __syncthreads();  // previous item's readers are done
-      stage_weights(sm, args.W + row * args.Dp);
-      __syncthreads();
-      staged = row;
-#pragma unroll
-      for (int st = 0; st < 2; ++st) {
-        const __nv_bfloat16* b = wc1 + g * kC1K + 16 * st + 2 * c;
-        bw1[st][0] = *reinterpret_cast<const uint32_t*>(b);
-        bw1[st][1] = *reinterpret_cast<const uint32_t*>(b + 8);
-      }
-#pragma unroll
-      for (int st = 0; st < 13; ++st)
-#pragma unroll
-        for (int n = 0; n < 2; ++n) {
-          const __nv_bfloat16* b = wc2 + (8 * n + g) * kC2S + 16 * st + 2 * c;
-          bw2[st][n][0] = *reinterpret_cast<const uint32_t*>(b);
-          bw2[st][n][1] = *reinterpret_cast<const uint32_t*>(b + 8);
-        }
-      b1a = bc1[2 * c];
-      b1b = bc1[2 * c + 1];
-      b2a = bc2[2 * c];
-      b2b = bc2[2 * c + 1];
-      b2c = bc2[8 + 2 * c];
-      b2d = bc2[9 + 2 * c];
-    }
-    if (s_lo + warp < s_hi) prefetch_img(img_s, args.pimg + (uint64_t)(s_lo + warp) * kImgWords, lane);
-    float loss = 0.0f;  // lanes 0..7 of warp 0: CE of their batch slot
-
-    for (uint32_t sb = s_lo; sb < s_hi; sb += kWarpsL) {
-      const uint32_t s = sb + warp;
-      if (s < s_hi) {
-        cp_async_wait_all();
-        __syncwarp();
-        // ------------------------------------------------ conv1 (this warp)
-        // 49 tiles of 4 windows (window 4t + wi of the 14 x 14 pooled map),
-        // kC1T tiles per step so that kC1T independent MMA chains are in flight
-        for (int t0 = 0; t0 < 49; t0 += kC1T) {
-          int wpos[kC1T];
-          float d[kC1T][4];
-#pragma unroll
-          for (int u = 0; u < kC1T; ++u) {
-            const int w = 4 * (t0 + u) + wi;
-            wpos[u] = w < 196 ? w : -1;
-            const int wc = w < 196 ? w : 0;
-            const int py = wc / 14, px = wc - 14 * py;
-            const int base0 = (2 * py) * kImgS + 2 * px + dx, base1 = base0 + kImgS;
-            d[u][0] = b1a, d[u][1] = b1b, d[u][2] = b1a, d[u][3] = b1b;
-            mma_bf16(d[u], imgc[base0], imgc[base1], imgc[base0 + 2], imgc[base1 + 2], bw1[0][0], bw1[0][1]);
-            mma_bf16(d[u], imgc[base0 + 4], imgc[base1 + 4], imgd[base0], imgd[base1], bw1[1][0], bw1[1][1]);
-          }
-#pragma unroll
-          for (int u = 0; u < kC1T; ++u) {
-            // ReLU, vertical pair in-thread (rows g, g+8), horizontal pair = lane ^ 4
-            float s0 = fmaxf(d[u][0], 0.f) + fmaxf(d[u][2], 0.f);
-            float s1 = fmaxf(d[u][1], 0.f) + fmaxf(d[u][3], 0.f);
-            s0 += __shfl_xor_sync(0xffffffffu, s0, 4);
-            s1 += __shfl_xor_sync(0xffffffffu, s1, 4);
-            if (dx == 0 && wpos[u] >= 0) p1[wpos[u] * 4 + c] = pack_bf16(0.25f * s0, 0.25f * s1);
-          }
-        }
-        __syncwarp();
-        // the pair image is consumed: prefetch this warp's next sample
-        if (s + kWarpsL < s_hi) prefetch_img(img_s, args.pimg + (uint64_t)(s + kWarpsL) * kImgWords, lane);
-        // ---------------------------------------------- conv2 (this warp)
-        // p1 word layout [py*14 + px][cpair]; A k = tap * 8 + ci
-        // A-fragment k = tap * 8 + ci: the lane's channel pair c is folded into
-        // the base pointer, the tap offsets are compile-time immediates
-        const uint32_t* p1c = p1 + c;
-        __nv_bfloat16* o = p2 + warp * kP2S;
-        // 7 tiles of 4 windows (window 4t + wi of the 5 x 5 pooled map), two
-        // tiles per step: 2 kC2T independent MMA chains (kC2T tiles x 2 n-tiles)
-        for (int t0 = 0; t0 < 7; t0 += kC2T) {
-          int wv[kC2T], b0[kC2T], b1[kC2T];
-          float d[kC2T][2][4];
-#pragma unroll
-          for (int u = 0; u < kC2T; ++u) {
-            const int w = 4 * (t0 + u) + wi;
-            wv[u] = w < 25 ? w : -1;
-            const int wc = w < 25 ? w : 0;
-            const int qy = wc / 5, qx = wc - 5 * qy;
-            b0[u] = ((2 * qy) * 14 + 2 * qx + dx) * 4;
-            b1[u] = b0[u] + 14 * 4;
-            d[u][0][0] = b2a, d[u][0][1] = b2b, d[u][0][2] = b2a, d[u][0][3] = b2b;
-            d[u][1][0] = b2c, d[u][1][1] = b2d, d[u][1][2] = b2c, d[u][1][3] = b2d;
-          }
-#pragma unroll
-          for (int st = 0; st < 13; ++st) {
-#pragma unroll
-            for (int u = 0; u < kC2T; ++u) {
-              const uint32_t a0 = p1c[b0[u] + tap_off(2 * st)];
-              const uint32_t a1 = p1c[b1[u] + tap_off(2 * st)];
-              const uint32_t a2 = st < 12 ? p1c[b0[u] + tap_off(2 * st + 1)] : 0u;  // tap 25: K padding
-              const uint32_t a3 = st < 12 ? p1c[b1[u] + tap_off(2 * st + 1)] : 0u;
-              mma_bf16(d[u][0], a0, a1, a2, a3, bw2[st][0][0], bw2[st][0][1]);
-              mma_bf16(d[u][1], a0, a1, a2, a3, bw2[st][1][0], bw2[st][1][1]);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < kC2T; ++u) {
-            float s0 = fmaxf(d[u][0][0], 0.f) + fmaxf(d[u][0][2], 0.f);
-            float s1 = fmaxf(d[u][0][1], 0.f) + fmaxf(d[u][0][3], 0.f);
-            float s2 = fmaxf(d[u][1][0], 0.f) + fmaxf(d[u][1][2], 0.f);
-            float s3 = fmaxf(d[u][1][1], 0.f) + fmaxf(d[u][1][3], 0.f);
-            s0 += __shfl_xor_sync(0xffffffffu, s0, 4);
-            s1 += __shfl_xor_sync(0xffffffffu, s1, 4);
-            s2 += __shfl_xor_sync(0xffffffffu, s2, 4);
-            s3 += __shfl_xor_sync(0xffffffffu, s3, 4);
-            if (dx == 0 && wv[u] >= 0) {
-              uint32_t* ow = reinterpret_cast<uint32_t*>(o + wv[u] * 16);
-              ow[c] = pack_bf16(0.25f * s0, 0.25f * s1);
-              ow[4 + c] = pack_bf16(0.25f * s2, 0.25f * s3);
-            }
-          }
-        }
-      } else {
-        // no sample in this batch slot: a zero activation row (finite)
-        for (int i = lane; i < 400; i += 32) p2[warp * kP2S + i] = __float2bfloat16(0.0f);
-      }
-      __syncthreads();
-      // ------------------------------------------------ fc1: 128 x 400 . 400 x 8
-      {
-        const int mt = warp;  // 16-row tile of the 128 (120) outputs
-        float d[4] = {0.f, 0.f, 0.f, 0.f}, e[4] = {0.f, 0.f, 0.f, 0.f};
-        const uint32_t a_base =
-            smem_addr(sm + Smem::wf1) +
-            (uint32_t)(((16 * mt + (lane & 7) + ((lane >> 3) & 1) * 8) * kF1S + (lane >> 4) * 8) * 2);
-        const __nv_bfloat16* bb = p2 + g * kP2S + 2 * c;
-#pragma unroll 4
-        for (int st = 0; st < 24; st += 2) {  // two independent accumulator chains
-          uint32_t a[4], a2[4];
-          ldmatrix_x4(a, a_base + st * 32);
-          ldmatrix_x4(a2, a_base + st * 32 + 32);
-          mma_bf16(d, a[0], a[1], a[2], a[3], *reinterpret_cast<const uint32_t*>(bb + 16 * st),
-                   *reinterpret_cast<const uint32_t*>(bb + 16 * st + 8));
-          mma_bf16(e, a2[0], a2[1], a2[2], a2[3], *reinterpret_cast<const uint32_t*>(bb + 16 * st + 16),
-                   *reinterpret_cast<const uint32_t*>(bb + 16 * st + 24));
-        }
-        {
-          uint32_t a[4];
-          ldmatrix_x4(a, a_base + 24 * 32);
-          mma_bf16(d, a[0], a[1], a[2], a[3], *reinterpret_cast<const uint32_t*>(bb + 16 * 24),
-                   *reinterpret_cast<const uint32_t*>(bb + 16 * 24 + 8));
-        }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) d[i] += e[i];
-        // rows (outputs) 16mt + g (+8), cols (samples) 2c, 2c+1
-        const int j0 = 16 * mt + g, j1 = j0 + 8;
-        const float c0 = j0 < 120 ? bf1[j0] : 0.f, c1 = j1 < 120 ? bf1[j1] : 0.f;
-        h1[(2 * c) * kH1S + j0] = __float2bfloat16(j0 < 120 ? fmaxf(d[0] + c0, 0.f) : 0.f);
-        h1[(2 * c + 1) * kH1S + j0] = __float2bfloat16(j0 < 120 ? fmaxf(d[1] + c0, 0.f) : 0.f);
-        h1[(2 * c) * kH1S + j1] = __float2bfloat16(j1 < 120 ? fmaxf(d[2] + c1, 0.f) : 0.f);
-        h1[(2 * c + 1) * kH1S + j1] = __float2bfloat16(j1 < 120 ? fmaxf(d[3] + c1, 0.f) : 0.f);
-      }
-      __syncthreads();
-      // ------------------------------------------------ fc2: 96 x 128 . 128 x 8
-      if (warp < 6) {
-        const int mt = warp;
-        float d[4] = {0.f, 0.f, 0.f, 0.f};
-        const uint32_t a_base =
-            smem_addr(sm + Smem::wf2) +
-            (uint32_t)(((16 * mt + (lane & 7) + ((lane >> 3) & 1) * 8) * kF2S + (lane >> 4) * 8) * 2);
-        const __nv_bfloat16* bb = h1 + g * kH1S + 2 * c;
-#pragma unroll
-        for (int st = 0; st < 8; ++st) {
-          uint32_t a[4];
-          ldmatrix_x4(a, a_base + st * 32);
-          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(bb + 16 * st);
-          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(bb + 16 * st + 8);
-          mma_bf16(d, a[0], a[1], a[2], a[3], b0, b1);
-        }
-        const int j0 = 16 * mt + g, j1 = j0 + 8;
-        const float c0 = j0 < 84 ? bf2[j0] : 0.f, c1 = j1 < 84 ? bf2[j1] : 0.f;
-        h2[(2 * c) * kH2S + j0] = __float2bfloat16(j0 < 84 ? fmaxf(d[0] + c0, 0.f) : 0.f);
-        h2[(2 * c + 1) * kH2S + j0] = __float2bfloat16(j0 < 84 ? fmaxf(d[1] + c0, 0.f) : 0.f);
-        h2[(2 * c) * kH2S + j1] = __float2bfloat16(j1 < 84 ? fmaxf(d[2] + c1, 0.f) : 0.f);
-        h2[(2 * c + 1) * kH2S + j1] = __float2bfloat16(j1 < 84 ? fmaxf(d[3] + c1, 0.f) : 0.f);
-      }
-      __syncthreads();
-      // ------------------------------------- fc3 (16 x 96 . 96 x 8) + CE
-      if (warp == kWarpsL - 1) {  // the warp with no fc2 tile
-        float d[4] = {0.f, 0.f, 0.f, 0.f};
-        const uint32_t a_base =
-            smem_addr(sm + Smem::wf3) +
-            (uint32_t)((((lane & 7) + ((lane >> 3) & 1) * 8) * kF3S + (lane >> 4) * 8) * 2);
-        const __nv_bfloat16* bb = h2 + g * kH2S + 2 * c;
-#pragma unroll
-        for (int st = 0; st < 6; ++st) {
-          uint32_t a[4];
-          ldmatrix_x4(a, a_base + st * 32);
-          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(bb + 16 * st);
-          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(bb + 16 * st + 8);
-          mma_bf16(d, a[0], a[1], a[2], a[3], b0, b1);
-        }
-        // logits[sample][class]: rows = classes g (+8), cols = samples 2c, 2c+1
-        logit[(2 * c) * 16 + g] = d[0] + bf3[g];
-        logit[(2 * c + 1) * 16 + g] = d[1] + bf3[g];
-        if (g < 2) {
-          logit[(2 * c) * 16 + g + 8] = d[2] + bf3[g + 8];
-          logit[(2 * c + 1) * 16 + g + 8] = d[3] + bf3[g + 8];
-        }
-        __syncwarp();
-        if (lane < 8 && sb + lane < s_hi) {
-          const float* z = logit + lane * 16;
-          float m = z[0];
-#pragma unroll
-          for (int o = 1; o < 10; ++o) m = fmaxf(m, z[o]);
-          float se = 0.f;
-#pragma unroll
-          for (int o = 0; o < 10; ++o) se += expf(z[o] - m);
-          loss += (m + logf(se)) - z[args.y[sb + lane]];
-        }
-        __syncwarp();
-      }
-    }
-    if (warp == kWarpsL - 1) {
-      // fixed-order sum of the 8 batch slots
-      float t = loss;
-      t += __shfl_xor_sync(0xffffffffu, t, 1);
-      t += __shfl_xor_sync(0xffffffffu, t, 2);
-      t += __shfl_xor_sync(0xffffffffu, t, 4);
-      if (lane == 0) {
-        args.part[(row * args.nparts + part) * 2] = t;
-        args.part[(row * args.nparts + part) * 2 + 1] = 0.0f;
-      }
-    }
-  }
-}
-
-// ------------------------------------------------------------ split path
-// Two kernels instead of one: k_lenet_conv (conv1 + conv2 of every sample,
-// one sample per warp, no block-wide synchronisation, only the conv weights
-// staged, 12 warps per SM) writes the pooled conv2 activations (window-major
-// bf16 [400]) to a per-plan scratch; k_lenet_fc (fc1/fc2/fc3 + CE on batches
-// of 16 samples, fc weights staged) reads them back.  Same arithmetic as the
-// fused kernel except the loss summation order (16 batch slots).
 namespace {
 
 #ifndef LENET_CV_WARPS
 #define LENET_CV_WARPS 12
 #endif
 #ifndef LENET_CV_C1T
-#define LENET_CV_C1T 4
+#define LENET_CV_C1T 7
 #endif
 #ifndef LENET_CV_C2T
 #define LENET_CV_C2T 2
@@ -528,6 +168,7 @@ constexpr int kCvC1T = LENET_CV_C1T;  // conv1 tiles in flight per warp
 constexpr int kCvC2T = LENET_CV_C2T;  // conv2 tiles in flight per warp (x 2 n-tiles)
 constexpr int kConvThreads = kConvWarps * 32;
 constexpr int kP2Row = 400;  // bf16 per sample in the scratch
+constexpr uint64_t kScratchBytes = 2ull << 30;  // activation scratch cap (C3: 1.23 GB)
 
 struct ConvSmem {
   static constexpr int wc1 = 0;                                // [8][32] bf16
@@ -566,6 +207,115 @@ struct LenetSplitArgs {
 };
 
 }  // namespace
+
+// conv1 on tiles t0 .. t0 + N - 1 (4 pool windows each) of one sample:
+// ReLU + 2x2 average pool -> p1[window][channel pair] (bf16 pairs).
+template <int N>
+__device__ __forceinline__ void conv1_tiles(int t0, const uint32_t* imgc, const uint32_t* imgd, uint32_t* p1,
+                                            int wi, int dx, int c, const uint32_t (&bw1)[2][2], float b1a,
+                                            float b1b) {
+  int wpos[N];
+  float d[N][4];
+#pragma unroll
+  for (int u = 0; u < N; ++u) {
+    const int w = 4 * (t0 + u) + wi;  // < 196 for every tile t < 49
+    wpos[u] = w;
+    const int py = w / 14, px = w - 14 * py;
+    const int base0 = (2 * py) * kImgS + 2 * px + dx, base1 = base0 + kImgS;
+    d[u][0] = b1a, d[u][1] = b1b, d[u][2] = b1a, d[u][3] = b1b;
+    mma_bf16(d[u], imgc[base0], imgc[base1], imgc[base0 + 2], imgc[base1 + 2], bw1[0][0], bw1[0][1]);
+    mma_bf16(d[u], imgc[base0 + 4], imgc[base1 + 4], imgd[base0], imgd[base1], bw1[1][0], bw1[1][1]);
+  }
+#pragma unroll
+  for (int u = 0; u < N; ++u) {
+    // ReLU, vertical pair in-thread (rows g, g+8), horizontal pair = lane ^ 4
+    float s0 = fmaxf(d[u][0], 0.f) + fmaxf(d[u][2], 0.f);
+    float s1 = fmaxf(d[u][1], 0.f) + fmaxf(d[u][3], 0.f);
+    s0 += __shfl_xor_sync(0xffffffffu, s0, 4);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, 4);
+    if (dx == 0) p1[wpos[u] * 4 + c] = pack_bf16(0.25f * s0, 0.25f * s1);
+  }
+}
+
+// conv2 K order for the column-reuse scheme (k_lenet_conv): k-step st holds
+// two taps A (k 0-7) and B (k 8-15), 8 channels each (6 + 2 zero).
+//   st = 2 kx + h (kx < 5, h < 2): A = (2h, kx), B = (2h + 1, kx)
+//   st = 10 + j (j < 3):           A = (4, 2j), B = (4, 2j + 1)   [(4, 5) = zero padding]
+// In the MMA fragment a lane's rows g and g + 8 are vertically adjacent
+// pixels, so a1 (row g + 8, tap A) is the same word as a2 (row g, tap B =
+// tap A one row down): per pool tile and kernel column the lane loads the 6
+// words of rows 0..5 once and feeds 2-3 MMAs from them — 30 shared-memory
+// loads per tile instead of 52.
+__host__ __device__ constexpr int conv2_k(int ky, int kx) {
+  return ky < 4 ? 16 * (2 * kx + (ky >> 1)) + 8 * (ky & 1) : 16 * (10 + (kx >> 1)) + 8 * (kx & 1);
+}
+
+template <int N>
+__device__ __forceinline__ void conv2_tiles(int t0, const uint32_t* p1c, __nv_bfloat16* o, int wi, int dx,
+                                            int c, const uint32_t (&bw2)[13][2][2], float b2a, float b2b,
+                                            float b2c, float b2d) {
+  int wv[N];
+  const uint32_t* q[N];
+  float d[N][2][4];
+#pragma unroll
+  for (int u = 0; u < N; ++u) {
+    const int w = 4 * (t0 + u) + wi;
+    wv[u] = w < 25 ? w : -1;
+    const int wc = w < 25 ? w : 0;
+    const int qy = wc / 5, qx = wc - 5 * qy;
+    q[u] = p1c + ((2 * qy) * 14 + 2 * qx + dx) * 4;
+    d[u][0][0] = b2a, d[u][0][1] = b2b, d[u][0][2] = b2a, d[u][0][3] = b2b;
+    d[u][1][0] = b2c, d[u][1][1] = b2d, d[u][1][2] = b2c, d[u][1][3] = b2d;
+  }
+  uint32_t r4p[N], r5p[N];
+#pragma unroll
+  for (int kx = 0; kx < 5; ++kx) {
+    uint32_t r[N][6];
+#pragma unroll
+    for (int u = 0; u < N; ++u)
+#pragma unroll
+      for (int j = 0; j < 6; ++j) r[u][j] = q[u][(j * 14 + kx) * 4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int u = 0; u < N; ++u)
+#pragma unroll
+        for (int n = 0; n < 2; ++n)
+          mma_bf16(d[u][n], r[u][2 * h], r[u][2 * h + 1], r[u][2 * h + 1], r[u][2 * h + 2],
+                   bw2[2 * kx + h][n][0], bw2[2 * kx + h][n][1]);
+    if (kx & 1) {
+#pragma unroll
+      for (int u = 0; u < N; ++u)
+#pragma unroll
+        for (int n = 0; n < 2; ++n)
+          mma_bf16(d[u][n], r4p[u], r5p[u], r[u][4], r[u][5], bw2[10 + kx / 2][n][0], bw2[10 + kx / 2][n][1]);
+    } else if (kx == 4) {
+#pragma unroll
+      for (int u = 0; u < N; ++u)
+#pragma unroll
+        for (int n = 0; n < 2; ++n)
+          mma_bf16(d[u][n], r[u][4], r[u][5], 0u, 0u, bw2[12][n][0], bw2[12][n][1]);
+    }
+#pragma unroll
+    for (int u = 0; u < N; ++u) r4p[u] = r[u][4], r5p[u] = r[u][5];
+  }
+#pragma unroll
+  for (int u = 0; u < N; ++u) {
+    float s0 = fmaxf(d[u][0][0], 0.f) + fmaxf(d[u][0][2], 0.f);
+    float s1 = fmaxf(d[u][0][1], 0.f) + fmaxf(d[u][0][3], 0.f);
+    float s2 = fmaxf(d[u][1][0], 0.f) + fmaxf(d[u][1][2], 0.f);
+    float s3 = fmaxf(d[u][1][1], 0.f) + fmaxf(d[u][1][3], 0.f);
+    s0 += __shfl_xor_sync(0xffffffffu, s0, 4);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, 4);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, 4);
+    s3 += __shfl_xor_sync(0xffffffffu, s3, 4);
+    if (dx == 0 && wv[u] >= 0) {
+      uint32_t* ow = reinterpret_cast<uint32_t*>(o + wv[u] * 16);
+      ow[c] = pack_bf16(0.25f * s0, 0.25f * s1);
+      ow[4 + c] = pack_bf16(0.25f * s2, 0.25f * s3);
+    }
+  }
+}
 
 __global__ void __launch_bounds__(kConvThreads, 1) k_lenet_conv(LenetSplitArgs sa) {
   pdl_enter();
@@ -611,7 +361,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) k_lenet_conv(LenetSplitArgs s
       }
       for (int i = threadIdx.x; i < 2400; i += kConvThreads) {
         const int ch = i / 150, r = i % 150, ci = r / 25, tap = r % 25;
-        wc2[ch * kC2S + tap * 8 + ci] = w[oC2W + i];
+        wc2[ch * kC2S + conv2_k(tap / 5, tap % 5) + ci] = w[oC2W + i];
       }
       if (threadIdx.x < 6) bc1[threadIdx.x] = bf(w[oC1B + threadIdx.x]);
       if (threadIdx.x < 16) bc2[threadIdx.x] = bf(w[oC2B + threadIdx.x]);
@@ -638,77 +388,19 @@ __global__ void __launch_bounds__(kConvThreads, 1) k_lenet_conv(LenetSplitArgs s
     for (uint32_t s = s_lo + warp; s < s_hi; s += kConvWarps) {
       cp_async_wait_all();
       __syncwarp();
-      // ---- conv1 + ReLU + pool -> p1 (as k_lenet_fitness)
-      for (int t0 = 0; t0 < 49; t0 += kCvC1T) {
-        int wpos[kCvC1T];
-        float d[kCvC1T][4];
-#pragma unroll
-        for (int u = 0; u < kCvC1T; ++u) {
-          const int w = 4 * (t0 + u) + wi;
-          wpos[u] = w < 196 ? w : -1;
-          const int wc = w < 196 ? w : 0;
-          const int py = wc / 14, px = wc - 14 * py;
-          const int base0 = (2 * py) * kImgS + 2 * px + dx, base1 = base0 + kImgS;
-          d[u][0] = b1a, d[u][1] = b1b, d[u][2] = b1a, d[u][3] = b1b;
-          mma_bf16(d[u], imgc[base0], imgc[base1], imgc[base0 + 2], imgc[base1 + 2], bw1[0][0], bw1[0][1]);
-          mma_bf16(d[u], imgc[base0 + 4], imgc[base1 + 4], imgd[base0], imgd[base1], bw1[1][0], bw1[1][1]);
-        }
-#pragma unroll
-        for (int u = 0; u < kCvC1T; ++u) {
-          float s0 = fmaxf(d[u][0], 0.f) + fmaxf(d[u][2], 0.f);
-          float s1 = fmaxf(d[u][1], 0.f) + fmaxf(d[u][3], 0.f);
-          s0 += __shfl_xor_sync(0xffffffffu, s0, 4);
-          s1 += __shfl_xor_sync(0xffffffffu, s1, 4);
-          if (dx == 0 && wpos[u] >= 0) p1[wpos[u] * 4 + c] = pack_bf16(0.25f * s0, 0.25f * s1);
-        }
-      }
+      // ---- conv1 + ReLU + pool -> p1: 49 tiles
+#pragma unroll 1
+      for (int t0 = 0; t0 + kCvC1T <= 49; t0 += kCvC1T)
+        conv1_tiles<kCvC1T>(t0, imgc, imgd, p1, wi, dx, c, bw1, b1a, b1b);
+      if constexpr (49 % kCvC1T != 0) conv1_tiles<49 % kCvC1T>(49 - 49 % kCvC1T, imgc, imgd, p1, wi, dx, c, bw1, b1a, b1b);
       __syncwarp();
       if (s + kConvWarps < s_hi)
         prefetch_img(img_s, args.pimg + (uint64_t)(s + kConvWarps) * kImgWords, lane);
-      // ---- conv2 + ReLU + pool -> o (window-major [25][16])
-      for (int t0 = 0; t0 < 7; t0 += kCvC2T) {
-        int wv[kCvC2T], b0[kCvC2T], b1[kCvC2T];
-        float d[kCvC2T][2][4];
-#pragma unroll
-        for (int u = 0; u < kCvC2T; ++u) {
-          const int w = 4 * (t0 + u) + wi;
-          wv[u] = w < 25 ? w : -1;
-          const int wc = w < 25 ? w : 0;
-          const int qy = wc / 5, qx = wc - 5 * qy;
-          b0[u] = ((2 * qy) * 14 + 2 * qx + dx) * 4;
-          b1[u] = b0[u] + 14 * 4;
-          d[u][0][0] = b2a, d[u][0][1] = b2b, d[u][0][2] = b2a, d[u][0][3] = b2b;
-          d[u][1][0] = b2c, d[u][1][1] = b2d, d[u][1][2] = b2c, d[u][1][3] = b2d;
-        }
-#pragma unroll
-        for (int st = 0; st < 13; ++st) {
-#pragma unroll
-          for (int u = 0; u < kCvC2T; ++u) {
-            const uint32_t a0 = p1c[b0[u] + tap_off(2 * st)];
-            const uint32_t a1 = p1c[b1[u] + tap_off(2 * st)];
-            const uint32_t a2 = st < 12 ? p1c[b0[u] + tap_off(2 * st + 1)] : 0u;
-            const uint32_t a3 = st < 12 ? p1c[b1[u] + tap_off(2 * st + 1)] : 0u;
-            mma_bf16(d[u][0], a0, a1, a2, a3, bw2[st][0][0], bw2[st][0][1]);
-            mma_bf16(d[u][1], a0, a1, a2, a3, bw2[st][1][0], bw2[st][1][1]);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < kCvC2T; ++u) {
-          float s0 = fmaxf(d[u][0][0], 0.f) + fmaxf(d[u][0][2], 0.f);
-          float s1 = fmaxf(d[u][0][1], 0.f) + fmaxf(d[u][0][3], 0.f);
-          float s2 = fmaxf(d[u][1][0], 0.f) + fmaxf(d[u][1][2], 0.f);
-          float s3 = fmaxf(d[u][1][1], 0.f) + fmaxf(d[u][1][3], 0.f);
-          s0 += __shfl_xor_sync(0xffffffffu, s0, 4);
-          s1 += __shfl_xor_sync(0xffffffffu, s1, 4);
-          s2 += __shfl_xor_sync(0xffffffffu, s2, 4);
-          s3 += __shfl_xor_sync(0xffffffffu, s3, 4);
-          if (dx == 0 && wv[u] >= 0) {
-            uint32_t* ow = reinterpret_cast<uint32_t*>(o + wv[u] * 16);
-            ow[c] = pack_bf16(0.25f * s0, 0.25f * s1);
-            ow[4 + c] = pack_bf16(0.25f * s2, 0.25f * s3);
-          }
-        }
-      }
+      // ---- conv2 + ReLU + pool -> o (window-major [25][16]): 7 tiles
+#pragma unroll 1
+      for (int t0 = 0; t0 + kCvC2T <= 7; t0 += kCvC2T)
+        conv2_tiles<kCvC2T>(t0, p1c, o, wi, dx, c, bw2, b2a, b2b, b2c, b2d);
+      if constexpr (7 % kCvC2T != 0) conv2_tiles<7 % kCvC2T>(7 - 7 % kCvC2T, p1c, o, wi, dx, c, bw2, b2a, b2b, b2c, b2d);
       __syncwarp();
       // ---- p2 row -> scratch (800 B, coalesced 16-byte stores)
       uint4* dst = reinterpret_cast<uint4*>(sa.p2 + (row * args.S + s) * (uint64_t)kP2Row);
@@ -917,24 +609,12 @@ __global__ void __launch_bounds__(kFcThreads, 1) k_lenet_fc(LenetSplitArgs sa) {
   }
 }
 
-#ifndef LENET_SPLIT_DEFAULT
-#define LENET_SPLIT_DEFAULT 1
-#endif
-static bool lenet_split() {  // MGFWA_LENET_SPLIT=0|1 (default LENET_SPLIT_DEFAULT)
-  static const bool on = [] {
-    const char* e = getenv("MGFWA_LENET_SPLIT");
-    if (e && (e[0] == '0' || e[0] == '1')) return e[0] == '1';
-    return LENET_SPLIT_DEFAULT != 0;
-  }();
-  return on;
-}
-
 struct LenetPlan {
   LenetArgs args;
-  unsigned grid;
-  uint32_t* pimg;      // owned
-  __nv_bfloat16* p2;   // owned scratch (split path)
-  bool split;
+  unsigned grid_conv, grid_fc;
+  uint64_t group_rows;  // candidates per conv/fc launch pair (bounds the scratch)
+  uint32_t* pimg;       // owned
+  __nv_bfloat16* p2;    // owned scratch [group_rows][S][400]
 };
 
 uint32_t lenet_num_parts(uint32_t S) { return (S + kChunkS - 1) / kChunkS; }
@@ -951,9 +631,7 @@ LenetPlan* lenet_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t 
     snprintf(err, errlen, "LeNet objective: bad row stride");
     return nullptr;
   }
-  if (cudaFuncSetAttribute(k_lenet_fitness, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           Smem::total) != cudaSuccess ||
-      cudaFuncSetAttribute(k_lenet_conv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(k_lenet_conv, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            ConvSmem::total) != cudaSuccess ||
       cudaFuncSetAttribute(k_lenet_fc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            FcSmem::total) != cudaSuccess) {
@@ -975,8 +653,12 @@ LenetPlan* lenet_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t 
     delete p;
     return nullptr;
   }
-  p->split = lenet_split();
-  if (p->split && cudaMalloc(&p->p2, (size_t)rows * S * kP2Row * 2) != cudaSuccess) {
+  // scratch of at most kScratchBytes (at least one candidate's activations)
+  const uint64_t per_row = (uint64_t)S * kP2Row * 2;
+  p->group_rows = kScratchBytes / per_row;
+  if (p->group_rows < 1) p->group_rows = 1;
+  if (p->group_rows > rows) p->group_rows = rows;
+  if (cudaMalloc(&p->p2, p->group_rows * per_row) != cudaSuccess) {
     snprintf(err, errlen, "LeNet objective: cudaMalloc of the activation scratch failed");
     cudaFree(p->pimg);
     delete p;
@@ -989,8 +671,8 @@ LenetPlan* lenet_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t 
   p->args.Dp = Dp;
   p->args.S = S;
   p->args.nparts = lenet_num_parts(S);
-  const uint64_t items = rows * p->args.nparts;
-  p->grid = (unsigned)(items < (uint64_t)nsm ? items : (uint64_t)nsm);
+  const uint64_t items = p->group_rows * p->args.nparts;
+  p->grid_conv = p->grid_fc = (unsigned)(items < (uint64_t)nsm ? items : (uint64_t)nsm);
   return p;
 }
 
@@ -1003,16 +685,20 @@ void lenet_plan_destroy(LenetPlan* p) {
 
 cudaError_t lenet_fitness_launch(const LenetPlan* p, float* part, const int* gate,
                                  cudaStream_t s) {
-  LenetArgs a = p->args;
-  a.part = part;
-  a.gate = gate;
-  if (p->split) {
-    const LenetSplitArgs sa{a, p->p2};
-    cudaError_t e = pdl_launch(k_lenet_conv, p->grid, kConvThreads, ConvSmem::total, s, sa);
+  for (uint64_t r0 = 0; r0 < p->args.rows; r0 += p->group_rows) {
+    LenetSplitArgs sa{p->args, p->p2};
+    sa.base.W += r0 * p->args.Dp;
+    sa.base.rows = p->args.rows - r0 < p->group_rows ? p->args.rows - r0 : p->group_rows;
+    sa.base.part = part + r0 * p->args.nparts * 2;
+    sa.base.gate = gate;
+    const uint64_t items = sa.base.rows * sa.base.nparts;
+    const unsigned gc = (unsigned)(items < p->grid_conv ? items : p->grid_conv);
+    cudaError_t e = pdl_launch(k_lenet_conv, gc, kConvThreads, ConvSmem::total, s, sa);
     if (e != cudaSuccess) return e;
-    return pdl_launch(k_lenet_fc, p->grid, kFcThreads, FcSmem::total, s, sa);
+    e = pdl_launch(k_lenet_fc, gc, kFcThreads, FcSmem::total, s, sa);
+    if (e != cudaSuccess) return e;
   }
-  return pdl_launch(k_lenet_fitness, p->grid, kThreads, Smem::total, s, a);
+  return cudaSuccess;
 }
 
 }  // namespace mgfwa_b200

@@ -23,5 +23,6 @@ cap mlp_fitness k_mlp_fitness 7 c2
 cap explode_map k_explode_map 2 c2
 cap guides k_guides 2 c2
 cap rank k_rank 2 c2
-cap lenet_fitness k_lenet_fitness 7 c3
+cap lenet_conv k_lenet_conv 7 c3
+cap lenet_fc k_lenet_fc 7 c3
 echo done
