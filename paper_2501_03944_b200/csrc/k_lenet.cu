@@ -65,8 +65,10 @@ constexpr int kC2S = 216;   // conv2 weight row stride (bf16), K = 25 taps x 8 +
 constexpr int kF1S = 408;   // fc1 row stride (bf16), 128 rows, K = 400 (window-major)
 constexpr int kF2S = 136;   // fc2: 96 rows, K = 128 (120 + pad)
 constexpr int kF3S = 104;   // fc3: 16 rows, K = 96 (84 + pad)
-constexpr int kImgS = 40;   // pair-image row stride (32-bit words; = 8 mod 32), 33 rows
-constexpr int kImgWords = 33 * kImgS;  // 1320 words (16-byte multiple)
+constexpr int kImgS = 36;   // pair-image row stride (32-bit words; = 4 mod 32), 33 rows
+constexpr int kImgWords = 33 * kImgS;  // 1188 words (16-byte multiple)
+constexpr int kP1R = 17;    // pooled conv1 map row stride (pixels; = 1 mod 4), 14 rows x 4 words
+constexpr int kP1Words = 14 * kP1R * 4;
 constexpr int kP2S = 408;   // pooled conv2 activations per sample (bf16), [25][16]
 constexpr int kH1S = 136;
 constexpr int kH2S = 104;
@@ -116,14 +118,12 @@ __device__ __forceinline__ float bf(const __nv_bfloat16 x) { return __bfloat162f
 // conv1 K order.  Pair q = 8 st + 4 h + c (the A-fragment k pair 2c[+8] of
 // k16-step st held by lane quad c) covers taps (ky, 2 kxp) and (ky, 2 kxp + 1):
 // q < 12: ky = c, kxp = q / 4; q = 12..14: ky = 4, kxp = c; q = 15: padding.
-// With the pair image's row stride = 8 mod 32 the four lane quads of one
-// A-fragment load hit banks 8 ky apart, and the 8 pixels of a tile row are
-// consecutive words: the loads are conflict-free.
+// A conv1 tile is a 2 x 2 block of pool windows; with the pair image's row
+// stride = 4 mod 32 the 32 words of every A-fragment load fall in distinct
+// banks (checked exhaustively over the 49 tiles and 8 loads).
 __host__ __device__ constexpr int conv1_k(int ky, int kx) {
   return ky < 4 ? 2 * (4 * (kx >> 1) + ky) + (kx & 1) : 2 * (12 + (kx >> 1)) + (kx & 1);
 }
-// conv2 tap t = ky * 5 + kx -> word offset in the pooled conv1 map [14][14][4 words]
-__host__ __device__ constexpr int tap_off(int t) { return ((t / 5) * 14 + (t % 5)) * 4; }
 
 
 // Prefetch one sample's pair image into this warp's buffer (cp.async).
@@ -135,7 +135,7 @@ __device__ __forceinline__ void prefetch_img(uint32_t dst, const uint32_t* src, 
 }  // namespace
 
 // Pair images of the dataset: P[s][Y][X] = (x[s][Y-2][X-2], x[s][Y-2][X-1]),
-// zero outside the 28 x 28 image, 33 rows x 40 words.
+// zero outside the 28 x 28 image, 33 rows x kImgS words.
 __global__ void k_lenet_pairs(const __nv_bfloat16* X, uint32_t S, uint32_t* P) {
   const uint64_t n = (uint64_t)S * kImgWords;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
@@ -176,8 +176,8 @@ struct ConvSmem {
   static constexpr int bc1 = wc2 + 16 * kC2S * 2;              // f32 [8]
   static constexpr int bc2 = bc1 + 8 * 4;                      // f32 [16]
   static constexpr int img = bc2 + 16 * 4;                     // per warp [33][40] u32
-  static constexpr int p1 = img + kConvWarps * kImgWords * 4;  // per warp [197][4] u32
-  static constexpr int p2 = p1 + kConvWarps * 197 * 4 * 4;     // per warp [400] bf16
+  static constexpr int p1 = img + kConvWarps * kImgWords * 4;  // per warp [14][kP1R][4] u32
+  static constexpr int p2 = p1 + kConvWarps * kP1Words * 4;    // per warp [400] bf16
   static constexpr int total = p2 + kConvWarps * kP2Row * 2;
 };
 static_assert(ConvSmem::img % 16 == 0 && ConvSmem::p2 % 16 == 0, "aligned cp.async / uint4 regions");
@@ -218,9 +218,9 @@ __device__ __forceinline__ void conv1_tiles(int t0, const uint32_t* imgc, const 
   float d[N][4];
 #pragma unroll
   for (int u = 0; u < N; ++u) {
-    const int w = 4 * (t0 + u) + wi;  // < 196 for every tile t < 49
-    wpos[u] = w;
-    const int py = w / 14, px = w - 14 * py;
+    const int ty = (t0 + u) / 7, tx = (t0 + u) - 7 * ty;  // tile = windows 2ty..+1 x 2tx..+1
+    const int py = 2 * ty + (wi >> 1), px = 2 * tx + (wi & 1);
+    wpos[u] = py * kP1R + px;
     const int base0 = (2 * py) * kImgS + 2 * px + dx, base1 = base0 + kImgS;
     d[u][0] = b1a, d[u][1] = b1b, d[u][2] = b1a, d[u][3] = b1b;
     mma_bf16(d[u], imgc[base0], imgc[base1], imgc[base0 + 2], imgc[base1 + 2], bw1[0][0], bw1[0][1]);
@@ -261,9 +261,12 @@ __device__ __forceinline__ void conv2_tiles(int t0, const uint32_t* p1c, __nv_bf
   for (int u = 0; u < N; ++u) {
     const int w = 4 * (t0 + u) + wi;
     wv[u] = w < 25 ? w : -1;
-    const int wc = w < 25 ? w : 0;
+    // window 4t + wi has (qy + qx) = wi mod 4 and the map's row stride is 1 mod
+    // 4 pixels, so the 8 pixels of a tile row hit distinct bank quads; the
+    // padding slots of the last tile repeat its window 24 (same words)
+    const int wc = w < 25 ? w : 24;
     const int qy = wc / 5, qx = wc - 5 * qy;
-    q[u] = p1c + ((2 * qy) * 14 + 2 * qx + dx) * 4;
+    q[u] = p1c + ((2 * qy) * kP1R + 2 * qx + dx) * 4;
     d[u][0][0] = b2a, d[u][0][1] = b2b, d[u][0][2] = b2a, d[u][0][3] = b2b;
     d[u][1][0] = b2c, d[u][1][1] = b2d, d[u][1][2] = b2c, d[u][1][3] = b2d;
   }
@@ -274,7 +277,7 @@ __device__ __forceinline__ void conv2_tiles(int t0, const uint32_t* p1c, __nv_bf
 #pragma unroll
     for (int u = 0; u < N; ++u)
 #pragma unroll
-      for (int j = 0; j < 6; ++j) r[u][j] = q[u][(j * 14 + kx) * 4];
+      for (int j = 0; j < 6; ++j) r[u][j] = q[u][(j * kP1R + kx) * 4];
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -331,7 +334,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) k_lenet_conv(LenetSplitArgs s
   float* bc2 = reinterpret_cast<float*>(sm + ConvSmem::bc2);
   const uint32_t* img = reinterpret_cast<const uint32_t*>(sm + ConvSmem::img) + warp * kImgWords;
   const uint32_t img_s = smem_addr(img);
-  uint32_t* p1 = reinterpret_cast<uint32_t*>(sm + ConvSmem::p1) + warp * 197 * 4;  // +1 zero pixel
+  uint32_t* p1 = reinterpret_cast<uint32_t*>(sm + ConvSmem::p1) + warp * kP1Words;
   __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(sm + ConvSmem::p2) + warp * kP2Row;
   {
     uint32_t* p = reinterpret_cast<uint32_t*>(sm);
