@@ -233,7 +233,7 @@ __device__ __forceinline__ void conv1_tiles(int t0, const uint32_t* imgc, const 
     float s1 = fmaxf(d[u][1], 0.f) + fmaxf(d[u][3], 0.f);
     s0 += __shfl_xor_sync(0xffffffffu, s0, 4);
     s1 += __shfl_xor_sync(0xffffffffu, s1, 4);
-    if (dx == 0) p1[wpos[u] * 4 + c] = pack_bf16(0.25f * s0, 0.25f * s1);
+    if (dx == 0) p1[wpos[u] * 4 + c] = pack_bf16(s0, s1);
   }
 }
 
@@ -314,8 +314,8 @@ __device__ __forceinline__ void conv2_tiles(int t0, const uint32_t* p1c, __nv_bf
     s3 += __shfl_xor_sync(0xffffffffu, s3, 4);
     if (dx == 0 && wv[u] >= 0) {
       uint32_t* ow = reinterpret_cast<uint32_t*>(o + wv[u] * 16);
-      ow[c] = pack_bf16(0.25f * s0, 0.25f * s1);
-      ow[4 + c] = pack_bf16(0.25f * s2, 0.25f * s3);
+      ow[c] = pack_bf16(s0, s1);
+      ow[4 + c] = pack_bf16(s2, s3);
     }
   }
 }
@@ -357,17 +357,19 @@ __global__ void __launch_bounds__(kConvThreads, 1) k_lenet_conv(LenetSplitArgs s
     const uint32_t s_lo = part * kChunkS, s_hi = min(args.S, s_lo + kChunkS);
     if (row != staged) {
       __syncthreads();
+      // conv weights and biases pre-scaled by 1/4 (exact): the 2 x 2 average
+      // pools then reduce to sums of ReLUs, relu(x) / 4 = relu(x / 4)
       const __nv_bfloat16* w = args.W + row * args.Dp;
       for (int i = threadIdx.x; i < 150; i += kConvThreads) {
         const int ch = i / 25, r = i % 25, ky = r / 5, kx = r % 5;
-        wc1[ch * kC1K + conv1_k(ky, kx)] = w[oC1W + i];
+        wc1[ch * kC1K + conv1_k(ky, kx)] = __float2bfloat16(0.25f * bf(w[oC1W + i]));
       }
       for (int i = threadIdx.x; i < 2400; i += kConvThreads) {
         const int ch = i / 150, r = i % 150, ci = r / 25, tap = r % 25;
-        wc2[ch * kC2S + conv2_k(tap / 5, tap % 5) + ci] = w[oC2W + i];
+        wc2[ch * kC2S + conv2_k(tap / 5, tap % 5) + ci] = __float2bfloat16(0.25f * bf(w[oC2W + i]));
       }
-      if (threadIdx.x < 6) bc1[threadIdx.x] = bf(w[oC1B + threadIdx.x]);
-      if (threadIdx.x < 16) bc2[threadIdx.x] = bf(w[oC2B + threadIdx.x]);
+      if (threadIdx.x < 6) bc1[threadIdx.x] = 0.25f * bf(w[oC1B + threadIdx.x]);
+      if (threadIdx.x < 16) bc2[threadIdx.x] = 0.25f * bf(w[oC2B + threadIdx.x]);
       __syncthreads();
       staged = row;
 #pragma unroll
