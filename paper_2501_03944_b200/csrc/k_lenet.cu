@@ -459,9 +459,23 @@ __global__ void __launch_bounds__(kFcThreads, 1) k_lenet_fc(LenetSplitArgs sa) {
     __syncthreads();  // previous item: readers of the region / h1 / logits are done
     if (row != staged) {
       const __nv_bfloat16* w = args.W + row * args.Dp;
-      for (int i = threadIdx.x; i < 120 * 400; i += kFcThreads) {  // window-major columns
-        const int j = i / 400, k = i % 400, ch = k / 25, win = k % 25;
-        rg[j * kF1S + win * 16 + ch] = w[oF1W + i];
+      // window-major columns: task (j, win) gathers f1w[j][ch * 25 + win] for
+      // the 16 channels (lanes read consecutive windows: coalesced) and
+      // writes them as two 16-byte words
+      for (int i = threadIdx.x; i < 120 * 25; i += kFcThreads) {
+        const int j = i / 25, win = i - 25 * j;
+        const __nv_bfloat16* src = w + oF1W + j * 400 + win;
+        uint32_t u[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          __nv_bfloat162 t;
+          t.x = src[(2 * q) * 25];
+          t.y = src[(2 * q + 1) * 25];
+          u[q] = *reinterpret_cast<uint32_t*>(&t);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(rg + j * kF1S + win * 16);
+        dst[0] = make_uint4(u[0], u[1], u[2], u[3]);
+        dst[1] = make_uint4(u[4], u[5], u[6], u[7]);
       }
       for (int i = threadIdx.x; i < 8 * kF1S / 2; i += kFcThreads)  // rows 120..127 = 0
         reinterpret_cast<uint32_t*>(rg + 120 * kF1S)[i] = 0u;
