@@ -67,7 +67,7 @@ constexpr int kF2S = 136;   // fc2: 96 rows, K = 128 (120 + pad)
 constexpr int kF3S = 104;   // fc3: 16 rows, K = 96 (84 + pad)
 constexpr int kImgS = 36;   // pair-image row stride (32-bit words; = 4 mod 32), 33 rows
 constexpr int kImgWords = 33 * kImgS;  // 1188 words (16-byte multiple)
-constexpr int kP1R = 17;    // pooled conv1 map row stride (pixels; = 1 mod 4), 14 rows x 4 words
+constexpr int kP1R = 21;    // pooled conv1 map row stride (pixels; = 1 mod 4, 4 kP1R = 20 mod 32), 14 rows x 4 words
 constexpr int kP1Words = 14 * kP1R * 4;
 constexpr int kP2S = 408;   // pooled conv2 activations per sample (bf16), [25][16]
 constexpr int kH1S = 136;
