@@ -240,6 +240,10 @@ def main():
                     help="take the torch.distributed / NCCL sharded code path even at N = 1 "
                          "(a 1-rank communicator; used to test the multi-GPU path on one GPU)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shard-mode", choices=["firework", "replica"], default="firework",
+                    help="N>1: firework = fireworks split over the ranks, selected state all-gathered each "
+                         "generation; replica = batches x N, each rank owns whole batches, only the loser count "
+                         "is exchanged (weak scaling)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     w = WORKLOADS[args.workload]
@@ -274,11 +278,15 @@ def main():
     # rank owns mu of them (firework sharding), one in-place NCCL all-gather
     # of the selected fireworks per generation.
     wn = dict(w)
-    if args.scaling == "weak":
+    replica = args.shard_mode == "replica"
+    if replica:
+        wn["B"] = w["B"] * world
+    elif args.scaling == "weak":
         wn["mu"] = w["mu"] * world
     elif (w["B"] * w["mu"]) % world != 0:
         raise SystemExit(f"--scaling strong needs B*mu divisible by the rank count ({w['B'] * w['mu']} % {world})")
-    eng = P.Engine(make_config(P, wn, 1 << 62), space, obj, seed=0, device=dev, rank=rank, world=world)
+    eng = P.Engine(make_config(P, wn, 1 << 62), space, obj, seed=0, device=dev, rank=rank, world=world,
+                   shard_mode=args.shard_mode)
     if sharded:
         uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
@@ -348,8 +356,10 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "bf16" if w["kind"] in ("mlp", "lenet") else "f32", "data": "synthetic",
-            "config": {"workload": w["desc"], "D": w["D"], "fireworks_total": wn["mu"] * w["B"],
-                       "parallelism": f"firework-sharded x{world}" + (" + NCCL all-gather/gen" if world > 1 else ""),
+            "config": {"workload": w["desc"], "D": w["D"], "fireworks_total": wn["mu"] * wn["B"],
+                       "parallelism": (f"batch replicas x{world} ({wn['B']} batches)" +
+                                       (" + 8-byte NCCL all-reduce/gen" if world > 1 else "")) if replica else
+                                      (f"firework-sharded x{world}" + (" + NCCL all-gather/gen" if world > 1 else "")),
                        "l2": "inputs larger than L2: spark matrix fp32+bf16 229 MB/generation > 126 MB"
                        if args.workload == "c2" else "n/a"},
             "gpu_launches": kpg * args.steps if kpg else 1,  # 1: the persistent small-problem loop
@@ -389,12 +399,12 @@ def main():
         # and the D2H of the best; wall-clock per rank, max over ranks.
         import torch.distributed as dist
 
-        cfg_e = make_config(P, wn, w["B"] * wn["mu"] + args.steps * w["B"] * wn["mu"] * (w["lam"] + w["M"]))
+        cfg_e = make_config(P, wn, wn["B"] * wn["mu"] + args.steps * wn["B"] * wn["mu"] * (w["lam"] + w["M"]))
 
         # the engine shard and its NCCL communicator are set up once (like a
         # long-lived service); each timed run() re-initializes from the host
         # config and reads the best back
-        e = P.Engine(cfg_e, space, obj, seed=7, device=dev, rank=rank, world=world)
+        e = P.Engine(cfg_e, space, obj, seed=7, device=dev, rank=rank, world=world, shard_mode=args.shard_mode)
         u = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
             u.copy_(torch.frombuffer(bytearray(P.Engine.nccl_unique_id()), dtype=torch.uint8))
@@ -415,12 +425,13 @@ def main():
         try:
             sharded_once()  # warm (module load, workspace, NCCL first use)
             used, dt = sharded_once()
-            B, D = w["B"], w["D"]
+            B, D = wn["B"], w["D"]
             line["e2e"] = {"value": used / dt, "unit": "evals/s",
                            "h2d_bytes_per_step": 0,  # config and bounds copied at engine creation
                            "d2h_bytes_per_step": (B * D * 8 + B * 8) / args.steps,
                            "what": f"run() (initialize from the host config + {args.steps} generations, per-"
-                                   f"generation NCCL all-gather) + best() D2H on {world} GPUs, wall-clock max over "
+                                   f"generation NCCL {'loser-count all-reduce' if replica else 'all-gather'}) + "
+                                   f"best() D2H on {world} GPUs, wall-clock max over "
                                    f"ranks; engine shard and communicator created once"}
         except Exception as ex:  # keep the device-timed line
             line["e2e"] = {"value": None, "unit": "evals/s", "error": str(ex)[:200]}

@@ -223,9 +223,22 @@ int mgfwa_create_shard(const mgfwa_config_t* config, const mgfwa_space_t* space,
 int mgfwa_nccl_unique_id(void* out128);
 int mgfwa_attach_nccl(mgfwa_ctx_t ctx, const void* unique_id128, int nranks,
                       int rank);
+/* Shard modes (before mgfwa_initialize).  MGFWA_SHARD_FIREWORK (default):
+ * as above.  MGFWA_SHARD_REPLICA (needs batches % world == 0): each rank
+ * owns whole batches — replicas of the optimisation, SURVEY.md §8(f) rank 4 —
+ * and runs loser-out, record_wave and the population range for its own
+ * batches only; batches interact only through the shared evaluation budget
+ * (loser-out adds every batch's losers, engine.cpp:309), so the
+ * per-generation exchange is a single 8-byte NCCL all-reduce of the loser
+ * count.  Results (trace, best, state) are valid for the rank's own batches;
+ * trace entries of other batches read NaN.  Counters are global. */
+#define MGFWA_SHARD_FIREWORK 0
+#define MGFWA_SHARD_REPLICA 1
+int mgfwa_set_shard_mode(mgfwa_ctx_t ctx, int mode);
 /* Manual stepping without NCCL (tests, one-process emulation): phase 1 =
  * pop range .. selection, phase 2 = loser-out .. record_wave; between them
- * every shard imports every other shard's owned rows. */
+ * every shard imports every other shard's owned rows (replica mode: adds
+ * their loser counts; phase 1 then ends with loser-out). */
 int mgfwa_generation_phase(mgfwa_ctx_t ctx, int phase);
 int mgfwa_shard_exchange(mgfwa_ctx_t dst, mgfwa_ctx_t src);
 

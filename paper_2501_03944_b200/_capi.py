@@ -91,6 +91,7 @@ SIGNATURES = {
     "mgfwa_attach_nccl": (_int, [_P, _P, _int, _int]),
     "mgfwa_generation_phase": (_int, [_P, _int]),
     "mgfwa_shard_exchange": (_int, [_P, _P]),
+    "mgfwa_set_shard_mode": (_int, [_P, _int]),
 }
 
 _lib = None

@@ -283,6 +283,9 @@ struct Workspace {
   Status configure(const HostConfig& c, const mgfwa_space_t* space, uint64_t seed) {
     const uint64_t D = space->dim;
     v.seed = seed;
+    v.replica = 0;  // firework sharding (the default); mgfwa_set_shard_mode switches
+    v.b_lo = 0;
+    v.b_hi = c.B;
     v.amp_amplify = c.amp_amplify;
     v.amp_reduce = c.amp_reduce;
     double max_range = 0.0;
@@ -509,6 +512,8 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
@@ -524,11 +529,12 @@ static const NcclApi& nccl() {
     a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
     a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
     a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
     a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(h, "ncclGroupStart"));
     a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
     a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
     a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
-    a.ok = a.GetUniqueId && a.CommInitRank && a.AllGather && a.GroupStart && a.GroupEnd &&
+    a.ok = a.GetUniqueId && a.CommInitRank && a.AllGather && a.AllReduce && a.GroupStart && a.GroupEnd &&
            a.CommDestroy && a.GetErrorString;
     return a;
   }();
@@ -669,8 +675,35 @@ class Engine {
     return ok();
   }
 
+  // Replica sharding (MGFWA_SHARD_REPLICA): the shards own whole batches,
+  // which interact only through the evaluation counter (loser-out adds the
+  // losers of every batch), so the exchange is one 8-byte sum.
+  Status set_shard_mode(int mode) {
+    if (initialized) return Status{MGFWA_ESTATE, "mgfwa_set_shard_mode: call before initialize()"};
+    if (mode != MGFWA_SHARD_FIREWORK && mode != MGFWA_SHARD_REPLICA)
+      return invalid("mgfwa_set_shard_mode: unknown mode");
+    EngineView& v = ws->v;
+    if (mode == MGFWA_SHARD_FIREWORK) {
+      v.replica = 0, v.b_lo = 0, v.b_hi = v.B;
+      return ok();
+    }
+    if (cfg.B % world != 0)
+      return invalid("mgfwa_set_shard_mode: replica sharding needs batches divisible by the number of ranks");
+    v.replica = 1;
+    v.b_lo = v.f_lo / v.mu;
+    v.b_hi = (v.f_lo + v.Fl) / v.mu;
+    CUDA_TRY(cudaMemsetAsync(v.loser, 0, v.F * sizeof(int), stream));
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    return ok();
+  }
+
   Status exchange_nccl() {
     const EngineView& v = ws->v;
+    if (v.replica) {
+      NCCL_TRY(nccl().AllReduce(&v.ctl->n_losers_all, &v.ctl->n_losers_all, 1, ncclUint64, ncclSum, comm,
+                                stream));
+      return ok();
+    }
     const size_t rows = v.Fl * v.Dp;
     NCCL_TRY(nccl().GroupStart());
     NCCL_TRY(nccl().AllGather(v.pos + v.f_lo * v.Dp, v.pos, rows, ncclFloat, comm, stream));
@@ -687,6 +720,13 @@ class Engine {
     const EngineView& a = ws->v;
     const EngineView& b = src.ws->v;
     if (a.F != b.F || a.Dp != b.Dp || a.Fl != b.Fl) return invalid("mgfwa_shard_exchange: shape mismatch");
+    if (a.replica != b.replica) return invalid("mgfwa_shard_exchange: shard modes differ");
+    if (a.replica) {
+      launch_add_losers(a.ctl, b.ctl, stream);
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaStreamSynchronize(stream));
+      return ok();
+    }
     CUDA_TRY(cudaMemcpyAsync(a.pos + b.f_lo * a.Dp, b.pos + b.f_lo * b.Dp, b.Fl * b.Dp * 4,
                              cudaMemcpyDeviceToDevice, stream));
     CUDA_TRY(cudaMemcpyAsync(a.fit + b.f_lo, b.fit + b.f_lo, b.Fl * 8, cudaMemcpyDeviceToDevice, stream));
@@ -988,6 +1028,8 @@ int mgfwa_generation_phase(mgfwa_ctx_t ctx, int phase) {
   if (s.code == MGFWA_OK && phase == 2) s = ctx->engine.sync();
   return fail(ctx, s);
 }
+
+int mgfwa_set_shard_mode(mgfwa_ctx_t ctx, int mode) { return fail(ctx, ctx->engine.set_shard_mode(mode)); }
 
 int mgfwa_shard_exchange(mgfwa_ctx_t dst, mgfwa_ctx_t src) {
   return fail(dst, dst->engine.import_shard(src->engine));

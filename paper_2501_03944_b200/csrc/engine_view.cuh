@@ -35,6 +35,7 @@ struct Ctl {
   unsigned small_done;    // blocks of k_small_b done in this generation
   unsigned bar_count;     // grid barrier of the persistent small-problem loop
   unsigned bar_gen;
+  uint64_t n_losers_all;  // replica sharding: losers of the generation over all shards
 };
 
 struct EngineView {
@@ -47,6 +48,11 @@ struct EngineView {
   // identically on every rank.
   uint64_t B, mu, lam, M, D, Dp, top, F;
   uint64_t Fl, f_lo;
+  // replica sharding (MGFWA_SHARD_REPLICA): the owned fireworks are whole
+  // batches [b_lo, b_hi); loser-out, record_wave and the population range run
+  // for those batches only and the shards exchange just the loser count.
+  int replica;
+  uint64_t b_lo, b_hi;
   uint32_t nparts;     // partial-sum slots per row
   uint32_t nch;        // coordinate chunks per row (kChunk each)
   int obj_kind;

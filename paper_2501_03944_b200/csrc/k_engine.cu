@@ -705,11 +705,11 @@ __global__ void k_loser(EngineView v) {
   if (threadIdx.x == 0) count = 0;
   __syncthreads();
   if (gen_inactive(v)) {
-    if (threadIdx.x == 0) v.ctl->n_losers = 0;
+    if (threadIdx.x == 0) v.ctl->n_losers = 0, v.ctl->n_losers_all = 0;
     return;
   }
   const double iters_rem = iters_remaining(v);
-  for (uint64_t b = threadIdx.x; b < v.B; b += blockDim.x) {
+  for (uint64_t b = v.b_lo + threadIdx.x; b < v.b_hi; b += blockDim.x) {
     // argmin_per_population (backend.cpp:69-83)
     uint64_t bi = 0;
     double bv = v.fit[b * v.mu];
@@ -737,10 +737,18 @@ __global__ void k_loser(EngineView v) {
   if (threadIdx.x == 0) {
     v.ctl->iters_rem = iters_rem;
     v.ctl->n_losers = count;
-    v.ctl->used += (uint64_t)count;
-    v.ctl->losers_total += (uint64_t)count;
+    if (v.replica) {
+      v.ctl->n_losers_all = (uint64_t)count;  // the exchange adds the other shards' counts
+    } else {
+      v.ctl->used += (uint64_t)count;
+      v.ctl->losers_total += (uint64_t)count;
+    }
   }
 }
+
+// Replica sharding, in-process exchange (tests): add another shard's loser
+// count of this generation.
+__global__ void k_add_losers(Ctl* dst, const Ctl* src) { dst->n_losers_all += (uint64_t)src->n_losers; }
 
 // ------------------------------------------------------------ fresh rows
 // mode 0: initialize (engine.cpp:56-64): every firework, kInit, iteration 0.
@@ -756,7 +764,7 @@ __global__ void __launch_bounds__(256) k_fresh_rows(EngineView v, int mode) {
   for (uint64_t item = blockIdx.x * (uint64_t)kWarps + (threadIdx.x >> 5);
        item < items; item += (uint64_t)gridDim.x * kWarps) {
     const uint64_t f = item / v.nch, c = item % v.nch;
-    if (mode == 1 && !v.loser[f]) continue;
+    if (mode == 1 && (!v.loser[f] || f < v.b_lo * v.mu || f >= v.b_hi * v.mu)) continue;
     const uint64_t b = f / v.mu, n = f % v.mu;
     const uint64_t pk = key_prefix(v.seed, stream, it, b, n, 0);
     float s0 = 0.0f, s1 = 0.0f;
@@ -809,7 +817,7 @@ __global__ void k_finalize_record(EngineView v, int mode) {
   unsigned nan_local = 0;
   const int lane = threadIdx.x & 31;
   for (uint64_t f = threadIdx.x >> 5; f < v.F; f += blockDim.x >> 5) {  // one warp per row
-    if (mode == 0 || v.loser[f]) {
+    if (mode == 0 || (v.loser[f] && f >= v.b_lo * v.mu && f < v.b_hi * v.mu)) {
       bool nan;
       const float x = finalize_row(v, v.fpart, f, &nan);
       nan_local += nan;
@@ -831,10 +839,21 @@ __global__ void k_finalize_record(EngineView v, int mode) {
     ctl->trace_n = 0;
     ctl->gens_run = 0;
   }
+  if (mode == 1 && v.replica && threadIdx.x == 0) {  // losers of every shard (exchanged)
+    ctl->used += ctl->n_losers_all;
+    ctl->losers_total += ctl->n_losers_all;
+  }
   __syncthreads();
   const uint64_t now = global_ns();
   const uint64_t slot = ctl->trace_n % v.trace_cap;
   for (uint64_t b = threadIdx.x; b < v.B; b += blockDim.x) {
+    if (mode == 1 && (b < v.b_lo || b >= v.b_hi)) {  // another shard's batch: not tracked here
+      v.rec_flag[b] = 0;
+      v.tr_evals[slot * v.B + b] = ctl->used;
+      v.tr_best[slot * v.B + b] = __longlong_as_double(0x7ff8000000000000ll);
+      v.tr_ns[slot * v.B + b] = now - ctl->start_ns;
+      continue;
+    }
     uint64_t bi = 0;
     double bv = v.fit[b * v.mu];
     for (uint64_t n = 1; n < v.mu; ++n)
@@ -877,10 +896,10 @@ __global__ void k_finalize_record(EngineView v, int mode) {
 // flight together.
 __global__ void __launch_bounds__(256) k_record_copy(EngineView v) {
   pdl_enter<true>();
-  const uint64_t n4 = (v.D + 3) / 4, items = v.B * n4;
+  const uint64_t n4 = (v.D + 3) / 4, items = (v.b_hi - v.b_lo) * n4;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < items;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t b = i / n4, d0 = (i % n4) * 4;
+    const uint64_t b = v.b_lo + i / n4, d0 = (i % n4) * 4;
     const float* pb = v.pos + b * v.mu * v.Dp + d0;
     if (v.rec_flag[b])
       *reinterpret_cast<float4*>(v.best_pos + b * v.Dp + d0) =
@@ -1455,8 +1474,10 @@ void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
     }
     pdl_launch(k_select, (unsigned)v.Fl, kSelectThreads, 0, s, v);
   }
+  // replica sharding: loser-out (own batches) closes phase A, the loser
+  // counts are exchanged, phase B starts at the reinit
+  if (v.replica ? phase != kGenB : phase != kGenA) pdl_launch(k_loser, 1, 128, 0, s, v);
   if (phase != kGenA) {
-    pdl_launch(k_loser, 1, 128, 0, s, v);
     pdl_launch(k_fresh_rows, capped((v.F * v.nch + kWarps - 1) / kWarps, nsm), 256, 0, s, v, 1);
     if (v.nn) hooks->eval_fresh(hooks->ctx, s);
     pdl_launch(k_finalize_record, 1, 256, 0, s, v, 1);
@@ -1486,6 +1507,8 @@ void launch_finalize_rows(const EngineView& v, const float* part, uint64_t nrows
                           float* fitness, unsigned long long* nan, cudaStream_t s) {
   pdl_launch(k_finalize_rows, (unsigned)((nrows + 7) / 8), 256, 0, s, v, part, nrows, fitness, nan);
 }
+
+void launch_add_losers(Ctl* dst, const Ctl* src, cudaStream_t s) { k_add_losers<<<1, 1, 0, s>>>(dst, src); }
 
 void launch_to_bf16(const float* src, __nv_bfloat16* dst, uint64_t n, cudaStream_t s) {
   pdl_launch(k_to_bf16, (unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, s, src, dst, n);

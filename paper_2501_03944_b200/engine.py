@@ -253,10 +253,19 @@ class RunRecord:
 class Engine:
     """One device-resident run: initialize(), step()/enqueue(), results."""
 
+    SHARD_MODES = {"firework": 0, "replica": 1}  # MGFWA_SHARD_* (include/mgfwa_b200.h)
+
     def __init__(self, config: MgfwaConfig, space: SearchSpace, objective: Objective, seed: int,
-                 device: int = 0, rank: int = 0, world: int = 1):
+                 device: int = 0, rank: int = 0, world: int = 1, shard_mode: str = "firework"):
+        """shard_mode (world > 1): "firework" — fireworks split evenly, one
+        all-gather of the selected state per generation; "replica" — each rank
+        owns whole batches (needs batches % world == 0), the per-generation
+        exchange is the loser count only, results are valid for the rank's own
+        batches (`owned_batches`)."""
         self.config, self.space, self.objective, self.seed = config, space, objective, seed
-        self.rank, self.world = rank, world
+        self.rank, self.world, self.shard_mode = rank, world, shard_mode
+        if shard_mode not in self.SHARD_MODES:
+            raise ValueError(f"shard_mode must be one of {sorted(self.SHARD_MODES)}")
         c, self._keep = config._c()
         sp = space._c()
         ob = objective._c()
@@ -267,6 +276,17 @@ class Engine:
             _check(A.lib().mgfwa_create_shard(C.byref(c), C.byref(sp), C.byref(ob), seed, device, rank, world,
                                               C.byref(h)))
         self.h = h
+        if shard_mode != "firework":
+            _check(A.lib().mgfwa_set_shard_mode(self.h, self.SHARD_MODES[shard_mode]), self.h)
+
+    @property
+    def owned_batches(self) -> range:
+        """Batches whose trace / best / state this context holds (all of them
+        except under replica sharding)."""
+        B = self.config.batches
+        if self.shard_mode != "replica":
+            return range(B)
+        return range(self.rank * B // self.world, (self.rank + 1) * B // self.world)
 
     # ---- firework sharding (one rank per GPU, NCCL all-gather per generation)
     @staticmethod

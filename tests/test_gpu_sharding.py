@@ -116,3 +116,66 @@ def test_shard_validation(P):
     cfg2 = P.MgfwaConfig(batches=1, fireworks=4, wall_clock_budget_ms=100.0)
     with pytest.raises(ValueError, match="evaluation budget"):
         P.Engine(cfg2, P.SearchSpace.box(4, -1, 1), P.Sphere(), 0, rank=0, world=2)
+
+
+def _replica(P, cfg, space, obj, seed, world):
+    shards = [P.Engine(cfg, space, obj, seed, rank=r, world=world, shard_mode="replica") for r in range(world)]
+    for s in shards:
+        s.initialize()
+    while shards[0].counters()["evaluations_used"] < cfg.max_evaluations:
+        for s in shards:
+            s.phase(1)  # ... selection, loser-out of the own batches
+        for dst in shards:
+            for src in shards:
+                if src is not dst:
+                    dst.import_shard(src)  # loser counts only
+        for s in shards:
+            s.phase(2)
+    out = [(s.owned_batches, s.record(), s.state(), s.counters()) for s in shards]
+    for s in shards:
+        s.close()
+    return out
+
+
+@pytest.mark.parametrize("kind", ["sphere", "mlp"])
+@pytest.mark.parametrize("batches,world", [(2, 2), (4, 2), (3, 3)])
+def test_replica_sharding_matches(P, kind, batches, world):
+    """Replica sharding: every rank owns whole
+    batches and exchanges only the per-generation loser count; the owned
+    batches' traces, best positions and states and the global counters equal
+    the single-context run bit for bit."""
+    if kind == "mlp":
+        obj = P.MlpWeights(samples=128)
+        space = P.SearchSpace.box(obj.dim(), -0.5, 0.5)
+        budget = batches * (5 + 6 * 5 * 13)
+    else:
+        obj = P.Sphere()
+        space = P.SearchSpace.box(29, -5.12, 5.12)
+        budget = batches * (5 + 40 * 5 * 13)
+    cfg = P.MgfwaConfig(batches=batches, fireworks=5, sparks_per_firework=10, guides_per_firework=3,
+                        max_evaluations=budget)
+    ref, ref_state = _reference(P, cfg, space, obj, 5)
+    assert ref.losers_reinitialized > 0  # the counter coupling is exercised
+    seen = set()
+    for owned, r, st, cnt in _replica(P, cfg, space, obj, 5, world):
+        seen.update(owned)
+        for b in owned:
+            assert np.array_equal(r.trace_best[b], ref.trace_best[b])
+            assert np.array_equal(r.trace_evaluations[b], ref.trace_evaluations[b])
+            assert np.array_equal(r.best_position[b], ref.best_position[b])
+            assert np.array_equal(st.positions[b], ref_state.positions[b])
+            assert np.array_equal(st.amplitudes[b], ref_state.amplitudes[b])
+        for b in set(range(batches)) - set(owned):
+            assert np.all(np.isnan(r.trace_best[b][1:]))  # not tracked on this rank
+        assert (r.evaluations_used, r.iterations, r.losers_reinitialized) == \
+               (ref.evaluations_used, ref.iterations, ref.losers_reinitialized)
+    assert seen == set(range(batches))
+
+
+def test_replica_mode_validation(P):
+    cfg = P.MgfwaConfig(batches=3, fireworks=4, max_evaluations=1000)
+    space = P.SearchSpace.box(4, -1, 1)
+    with pytest.raises(ValueError, match="batches divisible"):
+        P.Engine(cfg, space, P.Sphere(), 1, rank=0, world=2, shard_mode="replica")
+    with pytest.raises(ValueError, match="shard_mode"):
+        P.Engine(cfg, space, P.Sphere(), 1, shard_mode="pipeline")

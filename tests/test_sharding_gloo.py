@@ -136,14 +136,85 @@ def _sharded_run(rank, world, cfg, lower, upper, seed, kind):
     return np.array(trace), best_pos, used, it
 
 
+def _replica_run(rank, world, cfg, lower, upper, seed, kind):
+    """Replica sharding: rank r owns batch r
+    (B == world, one batch each); the only per-generation exchange is the
+    loser count, which the shared evaluation budget needs (engine.cpp:309)."""
+    import torch
+    import torch.distributed as dist
+
+    o = O.Oracle()
+    desc = O.ObjectiveDesc(kind=kind)
+    B, mu, lam, M = cfg.batches, cfg.fireworks, cfg.sparks_per_firework, cfg.guides_per_firework
+    assert B == world
+    b = rank
+    D = lower.size
+    top = cfg.top_spark_count()
+    max_range = float(np.max(upper - lower))
+    wave = cfg.evaluations_per_wave()
+
+    pos = o.initialize_positions(cfg, lower, upper, seed)  # [B][mu][D]: initialize is global
+    fit, _ = o.batched_apply(desc, pos)
+    a0 = cfg.initial_amplitude if cfg.initial_amplitude > 0 else 0.5 * max_range
+    amp = np.full((B, mu), a0)
+    li = np.zeros((B, mu))
+    used = B * mu
+    best, best_pos, trace = np.inf, np.zeros(D), []
+
+    def record():
+        nonlocal best, best_pos
+        v, i = fit[b, 0], 0
+        for j in range(1, mu):
+            if fit[b, j] < v:
+                v, i = fit[b, j], j
+        if v < best:
+            best, best_pos = v, pos[b, i].copy()
+        trace.append((used, best))
+
+    record()
+    it = 0
+    while used < cfg.max_evaluations:
+        it += 1
+        plo, phi = pos[b].min(axis=0), pos[b].max(axis=0)
+        sparks = np.empty((1, mu * lam, D))
+        for n in range(mu):
+            raw = pos[b, n][None, :] + _uniform(seed, O.K_EXPLODE, it, b, n, lam, D, -1.0, 1.0) * amp[b, n]
+            sparks[0, n * lam:(n + 1) * lam] = _map(raw, seed, O.K_MAPPING, it, b, n, lower, upper, plo, phi)
+        sfit, _ = o.batched_apply(desc, sparks)
+        lpos = pos[b:b + 1]
+        delta = o.guiding_vector(sparks, sfit, lam, top)
+        guides = np.empty((1, mu * M, D))
+        for n in range(mu):
+            g = np.stack([lpos[0, n] + cfg.boosts[m] * delta[0, n] for m in range(M)])
+            guides[0, n * M:(n + 1) * M] = _map(g, seed, O.K_GUIDE, it, b, n, lower, upper, plo, phi)
+        gfit, _ = o.batched_apply(desc, guides)
+        npos, nfit, nli, imp = o.select_best(lpos, fit[b:b + 1], sparks, sfit, lam, guides, gfit, M)
+        namp = o.update_amplitudes(amp[b:b + 1], imp, cfg.amp_amplify, cfg.amp_reduce, max_range)
+        pos[b], fit[b], amp[b], li[b] = npos[0], nfit[0], namp[0], nli[0]
+        used += wave
+        # loser-out of the own batch: the other batches get equal fitness and
+        # zero improvement rates, which never makes a loser
+        left = cfg.max_evaluations - used if cfg.max_evaluations > used else 0
+        p_, f_, a_, l_ = pos.copy(), np.zeros_like(fit), amp.copy(), np.zeros_like(li)
+        f_[b], l_[b] = fit[b], li[b]
+        p_, f_, a_, l_, nl = o.loser_out(p_, f_, a_, l_, cfg, lower, upper, it, seed, left / wave, desc)
+        pos[b], fit[b], amp[b], li[b] = p_[b], f_[b], a_[b], l_[b]
+        t = torch.tensor([nl], dtype=torch.int64)
+        dist.all_reduce(t)  # the exchange: losers of every batch
+        used += int(t.item())
+        record()
+    return np.array(trace), best_pos, used, it
+
+
 def _worker(rank, world, port, result_dir, case):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    cfg, D, lo, hi, seed, kind = case
-    tr, bp, used, it = _sharded_run(rank, world, cfg, np.full(D, lo), np.full(D, hi), seed, kind)
+    cfg, D, lo, hi, seed, kind = case[:6]
+    run = _replica_run if len(case) > 6 and case[6] == "replica" else _sharded_run
+    tr, bp, used, it = run(rank, world, cfg, np.full(D, lo), np.full(D, hi), seed, kind)
     np.savez(os.path.join(result_dir, f"r{rank}.npz"), trace=tr, best_pos=bp, used=used, it=it)
     dist.destroy_process_group()
 
@@ -172,4 +243,23 @@ def test_two_rank_sharded_run_matches_unsharded(tmp_path, kind):
         assert np.array_equal(got["trace"][:, 1], ref.trace_best[0])
         assert np.array_equal(got["trace"][:, 0].astype(np.uint64), ref.trace_evals[0])
         assert np.array_equal(got["best_pos"], ref.best_position)
+        assert int(got["used"]) == ref.evaluations_used and int(got["it"]) == ref.iterations
+
+
+@pytest.mark.parametrize("kind", [O.OBJ_SPHERE, O.OBJ_RASTRIGIN])
+def test_two_rank_replica_run_matches_unsharded(tmp_path, kind):
+    import torch.multiprocessing as mp
+
+    cfg = O.Config(batches=2, fireworks=4, sparks_per_firework=12, guides_per_firework=2, guide_fraction=0.25,
+                   boosts=[1.0, 2.0], max_evaluations=8 + 25 * 2 * 4 * 14)
+    D, lo, hi, seed = 6, -5.12, 5.12, 23
+    case = (cfg, D, lo, hi, seed, kind, "replica")
+    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), case), nprocs=2, join=True)
+    ref = O.Oracle().run(cfg, np.full(D, lo), np.full(D, hi), O.ObjectiveDesc(kind=kind), seed)
+    assert ref.losers_reinitialized > 0
+    for r in range(2):
+        got = np.load(tmp_path / f"r{r}.npz")
+        assert np.array_equal(got["trace"][:, 1], ref.trace_best[r])
+        assert np.array_equal(got["trace"][:, 0].astype(np.uint64), ref.trace_evals[r])
+        assert np.array_equal(got["best_pos"], ref.best_position[r])
         assert int(got["used"]) == ref.evaluations_used and int(got["it"]) == ref.iterations
