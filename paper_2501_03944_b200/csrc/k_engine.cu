@@ -500,7 +500,8 @@ static size_t rank_smem(const EngineView& v) {
 __global__ void __launch_bounds__(256) k_guides(EngineView v) {
   pdl_enter();
   if (gen_inactive(v)) return;
-  extern __shared__ int s_idx[];  // [2*top]: rank lists of the block's firework
+  extern __shared__ uint64_t s_pre[];  // [M] kGuide key prefixes, then [2*top] rank lists
+  int* s_idx = reinterpret_cast<int*>(s_pre + v.M);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t it = v.ctl->iteration;
   const uint64_t nsl = (v.D + 63) / 64;  // 64-coordinate slices (float2 per lane)
@@ -509,12 +510,14 @@ __global__ void __launch_bounds__(256) k_guides(EngineView v) {
   for (uint64_t blk = blockIdx.x; blk < v.Fl * bpf; blk += gridDim.x) {
     const uint64_t fl = blk / bpf, f = v.f_lo + fl;  // local / global firework
     const uint64_t c = (blk % bpf) * kWarps + warp;
+    const uint64_t b = f / v.mu, n = f % v.mu;
     __syncthreads();
     for (uint64_t i = threadIdx.x; i < 2 * top; i += blockDim.x) s_idx[i] = v.rank_idx[fl * 2 * top + i];
+    // hoisted rng.hpp:43-51 up to field m: one splitmix64 round per coordinate
+    for (uint64_t m = threadIdx.x; m < v.M; m += blockDim.x) s_pre[m] = key_prefix(v.seed, kGuide, it, b, n, m);
     __syncthreads();
     const uint64_t d0 = c * 64 + lane * 2;
     if (c >= nsl || d0 >= v.D) continue;
-    const uint64_t b = f / v.mu, n = f % v.mu;
     const float* sb = v.sparks + fl * v.lam * v.Dp + d0;
     double acc0 = 0.0, acc1 = 0.0;
     uint64_t t = 0;
@@ -528,6 +531,19 @@ __global__ void __launch_bounds__(256) k_guides(EngineView v) {
       }
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
+        acc0 = __dadd_rn(acc0, __dsub_rn((double)bb[i].x, (double)ww[i].x));
+        acc1 = __dadd_rn(acc1, __dsub_rn((double)bb[i].y, (double)ww[i].y));
+      }
+    }
+    for (; t + 4 <= top; t += 4) {
+      float2 bb[4], ww[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        bb[i] = *reinterpret_cast<const float2*>(sb + (uint64_t)s_idx[t + i] * v.Dp);
+        ww[i] = *reinterpret_cast<const float2*>(sb + (uint64_t)s_idx[top + t + i] * v.Dp);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
         acc0 = __dadd_rn(acc0, __dsub_rn((double)bb[i].x, (double)ww[i].x));
         acc1 = __dadd_rn(acc1, __dsub_rn((double)bb[i].y, (double)ww[i].y));
       }
@@ -546,7 +562,7 @@ __global__ void __launch_bounds__(256) k_guides(EngineView v) {
     const float* phi = v.pop_hi + b * v.Dp;
     for (uint64_t m = 0; m < v.M; ++m) {
       const double beta = v.boosts[m];
-      const uint64_t pg = key_prefix(v.seed, kGuide, it, b, n, m);
+      const uint64_t pg = s_pre[m];
       float x[2];
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
@@ -1437,6 +1453,8 @@ void launch_key_hash(const uint64_t* keys, uint64_t n, uint64_t* out,
 
 // ---------------------------------------------------------------- launch
 
+static size_t guides_smem(const EngineView& v) { return v.M * sizeof(uint64_t) + 2 * v.top * sizeof(int); }
+
 static unsigned guide_blocks(const EngineView& v, int nsm) {
   const uint64_t nsl = (v.D + 63) / 64;
   const uint64_t blocks = v.Fl * ((nsl + kWarps - 1) / kWarps);
@@ -1466,7 +1484,7 @@ void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
     if (v.nn) hooks->eval_sparks(hooks->ctx, s);
     pdl_launch(k_rank, (unsigned)v.Fl, kRankThreads, rank_smem(v), s, v);
     if (v.M > 0) {
-      pdl_launch(k_guides, guide_blocks(v, nsm), 256, 2 * v.top * sizeof(int), s, v);
+      pdl_launch(k_guides, guide_blocks(v, nsm), 256, guides_smem(v), s, v);
       if (v.nn)
         hooks->eval_guides(hooks->ctx, s);
       else
@@ -1528,7 +1546,7 @@ void launch_rank(const EngineView& v, cudaStream_t s) {
   pdl_launch(k_rank, (unsigned)v.Fl, kRankThreads, rank_smem(v), s, v);
 }
 void launch_guides(const EngineView& v, int nsm, cudaStream_t s) {
-  pdl_launch(k_guides, guide_blocks(v, nsm), 256, 2 * v.top * sizeof(int), s, v);
+  pdl_launch(k_guides, guide_blocks(v, nsm), 256, guides_smem(v), s, v);
   if (!v.nn) launch_analytic_partials(v.guides, v.Fl * v.M, v.D, v.Dp, v.nch, v.obj_kind, v.gpart, nsm, s);
 }
 void launch_select(const EngineView& v, int nsm, cudaStream_t s) {
