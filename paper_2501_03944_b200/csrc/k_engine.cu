@@ -387,7 +387,10 @@ static void explode_launch_k(const EngineView& v, unsigned grid, cudaStream_t s)
   pdl_launch(k_explode_map<KIND>, grid, 256, kExplodeSmem, s, v);
 }
 
-constexpr int kRankThreads = 1024;
+#ifndef RANK_THREADS
+#define RANK_THREADS 1024
+#endif
+constexpr int kRankThreads = RANK_THREADS;
 constexpr int kRankSmemMax = (int)(kMaxSparksPerFirework * sizeof(uint64_t));
 __global__ void __launch_bounds__(kRankThreads) k_rank(EngineView v);
 
@@ -426,8 +429,11 @@ __device__ __forceinline__ uint64_t rank_key(float x, uint32_t k) {
   return ((uint64_t)u << 32) | k;
 }
 
+#ifndef RANK_TRIGGER
+#define RANK_TRIGGER 0  // measured: no early trigger is 1.5 us faster per C2 generation
+#endif
 __global__ void __launch_bounds__(kRankThreads) k_rank(EngineView v) {
-  pdl_enter<true>();
+  pdl_enter<RANK_TRIGGER != 0>();
   if (gen_inactive(v)) return;
   extern __shared__ uint64_t keys[];  // [lambda] sort keys
   const uint64_t fl = blockIdx.x;     // local firework
