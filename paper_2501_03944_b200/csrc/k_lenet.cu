@@ -65,7 +65,15 @@ constexpr int kC2S = 216;   // conv2 weight row stride (bf16), K = 25 taps x 8 +
 constexpr int kF1S = 408;   // fc1 row stride (bf16), 128 rows, K = 400 (window-major)
 constexpr int kF2S = 136;   // fc2: 96 rows, K = 128 (120 + pad)
 constexpr int kF3S = 104;   // fc3: 16 rows, K = 96 (84 + pad)
-constexpr int kImgS = 36;   // pair-image row stride (32-bit words; = 4 mod 32), 33 rows
+#ifndef LENET_CONV1_PAIRS
+#define LENET_CONV1_PAIRS 1  // conv1 on tile pairs (whole pool windows per thread, 64-bit loads)
+#endif
+#ifndef LENET_CV_P1T
+#define LENET_CV_P1T 4  // conv1 tile pairs in flight per warp (measured: 4 < 3 < 5)
+#endif
+// pair-image row stride (32-bit words, 33 rows): tile pairs load 64-bit words and
+// are conflict-light at 8 mod 32; single tiles load 32-bit words, conflict-free at 4 mod 32
+constexpr int kImgS = LENET_CONV1_PAIRS ? 40 : 36;
 constexpr int kImgWords = 33 * kImgS;  // 1188 words (16-byte multiple)
 constexpr int kP1R = 21;    // pooled conv1 map row stride (pixels; = 1 mod 4, 4 kP1R = 20 mod 32), 14 rows x 4 words
 constexpr int kP1Words = 14 * kP1R * 4;
@@ -237,6 +245,45 @@ __device__ __forceinline__ void conv1_tiles(int t0, const uint32_t* imgc, const 
   }
 }
 
+// conv1 on tile pairs t0 .. t0 + N - 1 of one sample (25 pairs): pair t
+// covers pool windows 8t .. 8t + 7 (row g of the MMA tile = window 8t + g),
+// tile dy of the pair the window's pixel row dy, and MMA rows g / g + 8 its
+// columns dx = 0 / 1.  A thread then holds all four pixels of its window for
+// its two channels: ReLU + 2x2 pool in registers (same summation order as
+// conv1_tiles: (p00 + p10) + (p01 + p11), so p1 is bit-identical), no
+// shuffle, every lane stores, and each A-fragment register pair (rows g, g+8
+// = neighbouring pair-image words) is one 64-bit load.
+template <int N>
+__device__ __forceinline__ void conv1_pairs(int t0, const uint32_t* imgc, const uint32_t* imgd, uint32_t* p1, int g,
+                                            int c, const uint32_t (&bw1)[2][2], float b1a, float b1b) {
+  int wpos[N];
+  float d[N][2][4];
+#pragma unroll
+  for (int u = 0; u < N; ++u) {
+    const int w0 = 8 * (t0 + u) + g;
+    const int w = w0 < 196 ? w0 : 195;  // the last pair's 4 spare rows recompute window 195
+    const int py = w / 14, px = w - 14 * py;
+    wpos[u] = w0 < 196 ? py * kP1R + px : -1;
+    const int X = (2 * py) * kImgS + 2 * px;
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy) {
+      const uint2 a01 = *reinterpret_cast<const uint2*>(imgc + X + dy * kImgS);      // kxp 0, dx 0 / 1
+      const uint2 a23 = *reinterpret_cast<const uint2*>(imgc + X + dy * kImgS + 2);  // kxp 1
+      const uint2 e01 = *reinterpret_cast<const uint2*>(imgc + X + dy * kImgS + 4);  // kxp 2
+      const uint2 e23 = *reinterpret_cast<const uint2*>(imgd + X + dy * kImgS);      // ky 4
+      d[u][dy][0] = b1a, d[u][dy][1] = b1b, d[u][dy][2] = b1a, d[u][dy][3] = b1b;
+      mma_bf16(d[u][dy], a01.x, a01.y, a23.x, a23.y, bw1[0][0], bw1[0][1]);
+      mma_bf16(d[u][dy], e01.x, e01.y, e23.x, e23.y, bw1[1][0], bw1[1][1]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < N; ++u) {
+    const float s0 = (fmaxf(d[u][0][0], 0.f) + fmaxf(d[u][1][0], 0.f)) + (fmaxf(d[u][0][2], 0.f) + fmaxf(d[u][1][2], 0.f));
+    const float s1 = (fmaxf(d[u][0][1], 0.f) + fmaxf(d[u][1][1], 0.f)) + (fmaxf(d[u][0][3], 0.f) + fmaxf(d[u][1][3], 0.f));
+    if (wpos[u] >= 0) p1[wpos[u] * 4 + c] = pack_bf16(s0, s1);
+  }
+}
+
 // conv2 K order for the column-reuse scheme (k_lenet_conv): k-step st holds
 // two taps A (k 0-7) and B (k 8-15), 8 channels each (6 + 2 zero).
 //   st = 2 kx + h (kx < 5, h < 2): A = (2h, kx), B = (2h + 1, kx)
@@ -394,10 +441,18 @@ __global__ void __launch_bounds__(kConvThreads, 1) k_lenet_conv(LenetSplitArgs s
       cp_async_wait_all();
       __syncwarp();
       // ---- conv1 + ReLU + pool -> p1: 49 tiles
+#if LENET_CONV1_PAIRS
+#pragma unroll 1
+      for (int t0 = 0; t0 + LENET_CV_P1T <= 25; t0 += LENET_CV_P1T)
+        conv1_pairs<LENET_CV_P1T>(t0, imgc, imgd, p1, g, c, bw1, b1a, b1b);
+      if constexpr (25 % LENET_CV_P1T != 0)
+        conv1_pairs<25 % LENET_CV_P1T>(25 - 25 % LENET_CV_P1T, imgc, imgd, p1, g, c, bw1, b1a, b1b);
+#else
 #pragma unroll 1
       for (int t0 = 0; t0 + kCvC1T <= 49; t0 += kCvC1T)
         conv1_tiles<kCvC1T>(t0, imgc, imgd, p1, wi, dx, c, bw1, b1a, b1b);
       if constexpr (49 % kCvC1T != 0) conv1_tiles<49 % kCvC1T>(49 - 49 % kCvC1T, imgc, imgd, p1, wi, dx, c, bw1, b1a, b1b);
+#endif
       __syncwarp();
       if (s + kConvWarps < s_hi)
         prefetch_img(img_s, args.pimg + (uint64_t)(s + kConvWarps) * kImgWords, lane);
