@@ -42,6 +42,7 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <new>
 
 #include "common.cuh"
@@ -729,7 +730,10 @@ LenetPlan* lenet_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t 
   }
   // scratch of at most kScratchBytes (at least one candidate's activations)
   const uint64_t per_row = (uint64_t)S * kP2Row * 2;
-  p->group_rows = kScratchBytes / per_row;
+  uint64_t cap = kScratchBytes;
+  if (const char* e = getenv("MGFWA_LENET_SCRATCH_MB"))  // tests: force candidate groups
+    cap = (uint64_t)strtoull(e, nullptr, 10) << 20;
+  p->group_rows = cap / per_row;
   if (p->group_rows < 1) p->group_rows = 1;
   if (p->group_rows > rows) p->group_rows = rows;
   if (cudaMalloc(&p->p2, p->group_rows * per_row) != cudaSuccess) {

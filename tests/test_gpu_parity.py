@@ -330,3 +330,30 @@ def test_mlp_cta_pair_variant_matches(P, tmp_path):
     a, b = np.load(tmp_path / "1.npz"), np.load(tmp_path / "2.npz")
     for H in ("32", "64", "128", "256"):
         np.testing.assert_allclose(a[H], b[H], rtol=1e-5, atol=1e-6)
+
+
+def test_lenet_candidate_groups_bit_identical(P):
+    """Populations whose activation scratch exceeds the cap run in candidate
+    groups (one conv + fc launch pair each); the fitness must not depend on
+    the grouping.  The cap is forced down in a subprocess (read at plan
+    creation)."""
+    import os
+    import subprocess
+    import sys
+
+    code = ("import numpy as np, paper_2501_03944_b200 as P\n"
+            "W = np.random.default_rng(5).uniform(-0.3, 0.3, size=(23, P.LeNet(samples=300).dim())).astype(np.float32)\n"
+            "f, _ = P.batched_apply(P.LeNet(samples=300), W)\n"
+            "print(','.join(repr(float(x)) for x in f))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for mb in (None, "1"):  # 1 MiB: 4 candidates of 300 x 800 B per group
+        env = dict(os.environ)
+        env.pop("MGFWA_LENET_SCRATCH_MB", None)
+        if mb:
+            env["MGFWA_LENET_SCRATCH_MB"] = mb
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout.strip().splitlines()[-1])
+    assert outs[0] == outs[1]
