@@ -375,9 +375,12 @@ def main():
         top = -(-w["lam"] // 5)  # ceil(0.2 * lambda), the default guide fraction
         algo = {"explode": Fl * w["lam"] * w["D"] * (6 if nn else 4) + Fl * w["D"] * 4,
                 "guides": Fl * (2 * top * Dp4 + w["M"] * w["D"] * (6 if nn else 4) + Dp4),
-                "rank": Fl * w["lam"] * (4 if nn else 8) * 2}
+                "rank": Fl * w["lam"] * (4 if nn else 8) * 2,
+                # winner row read + firework row written (every firework's winner a spark or
+                # guide: the upper bound) + the spark fitness scan
+                "select": Fl * (2 * w["D"] * 4 + w["lam"] * 4)}
         kb = {}
-        for name in ("explode", "rank", "guides"):
+        for name in ("explode", "rank", "guides", "select"):
             kms, _ = eng.time_kernel(name, 10)
             kb[name] = {"us": 1e3 * kms, "algorithmic_bytes": algo[name],
                         "achieved_GBs": algo[name] / (kms * 1e-3) / 1e9,

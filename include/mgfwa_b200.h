@@ -254,13 +254,17 @@ int mgfwa_time_fitness(mgfwa_ctx_t ctx, uint64_t iters, double* ms,
 /* Same, for one kernel of the generation (state-idempotent ones only):
  * MGFWA_KERNEL_FITNESS (as above), _EXPLODE (explode + mapping (+ analytic
  * fitness)), _RANK (spark fitness finalize + ranking), _GUIDES (guiding
- * vector + guides + mapping), _GUIDE_FITNESS (NN fitness of the guides).
+ * vector + guides + mapping), _GUIDE_FITNESS (NN fitness of the guides),
+ * _SELECT (select_best + update_amplitudes + winner copy; the state it writes
+ * is restored before every timed launch and afterwards, so each launch sees
+ * the same post-guide pre-selection state).  *units = fireworks for _SELECT.
  * Run on the state the context holds (e.g. after some generations). */
 #define MGFWA_KERNEL_FITNESS 0
 #define MGFWA_KERNEL_EXPLODE 1
 #define MGFWA_KERNEL_RANK 2
 #define MGFWA_KERNEL_GUIDES 3
 #define MGFWA_KERNEL_GUIDE_FITNESS 4
+#define MGFWA_KERNEL_SELECT 5
 int mgfwa_time_kernel(mgfwa_ctx_t ctx, int kernel, uint64_t iters, double* ms,
                       uint64_t* units);
 

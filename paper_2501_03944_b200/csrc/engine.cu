@@ -362,6 +362,7 @@ struct Workspace {
     add(&boosts, std::max<uint64_t>(v.M, 1) * 8);
     add(&v.pos, F * Dp * 4);
     add(&v.fit, F * 8);
+    add(&v.fit_prev, F * 8);
     add(&v.amp, F * 8);
     add(&v.li, F * 8);
     add(&v.improved, F * 4);
@@ -1409,6 +1410,52 @@ int mgfwa_time_kernel(mgfwa_ctx_t ctx, int kernel, uint64_t iters, double* ms, u
         launch = [&]() { nn_fitness_launch(w.plan_guides, v.gpart, nullptr, e.stream); };
         *units = v.Fl * v.M;
         break;
+      case MGFWA_KERNEL_SELECT: {
+        // not state-idempotent: the state k_select writes is snapshotted and
+        // restored (untimed) before every timed launch and at the end
+        const size_t pos_b = v.F * v.Dp * 4, f8 = v.F * 8, f4 = v.F * 4, g4 = v.F * (v.M ? v.M : 1) * 4;
+        std::vector<std::pair<void*, size_t>> st = {{v.pos, pos_b}, {v.fit, f8}, {v.amp, f8}, {v.li, f8},
+                                                    {v.improved, f4}, {v.winner, f4}, {v.gfit, g4},
+                                                    {v.ctl, sizeof(Ctl)}};
+        size_t total = 0;
+        for (auto& x : st) total += (x.second + 255) & ~size_t(255);
+        char* snap = nullptr;
+        CUDA_TRY(cudaMalloc(&snap, total));
+        auto copy_all = [&](bool save) -> cudaError_t {
+          size_t off = 0;
+          for (auto& x : st) {
+            cudaError_t r = save ? cudaMemcpyAsync(snap + off, x.first, x.second, cudaMemcpyDeviceToDevice, e.stream)
+                                 : cudaMemcpyAsync(x.first, snap + off, x.second, cudaMemcpyDeviceToDevice, e.stream);
+            if (r != cudaSuccess) return r;
+            off += (x.second + 255) & ~size_t(255);
+          }
+          return cudaSuccess;
+        };
+        cudaEvent_t a, b;
+        float sum = 0.0f;
+        cudaError_t r = copy_all(true);
+        if (r == cudaSuccess) r = cudaEventCreate(&a);
+        if (r == cudaSuccess) r = cudaEventCreate(&b);
+        for (uint64_t i = 0; i <= iters && r == cudaSuccess; ++i) {  // launch 0: warm-up
+          r = copy_all(false);
+          if (r == cudaSuccess) r = cudaEventRecord(a, e.stream);
+          if (r == cudaSuccess) launch_select_gen(v, w.nsm, e.stream);
+          if (r == cudaSuccess) r = cudaEventRecord(b, e.stream);
+          if (r == cudaSuccess) r = cudaEventSynchronize(b);
+          float t = 0.0f;
+          if (r == cudaSuccess) r = cudaEventElapsedTime(&t, a, b);
+          if (i > 0) sum += t;
+        }
+        if (r == cudaSuccess) r = copy_all(false);
+        if (r == cudaSuccess) r = cudaStreamSynchronize(e.stream);
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        cudaFree(snap);
+        CUDA_TRY(r);
+        *ms = (double)sum / (double)(iters ? iters : 1);
+        *units = v.Fl;
+        return ok();
+      }
       default:
         return invalid("mgfwa_time_kernel: unknown kernel");
     }

@@ -73,6 +73,7 @@ struct EngineView {
   // state
   float* pos;
   double* fit;
+  double* fit_prev;  // pre-selection firework fitness (k_rank), read by every k_select part
   double* amp;
   double* li;
   int* improved;

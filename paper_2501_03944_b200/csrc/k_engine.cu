@@ -438,6 +438,7 @@ __global__ void __launch_bounds__(kRankThreads) k_rank(EngineView v) {
   extern __shared__ uint64_t keys[];  // [lambda] sort keys
   const uint64_t fl = blockIdx.x;     // local firework
   const uint32_t lam = (uint32_t)v.lam;
+  if (threadIdx.x == 0) v.fit_prev[v.f_lo + fl] = v.fit[v.f_lo + fl];  // for k_select's parts
   unsigned nan_local = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   constexpr int R = 4;  // rows per warp step (their loads in flight together)
@@ -597,12 +598,16 @@ constexpr int kSelectThreads = 512;
 // select_best + update_amplitudes + wave accounting + winner copy for local
 // firework fl, given the guide fitness gs[M] (all threads of the block;
 // any block size that is a multiple of 32, at most 1024).
-__device__ void select_core(const EngineView& v, uint64_t fl, const float* gs, unsigned nan_local);
+__device__ void select_core(const EngineView& v, uint64_t fl, const float* gs, unsigned nan_local,
+                            const double* old_fit, uint32_t part, uint32_t nparts);
 
+// grid (Fl, parts): parts > 1 split the winner copy; they need k_rank's
+// fit_prev (parts == 1 reads fit directly: the operator seam).
 __global__ void __launch_bounds__(kSelectThreads) k_select(EngineView v) {
   pdl_enter<true>();
   if (gen_inactive(v)) return;
   const uint64_t fl = blockIdx.x;  // local firework
+  const uint32_t part = blockIdx.y, nparts = gridDim.y;
   __shared__ float gs[16];
   unsigned nan_local = 0;
   // guide fitness: one warp per guide row (warp-cooperative finalize)
@@ -614,20 +619,24 @@ __global__ void __launch_bounds__(kSelectThreads) k_select(EngineView v) {
       bool nan;
       g = finalize_row(v, v.gpart, fl * v.M + m, &nan);
       nan_local += nan && (threadIdx.x & 31) == 0;  // once per row (select_core sums lanes)
-      if ((threadIdx.x & 31) == 0) v.gfit[fl * v.M + m] = g;
+      if ((threadIdx.x & 31) == 0 && part == 0) v.gfit[fl * v.M + m] = g;
     }
     if ((threadIdx.x & 31) == 0) gs[m] = g;
   }
   __syncthreads();
-  select_core(v, fl, gs, nan_local);
+  select_core(v, fl, gs, nan_local, nparts > 1 ? v.fit_prev : v.fit, part, nparts);
 }
 
-__device__ void select_core(const EngineView& v, uint64_t fl, const float* gs, unsigned nan_local) {
+// The decision is computed by every part (from old_fit, which part 0's state
+// update does not touch); part 0 writes the state, part p copies slice p of
+// the winner row.
+__device__ void select_core(const EngineView& v, uint64_t fl, const float* gs, unsigned nan_local,
+                            const double* old_fit, uint32_t part, uint32_t nparts) {
   const uint64_t f = v.f_lo + fl;  // global firework
   __shared__ double sv[32];
   __shared__ int so[32];
   __shared__ int s_win;
-  double best_v = v.fit[f];
+  double best_v = old_fit[f];
   int best_o = 0;
   if (threadIdx.x != 0) best_v = __longlong_as_double(0x7ff0000000000000ll), best_o = 0x7fffffff;
   for (uint64_t k = threadIdx.x; k < v.lam; k += blockDim.x) {
@@ -652,7 +661,7 @@ __device__ void select_core(const EngineView& v, uint64_t fl, const float* gs, u
   if ((threadIdx.x & 31) == 0) {
     sv[w] = best_v;
     so[w] = best_o;
-    if (nan_local)
+    if (nan_local && part == 0)
       atomicAdd((unsigned long long*)&v.ctl->nan_count, (unsigned long long)nan_local);
   }
   __syncthreads();
@@ -661,21 +670,23 @@ __device__ void select_core(const EngineView& v, uint64_t fl, const float* gs, u
       if (sv[i] < best_v || (sv[i] == best_v && so[i] < best_o)) best_v = sv[i], best_o = so[i];
     // If every candidate is NaN-free but the firework is +inf and all are
     // +inf, the firework (order 0) wins: strict < never fires.
-    if (!(best_v < v.fit[f])) {
-      best_v = v.fit[f];
+    const double old = old_fit[f];
+    if (!(best_v < old)) {
+      best_v = old;
       best_o = 0;
     }
-    const double old = v.fit[f];
-    const double gain = old - best_v;
-    v.fit[f] = best_v;
-    v.li[f] = (0.0 < gain) ? gain : 0.0;
-    const int imp = best_v < old;
-    v.improved[f] = imp;
-    v.winner[f] = best_o;
-    const double a = v.amp[f] * (imp ? v.amp_amplify : v.amp_reduce);
-    v.amp[f] = a < v.amp_floor ? v.amp_floor : (v.max_range < a ? v.max_range : a);
-    if (fl == 0) v.ctl->used += v.wave;  // the global wave, on every rank
     s_win = best_o;
+    if (part == 0) {
+      const double gain = old - best_v;
+      v.fit[f] = best_v;
+      v.li[f] = (0.0 < gain) ? gain : 0.0;
+      const int imp = best_v < old;
+      v.improved[f] = imp;
+      v.winner[f] = best_o;
+      const double a = v.amp[f] * (imp ? v.amp_amplify : v.amp_reduce);
+      v.amp[f] = a < v.amp_floor ? v.amp_floor : (v.max_range < a ? v.max_range : a);
+      if (fl == 0) v.ctl->used += v.wave;  // the global wave, on every rank
+    }
   }
   __syncthreads();
   // winner row -> firework row (padding included: rows are Dp wide)
@@ -685,7 +696,11 @@ __device__ void select_core(const EngineView& v, uint64_t fl, const float* gs, u
       (uint64_t)win <= v.lam ? v.sparks + (fl * v.lam + (win - 1)) * v.Dp
                              : v.guides + (fl * v.M + (win - 1 - v.lam)) * v.Dp);
   float4* dst = reinterpret_cast<float4*>(v.pos + f * v.Dp);
-  const uint64_t n4 = (v.D + 3) / 4;
+  const uint64_t n4all = (v.D + 3) / 4;
+  const uint64_t q0 = n4all * part / nparts, q1 = n4all * (part + 1) / nparts;
+  src += q0;
+  dst += q0;
+  const uint64_t n4 = q1 - q0;
   const uint32_t nt = blockDim.x;
   uint64_t i = threadIdx.x;
   for (; i + 3 * nt < n4; i += 4 * nt) {
@@ -1087,7 +1102,7 @@ __device__ void small_a_body(const EngineView& v, uint64_t fl, uint64_t* sa_keys
     }
     __syncthreads();
   }
-  select_core(v, fl, gs, nan_local);
+  select_core(v, fl, gs, nan_local, v.fit, 0, 1);
   if (fl == 0 && threadIdx.x == 0) v.ctl->iters_rem = iters_remaining(v);  // after the wave
   __syncthreads();  // shared state (s_idx, gs, keys) free for the next firework
 }
@@ -1467,6 +1482,17 @@ static unsigned guide_blocks(const EngineView& v, int nsm) {
   return (unsigned)(blocks < (uint64_t)nsm * 8 ? (blocks ? blocks : 1) : (uint64_t)nsm * 8);
 }
 
+// k_select blocks per firework: enough to spread the winner-row copy over the
+// SMs (about 8 KB per block), at most 16.
+static unsigned select_parts(const EngineView& v, int nsm) {
+  const uint64_t n4 = (v.D + 3) / 4;
+  uint64_t p = (n4 + 511) / 512;
+  const uint64_t cap = ((uint64_t)nsm * 4 + v.Fl - 1) / v.Fl;
+  p = p < cap ? p : cap;
+  p = p < 16 ? p : 16;
+  return (unsigned)(p ? p : 1);
+}
+
 static unsigned capped(uint64_t g, int nsm) {
   const uint64_t c = (uint64_t)nsm * 16;
   return (unsigned)(g == 0 ? 1 : (g < c ? g : c));
@@ -1496,7 +1522,7 @@ void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
       else
         launch_analytic_partials(v.guides, v.Fl * v.M, v.D, v.Dp, v.nch, v.obj_kind, v.gpart, nsm, s);
     }
-    pdl_launch(k_select, (unsigned)v.Fl, kSelectThreads, 0, s, v);
+    pdl_launch(k_select, dim3((unsigned)v.Fl, select_parts(v, nsm)), kSelectThreads, 0, s, v);
   }
   // replica sharding: loser-out (own batches) closes phase A, the loser
   // counts are exchanged, phase B starts at the reinit
@@ -1558,6 +1584,10 @@ void launch_guides(const EngineView& v, int nsm, cudaStream_t s) {
 void launch_select(const EngineView& v, int nsm, cudaStream_t s) {
   (void)nsm;
   pdl_launch(k_select, (unsigned)v.Fl, kSelectThreads, 0, s, v);
+}
+// The generation's multi-part k_select (needs k_rank's fit_prev).
+void launch_select_gen(const EngineView& v, int nsm, cudaStream_t s) {
+  pdl_launch(k_select, dim3((unsigned)v.Fl, select_parts(v, nsm)), kSelectThreads, 0, s, v);
 }
 void launch_loser(const EngineView& v, int nsm, cudaStream_t s) {
   const unsigned g = (unsigned)((v.F * v.nch + kWarps - 1) / kWarps);

@@ -39,6 +39,7 @@ void launch_explode_map(const EngineView& v, int nsm, cudaStream_t s);
 void launch_rank(const EngineView& v, cudaStream_t s);
 void launch_guides(const EngineView& v, int nsm, cudaStream_t s);
 void launch_select(const EngineView& v, int nsm, cudaStream_t s);
+void launch_select_gen(const EngineView& v, int nsm, cudaStream_t s);
 void launch_loser(const EngineView& v, int nsm, cudaStream_t s);
 void launch_loser_commit(const EngineView& v, int nsm, cudaStream_t s);
 void launch_analytic_partials(const float* rows, uint64_t nrows, uint64_t D,

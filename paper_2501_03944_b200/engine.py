@@ -335,7 +335,7 @@ class Engine:
         _check(A.lib().mgfwa_time_fitness(self.h, iters, C.byref(ms), C.byref(units)), self.h)
         return ms.value, int(units.value)
 
-    KERNELS = {"fitness": 0, "explode": 1, "rank": 2, "guides": 3, "guide_fitness": 4}
+    KERNELS = {"fitness": 0, "explode": 1, "rank": 2, "guides": 3, "guide_fitness": 4, "select": 5}
 
     def time_kernel(self, kernel: str, iters: int = 10):
         """(ms per launch, rows per launch) of one generation kernel on the

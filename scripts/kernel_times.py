@@ -32,7 +32,7 @@ def main():
     eng.sync()
     gen_ms = 1e3 * (time.perf_counter() - t) / a.iters
     out = {"workload": a.workload, "generation_ms_host": gen_ms}
-    ks = ["explode", "rank", "guides"] + (["fitness", "guide_fitness"] if w["kind"] in ("mlp", "lenet") else [])
+    ks = ["explode", "rank", "guides", "select"] + (["fitness", "guide_fitness"] if w["kind"] in ("mlp", "lenet") else [])
     for k in ks:
         ms, units = eng.time_kernel(k, a.iters)
         out[k + "_us"] = round(1e3 * ms, 2)
