@@ -504,15 +504,44 @@ static size_t rank_smem(const EngineView& v) {
 // gather-reduce over 2*top spark rows, HBM-bound).  The analytic fitness of
 // the guides is computed afterwards by k_analytic_partials (same grouping as
 // every other fitness, so cached fitness == re-evaluated fitness bit-wise).
+#ifndef GUIDES_VEC
+#define GUIDES_VEC 2  // coordinates per lane (2: float2, 4: float4; measured: 4 is slower on C2, 13.1 -> 15.2 us)
+#endif
+template <int V> struct VecT;
+template <> struct VecT<2> { using T = float2; };
+template <> struct VecT<4> { using T = float4; };
+template <int V>
+__device__ __forceinline__ void vec_split(const typename VecT<V>::T& q, float (&o)[V]) {
+  if constexpr (V == 2) {
+    o[0] = q.x, o[1] = q.y;
+  } else {
+    o[0] = q.x, o[1] = q.y, o[2] = q.z, o[3] = q.w;
+  }
+}
+
+template <int V>
+__device__ __forceinline__ void store_guide(const EngineView& v, uint64_t off, const float (&x)[V]) {
+  if constexpr (V == 2) {
+    *reinterpret_cast<float2*>(v.guides + off) = make_float2(x[0], x[1]);
+    if (v.nn) *reinterpret_cast<__nv_bfloat162*>(v.guides_h + off) = __floats2bfloat162_rn(x[0], x[1]);
+  } else {
+    *reinterpret_cast<float4*>(v.guides + off) = make_float4(x[0], x[1], x[2], x[3]);
+    if (v.nn) store_bf16x4(v.guides_h, off, x);
+  }
+}
+
 __global__ void __launch_bounds__(256) k_guides(EngineView v) {
+  constexpr int V = GUIDES_VEC;
+  using VT = typename VecT<V>::T;
+  constexpr int U = 32 / V;  // rank pairs per unrolled step (2U independent V-wide loads per lane)
   pdl_enter();
   if (gen_inactive(v)) return;
   extern __shared__ uint64_t s_pre[];  // [M] kGuide key prefixes, then [2*top] rank lists
   int* s_idx = reinterpret_cast<int*>(s_pre + v.M);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t it = v.ctl->iteration;
-  const uint64_t nsl = (v.D + 63) / 64;  // 64-coordinate slices (float2 per lane)
-  const uint64_t bpf = (nsl + kWarps - 1) / kWarps;  // blocks per firework
+  const uint64_t nsl = (v.D + 32 * V - 1) / (32 * V);  // 32V-coordinate slices (V per lane)
+  const uint64_t bpf = (nsl + kWarps - 1) / kWarps;     // blocks per firework
   const uint64_t top = v.top;
   for (uint64_t blk = blockIdx.x; blk < v.Fl * bpf; blk += gridDim.x) {
     const uint64_t fl = blk / bpf, f = v.f_lo + fl;  // local / global firework
@@ -523,56 +552,67 @@ __global__ void __launch_bounds__(256) k_guides(EngineView v) {
     // hoisted rng.hpp:43-51 up to field m: one splitmix64 round per coordinate
     for (uint64_t m = threadIdx.x; m < v.M; m += blockDim.x) s_pre[m] = key_prefix(v.seed, kGuide, it, b, n, m);
     __syncthreads();
-    const uint64_t d0 = c * 64 + lane * 2;
+    const uint64_t d0 = c * 32 * V + lane * V;
     if (c >= nsl || d0 >= v.D) continue;
     const float* sb = v.sparks + fl * v.lam * v.Dp + d0;
-    double acc0 = 0.0, acc1 = 0.0;
-    uint64_t t = 0;
-    // 32 independent 8-byte loads in flight per lane, summed in rank order
-    for (; t + 16 <= top; t += 16) {
-      float2 bb[16], ww[16];
+    double acc[V];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        bb[i] = *reinterpret_cast<const float2*>(sb + (uint64_t)s_idx[t + i] * v.Dp);
-        ww[i] = *reinterpret_cast<const float2*>(sb + (uint64_t)s_idx[top + t + i] * v.Dp);
+    for (int e = 0; e < V; ++e) acc[e] = 0.0;
+    uint64_t t = 0;
+    // 2U independent loads in flight per lane, summed in rank order
+    for (; t + U <= top; t += U) {
+      VT bb[U], ww[U];
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        bb[i] = *reinterpret_cast<const VT*>(sb + (uint64_t)s_idx[t + i] * v.Dp);
+        ww[i] = *reinterpret_cast<const VT*>(sb + (uint64_t)s_idx[top + t + i] * v.Dp);
       }
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        acc0 = __dadd_rn(acc0, __dsub_rn((double)bb[i].x, (double)ww[i].x));
-        acc1 = __dadd_rn(acc1, __dsub_rn((double)bb[i].y, (double)ww[i].y));
+      for (int i = 0; i < U; ++i) {
+        float bf_[V], wf_[V];
+        vec_split<V>(bb[i], bf_);
+        vec_split<V>(ww[i], wf_);
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc[e] = __dadd_rn(acc[e], __dsub_rn((double)bf_[e], (double)wf_[e]));
       }
     }
     for (; t + 4 <= top; t += 4) {
-      float2 bb[4], ww[4];
+      VT bb[4], ww[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        bb[i] = *reinterpret_cast<const float2*>(sb + (uint64_t)s_idx[t + i] * v.Dp);
-        ww[i] = *reinterpret_cast<const float2*>(sb + (uint64_t)s_idx[top + t + i] * v.Dp);
+        bb[i] = *reinterpret_cast<const VT*>(sb + (uint64_t)s_idx[t + i] * v.Dp);
+        ww[i] = *reinterpret_cast<const VT*>(sb + (uint64_t)s_idx[top + t + i] * v.Dp);
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        acc0 = __dadd_rn(acc0, __dsub_rn((double)bb[i].x, (double)ww[i].x));
-        acc1 = __dadd_rn(acc1, __dsub_rn((double)bb[i].y, (double)ww[i].y));
+        float bf_[V], wf_[V];
+        vec_split<V>(bb[i], bf_);
+        vec_split<V>(ww[i], wf_);
+#pragma unroll
+        for (int e = 0; e < V; ++e) acc[e] = __dadd_rn(acc[e], __dsub_rn((double)bf_[e], (double)wf_[e]));
       }
     }
     for (; t < top; ++t) {
-      const float2 bt = *reinterpret_cast<const float2*>(sb + (uint64_t)s_idx[t] * v.Dp);
-      const float2 wt = *reinterpret_cast<const float2*>(sb + (uint64_t)s_idx[top + t] * v.Dp);
-      acc0 = __dadd_rn(acc0, __dsub_rn((double)bt.x, (double)wt.x));
-      acc1 = __dadd_rn(acc1, __dsub_rn((double)bt.y, (double)wt.y));
+      float bf_[V], wf_[V];
+      vec_split<V>(*reinterpret_cast<const VT*>(sb + (uint64_t)s_idx[t] * v.Dp), bf_);
+      vec_split<V>(*reinterpret_cast<const VT*>(sb + (uint64_t)s_idx[top + t] * v.Dp), wf_);
+#pragma unroll
+      for (int e = 0; e < V; ++e) acc[e] = __dadd_rn(acc[e], __dsub_rn((double)bf_[e], (double)wf_[e]));
     }
     const double dtop = (double)top;
-    const double delta[2] = {__ddiv_rn(acc0, dtop), __ddiv_rn(acc1, dtop)};
-    const float2 p2 = *reinterpret_cast<const float2*>(v.pos + f * v.Dp + d0);
-    const float pv[2] = {p2.x, p2.y};
+    double delta[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) delta[e] = __ddiv_rn(acc[e], dtop);
+    float pv[V];
+    vec_split<V>(*reinterpret_cast<const VT*>(v.pos + f * v.Dp + d0), pv);
     const float* plo = v.pop_lo + b * v.Dp;
     const float* phi = v.pop_hi + b * v.Dp;
     for (uint64_t m = 0; m < v.M; ++m) {
       const double beta = v.boosts[m];
       const uint64_t pg = s_pre[m];
-      float x[2];
+      float x[V];
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
+      for (int e = 0; e < V; ++e) {
         const uint64_t d = d0 + e;
         if (d < v.D) {
           const double gx = __dadd_rn((double)pv[e], __dmul_rn(beta, delta[e]));
@@ -581,9 +621,7 @@ __global__ void __launch_bounds__(256) k_guides(EngineView v) {
           x[e] = 0.0f;
         }
       }
-      const uint64_t off = (fl * v.M + m) * v.Dp + d0;  // local guide row
-      *reinterpret_cast<float2*>(v.guides + off) = make_float2(x[0], x[1]);
-      if (v.nn) *reinterpret_cast<__nv_bfloat162*>(v.guides_h + off) = __floats2bfloat162_rn(x[0], x[1]);
+      store_guide<V>(v, (fl * v.M + m) * v.Dp + d0, x);  // local guide row
     }
   }
 }
@@ -1477,7 +1515,7 @@ void launch_key_hash(const uint64_t* keys, uint64_t n, uint64_t* out,
 static size_t guides_smem(const EngineView& v) { return v.M * sizeof(uint64_t) + 2 * v.top * sizeof(int); }
 
 static unsigned guide_blocks(const EngineView& v, int nsm) {
-  const uint64_t nsl = (v.D + 63) / 64;
+  const uint64_t nsl = (v.D + 32 * GUIDES_VEC - 1) / (32 * GUIDES_VEC);
   const uint64_t blocks = v.Fl * ((nsl + kWarps - 1) / kWarps);
   return (unsigned)(blocks < (uint64_t)nsm * 8 ? (blocks ? blocks : 1) : (uint64_t)nsm * 8);
 }
