@@ -85,7 +85,8 @@ def test_sharded_run_bit_identical(P, kind, world):
 
 
 @pytest.mark.parametrize("kind", ["sphere", "mlp"])
-def test_nccl_exchange_path_matches(P, kind):
+@pytest.mark.parametrize("mode", ["firework", "replica"])
+def test_nccl_exchange_path_matches(P, kind, mode):
     """A 1-rank NCCL communicator runs the sharded stepping (phase A, in-place
     all-gather over NCCL, phase B) on one GPU; results must equal the plain
     run bit for bit."""
@@ -99,7 +100,7 @@ def test_nccl_exchange_path_matches(P, kind):
     ref, _ = _reference(P, cfg, space, obj, 5)
     uid = P.Engine.nccl_unique_id()
     assert len(uid) == 128
-    e = P.Engine(cfg, space, obj, 5, rank=0, world=1)
+    e = P.Engine(cfg, space, obj, 5, rank=0, world=1, shard_mode=mode)
     e.attach_nccl(uid)
     e.run()
     r = e.record()
