@@ -220,7 +220,7 @@ def test_lenet_zero_weights_ln10(P):
     np.testing.assert_allclose(got, np.log(10.0), rtol=0, atol=1e-6)
 
 
-@pytest.mark.parametrize("S,scale", [(256, 0.1), (200, 0.3), (136, 0.05)])
+@pytest.mark.parametrize("S,scale", [(256, 0.1), (200, 0.3), (136, 0.05), (3, 0.2), (129, 0.1)])
 def test_lenet_fitness_vs_oracle(P, oracle, S, scale):
     desc = O.ObjectiveDesc(kind=O.OBJ_LENET, samples=S)
     rng = np.random.default_rng(S)
