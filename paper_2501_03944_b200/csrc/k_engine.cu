@@ -379,7 +379,10 @@ __global__ void __launch_bounds__(256, 2) k_explode_map(EngineView v) {
 static unsigned explode_blocks(const EngineView& v, int nsm) {
   const uint64_t ngrp = (v.lam + kSparkGroup - 1) / kSparkGroup;
   const uint64_t items = v.Fl * v.nch * ((ngrp + kWarps - 1) / kWarps);
-  const uint64_t cap = (uint64_t)nsm * 8;
+#ifndef EXPLODE_CAP_MULT
+#define EXPLODE_CAP_MULT 256  // blocks per SM cap (measured: 8 -> 256 is 4% faster on C2, C3, C5: finer tail)
+#endif
+  const uint64_t cap = (uint64_t)nsm * EXPLODE_CAP_MULT;
   return (unsigned)(items < cap ? items : cap);
 }
 
@@ -1518,7 +1521,11 @@ static size_t guides_smem(const EngineView& v) { return v.M * sizeof(uint64_t) +
 static unsigned guide_blocks(const EngineView& v, int nsm) {
   const uint64_t nsl = (v.D + 32 * GUIDES_VEC - 1) / (32 * GUIDES_VEC);
   const uint64_t blocks = v.Fl * ((nsl + kWarps - 1) / kWarps);
-  return (unsigned)(blocks < (uint64_t)nsm * 8 ? (blocks ? blocks : 1) : (uint64_t)nsm * 8);
+#ifndef GUIDES_CAP_MULT
+#define GUIDES_CAP_MULT 64  // measured: C5 guides 3.37 -> 3.17 ms vs 8
+#endif
+  const uint64_t cap = (uint64_t)nsm * GUIDES_CAP_MULT;
+  return (unsigned)(blocks < cap ? (blocks ? blocks : 1) : cap);
 }
 
 // k_select blocks per firework: enough to spread the winner-row copy over the
