@@ -155,7 +155,10 @@ __global__ void k_pop_range(EngineView v) {
 // per lane.  Out-of-box coordinates are common (C2: 35% of them once the
 // amplitudes reach the range, so nearly every warp has one in every spark
 // slice); this dense form beats every compaction variant measured.
-constexpr int kSparkGroup = 4;
+#ifndef EXPLODE_KG
+#define EXPLODE_KG 4
+#endif
+constexpr int kSparkGroup = EXPLODE_KG;
 
 // t = -1 + u * 2 for u = (h >> 11) * 2^-53, exactly as the reference's
 // uniform_sample(key, -1, 1) (rng.hpp:55-65): with m = h >> 11 and
