@@ -16,14 +16,17 @@
 // k_lenet_conv — one sample per warp, 12 warps per SM, no block-wide
 // synchronisation inside a work item (candidate x 128-sample chunk); only the
 // candidate's conv weights are staged (B fragments then live in registers):
-//   * conv1: M = 784 output pixels in pool order: a 16-row tile = 4 pool
-//     windows, rows r and r + 8 the two vertically adjacent pixels of a window,
-//     so in the accumulator layout a thread holds both rows of its window
-//     (vertical pool in-thread) and the horizontal pair is one shuffle;
-//     K = 5 rows x 6 taps (kx padded), A fragments read as 32-bit pairs from the
-//     sample's "pair image" (x, x+1), precomputed once per plan (the dataset
-//     never changes) and prefetched with cp.async;
-//   * conv2: M = 100 pixels (same pool order), K = 25 taps x 8 channels (6 + 2
+//   * conv1: M = 784 output pixels as 25 tile pairs (conv1_pairs): a pair =
+//     8 pool windows (MMA row g), its two tiles the windows' two pixel rows,
+//     MMA rows g / g + 8 their two columns, so a thread holds all four pixels
+//     of its window (ReLU + pool in registers, no shuffle); K = 5 rows x 6
+//     taps (kx padded), A fragments read from the sample's "pair image"
+//     (x, x+1) — each register pair one 64-bit load — precomputed once per
+//     plan (the dataset never changes) and prefetched with cp.async
+//     (conv1_tiles, the single-tile form with a shuffle, is kept behind
+//     LENET_CONV1_PAIRS=0 and gives bit-identical results);
+//   * conv2: M = 100 pixels in pool order (rows r / r + 8 a window's two pixel
+//     rows, the horizontal pair one shuffle), K = 25 taps x 8 channels (6 + 2
 //     zero), N = 16, taps ordered so that a fragment's row-(g+8) word equals
 //     its second tap's row-g word (conv2_k): 30 shared-memory loads per tile
 //     feed 26 MMAs;
