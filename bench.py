@@ -100,6 +100,20 @@ def make_objective(P, w):
     return {"sphere": P.Sphere(), "rastrigin": P.Rastrigin(), "ackley": P.Ackley()}[w["kind"]]
 
 
+class stdout_to_stderr:
+    """fd-level redirect of stdout to stderr (native libraries print there)."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 def make_config(P, w, max_evals):
     return P.MgfwaConfig(batches=w["B"], fireworks=w["mu"], sparks_per_firework=w["lam"],
                          guides_per_firework=w["M"], boosts=[1.0, 2.0, 4.0][: w["M"]],
@@ -265,7 +279,9 @@ def main():
         os.environ.setdefault("WORLD_SIZE", str(world))
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        with stdout_to_stderr():  # NCCL's version banner: keep stdout to the one JSON line
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()
     else:
         torch.cuda.set_device(0)
     import paper_2501_03944_b200 as P
@@ -292,7 +308,8 @@ def main():
         if rank == 0:
             uid.copy_(torch.frombuffer(bytearray(P.Engine.nccl_unique_id()), dtype=torch.uint8))
         torch.distributed.broadcast(uid, 0)
-        eng.attach_nccl(bytes(uid.cpu().numpy().tobytes()))
+        with stdout_to_stderr():
+            eng.attach_nccl(bytes(uid.cpu().numpy().tobytes()))
     eng.set_stream(stream.cuda_stream)
     eng.initialize()
     kpg = eng.kernels_per_generation()
@@ -412,7 +429,8 @@ def main():
         if rank == 0:
             u.copy_(torch.frombuffer(bytearray(P.Engine.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(u, 0)
-        e.attach_nccl(bytes(u.cpu().numpy().tobytes()))
+        with stdout_to_stderr():
+            e.attach_nccl(bytes(u.cpu().numpy().tobytes()))
 
         def sharded_once():
             dist.barrier()
