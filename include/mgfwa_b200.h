@@ -136,6 +136,18 @@ int mgfwa_get_trace(mgfwa_ctx_t ctx, uint64_t* evaluations, double* best,
 int mgfwa_get_state(mgfwa_ctx_t ctx, double* positions, double* fitness,
                     double* amplitudes, double* last_improvement);
 
+/* The candidate sets of the last generation run on ctx, as the reference's
+ * run() loop holds them before select_best (engine.cpp:369-384): the mapped
+ * sparks [Fl*lambda][D] (SparkSet.positions after random_mapping, kMapping)
+ * with their fitness, the mapped guiding sparks [Fl*M][D] (GuideSet after
+ * random_mapping, kGuide) with their fitness, and, for the tensor-core
+ * objectives, the bf16 shadow of the sparks the fitness kernel read.  Fl =
+ * fireworks owned by ctx (B*mu unsharded).  Any pointer may be NULL.  Used by
+ * the parity tests to check the real generation path step by step. */
+int mgfwa_get_candidates(mgfwa_ctx_t ctx, double* sparks, double* spark_fitness,
+                         double* guides, double* guide_fitness,
+                         uint16_t* sparks_bf16);
+
 /* One-shot run() over host buffers — the plain drop-in for
  * run(config, space, objective, backend, seed) (engine.hpp:130-132).
  * trace arrays are [B][trace_cap] and may be NULL. */

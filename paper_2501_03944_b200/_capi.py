@@ -62,6 +62,7 @@ SIGNATURES = {
     "mgfwa_get_best": (_int, [_P, _pd, _pd]),
     "mgfwa_get_trace": (_int, [_P, _pu64, _pd, _pd, _u64, _pu64]),
     "mgfwa_get_state": (_int, [_P, _pd, _pd, _pd, _pd]),
+    "mgfwa_get_candidates": (_int, [_P, _pd, _pd, _pd, _pd, C.POINTER(C.c_uint16)]),
     "mgfwa_run_once": (_int, [C.POINTER(mgfwa_config_t), C.POINTER(mgfwa_space_t),
                               C.POINTER(mgfwa_objective_t), _u64, _int, _pd, _pd, _pu64, _pd, _pd,
                               _u64, C.POINTER(mgfwa_counters_t)]),

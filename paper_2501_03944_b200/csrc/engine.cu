@@ -108,9 +108,11 @@ static Status validate_config(const HostConfig& c) {
       if (!(b > 0.0) || !std::isfinite(b))
         return invalid("MgfwaConfig: boost coefficients must be positive finite");
     if (c.M > 16) return invalid("mgfwa_b200: guides_per_firework > 16 is not supported");
-    if (c.lam > kMaxSparksPerFirework)
-      return invalid("mgfwa_b200: sparks_per_firework > 16384 is not supported");
   }
+  // k_rank keeps one 8-byte key per spark in shared memory on every
+  // generation, with or without guides
+  if (c.lam > kMaxSparksPerFirework)
+    return invalid("mgfwa_b200: sparks_per_firework > 16384 is not supported");
   return ok();
 }
 
@@ -581,6 +583,8 @@ class Engine {
   std::vector<std::vector<uint64_t>> tr_evals;
   std::vector<std::vector<double>> tr_best, tr_wall;
   uint64_t host_trace_n = 0;
+  uint64_t pending_gens = 0;  // generations enqueued since the last sync (trace ring bound)
+  bool nan_flushed = false;   // replica + NCCL: end-of-run NaN all-reduce done
   std::vector<uint64_t> ring_e;
   std::vector<double> ring_b;
   std::vector<uint64_t> ring_t;
@@ -619,6 +623,7 @@ class Engine {
       ws = std::make_unique<Workspace>();
       STATUS_TRY(ws->build(cfg, space, obj, seed, device, 1024, rank, world));
     }
+    ws->v.nan_mode = world > 1 ? 1 : 0;  // 2 once a communicator is attached
     if (!ws->stream) CUDA_TRY(cudaStreamCreateWithFlags(&ws->stream, cudaStreamNonBlocking));
     own_stream = ws->stream;
     stream = own_stream;
@@ -634,9 +639,15 @@ class Engine {
 
   Status capture_one(int phase, cudaGraphExec_t* out, size_t* nodes) {
     cudaGraph_t g = nullptr;
+    (void)cudaGetLastError();  // clear a stale error so the check below sees this capture's
     CUDA_TRY(cudaStreamBeginCapture(own_stream, cudaStreamCaptureModeThreadLocal));
     launch_generation_kernels(ws->v, ws->nsm, own_stream, &hooks, phase);
+    const cudaError_t le = cudaGetLastError();  // a failed launch inside the capture
     cudaError_t e = cudaStreamEndCapture(own_stream, &g);
+    if (le != cudaSuccess) {
+      if (g) cudaGraphDestroy(g);
+      return Status{MGFWA_ECUDA, std::string("kernel launch during graph capture: ") + cudaGetErrorString(le)};
+    }
     if (e != cudaSuccess) return Status{MGFWA_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e)};
     cudaGraphGetNodes(g, nullptr, nodes);
     e = cudaGraphInstantiate(out, g, 0);
@@ -697,6 +708,7 @@ class Engine {
     memcpy(&id, unique_id, sizeof(id));
     CUDA_TRY(cudaSetDevice(ws->device));
     NCCL_TRY(nccl().CommInitRank(&comm, nranks, id, r));
+    ws->v.nan_mode = 2;  // NaN counts of shard-local work are all-reduced by the exchange
     return ok();
   }
 
@@ -724,13 +736,15 @@ class Engine {
 
   Status exchange_nccl() {
     const EngineView& v = ws->v;
+    NCCL_TRY(nccl().GroupStart());
+    NCCL_TRY(nccl().AllReduce(&v.ctl->nan_own, &v.ctl->nan_all, 1, ncclUint64, ncclSum, comm, stream));
     if (v.replica) {
       NCCL_TRY(nccl().AllReduce(&v.ctl->n_losers_all, &v.ctl->n_losers_all, 1, ncclUint64, ncclSum, comm,
                                 stream));
+      NCCL_TRY(nccl().GroupEnd());
       return ok();
     }
     const size_t rows = v.Fl * v.Dp;
-    NCCL_TRY(nccl().GroupStart());
     NCCL_TRY(nccl().AllGather(v.pos + v.f_lo * v.Dp, v.pos, rows, ncclFloat, comm, stream));
     NCCL_TRY(nccl().AllGather(v.fit + v.f_lo, v.fit, v.Fl, ncclFloat64, comm, stream));
     NCCL_TRY(nccl().AllGather(v.amp + v.f_lo, v.amp, v.Fl, ncclFloat64, comm, stream));
@@ -746,8 +760,8 @@ class Engine {
     const EngineView& b = src.ws->v;
     if (a.F != b.F || a.Dp != b.Dp || a.Fl != b.Fl) return invalid("mgfwa_shard_exchange: shape mismatch");
     if (a.replica != b.replica) return invalid("mgfwa_shard_exchange: shard modes differ");
+    launch_add_losers(a.ctl, b.ctl, a.replica, stream);
     if (a.replica) {
-      launch_add_losers(a.ctl, b.ctl, stream);
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaStreamSynchronize(stream));
       return ok();
@@ -766,6 +780,7 @@ class Engine {
     launch_generation_kernels(ws->v, ws->nsm, stream, &hooks, ph);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaStreamSynchronize(stream));
+    if (ph == kGenB && ++pending_gens >= ws->v.trace_cap - 2) STATUS_TRY(sync());
     return ok();
   }
 
@@ -778,6 +793,7 @@ class Engine {
     tr_best.assign(cfg.B, {});
     tr_wall.assign(cfg.B, {});
     host_trace_n = 0;
+    nan_flushed = false;
     STATUS_TRY(sync());
     initialized = true;
     return capture();
@@ -787,6 +803,7 @@ class Engine {
   Status sync() {
     CUDA_TRY(cudaMemcpyAsync(host_ctl, ws->v.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
     CUDA_TRY(cudaStreamSynchronize(stream));
+    pending_gens = 0;
     const uint64_t n = host_ctl->trace_n;
     if (n > host_trace_n) {
       const uint64_t cap = ws->v.trace_cap, B = cfg.B;
@@ -808,8 +825,25 @@ class Engine {
     return ok();
   }
 
+  // The device trace is a ring of trace_cap waves; at most trace_cap - 2
+  // generations may run between two syncs or the oldest points would be
+  // overwritten before the host copies them.  enqueue() syncs internally
+  // when a request would cross that bound (so a long asynchronous enqueue
+  // becomes partly synchronous instead of losing trace points).
   Status enqueue(uint64_t n) {
     if (!initialized) return Status{MGFWA_ESTATE, "mgfwa: initialize() must precede the loop"};
+    const uint64_t room = ws->v.trace_cap - 2;
+    while (n > 0) {
+      if (pending_gens >= room) STATUS_TRY(sync());
+      const uint64_t k = std::min(n, room - pending_gens);
+      STATUS_TRY(enqueue_chunk(k));
+      pending_gens += k;
+      n -= k;
+    }
+    return ok();
+  }
+
+  Status enqueue_chunk(uint64_t n) {
     if (persistent()) {
       if (n > 0) CUDA_TRY(launch_small_run(ws->v, n, stream));
       return ok();
@@ -851,6 +885,15 @@ class Engine {
       STATUS_TRY(sync());
       done += host_ctl->gens_run - before;
       if (host_ctl->gens_run == before) break;
+    }
+    // Replica shards count their own losers' NaN evaluations after the
+    // exchange, so the last generation's travel with one more all-reduce.
+    if (comm && ws->v.replica && !host_ctl->active && !nan_flushed) {  // collective: every rank ends together
+      NCCL_TRY(nccl().AllReduce(&ws->v.ctl->nan_own, &ws->v.ctl->nan_all, 1, ncclUint64, ncclSum, comm, stream));
+      launch_fold_nan(ws->v.ctl, stream);
+      CUDA_TRY(cudaGetLastError());
+      nan_flushed = true;
+      STATUS_TRY(sync());
     }
     if (ran) *ran = done;
     return ok();
@@ -902,6 +945,49 @@ class Engine {
       if (fit) fit[i] = f[i];
       if (amp) amp[i] = a[i];
       if (li) li[i] = l[i];
+    }
+    return ok();
+  }
+
+  // The candidate buffers of the last generation (owned fireworks).
+  Status candidates(double* sparks, double* sfit, double* guides, double* gfit, uint16_t* sparks_bf16) {
+    const EngineView& v = ws->v;
+    const uint64_t P = v.Fl * v.lam, G = v.Fl * v.M, D = v.D, Dp = v.Dp;
+    if (sparks_bf16 && v.sparks_h == nullptr)
+      return invalid("mgfwa_get_candidates: no bf16 spark shadow (objective is not a tensor-core one)");
+    if ((guides || gfit) && G == 0) return invalid("mgfwa_get_candidates: no guiding sparks (M = 0)");
+    CUDA_TRY(cudaStreamSynchronize(stream));
+    const uint64_t chunk = 4096;  // rows per staging copy (bounded host memory at C5 shapes)
+    std::vector<float> rows;
+    std::vector<uint16_t> rows_h;
+    auto copy_rows = [&](const float* src, uint64_t n, double* dst) -> Status {
+      for (uint64_t r0 = 0; r0 < n; r0 += chunk) {
+        const uint64_t m = std::min(chunk, n - r0);
+        rows.resize(m * Dp);
+        CUDA_TRY(cudaMemcpy(rows.data(), src + r0 * Dp, m * Dp * 4, cudaMemcpyDeviceToHost));
+        for (uint64_t r = 0; r < m; ++r)
+          for (uint64_t d = 0; d < D; ++d) dst[(r0 + r) * D + d] = rows[r * Dp + d];
+      }
+      return ok();
+    };
+    auto copy_fit = [&](const float* src, uint64_t n, double* dst) -> Status {
+      std::vector<float> f(n);
+      CUDA_TRY(cudaMemcpy(f.data(), src, n * 4, cudaMemcpyDeviceToHost));
+      for (uint64_t i = 0; i < n; ++i) dst[i] = f[i];
+      return ok();
+    };
+    if (sparks) STATUS_TRY(copy_rows(v.sparks, P, sparks));
+    if (sfit) STATUS_TRY(copy_fit(v.sfit, P, sfit));
+    if (guides) STATUS_TRY(copy_rows(v.guides, G, guides));
+    if (gfit) STATUS_TRY(copy_fit(v.gfit, G, gfit));
+    if (sparks_bf16) {
+      for (uint64_t r0 = 0; r0 < P; r0 += chunk) {
+        const uint64_t m = std::min(chunk, P - r0);
+        rows_h.resize(m * Dp);
+        CUDA_TRY(cudaMemcpy(rows_h.data(), v.sparks_h + r0 * Dp, m * Dp * 2, cudaMemcpyDeviceToHost));
+        for (uint64_t r = 0; r < m; ++r)
+          for (uint64_t d = 0; d < D; ++d) sparks_bf16[(r0 + r) * D + d] = rows_h[r * Dp + d];
+      }
     }
     return ok();
   }
@@ -1101,7 +1187,7 @@ int mgfwa_get_trace(mgfwa_ctx_t ctx, uint64_t* evaluations, double* best, double
   const uint64_t n = e.host_trace_n;
   if (waves) *waves = n;
   for (uint64_t b = 0; b < e.cfg.B; ++b)
-    for (uint64_t w = 0; w < n && w < cap; ++w) {
+    for (uint64_t w = 0; w < n && w < cap && w < e.tr_evals[b].size(); ++w) {
       if (evaluations) evaluations[b * cap + w] = e.tr_evals[b][w];
       if (best) best[b * cap + w] = e.tr_best[b][w];
       if (wall_ms) wall_ms[b * cap + w] = e.tr_wall[b][w];
@@ -1112,6 +1198,11 @@ int mgfwa_get_trace(mgfwa_ctx_t ctx, uint64_t* evaluations, double* best, double
 int mgfwa_get_state(mgfwa_ctx_t ctx, double* positions, double* fitness, double* amplitudes,
                     double* last_improvement) {
   return fail(ctx, ctx->engine.state(positions, fitness, amplitudes, last_improvement));
+}
+
+int mgfwa_get_candidates(mgfwa_ctx_t ctx, double* sparks, double* spark_fitness, double* guides,
+                         double* guide_fitness, uint16_t* sparks_bf16) {
+  return fail(ctx, ctx->engine.candidates(sparks, spark_fitness, guides, guide_fitness, sparks_bf16));
 }
 
 int mgfwa_run_once(const mgfwa_config_t* config, const mgfwa_space_t* space,

@@ -36,6 +36,13 @@ struct Ctl {
   unsigned bar_count;     // grid barrier of the persistent small-problem loop
   unsigned bar_gen;
   uint64_t n_losers_all;  // replica sharding: losers of the generation over all shards
+  // sharded runs (EngineView::nan_mode != 0): NaN evaluations of work only
+  // this shard did (phase A; replica mode: also its own losers) go to
+  // nan_own; the exchange brings the other shards' counts into nan_all
+  // (NCCL: the all-reduced total), and k_finalize_record(1) folds them into
+  // nan_count, so nan_evaluations is the global count on every shard.
+  uint64_t nan_own;
+  uint64_t nan_all;
 };
 
 struct EngineView {
@@ -53,6 +60,9 @@ struct EngineView {
   // for those batches only and the shards exchange just the loser count.
   int replica;
   uint64_t b_lo, b_hi;
+  // NaN accounting across shards: 0 unsharded, 1 emulated shards (in-process
+  // exchange adds the peers' nan_own), 2 NCCL (all-reduced nan_own).
+  int nan_mode;
   uint32_t nparts;     // partial-sum slots per row
   uint32_t nch;        // coordinate chunks per row (kChunk each)
   int obj_kind;

@@ -32,6 +32,11 @@ namespace {
 
 constexpr int kWarps = 8;  // warps per block for the work-item kernels
 
+// Counter for NaN evaluations of work only this shard does (Ctl::nan_own).
+__device__ __forceinline__ unsigned long long* nan_counter_own(const EngineView& v) {
+  return (unsigned long long*)(v.nan_mode ? &v.ctl->nan_own : &v.ctl->nan_count);
+}
+
 __device__ __forceinline__ bool gen_inactive(const EngineView& v) {
   return *(volatile int*)&v.ctl->active == 0;
 }
@@ -472,8 +477,7 @@ __global__ void __launch_bounds__(kRankThreads) k_rank(EngineView v) {
       keys[k0 + lane] = rank_key(xl, k0 + lane);
     }
   }
-  if (lane == 0 && nan_local)
-    atomicAdd((unsigned long long*)&v.ctl->nan_count, (unsigned long long)nan_local);
+  if (lane == 0 && nan_local) atomicAdd(nan_counter_own(v), (unsigned long long)nan_local);
   if (v.M == 0) return;
   __syncthreads();
   // Rank by counting: keys are a total order with distinct values, so
@@ -706,8 +710,7 @@ __device__ void select_core(const EngineView& v, uint64_t fl, const float* gs, u
   if ((threadIdx.x & 31) == 0) {
     sv[w] = best_v;
     so[w] = best_o;
-    if (nan_local && part == 0)
-      atomicAdd((unsigned long long*)&v.ctl->nan_count, (unsigned long long)nan_local);
+    if (nan_local && part == 0) atomicAdd(nan_counter_own(v), (unsigned long long)nan_local);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -830,7 +833,16 @@ __global__ void k_loser(EngineView v) {
 
 // Replica sharding, in-process exchange (tests): add another shard's loser
 // count of this generation.
-__global__ void k_add_losers(Ctl* dst, const Ctl* src) { dst->n_losers_all += (uint64_t)src->n_losers; }
+__global__ void k_fold_nan(Ctl* ctl) {
+  ctl->nan_count += ctl->nan_all;
+  ctl->nan_own = ctl->nan_all = 0;
+}
+void launch_fold_nan(Ctl* ctl, cudaStream_t s) { k_fold_nan<<<1, 1, 0, s>>>(ctl); }
+
+__global__ void k_add_losers(Ctl* dst, const Ctl* src, int losers) {
+  if (losers) dst->n_losers_all += (uint64_t)src->n_losers;
+  dst->nan_all += src->nan_own;
+}
 
 // ------------------------------------------------------------ fresh rows
 // mode 0: initialize (engine.cpp:56-64): every firework, kInit, iteration 0.
@@ -892,6 +904,14 @@ __global__ void __launch_bounds__(256) k_fresh_rows(EngineView v, int mode) {
 __global__ void k_finalize_record(EngineView v, int mode) {
   pdl_enter<true>();
   Ctl* ctl = v.ctl;
+  if (mode == 1 && v.nan_mode) {
+    // fold the shards' NaN counts of this generation's exchange (Ctl::nan_own)
+    if (threadIdx.x == 0) {
+      ctl->nan_count += v.nan_mode == 2 ? ctl->nan_all : ctl->nan_own + ctl->nan_all;
+      ctl->nan_own = ctl->nan_all = 0;
+    }
+    __syncthreads();
+  }
   if (mode == 1 && gen_inactive(v)) {
     for (uint64_t b = threadIdx.x; b < v.B; b += blockDim.x) v.rec_flag[b] = 0;
     return;
@@ -912,8 +932,10 @@ __global__ void k_finalize_record(EngineView v, int mode) {
       }
     }
   }
+  // replica shards evaluate only their own batches' losers: shard-local work
   if (lane == 0 && nan_local)
-    atomicAdd((unsigned long long*)&ctl->nan_count, (unsigned long long)nan_local);
+    atomicAdd(mode == 1 && v.replica ? nan_counter_own(v) : (unsigned long long*)&ctl->nan_count,
+              (unsigned long long)nan_local);
   __syncthreads();
   if (mode == 0 && threadIdx.x == 0) {
     ctl->used = v.F;
@@ -1091,7 +1113,9 @@ __device__ void small_a_body(const EngineView& v, uint64_t fl, uint64_t* sa_keys
     float x[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) rows[r] = (k0 + r < lam) ? (int64_t)(fl * lam + k0 + r) : -1;
-    finalize_rows<R>(v, v.spart, rows, x, nan_local);
+    unsigned nan_rows = 0;  // equal on every lane: counted once (select_core sums the warp)
+    finalize_rows<R>(v, v.spart, rows, x, nan_rows);
+    nan_local += lane == 0 ? nan_rows : 0u;
 #pragma unroll
     for (int r = 0; r < R; ++r)
       if (lane == r && rows[r] >= 0) {
@@ -1607,7 +1631,9 @@ void launch_finalize_rows(const EngineView& v, const float* part, uint64_t nrows
   pdl_launch(k_finalize_rows, (unsigned)((nrows + 7) / 8), 256, 0, s, v, part, nrows, fitness, nan);
 }
 
-void launch_add_losers(Ctl* dst, const Ctl* src, cudaStream_t s) { k_add_losers<<<1, 1, 0, s>>>(dst, src); }
+void launch_add_losers(Ctl* dst, const Ctl* src, int losers, cudaStream_t s) {
+  k_add_losers<<<1, 1, 0, s>>>(dst, src, losers);
+}
 
 void launch_to_bf16(const float* src, __nv_bfloat16* dst, uint64_t n, cudaStream_t s) {
   pdl_launch(k_to_bf16, (unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096), 256, 0, s, src, dst, n);

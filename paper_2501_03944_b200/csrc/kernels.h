@@ -55,7 +55,10 @@ void launch_argmin_rows(const double* fit, uint64_t rows, uint64_t cols,
                         uint64_t* idx, double* val, cudaStream_t s);
 void launch_key_hash(const uint64_t* keys, uint64_t n, uint64_t* out,
                      cudaStream_t s);
-void launch_add_losers(Ctl* dst, const Ctl* src, cudaStream_t s);
+// dst->n_losers_all += src->n_losers (when losers), dst->nan_all += src->nan_own
+void launch_add_losers(Ctl* dst, const Ctl* src, int losers, cudaStream_t s);
+// ctl->nan_count += ctl->nan_all; nan_own = nan_all = 0 (after an all-reduce of nan_own)
+void launch_fold_nan(Ctl* ctl, cudaStream_t s);
 void launch_to_bf16(const float* src, __nv_bfloat16* dst, uint64_t n,
                     cudaStream_t s);
 

@@ -378,6 +378,23 @@ class Engine:
         _check(A.lib().mgfwa_get_state(self.h, _pd(pos), _pd(fit), _pd(amp), _pd(li)), self.h)
         return FireworkState(pos, fit, amp, li, self.counters()["evaluations_used"])
 
+    def candidates(self, bf16: bool = False):
+        """The last generation's mapped sparks / guides and their fitness
+        (mgfwa_get_candidates): (sparks [Fl*lam][D], spark_fitness,
+        guides [Fl*M][D] or None, guide_fitness or None, bf16 shadow as
+        uint16 [Fl*lam][D] or None)."""
+        cfg = self.config
+        Fl = cfg.batches * cfg.fireworks // self.world
+        D = self.space.dim()
+        sp, sf = np.empty((Fl * cfg.sparks_per_firework, D)), np.empty(Fl * cfg.sparks_per_firework)
+        M = cfg.guides_per_firework
+        gd, gf = (np.empty((Fl * M, D)), np.empty(Fl * M)) if M else (None, None)
+        sh = np.empty((Fl * cfg.sparks_per_firework, D), dtype=np.uint16) if bf16 else None
+        _check(A.lib().mgfwa_get_candidates(
+            self.h, _pd(sp), _pd(sf), _pd(gd) if M else None, _pd(gf) if M else None,
+            sh.ctypes.data_as(C.POINTER(C.c_uint16)) if bf16 else None), self.h)
+        return sp, sf, gd, gf, sh
+
     def record(self) -> RunRecord:
         cnt = self.counters()
         B = self.config.batches

@@ -180,3 +180,35 @@ def test_replica_mode_validation(P):
         P.Engine(cfg, space, P.Sphere(), 1, rank=0, world=2, shard_mode="replica")
     with pytest.raises(ValueError, match="shard_mode"):
         P.Engine(cfg, space, P.Sphere(), 1, shard_mode="pipeline")
+
+
+@pytest.mark.parametrize("mode,world,nccl", [("firework", 2, False), ("firework", 1, True), ("replica", 2, False),
+                                             ("replica", 1, True)])
+def test_sharded_nan_count_is_global(P, mode, world, nccl):
+    """nan_evaluations (backend.cpp:19-22, EvalStats::nan_flagged) of a
+    sharded run equals the single-context count: shard-local NaNs (own
+    sparks / guides; replica mode: own losers) travel with the exchange and
+    are folded once per generation.  Weights of 1e30 overflow the logits to
+    inf - inf = NaN, so every evaluation is NaN-flagged."""
+    obj = P.MlpWeights(samples=128)
+    space = P.SearchSpace.box(obj.dim(), -1e30, 1e30)
+    cfg = P.MgfwaConfig(batches=2, fireworks=4, sparks_per_firework=10, guides_per_firework=3,
+                        max_evaluations=8 + 5 * 2 * 4 * 13)
+    ref, _ = _reference(P, cfg, space, obj, 3)
+    assert ref.nan_evaluations > 0
+    if nccl:
+        e = P.Engine(cfg, space, obj, 3, rank=0, world=1, shard_mode=mode)
+        e.attach_nccl(P.Engine.nccl_unique_id())
+        e.run()
+        r = e.record()
+        e.close()
+        assert r.nan_evaluations == ref.nan_evaluations
+        return
+    if mode == "replica":
+        outs = _replica(P, cfg, space, obj, 3, world)
+        for _, r, _, _ in outs:
+            assert r.nan_evaluations == ref.nan_evaluations
+    else:
+        recs, _ = _sharded(P, cfg, space, obj, 3, world)
+        for r in recs:
+            assert r.nan_evaluations == ref.nan_evaluations
