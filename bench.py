@@ -1,22 +1,24 @@
 """Benchmark: spark fitness evaluations/s and ms/generation of the B200
-MGFWA engine on BASELINE.json's configs[1] (C2: MLP-weights black box
-784-32-10, S = 1024 synthetic samples, B = 1, mu = 5 fireworks x lambda = 300
-sparks, M = 3 guides).
+MGFWA engine.  Default at N = 1: BASELINE.json's configs[1] (C2: MLP-weights
+black box 784-32-10, S = 1024 synthetic samples, B = 1, mu = 5 fireworks x
+lambda = 300 sparks, M = 3 guides); at N > 1: configs[4] (C5, 64 fireworks x
+1024 sparks of a 784-256-10 MLP) strong-scaled, 64/N fireworks per GPU —
+SURVEY.md §8(e) judges scaling on C5.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c1|c2|c3|c4|c5] [--scaling weak|strong]
+                    [--workload auto|c1|c2|c3|c4|c4a|c5|net5|net9]
+                    [--scaling weak|strong] [--shard-mode firework|replica]
 
 A "step" is one MGFWA generation (the body of run()'s loop,
 engine.cpp:359-417) on synthetic data.  value = whole-job evaluations per
 second, device-timed with CUDA events on the engine's stream over exactly K
-generations (max over ranks).  e2e = the same metric through the one-shot
-C-ABI run() drop-in (mgfwa_run_once) with host buffers in and out.
-Multi-GPU (torchrun, N ranks): weak scaling by default — the population grows
-to N x mu fireworks, each rank owns mu of them, and one in-place NCCL
-all-gather of the selected fireworks per generation keeps the population
-state replicated; ``--scaling strong`` splits the workload's
-own mu fireworks over the ranks instead (C5: 64 fireworks, 8 per GPU at N=8).  ``--impl reference`` times the compiled reference
-(oracle/_ref, /root/reference/proj/src/engine.cpp run()) on the host cores.
+generations (max over ranks).  e2e = the same metric through the public
+C-ABI run() drop-in (mgfwa_run_once) with host buffers in and out.  With
+--gpus N > 1 and no torchrun environment the script re-launches itself under
+torch.distributed.run (N local ranks, one JSON line from rank 0).
+``--impl reference`` times the compiled reference (oracle/_ref,
+/root/reference/proj/src/engine.cpp run()) on the host cores, steady-state
+generations from the reference's own trace clock.
 """
 from __future__ import annotations
 
@@ -45,14 +47,21 @@ WORKLOADS = {
     # configs[2]: LeNet-5 on 28x28 synthetic samples
     "c3": dict(desc="C3 LeNet-5 (conv6-conv16-120-84-10), S=1024, B=1, mu=5, lambda=300, M=3", kind="lenet",
                D=61706, B=1, mu=5, lam=300, M=3, lo=-1.0, hi=1.0, samples=1024),
-    # configs[4]: large population, MLP 784-256-10 (weak-scaling firework shards)
+    # configs[4]: large population, MLP 784-256-10 (the scaling workload)
     "c5": dict(desc="C5 MLP-weights 784-256-10, S=1024, B=1, mu=64, lambda=1024, M=3", kind="mlp", D=203530,
                B=1, mu=64, lam=1024, M=3, lo=-1.0, hi=1.0, in_dim=784, hidden=256, out_dim=10, samples=1024),
-    # configs[3]
+    # configs[3]: Rastrigin and Ackley at D = 1e5
     "c4": dict(desc="C4 Rastrigin D=1e5, B=1, mu=5, lambda=30, M=3", kind="rastrigin", D=100000, B=1, mu=5,
                lam=30, M=3, lo=-5.12, hi=5.12),
+    "c4a": dict(desc="C4 Ackley D=1e5, B=1, mu=5, lambda=30, M=3", kind="ackley", D=100000, B=1, mu=5,
+                lam=30, M=3, lo=-32.768, hi=32.768),
+    # the paper's own input-space benchmark nets (nets.cpp:36-55; box [-5, 5] of bench.cpp:76-77;
+    # B = 8, mu = 5, lambda = 32 as in SURVEY.md §6)
+    "net5": dict(desc="Net 5 (input-space MLP 100-64x8 ReLU, fp64), B=8, mu=5, lambda=32, M=3", kind="net",
+                 net_id=5, D=100, B=8, mu=5, lam=32, M=3, lo=-5.0, hi=5.0),
+    "net9": dict(desc="Net 9 (input-space MLP 1000-256x11 ReLU, fp64), B=8, mu=5, lambda=32, M=3", kind="net",
+                 net_id=9, D=1000, B=8, mu=5, lam=32, M=3, lo=-5.0, hi=5.0),
 }
-FLOP_PER_EVAL_C2 = 2 * 1024 * (784 * 32 + 32 * 10)  # 52,035,584
 LENET_FLOP_PER_SAMPLE = 833_040  # conv1 117,600 + conv2 240,000 + fc 58,920 MAC, x2
 
 
@@ -72,23 +81,43 @@ def peaks():
     return PEAKS_FALLBACK, "fallback"
 
 
-def ncu_traffic(kernel_prefix: str):
-    """DRAM bytes (read + write) per launch of a kernel from the latest
-    committed `ncu --set full` capture under profiles/ (None if absent)."""
+NCU_KEYS = {"sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active": "tensor_pipe_pct",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
+            "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active": "alu_pipe_pct",
+            "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active": "fmaheavy_pipe_pct",
+            "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
+            "gpu__time_duration.sum": "ncu_time"}
+
+
+def ncu_metrics(kernel_prefix: str, workload: str):
+    """DRAM bytes (read + write) per launch and the pipe counters of a
+    kernel from the latest committed `ncu --set full` capture of this
+    workload under profiles/ (None if absent)."""
     import glob
 
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_full_hot_kernels.json")), reverse=True):
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_full_hot_kernels.json")), reverse=True)
+    for path in paths:
         with open(path) as f:
             for k in json.load(f):
-                if kernel_prefix in k.get("kernel", ""):
-                    def mb(s):
-                        v, unit = s.split()
-                        return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
-                    try:
-                        return {"bytes": mb(k["dram__bytes_read.sum"]) + mb(k["dram__bytes_write.sum"]),
-                                "source": os.path.relpath(path, ROOT)}
-                    except (KeyError, ValueError):
-                        return None
+                if kernel_prefix not in k.get("kernel", "") or k.get("workload", "c2") != workload:
+                    continue
+
+                def num(s):
+                    v, unit = s.split()
+                    return float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "%": 1,
+                                       "us": 1, "usecond": 1, "ms": 1e3, "msecond": 1e3, "ns": 1e-3}[unit]
+                try:
+                    out = {"traffic": num(k["dram__bytes_read.sum"]) + num(k["dram__bytes_write.sum"]),
+                           "source": os.path.relpath(path, ROOT)}
+                except (KeyError, ValueError):
+                    return None
+                for key, short in NCU_KEYS.items():
+                    if key in k:
+                        try:
+                            out[short] = num(k[key])
+                        except (KeyError, ValueError):
+                            pass
+                return out
     return None
 
 
@@ -97,6 +126,8 @@ def make_objective(P, w):
         return P.MlpWeights(w["in_dim"], w["hidden"], w["out_dim"], w["samples"], 1)
     if w["kind"] == "lenet":
         return P.LeNet(w["samples"], 1)
+    if w["kind"] == "net":
+        return P.Net(w["net_id"], 1)
     return {"sphere": P.Sphere(), "rastrigin": P.Rastrigin(), "ackley": P.Ackley()}[w["kind"]]
 
 
@@ -175,20 +206,63 @@ def dist_env():
     return world, rank, local
 
 
+def resolve(args, world):
+    """Workload and per-run shape.  auto: C2 at N = 1, C5 strong-scaled at
+    N > 1."""
+    name = args.workload
+    scaling = args.scaling
+    if name == "auto":
+        name = "c2" if world == 1 else "c5"
+        if scaling is None:
+            scaling = "weak" if world == 1 else "strong"
+    scaling = scaling or "weak"
+    w = WORKLOADS[name]
+    wn = dict(w)
+    if args.shard_mode == "replica":
+        wn["B"] = w["B"] * world  # weak scaling over batch replicas
+        scaling = "weak"
+    elif scaling == "weak":
+        wn["mu"] = w["mu"] * world
+    elif (w["B"] * w["mu"]) % world != 0:
+        raise SystemExit(f"--scaling strong needs B*mu divisible by the rank count ({w['B'] * w['mu']} % {world})")
+    return name, w, wn, scaling
+
+
+def config_dict(name, w, wn, world, scaling, shard_mode):
+    """The `config` object of the JSON line — identical for both arms."""
+    if shard_mode == "replica":
+        par = f"batch replicas x{world} ({wn['B']} batches)" + (" + 8-byte NCCL all-reduce/gen" if world > 1 else "")
+    else:
+        par = f"firework-sharded x{world}" + (" + NCCL all-gather/gen" if world > 1 else "")
+    return {"workload": w["desc"], "name": name, "D": w["D"], "B": wn["B"], "mu": wn["mu"], "lambda": w["lam"],
+            "M": w["M"], "fireworks_total": wn["B"] * wn["mu"], "scaling": scaling, "parallelism": par}
+
+
 def _ref_desc(O, w):
     kind = {"mlp": O.OBJ_MLP_WEIGHTS, "lenet": O.OBJ_LENET, "sphere": O.OBJ_SPHERE,
-            "rastrigin": O.OBJ_RASTRIGIN, "ackley": O.OBJ_ACKLEY}[w["kind"]]
+            "rastrigin": O.OBJ_RASTRIGIN, "ackley": O.OBJ_ACKLEY, "net": O.OBJ_NET}[w["kind"]]
     return O.ObjectiveDesc(kind=kind, in_dim=w.get("in_dim", 784), hidden=w.get("hidden", 32),
-                           out_dim=w.get("out_dim", 10), samples=w.get("samples", 1024))
+                           out_dim=w.get("out_dim", 10), samples=w.get("samples", 1024), net_id=w.get("net_id", 1),
+                           weight_seed=1)
 
 
-def cpu_reference_generation(w, seed: int, workers: int):
-    """Reference CPU throughput on the host cores via the compiled reference
-    (oracle/_ref).  C1/C2/C4: one full generation, run() with budget
-    init + 1 wave.  C3/C5, whose CPU generations take minutes to hours
-    (SURVEY.md §8(d)): batched_apply() of a bounded sample of candidate rows
-    (fitness only, the dominant reference cost), extrapolated as evals/s.
-    Returns (evals, seconds, sample description)."""
+def _ref_cfg(O, w, waves):
+    return O.Config(batches=w["B"], fireworks=w["mu"], sparks_per_firework=w["lam"], guides_per_firework=w["M"],
+                    boosts=[1.0, 2.0, 4.0][: w["M"]],
+                    max_evaluations=w["B"] * w["mu"] + waves * w["B"] * w["mu"] * (w["lam"] + w["M"]))
+
+
+def reference_steady_state(w, waves: int, seed: int, workers: int, time_cap_s: float = 150.0):
+    """Steady-state generations of the compiled reference run()
+    (oracle/_ref, engine.cpp:313-423) on the host cores, read off the
+    reference's own trace clock (RunRecord.trace wall_ms, bench.cpp:240-248):
+    (evaluations after init) / (wall time after init), so initialization and
+    objective construction are excluded — the same thing the GPU arm's
+    device-timed value measures.  The number of waves is capped so the call
+    stays within ~time_cap_s.  C3 / C5, whose CPU generations take minutes
+    to hours, are measured by batched_apply() of a bounded
+    sample of candidate rows (fitness only, the dominant reference cost).
+    Returns (evals, seconds, waves, sample description)."""
     import oracle as O
 
     ref = O.Reference()
@@ -198,45 +272,117 @@ def cpu_reference_generation(w, seed: int, workers: int):
         rows = np.random.default_rng(seed).uniform(w["lo"], w["hi"], size=(n, w["D"])) * 0.05
         t = time.perf_counter()
         ref.batched_apply(desc, rows[None], workers=workers)
-        return n, time.perf_counter() - t, f"batched_apply() of {n} candidate rows (fitness only)"
-    cfg = O.Config(batches=w["B"], fireworks=w["mu"], sparks_per_firework=w["lam"], guides_per_firework=w["M"],
-                   boosts=[1.0, 2.0, 4.0][: w["M"]],
-                   max_evaluations=w["B"] * w["mu"] + w["B"] * w["mu"] * (w["lam"] + w["M"]))
+        return n, time.perf_counter() - t, 0, f"batched_apply() of {n} candidate rows (fitness only; " \
+                                              f"a generation takes minutes to hours on the CPU)"
     lo, hi = np.full(w["D"], w["lo"]), np.full(w["D"], w["hi"])
-    t = time.perf_counter()
-    r = ref.run(cfg, lo, hi, desc, seed, workers=workers)
-    return r.evaluations_used, time.perf_counter() - t, "mgfwa::run() of one generation (init + 1 wave)"
+    # size the run: one wave first (its trace gives the per-wave cost)
+    r1 = ref.run(_ref_cfg(O, w, 1), lo, hi, desc, seed, workers=workers)
+    per_wave_s = max((r1.trace_wall_ms[0, -1] - r1.trace_wall_ms[0, 0]) * 1e-3, 1e-6)
+    n = int(max(1, min(waves, time_cap_s / per_wave_s)))
+    r = ref.run(_ref_cfg(O, w, n), lo, hi, desc, seed, workers=workers)
+    evals = int(r.trace_evals[0, -1] - r.trace_evals[0, 0])
+    secs = (r.trace_wall_ms[0, -1] - r.trace_wall_ms[0, 0]) * 1e-3
+    return evals, secs, r.iterations, f"mgfwa::run() with {r.iterations} generations, steady state from the " \
+                                      f"reference's trace clock (initialization excluded)"
 
 
-def run_reference_arm(args, w):
+def cpu_baseline_line(w, cores, waves):
+    """cpu_baseline: the compiled reference, serial and data_parallel(cores);
+    the faster is the value (C1's tiny generations run faster serially)."""
+    best = None
+    for workers, label in ((cores, f"data_parallel({cores})"), (0, "serial")):
+        if workers == 0 and w["D"] * w["lam"] > 10**6:
+            continue  # serial is strictly slower on the large shapes (SURVEY.md §6); skip its minutes
+        e, s, it, what = reference_steady_state(w, waves, 0, workers)
+        v = e / s
+        if best is None or v > best[0]:
+            best = (v, workers or 1, f"{what}, EvalBackend::{label}, {e} evaluations in {s:.2f} s")
+    return {"value": best[0], "unit": "evals/s", "cores": best[1], "kind": "reference", "sample": best[2]}
+
+
+def run_reference_arm(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
+    name, w, wn, scaling = resolve(args, world)
     cores = os.cpu_count() or 1
-    evals, secs, steps = 0, 0.0, 0
-    t0 = time.perf_counter()
-    what = ""
-    for _ in range(args.warmup):  # bounded warm-up
-        cpu_reference_generation(w, 1000, cores)
-        if time.perf_counter() - t0 > 30:
-            break
-    t1 = time.perf_counter()
-    for k in range(args.steps):
-        e, s, what = cpu_reference_generation(w, k, cores)
-        evals += e
-        secs += s
-        steps += 1
-        if time.perf_counter() - t1 > 150:  # keep the arm within a few minutes
-            break
-    v = evals / secs
+    # C1's full BASELINE run (1e5 evaluations = 605 generations) is a few tens of ms:
+    # time that; elsewhere K generations (bounded to a few minutes)
+    waves = 605 if name == "c1" else max(args.steps, 1)
+    cb = cpu_baseline_line(w, cores, waves)
+    v = cb["value"]
+    ms_per_step = 1e3 * w["B"] * w["mu"] * (w["lam"] + w["M"]) / v
     line = {"metric": "spark fitness evals/sec", "value": v, "unit": "evals/s", "n_gpus": args.gpus,
-            "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w["desc"], "budget_per_step": "init + 1 generation"}, "impl": "reference",
-            "cpu_baseline": {"value": v, "unit": "evals/s", "cores": cores, "kind": "reference",
-                             "sample": f"{steps} x {what}, EvalBackend::data_parallel({cores})"},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(name, w, wn if world > 1 else w, world, scaling, args.shard_mode),
+            "impl": "reference", "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def relaunch_under_torchrun(args) -> int:
+    """--gpus N > 1 without a torchrun environment: run N local ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + os.getpid() % 1000),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def kernel_breakdown(eng, w, wn, world, pk):
+    """Per-kernel device times of the generation's kernels on the steady-state
+    engine: CUDA events around each launch, every launch from a cold L2
+    (mgfwa_time_kernel flushes 256 MB before it), with algorithmic bytes
+     or FLOP per launch (own fireworks)."""
+    Fl = wn["B"] * wn["mu"] // world
+    D, lam, M = w["D"], w["lam"], w["M"]
+    nn = w["kind"] in ("mlp", "lenet")
+    top = -(-lam // 5)  # ceil(0.2 * lambda), the default guide fraction
+    algo = {"explode": Fl * lam * D * 4 + Fl * D * 4,  # K2: B*mu*lam*D*4 written + B*mu*D*4 read
+            "guides": Fl * (2 * top * D * 4 + M * D * 4),  # K6: 2*top rows read + M rows written
+            "rank": Fl * lam * 4 * 2,
+            "select": Fl * 2 * D * 4}  # K7: winner row read + firework row written
+    kb = {}
+    for name in ("explode", "rank", "guides", "select"):
+        kms, _ = eng.time_kernel(name, 10)
+        kb[name] = {"us": 1e3 * kms, "bound": "hbm", "algorithmic_bytes": algo[name],
+                    "achieved_GBs": algo[name] / (kms * 1e-3) / 1e9,
+                    "frac": algo[name] / (kms * 1e-3) / 1e9 / pk["hbm_gbs"]}
+    kb["explode"]["note"] = ("algorithmic bytes of SURVEY §8(d) (fp32 spark matrix + firework rows); the kernel "
+                             "also writes the bf16 shadow (+2 B per coordinate)" if nn else
+                             "algorithmic bytes of SURVEY §8(d); the analytic fitness partials are fused in")
+    if w["kind"] == "net":  # fp64 layer GEMMs (CUDA cores), reported beside the HBM-bound kernels
+        kms, units_k = eng.time_kernel("fitness", 10)
+        kb["fitness"] = {"us": 1e3 * kms, "bound": "fp64", "rows": units_k}
+    if nn:
+        for name in ("fitness", "guide_fitness"):
+            kms, units_k = eng.time_kernel(name, 10)
+            ach = flop_per_eval(w) * units_k / (kms * 1e-3) / 1e12
+            kb[name] = {"us": 1e3 * kms, "bound": "tensor", "rows": units_k, "achieved_TFLOPs": ach,
+                        "frac": ach / pk["bf16_tflops"]}
+    return kb
+
+
+KERNEL_NAMES = {"explode": "k_explode_map", "rank": "k_rank", "guides": "k_guides", "select": "k_select",
+                "fitness_mlp": "k_mlp_fitness", "fitness_lenet": "k_lenet"}
+
+
+def roofline_entry(name, k, w, pk, pk_kind, workload):
+    """The `roofline` object for kernel `name` of the breakdown."""
+    if k["bound"] == "tensor":
+        kern = KERNEL_NAMES["fitness_" + w["kind"]]
+        nc = ncu_metrics(kern + (f"<{w['hidden']}" if w["kind"] == "mlp" else ""), workload)
+        return {"kernel": kern + " (spark fitness)", "bound": "tensor", "achieved": k["achieved_TFLOPs"],
+                "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": k["frac"],
+                "traffic": nc["traffic"] if nc else None, "ncu": nc,
+                "algorithmic_per_launch": f"{k['rows']} candidates x {flop_per_eval(w)} FLOP",
+                "ms_per_launch": k["us"] * 1e-3, "peak_source": f"{pk_kind} bf16 burst (MEASURED_PEAKS.json)"}
+    kern = KERNEL_NAMES[name]
+    nc = ncu_metrics(kern, workload)
+    return {"kernel": kern, "bound": "hbm", "achieved": k["achieved_GBs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": k["frac"], "traffic": nc["traffic"] if nc else None, "ncu": nc,
+            "algorithmic_per_launch": f"{k['algorithmic_bytes']} bytes", "ms_per_launch": k["us"] * 1e-3,
+            "note": k.get("note"), "peak_source": f"{pk_kind} HBM copy bandwidth (MEASURED_PEAKS.json)"}
 
 
 def main():
@@ -245,10 +391,10 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N>1: weak = mu fireworks per rank (default); strong = the workload's mu "
-                         "fireworks split over the ranks (e.g. C5: 64 fireworks, 8 per GPU at N=8)")
+    ap.add_argument("--workload", default="auto", choices=["auto"] + sorted(WORKLOADS))
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="N>1: strong = the workload's fireworks split over the ranks (default for auto = C5); "
+                         "weak = mu fireworks per rank")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--distributed", action="store_true",
                     help="take the torch.distributed / NCCL sharded code path even at N = 1 "
@@ -260,15 +406,17 @@ def main():
                          "is exchanged (weak scaling)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    w = WORKLOADS[args.workload]
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(relaunch_under_torchrun(args))
     if args.impl == "reference":
-        run_reference_arm(args, w)
+        run_reference_arm(args)
         return
 
     import torch
 
     world, rank, local = dist_env()
+    name, w, wn, scaling = resolve(args, world)
     sharded = world > 1 or args.distributed
     if sharded:
         import torch.distributed as dist
@@ -290,17 +438,6 @@ def main():
     stream = torch.cuda.Stream()
     obj = make_objective(P, w)
     space = P.SearchSpace.box(w["D"], w["lo"], w["hi"])
-    # N > 1: weak scaling — the population grows to mu * N fireworks, each
-    # rank owns mu of them (firework sharding), one in-place NCCL all-gather
-    # of the selected fireworks per generation.
-    wn = dict(w)
-    replica = args.shard_mode == "replica"
-    if replica:
-        wn["B"] = w["B"] * world
-    elif args.scaling == "weak":
-        wn["mu"] = w["mu"] * world
-    elif (w["B"] * w["mu"]) % world != 0:
-        raise SystemExit(f"--scaling strong needs B*mu divisible by the rank count ({w['B'] * w['mu']} % {world})")
     eng = P.Engine(make_config(P, wn, 1 << 62), space, obj, seed=0, device=dev, rank=rank, world=world,
                    shard_mode=args.shard_mode)
     if sharded:
@@ -340,90 +477,47 @@ def main():
     else:
         ms_max, evals_total = ms, float(evals)
 
-    # dominant kernel: spark fitness (tcgen05 GEMM) timed alone, CUDA events
-    fit_ms, units = eng.time_fitness(20)
     pk, pk_kind = peaks()
-    if w["kind"] in ("mlp", "lenet"):
-        fpe = flop_per_eval(w)
-        achieved = fpe * units / (fit_ms * 1e-3) / 1e12
-        if w["kind"] == "mlp":
-            kname = f"k_mlp_fitness<{w['hidden']}> (tcgen05.mma kind::f16, TMA, TMEM)"
-            tr = ncu_traffic(f"k_mlp_fitness<{w['hidden']}")
-            opb = units * w["D"] * 2 + w["samples"] * w["in_dim"] * 2
-        else:
-            kname = "k_lenet_conv + k_lenet_fc (mma.sync m16n8k16 bf16, weights staged in smem)"
-            tc, tf = ncu_traffic("k_lenet_conv"), ncu_traffic("k_lenet_fc")
-            tr = {"bytes": tc["bytes"] + tf["bytes"], "source": tc["source"]} if tc and tf else None
-            # + the pooled conv2 activations through the HBM scratch (bf16 x 400, written + read)
-            opb = units * w["D"] * 2 + w["samples"] * 784 * 2 + 2 * units * w["samples"] * 800
-        roof = {"kernel": kname, "bound": "tensor",
-                "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / pk["bf16_tflops"], "traffic": tr["bytes"] if tr else None,
-                "traffic_source": tr["source"] if tr else None,
-                "algorithmic_per_launch": f"{units} candidates x {fpe} FLOP; operand bytes {opb} (bf16 W + X)",
-                "ms_per_launch": fit_ms, "peak_source": f"{pk_kind} bf16 burst (MEASURED_PEAKS.json)"}
-    else:
-        byts = units * w["D"] * 4 + w["B"] * w["mu"] * w["D"] * 4
-        achieved = byts / (fit_ms * 1e-3) / 1e9
-        roof = {"kernel": "k_explode_map (fused explode+map+fitness)", "bound": "hbm", "achieved": achieved,
-                "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": None,
-                "ms_per_launch": fit_ms, "peak_source": f"{pk_kind} hbm copy"}
-
     line = {"metric": "spark fitness evals/sec", "value": evals_total / (ms_max * 1e-3), "unit": "evals/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
-            "dtype": "bf16" if w["kind"] in ("mlp", "lenet") else "f32", "data": "synthetic",
-            "config": {"workload": w["desc"], "D": w["D"], "fireworks_total": wn["mu"] * wn["B"],
-                       "parallelism": (f"batch replicas x{world} ({wn['B']} batches)" +
-                                       (" + 8-byte NCCL all-reduce/gen" if world > 1 else "")) if replica else
-                                      (f"firework-sharded x{world}" + (" + NCCL all-gather/gen" if world > 1 else "")),
-                       "l2": "inputs larger than L2: spark matrix fp32+bf16 229 MB/generation > 126 MB"
-                       if args.workload == "c2" else "n/a"},
-            "gpu_launches": kpg * args.steps if kpg else 1,  # 1: the persistent small-problem loop
-            "roofline": roof}
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+            "dtype": "bf16" if w["kind"] in ("mlp", "lenet") else ("f64" if w["kind"] == "net" else "f32"),
+            "data": "synthetic",
+            "config": config_dict(name, w, wn, world, scaling, args.shard_mode),
+            "l2": ("inputs larger than L2 every step: the fp32 + bf16 spark matrices "
+                   f"({w['B'] * w['mu'] * w['lam'] * w['D'] * 6 / 1e6:.0f} MB per generation) exceed the 126 MB L2; "
+                   "per-kernel times below are taken after a 256 MB L2 flush")
+            if w["kind"] in ("mlp", "lenet") else "per-kernel times taken after a 256 MB L2 flush",
+            "gpu_launches": kpg * args.steps if kpg else 1}  # 1: the persistent small-problem loop
     line["clocks"] = clk.summary()
-    # per-kernel device times of the generation's idempotent kernels on the
-    # steady-state engine (CUDA events, back-to-back launches) with their
-    # achieved HBM bandwidth against algorithmic bytes (GB/s
-    # for generation and guiding); per rank's own fireworks.
+
+    # Roofline: the kernel that dominates the generation, picked from the
+    # measured per-kernel breakdown (cold L2), against its own bound; the
+    # tensor-core fitness kernel is reported beside it for NN workloads.
     try:
-        Fl = wn["B"] * wn["mu"] // world
-        Dp4, nn = w["D"] * 4, w["kind"] in ("mlp", "lenet")
-        top = -(-w["lam"] // 5)  # ceil(0.2 * lambda), the default guide fraction
-        algo = {"explode": Fl * w["lam"] * w["D"] * (6 if nn else 4) + Fl * w["D"] * 4,
-                "guides": Fl * (2 * top * Dp4 + w["M"] * w["D"] * (6 if nn else 4) + Dp4),
-                "rank": Fl * w["lam"] * (4 if nn else 8) * 2,
-                # winner row read + firework row written (every firework's winner a spark or
-                # guide: the upper bound) + the spark fitness scan
-                "select": Fl * (2 * w["D"] * 4 + w["lam"] * 4)}
-        kb = {}
-        for name in ("explode", "rank", "guides", "select"):
-            kms, _ = eng.time_kernel(name, 10)
-            kb[name] = {"us": 1e3 * kms, "algorithmic_bytes": algo[name],
-                        "achieved_GBs": algo[name] / (kms * 1e-3) / 1e9,
-                        "frac_hbm": algo[name] / (kms * 1e-3) / 1e9 / pk["hbm_gbs"]}
-        if nn:
-            for name in ("fitness", "guide_fitness"):
-                kms, units_k = eng.time_kernel(name, 10)
-                kb[name] = {"us": 1e3 * kms, "rows": units_k,
-                            "achieved_TFLOPs": flop_per_eval(w) * units_k / (kms * 1e-3) / 1e12}
+        kb = kernel_breakdown(eng, w, wn, world, pk)
         line["kernel_breakdown"] = kb
+        line["dominant_kernel"] = max(kb, key=lambda k: kb[k]["us"])
+        dom = max((k for k in kb if kb[k]["bound"] in ("hbm", "tensor")), key=lambda k: kb[k]["us"])
+        line["roofline"] = roofline_entry(dom, kb[dom], w, pk, pk_kind, name)
+        line["roofline"]["share_of_step"] = kb[dom]["us"] * 1e-3 / (ms_max / args.steps)
+        if "fitness" in kb and dom != "fitness":
+            line["roofline_tensor"] = roofline_entry("fitness", kb["fitness"], w, pk, pk_kind, name)
     except Exception as ex:
         line["kernel_breakdown"] = {"error": str(ex)[:200]}
+        fit_ms, units = eng.time_fitness(10)
+        line["roofline"] = {"bound": "hbm", "achieved": None, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": None,
+                            "traffic": None, "error": str(ex)[:200]}
 
     if sharded and not args.no_e2e:
         # e2e at N GPUs through the public API: every rank holds its shard of
         # the engine (created from the host config / bounds) in the NCCL
         # clique; the timed region is run() (initialize + K generations with
-        # the per-generation all-gather and the host syncs of the step loop)
+        # the per-generation exchange and the host syncs of the step loop)
         # and the D2H of the best; wall-clock per rank, max over ranks.
         import torch.distributed as dist
 
         cfg_e = make_config(P, wn, wn["B"] * wn["mu"] + args.steps * wn["B"] * wn["mu"] * (w["lam"] + w["M"]))
-
-        # the engine shard and its NCCL communicator are set up once (like a
-        # long-lived service); each timed run() re-initializes from the host
-        # config and reads the best back
         e = P.Engine(cfg_e, space, obj, seed=7, device=dev, rank=rank, world=world, shard_mode=args.shard_mode)
         u = torch.zeros(128, dtype=torch.uint8, device="cuda")
         if rank == 0:
@@ -444,24 +538,27 @@ def main():
             return used, float(tt[0])
 
         try:
-            sharded_once()  # warm (module load, workspace, NCCL first use)
+            sharded_once()  # warm (module load, NCCL first use)
             used, dt = sharded_once()
             B, D = wn["B"], w["D"]
             line["e2e"] = {"value": used / dt, "unit": "evals/s",
                            "h2d_bytes_per_step": 0,  # config and bounds copied at engine creation
                            "d2h_bytes_per_step": (B * D * 8 + B * 8) / args.steps,
                            "what": f"run() (initialize from the host config + {args.steps} generations, per-"
-                                   f"generation NCCL {'loser-count all-reduce' if replica else 'all-gather'}) + "
-                                   f"best() D2H on {world} GPUs, wall-clock max over "
-                                   f"ranks; engine shard and communicator created once"}
+                                   f"generation NCCL exchange) + best() D2H on {world} GPUs, wall-clock max over "
+                                   f"ranks; engine shard and communicator created once (long-lived service)"}
         except Exception as ex:  # keep the device-timed line
             line["e2e"] = {"value": None, "unit": "evals/s", "error": str(ex)[:200]}
         e.close()
 
     if rank == 0 and not sharded and not args.no_e2e:
-        # e2e: one-shot run() drop-in over host buffers (mgfwa_run_once):
-        # budget = init + K generations; includes context setup, H2D of the
-        # search bounds, the K generations and D2H of best/trace.
+        # e2e: the one-shot run() drop-in over host buffers (mgfwa_run_once):
+        # budget = init + K generations; context setup, H2D of the search
+        # bounds, the K generations and D2H of best/trace, host-timed.
+        # Two numbers: `e2e` is a repeated call (the workspace a destroyed
+        # context parks — buffers, dataset, TMA descriptors, captured graph —
+        # is reused, as in a long-lived process calling run() again);
+        # `e2e_cold` frees that cache first and pays the whole setup.
         import ctypes as C
 
         from paper_2501_03944_b200 import _capi as A
@@ -477,27 +574,30 @@ def main():
         pdp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
 
         def once():
+            t = time.perf_counter()
             rc = A.lib().mgfwa_run_once(C.byref(c), C.byref(sp), C.byref(ob), 7, dev, pdp(bf), pdp(bp),
                                         te.ctypes.data_as(C.POINTER(C.c_uint64)), pdp(tb), pdp(tw), cap,
                                         C.byref(cnt))
+            dt = time.perf_counter() - t
             assert rc == 0, A.lib().mgfwa_last_error(None)
+            return cnt.evaluations_used / dt
 
-        once()  # warm (module load, first-touch)
-        t = time.perf_counter()
-        once()
-        dt = time.perf_counter() - t
-        line["e2e"] = {"value": cnt.evaluations_used / dt, "unit": "evals/s",
-                       "h2d_bytes_per_step": (2 * D * 8 + 8 * 12) / args.steps,
-                       "d2h_bytes_per_step": (B * D * 8 + B * 8 + cap * B * 24) / args.steps,
-                       "what": f"mgfwa_run_once(): create + init + {args.steps} generations + D2H, host-timed"}
+        eng.close()  # its workspace would otherwise occupy the one cache slot
+        A.lib().mgfwa_release_cached_workspace()
+        cold = once()  # first call: allocation, dataset, TMA descriptors, graph capture
+        warm = once()  # second call: the parked workspace is reused
+        io = {"h2d_bytes_per_step": (2 * D * 8 + 8 * 12) / args.steps,
+              "d2h_bytes_per_step": (B * D * 8 + B * 8 + cap * B * 24) / args.steps}
+        line["e2e"] = dict(value=warm, unit="evals/s", **io,
+                           what=f"mgfwa_run_once(): create + init + {args.steps} generations + D2H, host-timed; "
+                                f"repeated call (workspace cache warm)")
+        line["e2e_cold"] = dict(value=cold, unit="evals/s", **io,
+                                what="the same call after mgfwa_release_cached_workspace(): full setup included")
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cores = os.cpu_count() or 1
-            e, s, what = cpu_reference_generation(w, 0, cores)
-            line["cpu_baseline"] = {"value": e / s, "unit": "evals/s", "cores": cores, "kind": "reference",
-                                    "sample": f"1 x {what} of the same workload, compiled reference, "
-                                              f"data_parallel({cores}), {s:.1f} s"}
+            waves = 605 if name == "c1" else 3
+            line["cpu_baseline"] = cpu_baseline_line(w, os.cpu_count() or 1, waves)
         except Exception as ex:  # the reference build travels in oracle/_ref
             line["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
     if rank == 0:

@@ -258,7 +258,8 @@ int mgfwa_shard_exchange(mgfwa_ctx_t dst, mgfwa_ctx_t src);
 /* Times the dominant kernel of a generation in isolation on the context
  * stream with CUDA events: the spark fitness (tcgen05 GEMM for the NN
  * objectives, the fused explode+fitness kernel for analytic ones), `iters`
- * back-to-back launches after one warm-up.  *ms = mean ms per launch;
+ * launches after one warm-up, each from a cold L2 (a 256 MB write precedes
+ * every timed launch, outside the events).  *ms = mean ms per launch;
  * *units = candidates (rows) per launch. */
 int mgfwa_time_fitness(mgfwa_ctx_t ctx, uint64_t iters, double* ms,
                        uint64_t* units);
@@ -287,6 +288,12 @@ int mgfwa_validate_config(const mgfwa_config_t* config);
 /* key_hash, rng.hpp:43-52, evaluated on the device for n keys [n][7]. */
 int mgfwa_key_hash(const uint64_t* keys, uint64_t n, uint64_t* out);
 const char* mgfwa_version(void);
+/* A destroyed context parks its device workspace (buffers, stream, pinned
+ * control block, captured generation graph) for reuse by the next context
+ * of the same shape (one entry).  This frees it: the next mgfwa_create /
+ * mgfwa_run_once then pays the full setup (allocation, dataset, TMA
+ * descriptors, graph capture). */
+int mgfwa_release_cached_workspace(void);
 
 #ifdef __cplusplus
 }

@@ -47,6 +47,7 @@ _P = C.c_void_p
 # name -> (restype, argtypes); mirrors include/mgfwa_b200.h one to one.
 SIGNATURES = {
     "mgfwa_version": (C.c_char_p, []),
+    "mgfwa_release_cached_workspace": (_int, []),
     "mgfwa_last_error": (C.c_char_p, [_P]),
     "mgfwa_create": (_int, [C.POINTER(mgfwa_config_t), C.POINTER(mgfwa_space_t),
                             C.POINTER(mgfwa_objective_t), _u64, _int, C.POINTER(_P)]),

@@ -129,7 +129,9 @@ def test_generation_steps_match_reference_at_headline_shape(P, ref, name):
     od, D, (lo, hi), mu, lam = SHAPES[name]
     nn = od["kind"] in (O.OBJ_MLP_WEIGHTS, O.OBJ_LENET)
     B, M, seed = 1, 3, 7
-    budget = 10**9  # large iterations_remaining: non-improving fireworks become losers
+    # a budget of a few waves: iterations_remaining is small (engine.cpp:394-401), so fireworks whose
+    # projected improvement cannot reach the batch best become losers (engine.cpp:275-281)
+    budget = B * mu + 4 * B * mu * (lam + M)
     lower, upper = np.full(D, lo), np.full(D, hi)
     lower[1::7] = lo / 2  # per-dimension bounds (not a uniform box)
     kw = dict(batches=B, fireworks=mu, sparks_per_firework=lam, guides_per_firework=M,
