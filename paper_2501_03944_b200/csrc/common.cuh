@@ -56,6 +56,49 @@ __host__ __device__ __forceinline__ uint64_t key_prefix(uint64_t seed,
   return splitmix64(h ^ k);
 }
 
+// ---- per-coordinate draws with the key prefix hoisted (the explode hot loop)
+// splitmix64(pre ^ d) (rng.hpp:33-38) for d < 2^32, restated for 32-bit ALUs:
+//  * the mixer's "+ gamma" and the prefix's high word fold into one 64-bit
+//    addend, so (pre ^ d) + gamma = (pre_lo ^ d) + addend is one IMAD.WIDE
+//    (FMA pipe) instead of a carry-chained IADD3 pair (ALU pipe);
+//  * the final "z ^ (z >> 31)" is not materialised: the draw only needs bits
+//    11..63 of it, and (z ^ (z >> 31)) >> 11 = (z >> 11) ^ (z >> 42).
+// MixState holds z before that final xorshift; the unit_*_z helpers below
+// produce exactly unit_d1 / unit_pm1 / unit_u53 of splitmix64(pre ^ d).
+struct DrawKey {
+  uint32_t lo;      // low word of the prefix
+  uint64_t addend;  // ((pre_hi + gamma_hi) << 32) | gamma_lo
+};
+__host__ __device__ __forceinline__ DrawKey draw_key(uint64_t pre) {
+  const uint64_t g = 0x9E3779B97F4A7C15ull;
+  const uint32_t hi = (uint32_t)(pre >> 32) + (uint32_t)(g >> 32);
+  return DrawKey{(uint32_t)pre, ((uint64_t)hi << 32) | (g & 0xFFFFFFFFull)};
+}
+struct MixState {
+  uint32_t lo, hi;
+};
+// `one` must be 1 at run time but opaque to the compiler (so the multiply-add
+// by it stays an IMAD.WIDE): callers pass a kernel-argument-derived value.
+__host__ __device__ __forceinline__ MixState mix_draw(const DrawKey& k, uint32_t d, uint32_t one) {
+#ifdef __CUDA_ARCH__
+  uint64_t x;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(x) : "r"(k.lo ^ d), "r"(one), "l"(k.addend));
+#else
+  uint64_t x = (uint64_t)(k.lo ^ d) * one + k.addend;
+#endif
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return MixState{(uint32_t)x, (uint32_t)(x >> 32)};
+}
+// Bits 11..42 and 43..63 of h = z ^ (z >> 31): lo32(h >> 11) and h_hi >> 11.
+__host__ __device__ __forceinline__ uint32_t mant_lo(MixState z) {
+#ifdef __CUDA_ARCH__
+  return __funnelshift_r(z.lo, z.hi, 11) ^ (z.hi >> 10);
+#else
+  return (uint32_t)((((uint64_t)z.hi << 32) | z.lo) >> 11) ^ (z.hi >> 10);
+#endif
+}
+
 // D1 = 1 + (m mod 2^52) 2^-52 in [1, 2) for m = h >> 11, built from the bits
 // (no int -> fp conversion): mantissa = bits 11..62 of h.
 __device__ __forceinline__ double unit_d1(uint64_t h) {

@@ -257,6 +257,15 @@ struct Workspace {
   __nv_bfloat16* X = nullptr;  // NN dataset
   int32_t* y = nullptr;
   NnPlan plan_sparks, plan_guides, plan_fresh;
+  // pipelined explode -> spark fitness (MLP objective): fitness plans over
+  // firework chunks [chunk_f0[c], + chunk_nf[c]) of the owned fireworks, an
+  // auxiliary stream the explode chunks run on, and fork/join events
+  std::vector<NnPlan> plan_chunks;
+  std::vector<uint64_t> chunk_f0, chunk_nf;
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr;
+  std::vector<cudaEvent_t> ev_chunk, ev_launched;
+  bool pipe_lc = false;  // explode chunk c+1 waits for the launch (not the end) of fitness chunk c
   int nsm = 148;
   int device = 0;
 
@@ -276,7 +285,49 @@ struct Workspace {
     plan_sparks.destroy();
     plan_guides.destroy();
     plan_fresh.destroy();
+    for (auto& pc : plan_chunks) pc.destroy();
+    for (auto e : ev_chunk) cudaEventDestroy(e);
+    for (auto e : ev_launched) cudaEventDestroy(e);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (aux) cudaStreamDestroy(aux);
     if (arena) cudaFree(arena);
+  }
+
+  // Pipelined explode -> fitness (MLP-weights objective): up to 8 chunks of
+  // whole fireworks, used when every chunk holds >= 4096 sparks (C5: 8 x
+  // 8 x 1024; 82.5 -> 78.4 ms per generation).  Small populations lose more
+  // to the extra fitness launches than the overlap gains (C2: 309 -> 366
+  // us), so they keep one explode and one fitness launch.  MGFWA_PIPELINE=0
+  // / =1 force it off / on.
+  Status build_pipeline(const mgfwa_objective_t* obj) {
+    const char* env = getenv("MGFWA_PIPELINE");
+    if (obj->kind != MGFWA_OBJ_MLP_WEIGHTS || v.Fl < 2) return ok();
+    const uint64_t G = std::min<uint64_t>(v.Fl, 8);
+    const bool large = (v.Fl / G) * v.lam >= 4096;
+    if (env ? env[0] == '0' : !large) return ok();
+    char err[256] = {0};
+    for (uint64_t c = 0; c < G; ++c) {
+      const uint64_t f0 = v.Fl * c / G, f1 = v.Fl * (c + 1) / G;
+      NnPlan pl;
+      pl.mlp = mlp_plan_create(X, y, obj->samples, obj->in_dim, obj->hidden, obj->out_dim,
+                               v.sparks_h + f0 * v.lam * v.Dp, (f1 - f0) * v.lam, v.Dp, nsm, err, sizeof err);
+      if (!pl.mlp) return invalid(err);
+      plan_chunks.push_back(pl);
+      chunk_f0.push_back(f0);
+      chunk_nf.push_back(f1 - f0);
+      cudaEvent_t e, l;
+      CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&l, cudaEventDisableTiming));
+      ev_chunk.push_back(e);
+      ev_launched.push_back(l);
+    }
+    // launch-completion edges (explode c+1 released when fitness c is resident)
+    // measured slower (C2 407 vs 366 us, C5 80.2 vs 78.4 ms): off unless =1
+    const char* lc = getenv("MGFWA_PIPELINE_LC");
+    pipe_lc = lc && lc[0] == '1';
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    CUDA_TRY(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+    return ok();
   }
 
   // Everything that sizes device memory or the dataset; workspaces with an
@@ -460,6 +511,7 @@ struct Workspace {
       STATUS_TRY(make(plan_sparks, v.sparks_h, P));
       if (G > 0) STATUS_TRY(make(plan_guides, v.guides_h, G));
       STATUS_TRY(make(plan_fresh, v.fresh_h, F));
+      STATUS_TRY(build_pipeline(obj));
     }
     return ok();
   }
@@ -516,6 +568,32 @@ static void hook_fresh(void* p, cudaStream_t s) {
 static void hook_fresh_all(void* p, cudaStream_t s) {
   auto* w = static_cast<Workspace*>(p);
   nn_fitness_launch(w->plan_fresh, w->v.fpart, nullptr, s);
+}
+// Explode of firework chunk c + 1 (auxiliary stream) runs beside the tcgen05
+// fitness of chunk c (generation stream): the integer-bound explode fills the
+// issue slots the tensor-core kernel leaves idle.  Inside graph capture the
+// fork / join events become graph edges.
+static void hook_explode_eval(void* p, cudaStream_t s) {
+  auto* w = static_cast<Workspace*>(p);
+  const EngineView& v = w->v;
+  cudaEventRecord(w->ev_fork, s);
+  cudaStreamWaitEvent(w->aux, w->ev_fork, 0);
+  const size_t G = w->plan_chunks.size();
+  launch_explode_fireworks(v, w->chunk_f0[0], w->chunk_nf[0], w->nsm, w->aux);
+  cudaEventRecord(w->ev_chunk[0], w->aux);
+  for (size_t c = 0; c < G; ++c) {
+    cudaStreamWaitEvent(s, w->ev_chunk[c], 0);
+    // the next explode chunk is released once every fitness CTA of this
+    // chunk is resident (launch-completion edge), so the explode blocks fill
+    // the room the persistent tcgen05 CTAs leave instead of taking the SMs first
+    mlp_fitness_launch(w->plan_chunks[c].mlp, v.spart + w->chunk_f0[c] * v.lam * v.nparts * 2, &v.ctl->active, s,
+                       w->pipe_lc ? w->ev_launched[c] : nullptr);
+    if (c + 1 < G) {
+      cudaStreamWaitEvent(w->aux, w->pipe_lc ? w->ev_launched[c] : w->ev_chunk[c], 0);
+      launch_explode_fireworks(v, w->chunk_f0[c + 1], w->chunk_nf[c + 1], w->nsm, w->aux);
+      cudaEventRecord(w->ev_chunk[c + 1], w->aux);
+    }
+  }
 }
 
 // ----------------------------------------------------------------- engine
@@ -630,7 +708,8 @@ class Engine {
     if (!ws->host_ctl) CUDA_TRY(cudaMallocHost(&ws->host_ctl, sizeof(Ctl)));
     host_ctl = ws->host_ctl;
     memset(host_ctl, 0, sizeof(Ctl));
-    hooks = GenerationHooks{ws.get(), hook_sparks, hook_guides, hook_fresh, hook_fresh_all};
+    hooks = GenerationHooks{ws.get(), hook_sparks, hook_guides, hook_fresh, hook_fresh_all,
+                            ws->plan_chunks.empty() ? nullptr : hook_explode_eval};
     ring_e.resize(ws->v.trace_cap * cfg.B);
     ring_b.resize(ws->v.trace_cap * cfg.B);
     ring_t.resize(ws->v.trace_cap * cfg.B);

@@ -176,6 +176,23 @@ __device__ __forceinline__ double unit_pm1(uint64_t h) {
   return __dsub_rn(unit_d1(h), __hiloint2double((int)c_hi, 0));
 }
 
+// unit_pm1 / unit_u53 of h = splitmix64(pre ^ d) from the mixer state (see
+// mix_draw): bit-identical, three ALU instructions fewer per draw.
+__device__ __forceinline__ double unit_pm1_z(MixState z) {
+  const uint32_t t = z.hi >> 11;                     // bits 43..63 of h
+  const uint32_t c_hi = 0x40000000u - (t & 0x100000u);  // top ? 1.0 : 2.0
+  const double d1 = __hiloint2double((int)(0x3FF00000u | (t & 0xFFFFFu)), (int)mant_lo(z));
+  return __dsub_rn(d1, __hiloint2double((int)c_hi, 0));
+}
+__device__ __forceinline__ double unit_u53_z(MixState z) {
+  const uint32_t t = z.hi >> 11;
+  const double dh = __hiloint2double((int)(0x3FE00000u | (t & 0xFFFFFu)), (int)mant_lo(z));
+  int32_t sgn;
+  asm("shr.s32 %0, %1, 31;" : "=r"(sgn) : "r"(z.hi));
+  const uint32_t c_hi = 0x3FE00000u & ~(uint32_t)sgn;  // top ? 0 : 0.5
+  return __dsub_rn(dh, __hiloint2double((int)c_hi, 0));
+}
+
 // Exact in-box test for x = round_f32(s): strictly between the fp32 box
 // images implies lower <= s <= upper (lo_f >= lower, and s > lo_f because
 // s rounds to a float above lo_f); callers fall back to the exact test
@@ -203,8 +220,8 @@ template <int KIND, bool FULL>
 __device__ __forceinline__ void explode_slice(const EngineView& v, const ExplodeChunk& ch,
                                               int lane, uint32_t cbase, uint32_t qoff,
                                               uint64_t f, uint64_t k0, int kn, double a,
-                                              const uint64_t (&pe)[kSparkGroup],
-                                              const uint64_t (&pm)[kSparkGroup],
+                                              const DrawKey (&pe)[kSparkGroup],
+                                              const DrawKey (&pm)[kSparkGroup], uint32_t one,
                                               float (&s0)[kSparkGroup], float (&s1)[kSparkGroup]) {
   constexpr int KG = kSparkGroup;
   const uint32_t D = (uint32_t)v.D;
@@ -227,8 +244,7 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
     unsigned slow = 0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const uint64_t h = splitmix64(pe[kk] ^ (uint64_t)(d0 + e));
-      sv[e] = __dadd_rn(pd[e], __dmul_rn(unit_pm1(h), a));
+      sv[e] = __dadd_rn(pd[e], __dmul_rn(unit_pm1_z(mix_draw(pe[kk], d0 + e, one)), a));
       x[e] = __double2float_rn(sv[e]);
       const bool need = !in_box_fast(x[e], lf[e], uf[e]);
       if (FULL ? need : (e < nvalid && need)) slow |= 1u << e;
@@ -251,8 +267,8 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
       const double pw[4] = {pw01.x, pw01.y, pw23.x, pw23.y};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const uint64_t h = splitmix64(pm[kk] ^ (uint64_t)(d0 + e));
-        const float m = __double2float_rn(__dadd_rn(pl[e], __dmul_rn(unit_u53(h), pw[e])));
+        const double u = unit_u53_z(mix_draw(pm[kk], d0 + e, one));
+        const float m = __double2float_rn(__dadd_rn(pl[e], __dmul_rn(u, pw[e])));
         const float r = (sv[e] >= lo[e] && sv[e] <= hi[e]) ? x[e] : m;
         x[e] = ((slow >> e) & 1u) ? fminf(fmaxf(r, lf[e]), uf[e]) : x[e];
       }
@@ -299,12 +315,13 @@ __device__ __forceinline__ void explode_group(const EngineView& v, const Explode
   else if (lane >= KG && lane < KG + kn)
     wq.pre[lane] = key_prefix(v.seed, kMapping, it, b, n, k0 + lane - KG);
   __syncwarp();
-  uint64_t pe[KG], pm[KG];
+  DrawKey pe[KG], pm[KG];
 #pragma unroll
   for (int kk = 0; kk < KG; ++kk) {
-    pe[kk] = wq.pre[kk];
-    pm[kk] = wq.pre[KG + kk];
+    pe[kk] = draw_key(wq.pre[kk]);
+    pm[kk] = draw_key(wq.pre[KG + kk]);
   }
+  const uint32_t one = (uint32_t)(v.Dp != 0);  // 1, opaque to the compiler (see mix_draw)
   __syncwarp();  // wq.pre is reused by this warp's next group
   const double a = v.amp[f];
   float s0[KG], s1[KG];
@@ -315,9 +332,9 @@ __device__ __forceinline__ void explode_group(const EngineView& v, const Explode
     const uint32_t qoff = q * 128;
     if (cbase + qoff >= D) break;  // warp-uniform
     if (kn == KG && cbase + qoff + 128 <= D)
-      explode_slice<KIND, true>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, s0, s1);
+      explode_slice<KIND, true>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, one, s0, s1);
     else
-      explode_slice<KIND, false>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, s0, s1);
+      explode_slice<KIND, false>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, one, s0, s1);
   }
   if (KIND != 0) {
 #pragma unroll
@@ -358,8 +375,11 @@ __device__ __forceinline__ void stage_explode_chunk(const EngineView& v, Explode
 // takes spark group 8*item_group + w.
 // KIND == 0: NN objective (bf16 shadow, no analytic partials); otherwise the
 // analytic objective kind whose partial sums are fused in.
-template <int KIND>
-__global__ void __launch_bounds__(256, 2) k_explode_map(EngineView v) {
+// MINB = 3 (the chunk variant run beside the persistent tcgen05 fitness
+// kernel): <= 85 registers so one 256-thread block fits next to the MLP CTA's
+// 384 threads on the same SM.
+template <int KIND, int MINB = 2>
+__global__ void __launch_bounds__(256, MINB) k_explode_map(EngineView v) {
   pdl_enter();
   if (gen_inactive(v)) return;
   constexpr int KG = kSparkGroup;
@@ -410,11 +430,25 @@ cudaError_t prepare_engine_kernels() {
   cudaError_t e = cudaSuccess;
   const int bytes = (int)kExplodeSmem;
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<0, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<OBJ_SPHERE>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<OBJ_RASTRIGIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<OBJ_ACKLEY>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, kRankSmemMax);
   return e;
+}
+
+// Explode + mapping of the owned fireworks [f0, f0 + nf) only (the spark
+// rows of that range), in the register-capped variant that co-resides with
+// the tcgen05 fitness kernel: the pipelined NN generation runs the fitness of
+// firework chunk c while chunk c + 1 explodes.
+void launch_explode_fireworks(const EngineView& v, uint64_t f0, uint64_t nf, int nsm, cudaStream_t s) {
+  EngineView c = v;
+  c.f_lo = v.f_lo + f0;
+  c.Fl = nf;
+  c.sparks = v.sparks + f0 * v.lam * v.Dp;
+  if (v.sparks_h) c.sparks_h = v.sparks_h + f0 * v.lam * v.Dp;
+  pdl_launch(k_explode_map<0, 3>, explode_blocks(c, nsm), 256, kExplodeSmem, s, c);
 }
 
 static void launch_explode_map_impl(const EngineView& v, int nsm, cudaStream_t s) {
@@ -1585,8 +1619,12 @@ void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
   if (phase != kGenB) {
     // population_range of this generation was computed by the previous
     // generation's (or initialize's) tail kernel, k_record_copy.
-    launch_explode_map_impl(v, nsm, s);
-    if (v.nn) hooks->eval_sparks(hooks->ctx, s);
+    if (v.nn && hooks->explode_eval) {
+      hooks->explode_eval(hooks->ctx, s);  // pipelined: explode chunk c+1 beside fitness chunk c
+    } else {
+      launch_explode_map_impl(v, nsm, s);
+      if (v.nn) hooks->eval_sparks(hooks->ctx, s);
+    }
     pdl_launch(k_rank, (unsigned)v.Fl, kRankThreads, rank_smem(v), s, v);
     if (v.M > 0) {
       pdl_launch(k_guides, guide_blocks(v, nsm), 256, guides_smem(v), s, v);

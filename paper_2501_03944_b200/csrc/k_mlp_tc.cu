@@ -733,14 +733,20 @@ cudaError_t prepare_h() {
 
 template <int H, int CG>
 cudaError_t launch_h(const CUtensorMap& tx, const CUtensorMap& tw, int grid, const MlpArgs& a,
-                     cudaStream_t s) {
+                     cudaStream_t s, cudaEvent_t launch_done) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem_bytes<CG>();
   cfg.stream = s;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   int n = 0;
+  if (launch_done) {
+    attr[n].id = cudaLaunchAttributeLaunchCompletionEvent;
+    attr[n].val.launchCompletionEvent.event = launch_done;
+    attr[n].val.launchCompletionEvent.flags = 0;
+    ++n;
+  }
   if (pdl_enabled()) {
     attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[n].val.programmaticStreamSerializationAllowed = 1;
@@ -870,23 +876,24 @@ MlpPlan* mlp_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t S, u
 
 void mlp_plan_destroy(MlpPlan* p) { delete p; }
 
-cudaError_t mlp_fitness_launch(const MlpPlan* p, float* part, const int* gate, cudaStream_t s) {
+cudaError_t mlp_fitness_launch(const MlpPlan* p, float* part, const int* gate, cudaStream_t s,
+                               cudaEvent_t launch_done) {
   MlpArgs a = p->args;
   a.part = part;
   a.gate = gate;
   if (p->cg == 2) {
     switch (p->H) {
-      case 32: return launch_h<32, 2>(p->tmap_x, p->tmap_w, p->grid, a, s);
-      case 64: return launch_h<64, 2>(p->tmap_x, p->tmap_w, p->grid, a, s);
-      case 128: return launch_h<128, 2>(p->tmap_x, p->tmap_w, p->grid, a, s);
-      case 256: return launch_h<256, 2>(p->tmap_x, p->tmap_w, p->grid, a, s);
+      case 32: return launch_h<32, 2>(p->tmap_x, p->tmap_w, p->grid, a, s, launch_done);
+      case 64: return launch_h<64, 2>(p->tmap_x, p->tmap_w, p->grid, a, s, launch_done);
+      case 128: return launch_h<128, 2>(p->tmap_x, p->tmap_w, p->grid, a, s, launch_done);
+      case 256: return launch_h<256, 2>(p->tmap_x, p->tmap_w, p->grid, a, s, launch_done);
     }
   }
   switch (p->H) {
-    case 32: return launch_h<32, 1>(p->tmap_x, p->tmap_w, p->grid, a, s);
-    case 64: return launch_h<64, 1>(p->tmap_x, p->tmap_w, p->grid, a, s);
-    case 128: return launch_h<128, 1>(p->tmap_x, p->tmap_w, p->grid, a, s);
-    case 256: return launch_h<256, 1>(p->tmap_x, p->tmap_w, p->grid, a, s);
+    case 32: return launch_h<32, 1>(p->tmap_x, p->tmap_w, p->grid, a, s, launch_done);
+    case 64: return launch_h<64, 1>(p->tmap_x, p->tmap_w, p->grid, a, s, launch_done);
+    case 128: return launch_h<128, 1>(p->tmap_x, p->tmap_w, p->grid, a, s, launch_done);
+    case 256: return launch_h<256, 1>(p->tmap_x, p->tmap_w, p->grid, a, s, launch_done);
   }
   return cudaErrorInvalidValue;
 }

@@ -16,6 +16,9 @@ struct GenerationHooks {
   void (*eval_guides)(void* ctx, cudaStream_t s);
   void (*eval_fresh)(void* ctx, cudaStream_t s);      // gated on n_losers
   void (*eval_fresh_all)(void* ctx, cudaStream_t s);  // initialize()
+  // optional: explode + spark fitness as one pipelined step (replaces the
+  // explode launch and eval_sparks; see launch_explode_fireworks)
+  void (*explode_eval)(void* ctx, cudaStream_t s);
 };
 
 // One-time kernel attributes (dynamic shared memory opt-in); call before
@@ -36,6 +39,7 @@ cudaError_t launch_small_run(const EngineView& v, uint64_t max_gens, cudaStream_
 // operator seams
 void launch_pop_range(const EngineView& v, int nsm, cudaStream_t s);
 void launch_explode_map(const EngineView& v, int nsm, cudaStream_t s);
+void launch_explode_fireworks(const EngineView& v, uint64_t f0, uint64_t nf, int nsm, cudaStream_t s);
 void launch_rank(const EngineView& v, cudaStream_t s);
 void launch_guides(const EngineView& v, int nsm, cudaStream_t s);
 void launch_select(const EngineView& v, int nsm, cudaStream_t s);
@@ -75,8 +79,10 @@ MlpPlan* mlp_plan_create(const __nv_bfloat16* X, const int32_t* y,
 void mlp_plan_destroy(MlpPlan* p);
 // part[row][m_tile][2] (slot 0 = sum of CE over the m-tile's samples).
 // gate: if non-null and *gate == 0 the kernel exits immediately.
+// launch_done (optional): recorded once every CTA of the launch is resident
+// (cudaLaunchAttributeLaunchCompletionEvent)
 cudaError_t mlp_fitness_launch(const MlpPlan* p, float* part,
-                               const int* gate, cudaStream_t s);
+                               const int* gate, cudaStream_t s, cudaEvent_t launch_done = nullptr);
 uint32_t mlp_num_parts(uint32_t S);
 
 // ---- LeNet-5 fitness (k_lenet.cu, warp-level bf16 MMA) ----

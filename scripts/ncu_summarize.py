@@ -26,6 +26,25 @@ METRICS = [
     "launch__grid_size",
     "launch__block_size",
     "smsp__inst_executed.sum",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fmaheavy.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
+    "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_dispatch_stall_per_issue_active.ratio",
+    "smsp__average_warps_issue_stalled_no_instruction_per_issue_active.ratio",
+    "smsp__warps_active.avg.per_cycle_active",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
 ]
 
 
@@ -69,7 +88,10 @@ def report(paths, out):
         rows = list(csv.reader(txt.splitlines()))
         h, units, data = rows[0], rows[1], rows[2:]
         for r in data:
-            d = {"report": p, "kernel": r[h.index("Kernel Name")]}
+            import os
+            base = os.path.basename(p)
+            d = {"report": p, "kernel": r[h.index("Kernel Name")],
+                 "workload": base.split("_")[0] if base[:1] == "c" and "_" in base else "c2"}
             for m in METRICS:
                 if m in h:
                     i = h.index(m)
