@@ -651,6 +651,7 @@ class Engine {
   cudaGraphExec_t gen_exec = nullptr;    // whole loop body (one rank)
   cudaGraphExec_t gen_exec_a = nullptr;  // sharded: up to selection
   cudaGraphExec_t gen_exec_b = nullptr;  // sharded: loser-out .. record
+  cudaGraphExec_t gen_exec_ab = nullptr;  // sharded with NCCL: A + captured exchange + B
   uint64_t rank = 0, world = 1;
   ncclComm_t comm = nullptr;
   uint64_t kernels_per_gen = 0;
@@ -671,6 +672,7 @@ class Engine {
     // gen_exec, own_stream and host_ctl belong to the workspace
     if (gen_exec_a) cudaGraphExecDestroy(gen_exec_a);
     if (gen_exec_b) cudaGraphExecDestroy(gen_exec_b);
+    if (gen_exec_ab) cudaGraphExecDestroy(gen_exec_ab);
     if (stream) cudaStreamSynchronize(stream);
     if (own_stream && own_stream != stream) cudaStreamSynchronize(own_stream);
     if (comm) nccl().CommDestroy(comm);
@@ -717,14 +719,23 @@ class Engine {
   }
 
   Status capture_one(int phase, cudaGraphExec_t* out, size_t* nodes) {
+    return capture_body([&]() -> Status {
+      launch_generation_kernels(ws->v, ws->nsm, own_stream, &hooks, phase);
+      return ok();
+    }, out, nodes);
+  }
+
+  template <typename Body>
+  Status capture_body(Body body, cudaGraphExec_t* out, size_t* nodes) {
     cudaGraph_t g = nullptr;
     (void)cudaGetLastError();  // clear a stale error so the check below sees this capture's
     CUDA_TRY(cudaStreamBeginCapture(own_stream, cudaStreamCaptureModeThreadLocal));
-    launch_generation_kernels(ws->v, ws->nsm, own_stream, &hooks, phase);
+    const Status bs = body();
     const cudaError_t le = cudaGetLastError();  // a failed launch inside the capture
     cudaError_t e = cudaStreamEndCapture(own_stream, &g);
-    if (le != cudaSuccess) {
+    if (bs.code != MGFWA_OK || le != cudaSuccess) {
       if (g) cudaGraphDestroy(g);
+      if (bs.code != MGFWA_OK) return bs;
       return Status{MGFWA_ECUDA, std::string("kernel launch during graph capture: ") + cudaGetErrorString(le)};
     }
     if (e != cudaSuccess) return Status{MGFWA_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e)};
@@ -767,7 +778,29 @@ class Engine {
       ws->exec_nodes = kernels_per_gen = n;
       return ok();
     }
-    if (gen_exec_a) return ok();
+    if (gen_exec_a || gen_exec_ab) return ok();
+    if (comm != nullptr) {
+      // One graph per generation: phase A, the NCCL exchange (captured:
+      // NCCL >= 2.9 records its kernels into the graph) and phase B — no
+      // host round trip between the phases.  Falls back to two graphs with
+      // host-enqueued collectives when the capture is refused.
+      const char* env = getenv("MGFWA_NCCL_GRAPH");
+      if (!(env && env[0] == '0')) {
+        size_t n = 0;
+        const Status st = capture_body([&]() -> Status {
+          launch_generation_kernels(ws->v, ws->nsm, own_stream, &hooks, kGenA);
+          STATUS_TRY(exchange_nccl(own_stream));
+          launch_generation_kernels(ws->v, ws->nsm, own_stream, &hooks, kGenB);
+          return ok();
+        }, &gen_exec_ab, &n);
+        if (st.code == MGFWA_OK) {
+          kernels_per_gen = n;
+          return ok();
+        }
+        gen_exec_ab = nullptr;
+        (void)cudaGetLastError();
+      }
+    }
     size_t na = 0, nb = 0;
     STATUS_TRY(capture_one(kGenA, &gen_exec_a, &na));
     STATUS_TRY(capture_one(kGenB, &gen_exec_b, &nb));
@@ -813,21 +846,21 @@ class Engine {
     return ok();
   }
 
-  Status exchange_nccl() {
+  Status exchange_nccl(cudaStream_t st) {
     const EngineView& v = ws->v;
     NCCL_TRY(nccl().GroupStart());
-    NCCL_TRY(nccl().AllReduce(&v.ctl->nan_own, &v.ctl->nan_all, 1, ncclUint64, ncclSum, comm, stream));
+    NCCL_TRY(nccl().AllReduce(&v.ctl->nan_own, &v.ctl->nan_all, 1, ncclUint64, ncclSum, comm, st));
     if (v.replica) {
       NCCL_TRY(nccl().AllReduce(&v.ctl->n_losers_all, &v.ctl->n_losers_all, 1, ncclUint64, ncclSum, comm,
-                                stream));
+                                st));
       NCCL_TRY(nccl().GroupEnd());
       return ok();
     }
     const size_t rows = v.Fl * v.Dp;
-    NCCL_TRY(nccl().AllGather(v.pos + v.f_lo * v.Dp, v.pos, rows, ncclFloat, comm, stream));
-    NCCL_TRY(nccl().AllGather(v.fit + v.f_lo, v.fit, v.Fl, ncclFloat64, comm, stream));
-    NCCL_TRY(nccl().AllGather(v.amp + v.f_lo, v.amp, v.Fl, ncclFloat64, comm, stream));
-    NCCL_TRY(nccl().AllGather(v.li + v.f_lo, v.li, v.Fl, ncclFloat64, comm, stream));
+    NCCL_TRY(nccl().AllGather(v.pos + v.f_lo * v.Dp, v.pos, rows, ncclFloat, comm, st));
+    NCCL_TRY(nccl().AllGather(v.fit + v.f_lo, v.fit, v.Fl, ncclFloat64, comm, st));
+    NCCL_TRY(nccl().AllGather(v.amp + v.f_lo, v.amp, v.Fl, ncclFloat64, comm, st));
+    NCCL_TRY(nccl().AllGather(v.li + v.f_lo, v.li, v.Fl, ncclFloat64, comm, st));
     NCCL_TRY(nccl().GroupEnd());
     return ok();
   }
@@ -935,8 +968,12 @@ class Engine {
     if (comm == nullptr)
       return Status{MGFWA_ESTATE, "mgfwa: sharded context needs mgfwa_attach_nccl (or phases + exchange)"};
     for (uint64_t i = 0; i < n; ++i) {
+      if (gen_exec_ab) {
+        CUDA_TRY(cudaGraphLaunch(gen_exec_ab, stream));
+        continue;
+      }
       CUDA_TRY(cudaGraphLaunch(gen_exec_a, stream));
-      STATUS_TRY(exchange_nccl());
+      STATUS_TRY(exchange_nccl(stream));
       CUDA_TRY(cudaGraphLaunch(gen_exec_b, stream));
     }
     return ok();
