@@ -794,7 +794,14 @@ class Engine {
           return ok();
         }, &gen_exec_ab, &n);
         if (st.code == MGFWA_OK) {
-          kernels_per_gen = n;
+          // count this library's kernels only (the graph also holds NCCL's)
+          size_t na = 0, nb = 0;
+          cudaGraphExec_t ga = nullptr, gb = nullptr;
+          STATUS_TRY(capture_one(kGenA, &ga, &na));
+          STATUS_TRY(capture_one(kGenB, &gb, &nb));
+          cudaGraphExecDestroy(ga);
+          cudaGraphExecDestroy(gb);
+          kernels_per_gen = na + nb;
           return ok();
         }
         gen_exec_ab = nullptr;
