@@ -50,6 +50,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tc_glue.cuh"
 
 namespace mgfwa_b200 {
 
@@ -301,7 +302,11 @@ __host__ __device__ constexpr int conv2_k(int ky, int kx) {
   return ky < 4 ? 16 * (2 * kx + (ky >> 1)) + 8 * (ky & 1) : 16 * (10 + (kx >> 1)) + 8 * (kx & 1);
 }
 
-template <int N>
+// IL = false: o = the sample's [25 windows][16 channels] bf16 row (scratch
+// path).  IL = true: o = the sample's row base inside the fc1 A operand of
+// the fused kernel (tcgen05 no-swizzle K-major layout, K = ch * 25 + window,
+// see fc1_a_off): each value goes straight to its slot.
+template <int N, bool IL = false>
 __device__ __forceinline__ void conv2_tiles(int t0, const uint32_t* p1c, __nv_bfloat16* o, int wi, int dx,
                                             int c, const uint32_t (&bw2)[13][2][2], float b2a, float b2b,
                                             float b2c, float b2d) {
@@ -364,9 +369,21 @@ __device__ __forceinline__ void conv2_tiles(int t0, const uint32_t* p1c, __nv_bf
     s2 += __shfl_xor_sync(0xffffffffu, s2, 4);
     s3 += __shfl_xor_sync(0xffffffffu, s3, 4);
     if (dx == 0 && wv[u] >= 0) {
-      uint32_t* ow = reinterpret_cast<uint32_t*>(o + wv[u] * 16);
-      ow[c] = pack_bf16(s0, s1);
-      ow[4 + c] = pack_bf16(s2, s3);
+      if (IL) {
+        // K = ch * 25 + w: byte (K / 8) * 2048 + (K % 8) * 2 from the row base
+        const int w = wv[u];
+        const float vals[4] = {s0, s1, s2, s3};
+        const int chs[4] = {2 * c, 2 * c + 1, 8 + 2 * c, 9 + 2 * c};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int k = chs[q] * 25 + w;
+          o[(k >> 3) * 1024 + (k & 7)] = __float2bfloat16(vals[q]);
+        }
+      } else {
+        uint32_t* ow = reinterpret_cast<uint32_t*>(o + wv[u] * 16);
+        ow[c] = pack_bf16(s0, s1);
+        ow[4 + c] = pack_bf16(s2, s3);
+      }
     }
   }
 }
@@ -687,8 +704,346 @@ __global__ void __launch_bounds__(kFcThreads, 1) k_lenet_fc(LenetSplitArgs sa) {
   }
 }
 
+// ============================================================ fused kernel
+// k_lenet_fused — conv (warp-level MMA, as k_lenet_conv) and the fc stack on
+// the 5th-gen tensor cores in one CTA per SM, with no activation scratch in
+// HBM.  Work item = (candidate, 128-sample chunk):
+//   1. conv: 8 warps, one sample each at a time (conv1_pairs + conv2_tiles);
+//      each sample's pooled conv2 output (400 bf16) goes straight into the
+//      fc1 A operand in shared memory (tcgen05 no-swizzle K-major layout,
+//      K = channel * 25 + window, the natural f1w column order);
+//   2. fc1 = tcgen05.mma kind::f16 M = 128 samples, N = 128 (120 outputs),
+//      K = 400 with A and B (f1w, staged from the candidate row in two
+//      K halves through the conv buffers) in shared memory, D1 in TMEM;
+//   3. +b1, ReLU, bf16 -> back into TMEM (tcgen05.st) as the A operand of
+//      fc2 (M = 128, N = 96 (84), K = 128 (120), B = f2w in shared memory),
+//      the same for fc3 (N = 16 (10), K = 96 (84)) — MMAs with A in TMEM;
+//   4. logits (tcgen05.ld, one sample per thread) -> CE -> fixed-order sums.
+// TMEM columns: A2 [0, 64), A3 [64, 112), D1 [256, 384), D2 [384, 480),
+// D3 [480, 496) of a 512-column allocation.
+namespace {
+
+constexpr int kFW = 8;  // conv warps (smem: 8 x (pair image + pooled map) + the fc1 A operand)
+constexpr int kFThreads = kFW * 32;
+
+// byte offset of element (r, k) in a no-swizzle K-major tcgen05 operand of
+// R rows: 8-row x 16-byte core matrices, LBO (along K) = R * 16, SBO = 128
+__host__ __device__ constexpr uint32_t il_off(uint32_t r, uint32_t k, uint32_t R) {
+  return (k >> 3) * (R * 16) + (r >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2;
+}
+
+struct FusedSmem {
+  static constexpr int wc1 = 0;                                // [8][32] bf16
+  static constexpr int wc2 = wc1 + 8 * kC1K * 2;               // [16][216] bf16
+  static constexpr int bc1 = wc2 + 16 * kC2S * 2;              // f32 [8]
+  static constexpr int bc2 = bc1 + 8 * 4;                      // f32 [16]
+  static constexpr int img = bc2 + 16 * 4;                     // per warp [33][40] u32 | f1w half
+  static constexpr int p1 = img + kFW * kImgWords * 4;         // per warp [14][kP1R][4] u32
+  static constexpr int a1 = p1 + kFW * kP1Words * 4;           // fc1 A: 128 x 400 bf16
+  static constexpr int w2 = a1 + 128 * 400 * 2;                // fc2 B: 96 x 128 bf16
+  static constexpr int w3 = w2 + 96 * 128 * 2;                 // fc3 B: 16 x 96 bf16
+  static constexpr int b1 = w3 + 16 * 96 * 2;                  // f32 [128]
+  static constexpr int b2 = b1 + 128 * 4;                      // f32 [96]
+  static constexpr int b3 = b2 + 96 * 4;                       // f32 [16]
+  static constexpr int red = b3 + 16 * 4;                      // f32 [8]
+  static constexpr int bar = red + 8 * 4;                      // u64 mbarrier
+  static constexpr int slot = bar + 8;                         // TMEM base
+  static constexpr int total = slot + 16;
+};
+constexpr int kF1Half0 = 208, kF1Half1 = 192;  // K per f1w half (13 + 12 MMA k-steps)
+static_assert(FusedSmem::total <= 227 * 1024, "fused LeNet shared memory");
+static_assert(FusedSmem::img % 16 == 0 && FusedSmem::a1 % 16 == 0 && FusedSmem::w2 % 16 == 0 &&
+                  FusedSmem::w3 % 16 == 0 && FusedSmem::bar % 8 == 0, "aligned operands");
+static_assert(128 * 208 * 2 <= FusedSmem::a1 - FusedSmem::img, "an f1w half fits the conv buffers");
+
+constexpr uint32_t kColA2 = 0, kColA3 = 64, kColD1 = 256, kColD2 = 384, kColD3 = 480;
+
+// 16 bytes = parameters [k0, k0 + 8) of row `j` (8-byte aligned source), 0 past `kmax`
+__device__ __forceinline__ uint4 load8(const __nv_bfloat16* rowp, int k0, int kmax) {
+  if (k0 + 8 <= kmax) {
+    const uint2 a = *reinterpret_cast<const uint2*>(rowp + k0);
+    const uint2 b = *reinterpret_cast<const uint2*>(rowp + k0 + 4);
+    return make_uint4(a.x, a.y, b.x, b.y);
+  }
+  uint16_t v[8];
+  const uint16_t* r = reinterpret_cast<const uint16_t*>(rowp);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) v[q] = k0 + q < kmax ? r[k0 + q] : (uint16_t)0;
+  return make_uint4(v[0] | (uint32_t)v[1] << 16, v[2] | (uint32_t)v[3] << 16, v[4] | (uint32_t)v[5] << 16,
+                    v[6] | (uint32_t)v[7] << 16);
+}
+
+// stage f1w[:, k0 .. k0 + kh) (rows 120..127 zero) as a 128-row operand
+__device__ __forceinline__ void stage_f1_half(uint8_t* dst, const __nv_bfloat16* w, int k0, int kh) {
+  const int chunks = kh / 8;
+  for (int i = threadIdx.x; i < 128 * chunks; i += kFThreads) {
+    const int j = i / chunks, cc = i - chunks * j;
+    const uint4 v = j < 120 ? load8(w + oF1W + j * 400, k0 + 8 * cc, 400) : make_uint4(0u, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(dst + il_off(j, 8 * cc, 128)) = v;
+  }
+}
+
+__device__ __forceinline__ void async_smem_fence() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kFThreads, 1) k_lenet_fused(LenetArgs args) {
+  using namespace tc;
+  pdl_enter();
+  if (args.gate != nullptr && *args.gate == 0) return;
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, c = lane & 3;
+  const int wi = g >> 1, dx = g & 1;
+  __nv_bfloat16* wc1 = reinterpret_cast<__nv_bfloat16*>(sm + FusedSmem::wc1);
+  __nv_bfloat16* wc2 = reinterpret_cast<__nv_bfloat16*>(sm + FusedSmem::wc2);
+  float* bc1 = reinterpret_cast<float*>(sm + FusedSmem::bc1);
+  float* bc2 = reinterpret_cast<float*>(sm + FusedSmem::bc2);
+  const uint32_t* img = reinterpret_cast<const uint32_t*>(sm + FusedSmem::img) + warp * kImgWords;
+  const uint32_t img_s = smem_addr(img);
+  uint32_t* p1 = reinterpret_cast<uint32_t*>(sm + FusedSmem::p1) + warp * kP1Words;
+  __nv_bfloat16* a1 = reinterpret_cast<__nv_bfloat16*>(sm + FusedSmem::a1);
+  float* sb1 = reinterpret_cast<float*>(sm + FusedSmem::b1);
+  float* sb2 = reinterpret_cast<float*>(sm + FusedSmem::b2);
+  float* sb3 = reinterpret_cast<float*>(sm + FusedSmem::b3);
+  float* red = reinterpret_cast<float*>(sm + FusedSmem::red);
+  const uint32_t bar = smem_u32(sm + FusedSmem::bar);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + FusedSmem::slot);
+  {
+    uint32_t* p = reinterpret_cast<uint32_t*>(sm);
+    for (int i = threadIdx.x; i < FusedSmem::bar / 4; i += kFThreads) p[i] = 0u;
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int q = warp & 3, hf = warp >> 2;           // TMEM lane quarter, column half
+  const uint32_t lanes = tmem + ((uint32_t)(q * 32) << 16);
+  const uint32_t r_s = smem_u32(sm + FusedSmem::img), a1_s = smem_u32(a1);
+  const uint32_t w2_s = smem_u32(sm + FusedSmem::w2), w3_s = smem_u32(sm + FusedSmem::w3);
+  uint32_t phase = 0;
+  auto mma_round = [&]() {  // every thread: wait for the MMAs committed to `bar`
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+  };
+
+  const uint32_t* imgc = img + c * kImgS;
+  const uint32_t* imgd = img + 4 * kImgS + 2 * (c < 3 ? c : 2);
+  const uint32_t* p1c = p1 + c;
+  const uint64_t total = args.rows * args.nparts;
+  const uint64_t t_begin = total * blockIdx.x / gridDim.x;
+  const uint64_t t_end = total * (blockIdx.x + 1) / gridDim.x;
+  uint64_t staged = ~0ull;
+  uint32_t bw1[2][2], bw2[13][2][2];
+  float b1a = 0.f, b1b = 0.f, b2a = 0.f, b2b = 0.f, b2c = 0.f, b2d = 0.f;
+  for (uint64_t item = t_begin; item < t_end; ++item) {
+    const uint64_t row = item / args.nparts;
+    const uint32_t part = (uint32_t)(item % args.nparts);
+    const uint32_t s_lo = part * kChunkS, s_hi = min(args.S, s_lo + kChunkS);
+    const __nv_bfloat16* w = args.W + row * args.Dp;
+    __syncthreads();  // the previous item's readers of every buffer are done
+    if (row != staged) {
+      // conv weights / biases pre-scaled by 1/4 (average pools = sums of ReLUs)
+      for (int i = threadIdx.x; i < 150; i += kFThreads) {
+        const int ch = i / 25, r = i % 25, ky = r / 5, kx = r % 5;
+        wc1[ch * kC1K + conv1_k(ky, kx)] = __float2bfloat16(0.25f * bf(w[oC1W + i]));
+      }
+      for (int i = threadIdx.x; i < 2400; i += kFThreads) {
+        const int ch = i / 150, r = i % 150, ci = r / 25, tap = r % 25;
+        wc2[ch * kC2S + conv2_k(tap / 5, tap % 5) + ci] = __float2bfloat16(0.25f * bf(w[oC2W + i]));
+      }
+      if (threadIdx.x < 6) bc1[threadIdx.x] = 0.25f * bf(w[oC1B + threadIdx.x]);
+      if (threadIdx.x < 16) bc2[threadIdx.x] = 0.25f * bf(w[oC2B + threadIdx.x]);
+      // fc2 / fc3 B operands (rows past 84 / 10 and K past 120 / 84 are zero) and biases
+      for (int i = threadIdx.x; i < 96 * 16; i += kFThreads) {
+        const int j = i / 16, cc = i - 16 * j;
+        const uint4 v = j < 84 ? load8(w + oF2W + j * 120, 8 * cc, 120) : make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(sm + FusedSmem::w2 + il_off(j, 8 * cc, 96)) = v;
+      }
+      for (int i = threadIdx.x; i < 16 * 12; i += kFThreads) {
+        const int j = i / 12, cc = i - 12 * j;
+        const uint4 v = j < 10 ? load8(w + oF3W + j * 84, 8 * cc, 84) : make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(sm + FusedSmem::w3 + il_off(j, 8 * cc, 16)) = v;
+      }
+      if (threadIdx.x < 128) sb1[threadIdx.x] = threadIdx.x < 120 ? bf(w[oF1B + threadIdx.x]) : 0.f;
+      if (threadIdx.x < 96) sb2[threadIdx.x] = threadIdx.x < 84 ? bf(w[oF2B + threadIdx.x]) : 0.f;
+      if (threadIdx.x < 16) sb3[threadIdx.x] = threadIdx.x < 10 ? bf(w[oF3B + threadIdx.x]) : 0.f;
+      __syncthreads();
+      staged = row;
+#pragma unroll
+      for (int st = 0; st < 2; ++st) {
+        const __nv_bfloat16* b = wc1 + g * kC1K + 16 * st + 2 * c;
+        bw1[st][0] = *reinterpret_cast<const uint32_t*>(b);
+        bw1[st][1] = *reinterpret_cast<const uint32_t*>(b + 8);
+      }
+#pragma unroll
+      for (int st = 0; st < 13; ++st)
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+          const __nv_bfloat16* b = wc2 + (8 * n + g) * kC2S + 16 * st + 2 * c;
+          bw2[st][n][0] = *reinterpret_cast<const uint32_t*>(b);
+          bw2[st][n][1] = *reinterpret_cast<const uint32_t*>(b + 8);
+        }
+      b1a = bc1[2 * c], b1b = bc1[2 * c + 1];
+      b2a = bc2[2 * c], b2b = bc2[2 * c + 1], b2c = bc2[8 + 2 * c], b2d = bc2[9 + 2 * c];
+    }
+    // ---- 1. conv for the chunk's samples -> fc1 A operand
+    if (s_lo + warp < s_hi) prefetch_img(img_s, args.pimg + (uint64_t)(s_lo + warp) * kImgWords, lane);
+    for (uint32_t s = s_lo + warp; s < s_hi; s += kFW) {
+      cp_async_wait_all();
+      __syncwarp();
+#pragma unroll 1
+      for (int t0 = 0; t0 + LENET_CV_P1T <= 25; t0 += LENET_CV_P1T)
+        conv1_pairs<LENET_CV_P1T>(t0, imgc, imgd, p1, g, c, bw1, b1a, b1b);
+      if constexpr (25 % LENET_CV_P1T != 0)
+        conv1_pairs<25 % LENET_CV_P1T>(25 - 25 % LENET_CV_P1T, imgc, imgd, p1, g, c, bw1, b1a, b1b);
+      __syncwarp();
+      if (s + kFW < s_hi) prefetch_img(img_s, args.pimg + (uint64_t)(s + kFW) * kImgWords, lane);
+      const uint32_t r = s - s_lo;
+      __nv_bfloat16* orow = a1 + ((r >> 3) * 128 + (r & 7) * 16) / 2;
+#pragma unroll 1
+      for (int t0 = 0; t0 + kCvC2T <= 7; t0 += kCvC2T)
+        conv2_tiles<kCvC2T, true>(t0, p1c, orow, wi, dx, c, bw2, b2a, b2b, b2c, b2d);
+      if constexpr (7 % kCvC2T != 0)
+        conv2_tiles<7 % kCvC2T, true>(7 - 7 % kCvC2T, p1c, orow, wi, dx, c, bw2, b2a, b2b, b2c, b2d);
+      __syncwarp();
+    }
+    async_smem_fence();  // generic-proxy writes of the A operand -> visible to the tensor core
+    __syncthreads();
+    // ---- 2. fc1: D1 = A1 (128 x 400) . f1w^T, two K halves of f1w through the conv buffers
+    uint32_t kk0 = 0;
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const int k0 = h == 0 ? 0 : kF1Half0, kh = h == 0 ? kF1Half0 : kF1Half1;
+      stage_f1_half(sm + FusedSmem::img, w, k0, kh);
+      async_smem_fence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        tc_fence_after();
+        constexpr uint32_t id1 = idesc_bf16(128, 128);
+        for (int kk = 0; kk < kh / 16; ++kk) {
+          const uint64_t da = interleaved_desc(a1_s + (kk0 + kk) * 2 * 2048, 2048, 128);
+          const uint64_t db = interleaved_desc(r_s + kk * 2 * 2048, 2048, 128);
+          mma_ss(tmem + kColD1, da, db, id1, (kk0 + kk) != 0);
+        }
+        mma_commit(bar);
+      }
+      kk0 += kh / 16;
+      mma_round();  // also frees the f1w half buffer
+    }
+    // ---- 3. fc1 epilogue -> A2, fc2, fc2 epilogue -> A3, fc3
+#pragma unroll 1
+    for (int cc = 0; cc < 2; ++cc) {
+      const int col0 = hf * 64 + cc * 32;
+      float acc[32];
+      tmem_ld32(lanes + kColD1 + col0, acc);
+      uint32_t pk[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        pk[u] = pack_bf16(fmaxf(acc[2 * u] + sb1[col0 + 2 * u], 0.f), fmaxf(acc[2 * u + 1] + sb1[col0 + 2 * u + 1], 0.f));
+      tmem_st16(lanes + kColA2 + col0 / 2, pk);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tc_fence_after();
+      constexpr uint32_t id2 = idesc_bf16(128, 96);
+      for (int kk = 0; kk < 8; ++kk)
+        mma_ts(tmem + kColD2, tmem + kColA2 + 8 * kk, interleaved_desc(w2_s + kk * 2 * 1536, 1536, 128), id2, kk != 0);
+      mma_commit(bar);
+    }
+    mma_round();
+    {
+      // D2 columns [hf * 48, hf * 48 + 48): 32 + 16
+      const int col0 = hf * 48;
+      float acc[32];
+      tmem_ld32(lanes + kColD2 + col0, acc);
+      uint32_t pk[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        pk[u] = pack_bf16(fmaxf(acc[2 * u] + sb2[col0 + 2 * u], 0.f), fmaxf(acc[2 * u + 1] + sb2[col0 + 2 * u + 1], 0.f));
+      tmem_st16(lanes + kColA3 + col0 / 2, pk);
+      float acc2[16];
+      tmem_ld16(lanes + kColD2 + col0 + 32, acc2);
+      uint32_t pk2[16];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        pk2[u] = pack_bf16(fmaxf(acc2[2 * u] + sb2[col0 + 32 + 2 * u], 0.f),
+                           fmaxf(acc2[2 * u + 1] + sb2[col0 + 32 + 2 * u + 1], 0.f));
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                       lanes + kColA3 + (col0 + 32) / 2),
+                   "r"(pk2[0]), "r"(pk2[1]), "r"(pk2[2]), "r"(pk2[3]), "r"(pk2[4]), "r"(pk2[5]), "r"(pk2[6]),
+                   "r"(pk2[7])
+                   : "memory");
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tc_fence_after();
+      constexpr uint32_t id3 = idesc_bf16(128, 16);
+      for (int kk = 0; kk < 6; ++kk)
+        mma_ts(tmem + kColD3, tmem + kColA3 + 8 * kk, interleaved_desc(w3_s + kk * 2 * 256, 256, 128), id3, kk != 0);
+      mma_commit(bar);
+    }
+    mma_round();
+    // ---- 4. logits -> CE (thread = sample), fixed-order sums
+    float loss = 0.f;
+    if (hf == 0) {
+      float z[16];
+      tmem_ld16(lanes + kColD3, z);
+      const uint32_t smp = s_lo + q * 32 + lane;
+      if (smp < s_hi) {
+        float m = -INFINITY;
+#pragma unroll
+        for (int o = 0; o < 10; ++o) {
+          z[o] += sb3[o];
+          m = fmaxf(m, z[o]);
+        }
+        float se = 0.f;
+#pragma unroll
+        for (int o = 0; o < 10; ++o) se += expf(z[o] - m);
+        const int lab = args.y[smp];
+        float zl = z[0];
+#pragma unroll
+        for (int o = 1; o < 10; ++o) zl = o == lab ? z[o] : zl;
+        loss = (m + logf(se)) - zl;
+      }
+      loss = warp_sum(loss);
+      if (lane == 0) red[q] = loss;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const float t = ((red[0] + red[1]) + red[2]) + red[3];
+      args.part[(row * args.nparts + part) * 2] = t;
+      args.part[(row * args.nparts + part) * 2 + 1] = 0.0f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
 struct LenetPlan {
   LenetArgs args;
+  bool fused;  // k_lenet_fused (default); MGFWA_LENET_FUSED=0: conv + fc kernels through the HBM scratch
+  unsigned grid_fused;
   unsigned grid_conv, grid_fc;
   uint64_t group_rows;  // candidates per conv/fc launch pair (bounds the scratch)
   uint32_t* pimg;       // owned
@@ -712,7 +1067,9 @@ LenetPlan* lenet_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t 
   if (cudaFuncSetAttribute(k_lenet_conv, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            ConvSmem::total) != cudaSuccess ||
       cudaFuncSetAttribute(k_lenet_fc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           FcSmem::total) != cudaSuccess) {
+                           FcSmem::total) != cudaSuccess ||
+      cudaFuncSetAttribute(k_lenet_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           FusedSmem::total) != cudaSuccess) {
     snprintf(err, errlen, "LeNet objective: shared memory opt-in failed");
     return nullptr;
   }
@@ -730,6 +1087,22 @@ LenetPlan* lenet_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t 
     cudaFree(p->pimg);
     delete p;
     return nullptr;
+  }
+  p->args.pimg = p->pimg;
+  p->args.y = y;
+  p->args.W = W;
+  p->args.rows = rows;
+  p->args.Dp = Dp;
+  p->args.S = S;
+  p->args.nparts = lenet_num_parts(S);
+  {
+    const char* e = getenv("MGFWA_LENET_FUSED");
+    p->fused = !(e && e[0] == '0');
+  }
+  if (p->fused) {
+    const uint64_t items = rows * p->args.nparts;
+    p->grid_fused = (unsigned)(items < (uint64_t)nsm ? items : (uint64_t)nsm);
+    return p;
   }
   // scratch of at most kScratchBytes (at least one candidate's activations)
   const uint64_t per_row = (uint64_t)S * kP2Row * 2;
@@ -766,6 +1139,12 @@ void lenet_plan_destroy(LenetPlan* p) {
 
 cudaError_t lenet_fitness_launch(const LenetPlan* p, float* part, const int* gate,
                                  cudaStream_t s) {
+  if (p->fused) {
+    LenetArgs a = p->args;
+    a.part = part;
+    a.gate = gate;
+    return pdl_launch(k_lenet_fused, p->grid_fused, kFThreads, FusedSmem::total, s, a);
+  }
   for (uint64_t r0 = 0; r0 < p->args.rows; r0 += p->group_rows) {
     LenetSplitArgs sa{p->args, p->p2};
     sa.base.W += r0 * p->args.Dp;
