@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmgfwa_b200.so")
+# MGFWA_LIB: an alternative build of the same library (A/B experiments,
+# scripts/build_variant.py); the in-tree build is the default.
+LIB_PATH = os.environ.get("MGFWA_LIB") or os.path.join(HERE, "libmgfwa_b200.so")
 
 MGFWA_OK, MGFWA_EINVAL, MGFWA_ECUDA, MGFWA_ENOMEM, MGFWA_ENCCL, MGFWA_ESTATE = range(6)
 OBJ_SPHERE, OBJ_RASTRIGIN, OBJ_ACKLEY, OBJ_MLP_WEIGHTS, OBJ_LENET, OBJ_NET = 1, 2, 3, 4, 5, 6

@@ -737,7 +737,7 @@ struct FusedSmem {
   static constexpr int wc2 = wc1 + 8 * kC1K * 2;               // [16][216] bf16
   static constexpr int bc1 = wc2 + 16 * kC2S * 2;              // f32 [8]
   static constexpr int bc2 = bc1 + 8 * 4;                      // f32 [16]
-  static constexpr int img = bc2 + 16 * 4;                     // per warp [33][40] u32 | f1w half
+  static constexpr int img = (bc2 + 16 * 4 + 127) / 128 * 128;  // per warp [33][40] u32 | f1w half (TMA dst)
   static constexpr int p1 = img + kFW * kImgWords * 4;         // per warp [14][kP1R][4] u32
   static constexpr int a1 = p1 + kFW * kP1Words * 4;           // fc1 A: 128 x 400 bf16
   static constexpr int w2 = a1 + 128 * 400 * 2;                // fc2 B: 96 x 128 bf16
@@ -746,8 +746,8 @@ struct FusedSmem {
   static constexpr int b2 = b1 + 128 * 4;                      // f32 [96]
   static constexpr int b3 = b2 + 96 * 4;                       // f32 [16]
   static constexpr int red = b3 + 16 * 4;                      // f32 [8]
-  static constexpr int bar = red + 8 * 4;                      // u64 mbarrier
-  static constexpr int slot = bar + 8;                         // TMEM base
+  static constexpr int bar = red + 8 * 4;                      // u64 mbarriers: MMA commit, TMA
+  static constexpr int slot = bar + 16;                        // TMEM base
   static constexpr int total = slot + 16;
 };
 constexpr int kF1Half0 = 208, kF1Half1 = 192;  // K per f1w half (13 + 12 MMA k-steps)
@@ -773,15 +773,9 @@ __device__ __forceinline__ uint4 load8(const __nv_bfloat16* rowp, int k0, int km
                     v[6] | (uint32_t)v[7] << 16);
 }
 
-// stage f1w[:, k0 .. k0 + kh) (rows 120..127 zero) as a 128-row operand
-__device__ __forceinline__ void stage_f1_half(uint8_t* dst, const __nv_bfloat16* w, int k0, int kh) {
-  const int chunks = kh / 8;
-  for (int i = threadIdx.x; i < 128 * chunks; i += kFThreads) {
-    const int j = i / chunks, cc = i - chunks * j;
-    const uint4 v = j < 120 ? load8(w + oF1W + j * 400, k0 + 8 * cc, 400) : make_uint4(0u, 0u, 0u, 0u);
-    *reinterpret_cast<uint4*>(dst + il_off(j, 8 * cc, 128)) = v;
-  }
-}
+#ifndef LENET_PROBE
+#define LENET_PROBE 0  // 1: profiling probe, conv only (fc stage skipped, partials 0)
+#endif
 
 __device__ __forceinline__ void async_smem_fence() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -789,11 +783,17 @@ __device__ __forceinline__ void async_smem_fence() {
 
 }  // namespace
 
-__global__ void __launch_bounds__(kFThreads, 1) k_lenet_fused(LenetArgs args) {
+// tmap_f1: 3-D view (k + 4, j, candidate) of every candidate's f1w block,
+// based 4 parameters before it (the block starts 8 bytes off a 16-byte
+// boundary); a box (8, 128, 1) = one 16-byte K chunk of the 128 (120 + 8
+// zero-filled) rows, which lands in shared memory as one 2048-byte column of
+// core matrices of the no-swizzle operand layout.
+__global__ void __launch_bounds__(kFThreads, 1) k_lenet_fused(LenetArgs args,
+                                                              const __grid_constant__ CUtensorMap tmap_f1) {
   using namespace tc;
   pdl_enter();
   if (args.gate != nullptr && *args.gate == 0) return;
-  extern __shared__ __align__(16) uint8_t sm[];
+  extern __shared__ __align__(1024) uint8_t sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, c = lane & 3;
   const int wi = g >> 1, dx = g & 1;
@@ -809,7 +809,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_lenet_fused(LenetArgs args) {
   float* sb2 = reinterpret_cast<float*>(sm + FusedSmem::b2);
   float* sb3 = reinterpret_cast<float*>(sm + FusedSmem::b3);
   float* red = reinterpret_cast<float*>(sm + FusedSmem::red);
-  const uint32_t bar = smem_u32(sm + FusedSmem::bar);
+  const uint32_t bar = smem_u32(sm + FusedSmem::bar), bar_tma = bar + 8;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + FusedSmem::slot);
   {
     uint32_t* p = reinterpret_cast<uint32_t*>(sm);
@@ -817,7 +817,9 @@ __global__ void __launch_bounds__(kFThreads, 1) k_lenet_fused(LenetArgs args) {
   }
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
+    mbar_init(bar_tma, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_f1)));
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
@@ -831,7 +833,7 @@ __global__ void __launch_bounds__(kFThreads, 1) k_lenet_fused(LenetArgs args) {
   const uint32_t lanes = tmem + ((uint32_t)(q * 32) << 16);
   const uint32_t r_s = smem_u32(sm + FusedSmem::img), a1_s = smem_u32(a1);
   const uint32_t w2_s = smem_u32(sm + FusedSmem::w2), w3_s = smem_u32(sm + FusedSmem::w3);
-  uint32_t phase = 0;
+  uint32_t phase = 0, tphase = 0;
   auto mma_round = [&]() {  // every thread: wait for the MMAs committed to `bar`
     mbar_wait(bar, phase);
     phase ^= 1;
@@ -921,14 +923,25 @@ __global__ void __launch_bounds__(kFThreads, 1) k_lenet_fused(LenetArgs args) {
     }
     async_smem_fence();  // generic-proxy writes of the A operand -> visible to the tensor core
     __syncthreads();
+#if LENET_PROBE == 1
+    if (threadIdx.x == 0) {
+      args.part[(row * args.nparts + part) * 2] = 0.0f;
+      args.part[(row * args.nparts + part) * 2 + 1] = 0.0f;
+    }
+    continue;
+#endif
     // ---- 2. fc1: D1 = A1 (128 x 400) . f1w^T, two K halves of f1w through the conv buffers
     uint32_t kk0 = 0;
 #pragma unroll 1
     for (int h = 0; h < 2; ++h) {
       const int k0 = h == 0 ? 0 : kF1Half0, kh = h == 0 ? kF1Half0 : kF1Half1;
-      stage_f1_half(sm + FusedSmem::img, w, k0, kh);
-      async_smem_fence();
-      __syncthreads();
+      if (threadIdx.x == 0) {  // TMA: one 2048-byte K chunk of f1w per box
+        mbar_expect_tx(bar_tma, (uint32_t)kh / 8 * 2048);
+        for (int cc = 0; cc < kh / 8; ++cc)
+          tma_load_3d(r_s + cc * 2048, &tmap_f1, bar_tma, k0 + 8 * cc, 0, (int)row);
+      }
+      mbar_wait(bar_tma, tphase);
+      tphase ^= 1;
       if (threadIdx.x == 0) {
         tc_fence_after();
         constexpr uint32_t id1 = idesc_bf16(128, 128);
@@ -1044,6 +1057,7 @@ struct LenetPlan {
   LenetArgs args;
   bool fused;  // k_lenet_fused (default); MGFWA_LENET_FUSED=0: conv + fc kernels through the HBM scratch
   unsigned grid_fused;
+  CUtensorMap tmap_f1;
   unsigned grid_conv, grid_fc;
   uint64_t group_rows;  // candidates per conv/fc launch pair (bounds the scratch)
   uint32_t* pimg;       // owned
@@ -1100,6 +1114,19 @@ LenetPlan* lenet_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t 
     p->fused = !(e && e[0] == '0');
   }
   if (p->fused) {
+    tc::EncodeTiledFn enc = tc::get_encode_fn();
+    cuuint64_t dims[3] = {404, 120, rows};
+    cuuint64_t strides[2] = {800, Dp * 2};
+    cuuint32_t box[3] = {8, 128, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (!enc || enc(&p->tmap_f1, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<__nv_bfloat16*>(W + oF1W - 4),
+                    dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      snprintf(err, errlen, "LeNet objective: f1w tensor map encode failed");
+      cudaFree(p->pimg);
+      delete p;
+      return nullptr;
+    }
     const uint64_t items = rows * p->args.nparts;
     p->grid_fused = (unsigned)(items < (uint64_t)nsm ? items : (uint64_t)nsm);
     return p;
@@ -1143,7 +1170,7 @@ cudaError_t lenet_fitness_launch(const LenetPlan* p, float* part, const int* gat
     LenetArgs a = p->args;
     a.part = part;
     a.gate = gate;
-    return pdl_launch(k_lenet_fused, p->grid_fused, kFThreads, FusedSmem::total, s, a);
+    return pdl_launch(k_lenet_fused, p->grid_fused, kFThreads, FusedSmem::total, s, a, p->tmap_f1);
   }
   for (uint64_t r0 = 0; r0 < p->args.rows; r0 += p->group_rows) {
     LenetSplitArgs sa{p->args, p->p2};
