@@ -21,7 +21,7 @@ cap)
   declare -A RE=([c2_mlp_fitness]="k_mlp_fitness 4 c2" [c2_explode_map]="k_explode_map 1 c2"
                  [c2_guides]="k_guides 1 c2" [c2_rank]="k_rank 1 c2" [c2_select]="k_select 1 c2"
                  [c2_guide_fitness]="k_mlp_fitness 5 c2"
-                 [c3_lenet_conv]="k_lenet_conv 3 c3" [c3_lenet_fc]="k_lenet_fc 3 c3"
+                 [c3_lenet_conv]="k_lenet_conv 4 c3" [c3_lenet_fc]="k_lenet_fc_tc 4 c3"
                  [c5_explode_map]="k_explode_map 1 c5" [c5_mlp_fitness]="k_mlp_fitness 1 c5"
                  [c4_explode_map]="k_explode_map 1 c4")
   set -- $2 ${RE[$2]}
