@@ -364,7 +364,7 @@ def kernel_breakdown(eng, w, wn, world, pk):
 
 
 KERNEL_NAMES = {"explode": "k_explode_map", "rank": "k_rank", "guides": "k_guides", "select": "k_select",
-                "fitness_mlp": "k_mlp_fitness", "fitness_lenet": "k_lenet"}
+                "fitness_mlp": "k_mlp_fitness", "fitness_lenet": "k_lenet_conv + k_lenet_fc_tc"}
 
 
 def roofline_entry(name, k, w, pk, pk_kind, workload):
@@ -372,6 +372,11 @@ def roofline_entry(name, k, w, pk, pk_kind, workload):
     if k["bound"] == "tensor":
         kern = KERNEL_NAMES["fitness_" + w["kind"]]
         nc = ncu_metrics(kern + (f"<{w['hidden']}" if w["kind"] == "mlp" else ""), workload)
+        if w["kind"] == "lenet":  # conv (warp MMA) + fc (tcgen05) launches: traffic of both
+            conv, fc = ncu_metrics("k_lenet_conv", workload), ncu_metrics("k_lenet_fc_tc", workload)
+            if conv and fc:
+                nc = {"traffic": conv["traffic"] + fc["traffic"], "source": conv["source"],
+                      "conv_tensor_pipe_pct": conv.get("tensor_pipe_pct"), "fc_tensor_pipe_pct": fc.get("tensor_pipe_pct")}
         return {"kernel": kern + " (spark fitness)", "bound": "tensor", "achieved": k["achieved_TFLOPs"],
                 "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": k["frac"],
                 "traffic": nc["traffic"] if nc else None, "ncu": nc,
@@ -501,8 +506,21 @@ def main():
         dom = max((k for k in kb if kb[k]["bound"] in ("hbm", "tensor")), key=lambda k: kb[k]["us"])
         line["roofline"] = roofline_entry(dom, kb[dom], w, pk, pk_kind, name)
         line["roofline"]["share_of_step"] = kb[dom]["us"] * 1e-3 / (ms_max / args.steps)
-        if "fitness" in kb and dom != "fitness":
+        if "fitness" in kb and dom != "fitness" and kb["fitness"]["bound"] == "tensor":
             line["roofline_tensor"] = roofline_entry("fitness", kb["fitness"], w, pk, pk_kind, name)
+        if not kpg:
+            # the persistent small-problem loop (C1): one kernel runs every phase of every
+            # generation; its bytes per generation against the generation time
+            byts = sum(kb[k]["algorithmic_bytes"] for k in ("explode", "guides", "select"))
+            ach = byts / (ms_max / args.steps * 1e-3) / 1e9
+            line["dominant_kernel"] = "k_small_run"
+            line["roofline"] = {"kernel": "k_small_run (persistent cooperative whole-loop kernel)", "bound": "hbm",
+                                "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": ach / pk["hbm_gbs"],
+                                "traffic": None, "share_of_step": 1.0,
+                                "algorithmic_per_launch": f"{byts} bytes per generation (explode + guides + select)",
+                                "note": "latency-bound: one block per firework, grid barriers between the phases; "
+                                        "the per-kernel breakdown above times the general (multi-kernel) path",
+                                "peak_source": f"{pk_kind} HBM copy bandwidth (MEASURED_PEAKS.json)"}
     except Exception as ex:
         line["kernel_breakdown"] = {"error": str(ex)[:200]}
         fit_ms, units = eng.time_fitness(10)
