@@ -42,9 +42,33 @@ __device__ __forceinline__ bool gen_inactive(const EngineView& v) {
 }
 
 // Partial sums of one row -> fitness (fp32), NaN -> +inf (backend.cpp:15-24).
-// Warp-cooperative with a fixed order (lane-strided sums, butterfly, lane 0's
-// value broadcast), used by every caller, so a candidate's cached fitness and
-// its re-evaluation are bit-identical.  All 32 lanes must call it.
+// One fixed order per run, whichever kernel finalizes, so a candidate's
+// cached fitness and its re-evaluation are bit-identical:
+//   nparts <= kSeqParts (the tensor-core objectives: one partial per 128
+//   samples; D <= 8192 analytic rows): ((p0 + p1) + p2) + ... in one thread
+//   (row_sums_seq) — no shuffles, so a finalizing thread per row is cheap;
+//   larger nparts (the 512-coordinate chunks of long analytic rows):
+//   lane-strided sums and a butterfly over the warp.
+constexpr uint32_t kSeqParts = 16;
+
+__device__ __forceinline__ float2 row_sums_seq(const EngineView& v, const float* part, uint64_t row) {
+  const float2* p = reinterpret_cast<const float2*>(part + row * (uint64_t)v.nparts * 2);
+  float a = 0.0f, b = 0.0f;
+  for (uint32_t c = 0; c < v.nparts; ++c) {
+    const float2 q = p[c];
+    a += q.x;
+    b += q.y;
+  }
+  return make_float2(a, b);
+}
+
+__device__ __forceinline__ float finalize_value(const EngineView& v, float a, float b, bool* was_nan) {
+  const float f = v.nn ? a / (float)v.samples : analytic_finalize(v.obj_kind, a, b, v.D);
+  *was_nan = isnan(f);
+  return isnan(f) ? __int_as_float(0x7f800000) : f;
+}
+
+// Warp-cooperative form (all 32 lanes call it and get every row's value):
 // R rows at once (their loads in flight together); rows[r] < 0 are skipped.
 template <int R>
 __device__ __forceinline__ void finalize_rows(const EngineView& v, const float* part,
@@ -52,10 +76,16 @@ __device__ __forceinline__ void finalize_rows(const EngineView& v, const float* 
                                               unsigned& nan_count) {
   const int lane = threadIdx.x & 31;
   float s0[R], s1[R];
+  const bool seq = v.nparts <= kSeqParts;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     s0[r] = s1[r] = 0.0f;
     if (rows[r] < 0) continue;
+    if (seq) {  // every lane: the same sequential sums (broadcast loads)
+      const float2 q = row_sums_seq(v, part, (uint64_t)rows[r]);
+      s0[r] = q.x, s1[r] = q.y;
+      continue;
+    }
     const float* p = part + (uint64_t)rows[r] * (uint64_t)v.nparts * 2;
     for (uint32_t c = lane; c < v.nparts; c += 32) {
       s0[r] += p[2 * c];
@@ -64,12 +94,11 @@ __device__ __forceinline__ void finalize_rows(const EngineView& v, const float* 
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const float a = __shfl_sync(0xffffffffu, warp_sum(s0[r]), 0);
-    const float b = __shfl_sync(0xffffffffu, warp_sum(s1[r]), 0);
-    const float f = v.nn ? a / (float)v.samples : analytic_finalize(v.obj_kind, a, b, v.D);
-    const bool nan = isnan(f) && rows[r] >= 0;
-    nan_count += nan;
-    out[r] = isnan(f) ? __int_as_float(0x7f800000) : f;
+    const float a = seq ? s0[r] : __shfl_sync(0xffffffffu, warp_sum(s0[r]), 0);
+    const float b = seq ? s1[r] : __shfl_sync(0xffffffffu, warp_sum(s1[r]), 0);
+    bool nan;
+    out[r] = finalize_value(v, a, b, &nan);
+    nan_count += nan && rows[r] >= 0;
   }
 }
 
@@ -481,34 +510,48 @@ __device__ __forceinline__ uint64_t rank_key(float x, uint32_t k) {
 __global__ void __launch_bounds__(kRankThreads) k_rank(EngineView v) {
   pdl_enter<RANK_TRIGGER != 0>();
   if (gen_inactive(v)) return;
-  extern __shared__ uint64_t keys[];  // [lambda] sort keys
+  extern __shared__ uint64_t keys[];  // [lambda] sort keys, then [lambda] rank counts (split counting)
   const uint64_t fl = blockIdx.x;     // local firework
   const uint32_t lam = (uint32_t)v.lam;
   if (threadIdx.x == 0) v.fit_prev[v.f_lo + fl] = v.fit[v.f_lo + fl];  // for k_select's parts
   unsigned nan_local = 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  constexpr int R = 4;  // rows per warp step (their loads in flight together)
-  for (uint32_t k0 = warp * R; k0 < lam; k0 += nwarp * R) {
-    int64_t rows[R];
-    float x[R];
+  if (v.nparts <= kSeqParts || v.injected_fitness) {
+    // one thread per spark row (sequential partial sums, see finalize_rows)
+    for (uint32_t k = threadIdx.x; k < lam; k += blockDim.x) {
+      const uint64_t row = fl * lam + k;
+      float x;
+      if (v.injected_fitness) {
+        x = v.sfit[row];
+      } else {
+        const float2 q = row_sums_seq(v, v.spart, row);
+        bool nan;
+        x = finalize_value(v, q.x, q.y, &nan);
+        nan_local += nan;
+        v.sfit[row] = x;
+      }
+      keys[k] = rank_key(x, k);
+    }
+    nan_local = __reduce_add_sync(0xffffffffu, nan_local);
+  } else {
+    constexpr int R = 4;  // rows per warp step (their loads in flight together)
+    for (uint32_t k0 = warp * R; k0 < lam; k0 += nwarp * R) {
+      int64_t rows[R];
+      float x[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) rows[r] = (k0 + r < lam) ? (int64_t)(fl * lam + k0 + r) : -1;
-    if (v.injected_fitness) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) x[r] = rows[r] >= 0 ? v.sfit[rows[r]] : 0.0f;
-    } else {
+      for (int r = 0; r < R; ++r) rows[r] = (k0 + r < lam) ? (int64_t)(fl * lam + k0 + r) : -1;
       finalize_rows<R>(v, v.spart, rows, x, nan_local);
-    }
-    float xl = x[0];
-    int64_t rl = rows[0];
+      float xl = x[0];
+      int64_t rl = rows[0];
 #pragma unroll
-    for (int r = 1; r < R; ++r) {
-      xl = lane == r ? x[r] : xl;
-      rl = lane == r ? rows[r] : rl;
-    }
-    if (lane < R && rl >= 0) {
-      if (!v.injected_fitness) v.sfit[rl] = xl;
-      keys[k0 + lane] = rank_key(xl, k0 + lane);
+      for (int r = 1; r < R; ++r) {
+        xl = lane == r ? x[r] : xl;
+        rl = lane == r ? rows[r] : rl;
+      }
+      if (lane < R && rl >= 0) {
+        v.sfit[rl] = xl;
+        keys[k0 + lane] = rank_key(xl, k0 + lane);
+      }
     }
   }
   if (lane == 0 && nan_local) atomicAdd(nan_counter_own(v), (unsigned long long)nan_local);
@@ -517,9 +560,36 @@ __global__ void __launch_bounds__(kRankThreads) k_rank(EngineView v) {
   // Rank by counting: keys are a total order with distinct values, so
   // rank(k) = #{j : key_j < key_k} is the position std::sort with the
   // reference comparator (engine.cpp:152-157) gives spark k.  All threads
-  // read the same key_j at once (shared-memory broadcast); no barriers.
+  // read the same key_j at once (shared-memory broadcast).  With room for
+  // P >= 2 threads per spark, the j range is split P ways and the partial
+  // counts summed in shared memory.
   const uint32_t top = (uint32_t)v.top;
   int* out = v.rank_idx + fl * 2 * top;
+  const uint32_t P = lam * 2 <= blockDim.x && lam * 12 <= kRankSmemMax ? blockDim.x / lam : 1u;
+  if (P >= 2) {
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(keys + ((lam + 1) & ~1u));
+    for (uint32_t k = threadIdx.x; k < lam; k += blockDim.x) cnt[k] = 0;
+    __syncthreads();
+    const uint32_t k = threadIdx.x % lam, p = threadIdx.x / lam;
+    if (p < P) {
+      const uint64_t kk = keys[k];
+      const uint32_t j0 = lam * p / P, j1 = lam * (p + 1) / P;
+      uint32_t r0 = 0, r1 = 0, j = j0;
+      for (; j + 2 <= j1; j += 2) {
+        r0 += keys[j] < kk;
+        r1 += keys[j + 1] < kk;
+      }
+      if (j < j1) r0 += keys[j] < kk;
+      atomicAdd(&cnt[k], r0 + r1);
+    }
+    __syncthreads();
+    for (uint32_t k2 = threadIdx.x; k2 < lam; k2 += blockDim.x) {
+      const uint32_t r = cnt[k2];
+      if (r < top) out[r] = (int)k2;
+      if (r >= lam - top) out[top + (r - (lam - top))] = (int)k2;
+    }
+    return;
+  }
   for (uint32_t k = threadIdx.x; k < lam; k += blockDim.x) {
     const uint64_t kk = keys[k];
     uint32_t r0 = 0, r1 = 0;
@@ -537,7 +607,9 @@ __global__ void __launch_bounds__(kRankThreads) k_rank(EngineView v) {
 }
 
 static size_t rank_smem(const EngineView& v) {
-  return ((v.lam + 1) & ~1ull) * sizeof(uint64_t);
+  const size_t keys = ((v.lam + 1) & ~1ull) * sizeof(uint64_t);
+  const bool split = v.lam * 2 <= (uint64_t)kRankThreads && v.lam * 12 <= (uint64_t)kRankSmemMax;
+  return keys + (split ? v.lam * sizeof(uint32_t) : 0);
 }
 
 // ----------------------------------------------------------------- guides
@@ -575,7 +647,11 @@ __device__ __forceinline__ void store_guide(const EngineView& v, uint64_t off, c
   }
 }
 
-__global__ void __launch_bounds__(256) k_guides(EngineView v) {
+#ifndef GUIDES_WARPS
+#define GUIDES_WARPS 8  // warps per k_guides block (one 32 * GUIDES_VEC-coordinate slice each)
+#endif
+constexpr int kGuideWarps = GUIDES_WARPS;
+__global__ void __launch_bounds__(kGuideWarps * 32) k_guides(EngineView v) {
   constexpr int V = GUIDES_VEC;
   using VT = typename VecT<V>::T;
   constexpr int U = 32 / V;  // rank pairs per unrolled step (2U independent V-wide loads per lane)
@@ -586,11 +662,11 @@ __global__ void __launch_bounds__(256) k_guides(EngineView v) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t it = v.ctl->iteration;
   const uint64_t nsl = (v.D + 32 * V - 1) / (32 * V);  // 32V-coordinate slices (V per lane)
-  const uint64_t bpf = (nsl + kWarps - 1) / kWarps;     // blocks per firework
+  const uint64_t bpf = (nsl + kGuideWarps - 1) / kGuideWarps;  // blocks per firework
   const uint64_t top = v.top;
   for (uint64_t blk = blockIdx.x; blk < v.Fl * bpf; blk += gridDim.x) {
     const uint64_t fl = blk / bpf, f = v.f_lo + fl;  // local / global firework
-    const uint64_t c = (blk % bpf) * kWarps + warp;
+    const uint64_t c = (blk % bpf) * kGuideWarps + warp;
     const uint64_t b = f / v.mu, n = f % v.mu;
     __syncthreads();
     for (uint64_t i = threadIdx.x; i < 2 * top; i += blockDim.x) s_idx[i] = v.rank_idx[fl * 2 * top + i];
@@ -1122,7 +1198,7 @@ __device__ __forceinline__ float small_row_fitness(const EngineView& v, const fl
     part[0] = s0;
     part[1] = s1;
   }
-  // finalize_rows with nparts == 1: lane 0's partial plus zeros
+  // finalize_rows with nparts == 1: the partial itself (0 + p0, row_sums_seq)
   const float a = __shfl_sync(0xffffffffu, warp_sum(lane == 0 ? s0 : 0.0f), 0);
   const float b = __shfl_sync(0xffffffffu, warp_sum(lane == 0 ? s1 : 0.0f), 0);
   const float f = analytic_finalize(v.obj_kind, a, b, v.D);
@@ -1581,7 +1657,7 @@ static size_t guides_smem(const EngineView& v) { return v.M * sizeof(uint64_t) +
 
 static unsigned guide_blocks(const EngineView& v, int nsm) {
   const uint64_t nsl = (v.D + 32 * GUIDES_VEC - 1) / (32 * GUIDES_VEC);
-  const uint64_t blocks = v.Fl * ((nsl + kWarps - 1) / kWarps);
+  const uint64_t blocks = v.Fl * ((nsl + kGuideWarps - 1) / kGuideWarps);
 #ifndef GUIDES_CAP_MULT
 #define GUIDES_CAP_MULT 64  // measured: C5 guides 3.37 -> 3.17 ms vs 8
 #endif
@@ -1627,7 +1703,7 @@ void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
     }
     pdl_launch(k_rank, (unsigned)v.Fl, kRankThreads, rank_smem(v), s, v);
     if (v.M > 0) {
-      pdl_launch(k_guides, guide_blocks(v, nsm), 256, guides_smem(v), s, v);
+      pdl_launch(k_guides, guide_blocks(v, nsm), kGuideWarps * 32, guides_smem(v), s, v);
       if (v.nn)
         hooks->eval_guides(hooks->ctx, s);
       else
@@ -1691,7 +1767,7 @@ void launch_rank(const EngineView& v, cudaStream_t s) {
   pdl_launch(k_rank, (unsigned)v.Fl, kRankThreads, rank_smem(v), s, v);
 }
 void launch_guides(const EngineView& v, int nsm, cudaStream_t s) {
-  pdl_launch(k_guides, guide_blocks(v, nsm), 256, guides_smem(v), s, v);
+  pdl_launch(k_guides, guide_blocks(v, nsm), kGuideWarps * 32, guides_smem(v), s, v);
   if (!v.nn) launch_analytic_partials(v.guides, v.Fl * v.M, v.D, v.Dp, v.nch, v.obj_kind, v.gpart, nsm, s);
 }
 void launch_select(const EngineView& v, int nsm, cudaStream_t s) {
