@@ -238,8 +238,15 @@ struct ExplodeChunk {
   double plo[kChunk], pw[kChunk];  // pop_lo and (pop_hi - pop_lo) in fp64
   float lof[kChunk], hif[kChunk];
 };
+#ifndef EXPLODE_SMEM_KEYS
+#define EXPLODE_SMEM_KEYS 1  // draw keys in shared memory: 80 registers, 3 blocks/SM, no spills (C2 explode 157 -> 156.6 us; in registers at 3 blocks/SM it spills: 172 us)
+#endif
+#ifndef EXPLODE_MINB
+#define EXPLODE_MINB 3  // blocks per SM the main explode kernel is compiled for
+#endif
 struct ExplodeWarp {
   uint64_t pre[2 * kSparkGroup];  // explode / mapping key prefixes
+  DrawKey keys[2 * kSparkGroup];  // their draw keys (EXPLODE_SMEM_KEYS)
 };
 constexpr size_t kExplodeSmem = sizeof(ExplodeChunk) + kWarps * sizeof(ExplodeWarp);
 
@@ -249,8 +256,7 @@ template <int KIND, bool FULL>
 __device__ __forceinline__ void explode_slice(const EngineView& v, const ExplodeChunk& ch,
                                               int lane, uint32_t cbase, uint32_t qoff,
                                               uint64_t f, uint64_t k0, int kn, double a,
-                                              const DrawKey (&pe)[kSparkGroup],
-                                              const DrawKey (&pm)[kSparkGroup], uint32_t one,
+                                              const DrawKey* pe, const DrawKey* pm, uint32_t one,
                                               float (&s0)[kSparkGroup], float (&s1)[kSparkGroup]) {
   constexpr int KG = kSparkGroup;
   const uint32_t D = (uint32_t)v.D;
@@ -271,9 +277,10 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
     float x[4];
     double sv[4];
     unsigned slow = 0;
+    const DrawKey ke = pe[kk];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      sv[e] = __dadd_rn(pd[e], __dmul_rn(unit_pm1_z(mix_draw(pe[kk], d0 + e, one)), a));
+      sv[e] = __dadd_rn(pd[e], __dmul_rn(unit_pm1_z(mix_draw(ke, d0 + e, one)), a));
       x[e] = __double2float_rn(sv[e]);
       const bool need = !in_box_fast(x[e], lf[e], uf[e]);
       if (FULL ? need : (e < nvalid && need)) slow |= 1u << e;
@@ -294,9 +301,10 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
       const double hi[4] = {hi01.x, hi01.y, hi23.x, hi23.y};
       const double pl[4] = {pl01.x, pl01.y, pl23.x, pl23.y};
       const double pw[4] = {pw01.x, pw01.y, pw23.x, pw23.y};
+      const DrawKey km = pm[kk];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const double u = unit_u53_z(mix_draw(pm[kk], d0 + e, one));
+        const double u = unit_u53_z(mix_draw(km, d0 + e, one));
         const float m = __double2float_rn(__dadd_rn(pl[e], __dmul_rn(u, pw[e])));
         const float r = (sv[e] >= lo[e] && sv[e] <= hi[e]) ? x[e] : m;
         x[e] = ((slow >> e) & 1u) ? fminf(fmaxf(r, lf[e]), uf[e]) : x[e];
@@ -344,14 +352,21 @@ __device__ __forceinline__ void explode_group(const EngineView& v, const Explode
   else if (lane >= KG && lane < KG + kn)
     wq.pre[lane] = key_prefix(v.seed, kMapping, it, b, n, k0 + lane - KG);
   __syncwarp();
+#if EXPLODE_SMEM_KEYS
+  if (lane < 2 * KG) wq.keys[lane] = draw_key(wq.pre[lane]);
+  __syncwarp();
+  const DrawKey* pe = wq.keys;
+  const DrawKey* pm = wq.keys + KG;
+#else
   DrawKey pe[KG], pm[KG];
 #pragma unroll
   for (int kk = 0; kk < KG; ++kk) {
     pe[kk] = draw_key(wq.pre[kk]);
     pm[kk] = draw_key(wq.pre[KG + kk]);
   }
-  const uint32_t one = (uint32_t)(v.Dp != 0);  // 1, opaque to the compiler (see mix_draw)
   __syncwarp();  // wq.pre is reused by this warp's next group
+#endif
+  const uint32_t one = (uint32_t)(v.Dp != 0);  // 1, opaque to the compiler (see mix_draw)
   const double a = v.amp[f];
   float s0[KG], s1[KG];
 #pragma unroll
@@ -365,6 +380,9 @@ __device__ __forceinline__ void explode_group(const EngineView& v, const Explode
     else
       explode_slice<KIND, false>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, one, s0, s1);
   }
+#if EXPLODE_SMEM_KEYS
+  __syncwarp();  // wq.keys are reused by this warp's next group
+#endif
   if (KIND != 0) {
 #pragma unroll
     for (int kk = 0; kk < KG; ++kk) {
@@ -445,7 +463,7 @@ static unsigned explode_blocks(const EngineView& v, int nsm) {
 
 template <int KIND>
 static void explode_launch_k(const EngineView& v, unsigned grid, cudaStream_t s) {
-  pdl_launch(k_explode_map<KIND>, grid, 256, kExplodeSmem, s, v);
+  pdl_launch(k_explode_map<KIND, EXPLODE_MINB>, grid, 256, kExplodeSmem, s, v);
 }
 
 #ifndef RANK_THREADS
@@ -458,11 +476,11 @@ __global__ void __launch_bounds__(kRankThreads) k_rank(EngineView v);
 cudaError_t prepare_engine_kernels() {
   cudaError_t e = cudaSuccess;
   const int bytes = (int)kExplodeSmem;
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<0, EXPLODE_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<0, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<OBJ_SPHERE>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<OBJ_RASTRIGIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<OBJ_ACKLEY>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<OBJ_SPHERE, EXPLODE_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<OBJ_RASTRIGIN, EXPLODE_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_explode_map<OBJ_ACKLEY, EXPLODE_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, kRankSmemMax);
   return e;
 }
