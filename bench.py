@@ -234,8 +234,15 @@ def config_dict(name, w, wn, world, scaling, shard_mode):
         par = f"batch replicas x{world} ({wn['B']} batches)" + (" + 8-byte NCCL all-reduce/gen" if world > 1 else "")
     else:
         par = f"firework-sharded x{world}" + (" + NCCL all-gather/gen" if world > 1 else "")
+    nn = w["kind"] in ("mlp", "lenet")
+    mb = wn["B"] * wn["mu"] * w["lam"] * w["D"] * (6 if nn else 4) / (world * 1e6)
+    l2 = (f"inputs larger than L2 every step: {mb:.0f} MB of spark matrices written and read per generation "
+          f"per GPU (L2 126 MB)") if mb > 126 else (
+        f"{mb:.1f} MB of spark matrices per generation (< 126 MB L2), regenerated by the explode kernel every "
+        f"generation; no L2 flush between generations")
     return {"workload": w["desc"], "name": name, "D": w["D"], "B": wn["B"], "mu": wn["mu"], "lambda": w["lam"],
-            "M": w["M"], "fireworks_total": wn["B"] * wn["mu"], "scaling": scaling, "parallelism": par}
+            "M": w["M"], "fireworks_total": wn["B"] * wn["mu"], "scaling": scaling, "parallelism": par,
+            "l2_policy": l2}
 
 
 def _ref_desc(O, w):
@@ -489,10 +496,7 @@ def main():
             "dtype": "bf16" if w["kind"] in ("mlp", "lenet") else ("f64" if w["kind"] == "net" else "f32"),
             "data": "synthetic",
             "config": config_dict(name, w, wn, world, scaling, args.shard_mode),
-            "l2": ("inputs larger than L2 every step: the fp32 + bf16 spark matrices "
-                   f"({w['B'] * w['mu'] * w['lam'] * w['D'] * 6 / 1e6:.0f} MB per generation) exceed the 126 MB L2; "
-                   "per-kernel times below are taken after a 256 MB L2 flush")
-            if w["kind"] in ("mlp", "lenet") else "per-kernel times taken after a 256 MB L2 flush",
+            "kernel_timing": "per-kernel times (kernel_breakdown, roofline) each after a 256 MB L2 flush",
             "gpu_launches": kpg * args.steps if kpg else 1}  # 1: the persistent small-problem loop
     line["clocks"] = clk.summary()
 
