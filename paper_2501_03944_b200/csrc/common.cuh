@@ -116,6 +116,64 @@ __host__ __device__ __forceinline__ MixState mix_draw(const DrawKey& k, uint32_t
 #endif
   return MixState{(uint32_t)x, (uint32_t)(x >> 32)};
 }
+// ---- chunk-constant form of splitmix64(pre ^ d) for d in one 512-coordinate
+// chunk [cbase, cbase + 512) (cbase a multiple of 512).  With P = pre ^ cbase
+// and j = d - cbase, pre ^ d = (P & ~511) + ((P & 511) ^ j) (disjoint bits),
+// so the mixer input is z = Q + ((P & 511) ^ j) with Q = (P & ~511) + gamma.
+// When lo32(Q) <= 2^32 - 512 that addition never carries: the high word of z
+// is the chunk constant Q_hi, so is the high word of the first xorshift
+// (Q_hi ^ (Q_hi >> 30)), and so is its share of the first product's high
+// word.  Per coordinate the first two mixer steps then cost one add, one
+// shift and one 3-input xor (low word only) and two multiply-adds.  A chunk
+// whose Q_lo is within 512 of 2^32 (probability 2^-23 per key and chunk) is
+// flagged not `fast` and takes the general draw (mix_draw).
+struct ChunkDraw {
+  uint32_t qe[4];  // Q_lo + ((p9 & 3) ^ e), e = 0..3
+  uint32_t p9;     // P & 511
+  uint32_t k1;     // Q_hi << 2: the high word's bits in lo32(z >> 30)
+  uint32_t k2;     // lo32((Q_hi ^ (Q_hi >> 30)) * lo32(C1)): high-word share of lo32(y * C1) >> 32
+  uint32_t fast;   // 1 when lo32(Q) <= 2^32 - 512
+};
+__host__ __device__ __forceinline__ ChunkDraw chunk_draw(uint64_t pre, uint32_t cbase) {
+  const uint64_t P = pre ^ (uint64_t)cbase;
+  const uint64_t Q = (P & ~511ull) + 0x9E3779B97F4A7C15ull;
+  const uint32_t qlo = (uint32_t)Q, qhi = (uint32_t)(Q >> 32);
+  const uint32_t p9 = (uint32_t)P & 511u;
+  ChunkDraw k;
+  for (uint32_t e = 0; e < 4; ++e) k.qe[e] = qlo + ((p9 & 3u) ^ e);
+  k.p9 = p9;
+  k.k1 = qhi << 2;
+  k.k2 = (qhi ^ (qhi >> 30)) * 0x1CE4E5B9u;
+  k.fast = qlo <= 0xFFFFFE00u;
+  return k;
+}
+// Low word of z for the lane's coordinate slice j = J0 + e (J0 a multiple of
+// 4): (p9 ^ (J0 + e)) = ((p9 ^ J0) & ~3) + ((p9 & 3) ^ e), so
+// zlo[e] = qe[e] + chunk_slice(k, J0).
+__host__ __device__ __forceinline__ uint32_t chunk_slice(const ChunkDraw& k, uint32_t J0) {
+  return (k.p9 ^ J0) & ~3u;
+}
+// The mixer state (z before its final xorshift, as mix_draw) from zlo.
+__host__ __device__ __forceinline__ MixState mix_chunk(const ChunkDraw& k, uint32_t zlo) {
+  // y = z ^ (z >> 30): low word only (the high word is folded into k2)
+  const uint32_t ylo = zlo ^ (zlo >> 30) ^ k.k1;
+  // w = y * C1 mod 2^64
+  const uint64_t w = (uint64_t)ylo * 0x1CE4E5B9u + ((uint64_t)k.k2 << 32);
+  const uint32_t wlo = (uint32_t)w;
+  const uint32_t whi = (uint32_t)(w >> 32) + ylo * 0xBF58476Du;
+  // v = w ^ (w >> 27)
+#ifdef __CUDA_ARCH__
+  const uint32_t vlo = wlo ^ __funnelshift_r(wlo, whi, 27);
+#else
+  const uint32_t vlo = wlo ^ (uint32_t)((((uint64_t)whi << 32) | wlo) >> 27);
+#endif
+  const uint32_t vhi = whi ^ (whi >> 27);
+  // z = v * C2 mod 2^64
+  const uint64_t z = (uint64_t)vlo * 0x133111EBu;
+  const uint32_t zhi = (uint32_t)(z >> 32) + vlo * 0x94D049BBu + vhi * 0x133111EBu;
+  return MixState{(uint32_t)z, zhi};
+}
+
 // Bits 11..42 and 43..63 of h = z ^ (z >> 31): lo32(h >> 11) and h_hi >> 11.
 __host__ __device__ __forceinline__ uint32_t mant_lo(MixState z) {
 #ifdef __CUDA_ARCH__

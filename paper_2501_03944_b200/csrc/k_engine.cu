@@ -247,16 +247,20 @@ struct ExplodeChunk {
 struct ExplodeWarp {
   uint64_t pre[2 * kSparkGroup];  // explode / mapping key prefixes
   DrawKey keys[2 * kSparkGroup];  // their draw keys (EXPLODE_SMEM_KEYS)
+  ChunkDraw ck[2 * kSparkGroup];  // their chunk-constant draws for the current chunk
 };
 constexpr size_t kExplodeSmem = sizeof(ExplodeChunk) + kWarps * sizeof(ExplodeWarp);
 
 // One 128-coordinate slice of kSparkGroup sparks.  FULL: every spark of the
 // group exists and the slice lies inside [0, D) (no per-element guards).
-template <int KIND, bool FULL>
+// CHUNK: draws from the chunk-constant form (ck, every key of the group
+// `fast` in this chunk); otherwise from the general draw keys (pe, pm).
+template <int KIND, bool FULL, bool CHUNK>
 __device__ __forceinline__ void explode_slice(const EngineView& v, const ExplodeChunk& ch,
                                               int lane, uint32_t cbase, uint32_t qoff,
                                               uint64_t f, uint64_t k0, int kn, double a,
-                                              const DrawKey* pe, const DrawKey* pm, uint32_t one,
+                                              const DrawKey* pe, const DrawKey* pm,
+                                              const ChunkDraw* ck, uint32_t one,
                                               float (&s0)[kSparkGroup], float (&s1)[kSparkGroup]) {
   constexpr int KG = kSparkGroup;
   const uint32_t D = (uint32_t)v.D;
@@ -277,10 +281,20 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
     float x[4];
     double sv[4];
     unsigned slow = 0;
-    const DrawKey ke = pe[kk];
+    MixState ze[4];
+    if constexpr (CHUNK) {
+      const ChunkDraw& kc = ck[kk];
+      const uint32_t tj = chunk_slice(kc, li0);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) ze[e] = mix_chunk(kc, kc.qe[e] + tj);
+    } else {
+      const DrawKey ke = pe[kk];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) ze[e] = mix_draw(ke, d0 + e, one);
+    }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      sv[e] = __dadd_rn(pd[e], __dmul_rn(unit_pm1_z(mix_draw(ke, d0 + e, one)), a));
+      sv[e] = __dadd_rn(pd[e], __dmul_rn(unit_pm1_z(ze[e]), a));
       x[e] = __double2float_rn(sv[e]);
       const bool need = !in_box_fast(x[e], lf[e], uf[e]);
       if (FULL ? need : (e < nvalid && need)) slow |= 1u << e;
@@ -301,10 +315,20 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
       const double hi[4] = {hi01.x, hi01.y, hi23.x, hi23.y};
       const double pl[4] = {pl01.x, pl01.y, pl23.x, pl23.y};
       const double pw[4] = {pw01.x, pw01.y, pw23.x, pw23.y};
-      const DrawKey km = pm[kk];
+      MixState zm[4];
+      if constexpr (CHUNK) {
+        const ChunkDraw& kc = ck[kSparkGroup + kk];
+        const uint32_t tj = chunk_slice(kc, li0);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) zm[e] = mix_chunk(kc, kc.qe[e] + tj);
+      } else {
+        const DrawKey km = pm[kk];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) zm[e] = mix_draw(km, d0 + e, one);
+      }
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const double u = unit_u53_z(mix_draw(km, d0 + e, one));
+        const double u = unit_u53_z(zm[e]);
         const float m = __double2float_rn(__dadd_rn(pl[e], __dmul_rn(u, pw[e])));
         const float r = (sv[e] >= lo[e] && sv[e] <= hi[e]) ? x[e] : m;
         x[e] = ((slow >> e) & 1u) ? fminf(fmaxf(r, lf[e]), uf[e]) : x[e];
@@ -352,6 +376,14 @@ __device__ __forceinline__ void explode_group(const EngineView& v, const Explode
   else if (lane >= KG && lane < KG + kn)
     wq.pre[lane] = key_prefix(v.seed, kMapping, it, b, n, k0 + lane - KG);
   __syncwarp();
+  // chunk-constant draws of this chunk; the general keys serve a group with
+  // any key near a carry boundary (2^-23 per key and chunk)
+  bool fast_key = true;
+  if (lane < 2 * KG) {
+    wq.ck[lane] = chunk_draw(wq.pre[lane], cbase);
+    fast_key = wq.ck[lane].fast != 0;
+  }
+  const bool fast = __all_sync(0xffffffffu, fast_key);
 #if EXPLODE_SMEM_KEYS
   if (lane < 2 * KG) wq.keys[lane] = draw_key(wq.pre[lane]);
   __syncwarp();
@@ -375,10 +407,12 @@ __device__ __forceinline__ void explode_group(const EngineView& v, const Explode
   for (int q = 0; q < 4; ++q) {
     const uint32_t qoff = q * 128;
     if (cbase + qoff >= D) break;  // warp-uniform
-    if (kn == KG && cbase + qoff + 128 <= D)
-      explode_slice<KIND, true>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, one, s0, s1);
+    if (!fast)
+      explode_slice<KIND, false, false>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, wq.ck, one, s0, s1);
+    else if (kn == KG && cbase + qoff + 128 <= D)
+      explode_slice<KIND, true, true>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, wq.ck, one, s0, s1);
     else
-      explode_slice<KIND, false>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, one, s0, s1);
+      explode_slice<KIND, false, true>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, wq.ck, one, s0, s1);
   }
 #if EXPLODE_SMEM_KEYS
   __syncwarp();  // wq.keys are reused by this warp's next group
