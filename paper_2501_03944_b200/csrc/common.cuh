@@ -129,10 +129,10 @@ __host__ __device__ __forceinline__ MixState mix_draw(const DrawKey& k, uint32_t
 // flagged not `fast` and takes the general draw (mix_draw).
 struct ChunkDraw {
   uint32_t qe[4];  // Q_lo + ((p9 & 3) ^ e), e = 0..3
-  uint32_t p9;     // P & 511
+  uint64_t k2w;    // lo32((Q_hi ^ (Q_hi >> 30)) * lo32(C1)) << 32: the high word's share of
+                   // y * lo32(C1), a 64-bit addend whose low word (0) the compiler cannot see
+  uint32_t p9;     // P & 511, bit 31 set when the chunk is not `fast`
   uint32_t k1;     // Q_hi << 2: the high word's bits in lo32(z >> 30)
-  uint32_t k2;     // lo32((Q_hi ^ (Q_hi >> 30)) * lo32(C1)): high-word share of lo32(y * C1) >> 32
-  uint32_t fast;   // 1 when lo32(Q) <= 2^32 - 512
 };
 __host__ __device__ __forceinline__ ChunkDraw chunk_draw(uint64_t pre, uint32_t cbase) {
   const uint64_t P = pre ^ (uint64_t)cbase;
@@ -141,24 +141,24 @@ __host__ __device__ __forceinline__ ChunkDraw chunk_draw(uint64_t pre, uint32_t 
   const uint32_t p9 = (uint32_t)P & 511u;
   ChunkDraw k;
   for (uint32_t e = 0; e < 4; ++e) k.qe[e] = qlo + ((p9 & 3u) ^ e);
-  k.p9 = p9;
+  k.k2w = (uint64_t)((qhi ^ (qhi >> 30)) * 0x1CE4E5B9u) << 32;
+  k.p9 = p9 | (qlo <= 0xFFFFFE00u ? 0u : 0x80000000u);
   k.k1 = qhi << 2;
-  k.k2 = (qhi ^ (qhi >> 30)) * 0x1CE4E5B9u;
-  k.fast = qlo <= 0xFFFFFE00u;
   return k;
 }
+__host__ __device__ __forceinline__ bool chunk_fast(const ChunkDraw& k) { return (k.p9 >> 31) == 0; }
 // Low word of z for the lane's coordinate slice j = J0 + e (J0 a multiple of
 // 4): (p9 ^ (J0 + e)) = ((p9 ^ J0) & ~3) + ((p9 & 3) ^ e), so
 // zlo[e] = qe[e] + chunk_slice(k, J0).
 __host__ __device__ __forceinline__ uint32_t chunk_slice(const ChunkDraw& k, uint32_t J0) {
-  return (k.p9 ^ J0) & ~3u;
+  return (k.p9 ^ J0) & 0x1FCu;  // J0 < 512
 }
 // The mixer state (z before its final xorshift, as mix_draw) from zlo.
 __host__ __device__ __forceinline__ MixState mix_chunk(const ChunkDraw& k, uint32_t zlo) {
   // y = z ^ (z >> 30): low word only (the high word is folded into k2)
   const uint32_t ylo = zlo ^ (zlo >> 30) ^ k.k1;
   // w = y * C1 mod 2^64
-  const uint64_t w = (uint64_t)ylo * 0x1CE4E5B9u + ((uint64_t)k.k2 << 32);
+  const uint64_t w = (uint64_t)ylo * 0x1CE4E5B9u + k.k2w;
   const uint32_t wlo = (uint32_t)w;
   const uint32_t whi = (uint32_t)(w >> 32) + ylo * 0xBF58476Du;
   // v = w ^ (w >> 27)

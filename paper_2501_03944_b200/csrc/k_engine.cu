@@ -207,19 +207,65 @@ __device__ __forceinline__ double unit_pm1(uint64_t h) {
 
 // unit_pm1 / unit_u53 of h = splitmix64(pre ^ d) from the mixer state (see
 // mix_draw): bit-identical, three ALU instructions fewer per draw.
-__device__ __forceinline__ double unit_pm1_z(MixState z) {
-  const uint32_t t = z.hi >> 11;                     // bits 43..63 of h
-  const uint32_t c_hi = 0x40000000u - (t & 0x100000u);  // top ? 1.0 : 2.0
-  const double d1 = __hiloint2double((int)(0x3FF00000u | (t & 0xFFFFFu)), (int)mant_lo(z));
+// Logical right shifts as mul.hi(x, 2^(32-k)) with an opaque multiplier:
+// IMAD.HI on the FMA pipe instead of SHF on the ALU pipe.  Level 0: none;
+// 1: the mantissa shifts of the draws; 2: also the mixer's xorshifts.
+#ifndef EXPLODE_IMAD_SHR
+#define EXPLODE_IMAD_SHR 0
+#endif
+__device__ __forceinline__ uint32_t shr_fma(uint32_t x, uint32_t pow2) {
+  uint32_t r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(pow2));
+  return r;
+}
+template <int K>
+__device__ __forceinline__ uint32_t shr_k(uint32_t x, uint32_t one, int level) {
+  return level ? shr_fma(x, one << (32 - K)) : x >> K;
+}
+// mix_chunk (common.cuh) with the xorshifts' shifts on the FMA pipe at level 2.
+__device__ __forceinline__ MixState mix_chunk_k(const ChunkDraw& k, uint32_t zlo, uint32_t one) {
+  constexpr int L = EXPLODE_IMAD_SHR >= 2;
+  const uint32_t ylo = zlo ^ shr_k<30>(zlo, one, L) ^ k.k1;
+  const uint64_t w = (uint64_t)ylo * 0x1CE4E5B9u + k.k2w;
+  const uint32_t wlo = (uint32_t)w;
+  const uint32_t whi = (uint32_t)(w >> 32) + ylo * 0xBF58476Du;
+  const uint32_t vlo = wlo ^ __funnelshift_r(wlo, whi, 27);
+  const uint32_t vhi = whi ^ shr_k<27>(whi, one, L);
+  const uint64_t z = (uint64_t)vlo * 0x133111EBu;
+  const uint32_t zhi = (uint32_t)(z >> 32) + vlo * 0x94D049BBu + vhi * 0x133111EBu;
+  return MixState{(uint32_t)z, zhi};
+}
+// D1 = 1 + (m mod 2^52) 2^-52 of h = z ^ (z >> 31), m = h >> 11 (mant_lo,
+// common.cuh): the top bit of z.hi >> 11 (bit 20) is absorbed by the exponent
+// bits of 1.0.
+__device__ __forceinline__ double draw_d1(MixState z, uint32_t one) {
+  constexpr int L = EXPLODE_IMAD_SHR >= 1;
+  const uint32_t lo = __funnelshift_r(z.lo, z.hi, 11) ^ shr_k<10>(z.hi, one, L);
+  return __hiloint2double((int)(0x3FF00000u | shr_k<11>(z.hi, one, L)), (int)lo);
+}
+
+// `one` = 1, opaque to the compiler: the sign mask s = (z.hi < 0 ? -1 : 0)
+// is mul.hi(z.hi, one), an IMAD.HI on the FMA pipe instead of a shift on the
+// (saturated) ALU pipe.
+__device__ __forceinline__ int32_t sign_mask(uint32_t x, uint32_t one) {
+  int32_t s;
+  asm("mul.hi.s32 %0, %1, %2;" : "=r"(s) : "r"(x), "r"(one));
+  return s;
+}
+__device__ __forceinline__ double unit_pm1_z(MixState z, uint32_t one) {
+  // t = D1 - (top ? 1 : 2), exact
+  const double d1 = draw_d1(z, one);
+  const uint32_t s = (uint32_t)sign_mask(z.hi, one);
+  const uint32_t c_hi = (s & 0x3FF00000u) | (~s & 0x40000000u);  // top ? 1.0 : 2.0
   return __dsub_rn(d1, __hiloint2double((int)c_hi, 0));
 }
-__device__ __forceinline__ double unit_u53_z(MixState z) {
-  const uint32_t t = z.hi >> 11;
-  const double dh = __hiloint2double((int)(0x3FE00000u | (t & 0xFFFFFu)), (int)mant_lo(z));
-  int32_t sgn;
-  asm("shr.s32 %0, %1, 31;" : "=r"(sgn) : "r"(z.hi));
-  const uint32_t c_hi = 0x3FE00000u & ~(uint32_t)sgn;  // top ? 0 : 0.5
-  return __dsub_rn(dh, __hiloint2double((int)c_hi, 0));
+// 2u = D1 - (top ? 0 : 1) for u = (h >> 11) 2^-53 (exact); the caller
+// multiplies by half the interval width (exact scaling), so
+// lo + u * w == lo + unit_2u_z(z) * (w / 2) bit for bit.
+__device__ __forceinline__ double unit_2u_z(MixState z, uint32_t one) {
+  const double d1 = draw_d1(z, one);
+  const uint32_t s = (uint32_t)sign_mask(z.hi, one);
+  return __dsub_rn(d1, __hiloint2double((int)(~s & 0x3FF00000u), 0));
 }
 
 // Exact in-box test for x = round_f32(s): strictly between the fp32 box
@@ -235,7 +281,7 @@ __device__ __forceinline__ bool in_box_fast(float x, float lo_f, float hi_f) {
 // staged once per work item, plus the per-warp key prefixes.
 struct ExplodeChunk {
   double lo[kChunk], hi[kChunk];
-  double plo[kChunk], pw[kChunk];  // pop_lo and (pop_hi - pop_lo) in fp64
+  double plo[kChunk], pw[kChunk];  // pop_lo and (pop_hi - pop_lo) / 2 in fp64
   float lof[kChunk], hif[kChunk];
 };
 #ifndef EXPLODE_SMEM_KEYS
@@ -286,7 +332,7 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
       const ChunkDraw& kc = ck[kk];
       const uint32_t tj = chunk_slice(kc, li0);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) ze[e] = mix_chunk(kc, kc.qe[e] + tj);
+      for (int e = 0; e < 4; ++e) ze[e] = mix_chunk_k(kc, kc.qe[e] + tj, one);
     } else {
       const DrawKey ke = pe[kk];
 #pragma unroll
@@ -294,7 +340,7 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      sv[e] = __dadd_rn(pd[e], __dmul_rn(unit_pm1_z(ze[e]), a));
+      sv[e] = __dadd_rn(pd[e], __dmul_rn(unit_pm1_z(ze[e], one), a));
       x[e] = __double2float_rn(sv[e]);
       const bool need = !in_box_fast(x[e], lf[e], uf[e]);
       if (FULL ? need : (e < nvalid && need)) slow |= 1u << e;
@@ -320,7 +366,7 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
         const ChunkDraw& kc = ck[kSparkGroup + kk];
         const uint32_t tj = chunk_slice(kc, li0);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) zm[e] = mix_chunk(kc, kc.qe[e] + tj);
+        for (int e = 0; e < 4; ++e) zm[e] = mix_chunk_k(kc, kc.qe[e] + tj, one);
       } else {
         const DrawKey km = pm[kk];
 #pragma unroll
@@ -328,7 +374,7 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
       }
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const double u = unit_u53_z(zm[e]);
+        const double u = unit_2u_z(zm[e], one);  // 2u; pw holds half the width
         const float m = __double2float_rn(__dadd_rn(pl[e], __dmul_rn(u, pw[e])));
         const float r = (sv[e] >= lo[e] && sv[e] <= hi[e]) ? x[e] : m;
         x[e] = ((slow >> e) & 1u) ? fminf(fmaxf(r, lf[e]), uf[e]) : x[e];
@@ -381,7 +427,7 @@ __device__ __forceinline__ void explode_group(const EngineView& v, const Explode
   bool fast_key = true;
   if (lane < 2 * KG) {
     wq.ck[lane] = chunk_draw(wq.pre[lane], cbase);
-    fast_key = wq.ck[lane].fast != 0;
+    fast_key = chunk_fast(wq.ck[lane]);
   }
   const bool fast = __all_sync(0xffffffffu, fast_key);
 #if EXPLODE_SMEM_KEYS
@@ -447,7 +493,7 @@ __device__ __forceinline__ void stage_explode_chunk(const EngineView& v, Explode
     const double pl = in ? (double)v.pop_lo[b * v.Dp + d] : 0.0;
     const double ph = in ? (double)v.pop_hi[b * v.Dp + d] : 0.0;
     ch.plo[i] = pl;
-    ch.pw[i] = __dsub_rn(ph, pl);
+    ch.pw[i] = 0.5 * __dsub_rn(ph, pl);  // half the width (see unit_2u_z)
   }
 }
 

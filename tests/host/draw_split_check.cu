@@ -34,7 +34,7 @@ int main(int argc, char** argv) {
     const uint32_t cbase = d & ~511u, j = d & 511u;
     const ChunkDraw k = chunk_draw(pre, cbase);
     const uint64_t q = ((pre ^ cbase) & ~511ull) + 0x9E3779B97F4A7C15ull;
-    if (k.fast) {
+    if (chunk_fast(k)) {
       const uint32_t zlo = k.qe[j & 3u] + chunk_slice(k, j & ~3u);
       const MixState c = mix_chunk(k, zlo);
       bad += c.lo != z.lo || c.hi != z.hi;
