@@ -43,7 +43,8 @@ namespace mgfwa_b200 {
 namespace {
 
 constexpr int BM = 128;  // samples per tile (TMEM lanes)
-constexpr int BN = 256;  // (spark, hidden) columns per tile
+constexpr int BN = 256;  // (spark, hidden) columns per tile (BNT: the kernel's tile width)
+constexpr int BN_NARROW = 64;  // narrow tile for few-row launches (guides, losers; H == 32)
 constexpr int BK = 64;   // K per pipeline stage (one 128-byte swizzle atom)
 #ifndef MLP_STAGES
 #define MLP_STAGES 4
@@ -56,12 +57,12 @@ constexpr int kABytes = BM * BK * 2;  // 16 KB
 // CG = CTA group: 1 (one SM per tile, M = 128) or 2 (an SM pair per tile,
 // M = 256, cta_group::2: each CTA stages its own 128 A rows and HALF of B,
 // which halves the per-SM operand traffic through shared memory and L2).
-template <int CG>
+template <int CG, int BNT = BN>
 struct Cfg {
-  static constexpr int kBRows = BN / CG;                 // B rows staged per CTA
-  static constexpr int kBBytes = kBRows * BK * 2;        // 32 KB | 16 KB
+  static constexpr int kBRows = BNT / CG;                // B rows staged per CTA
+  static constexpr int kBBytes = kBRows * BK * 2;        // 32 KB | 16 KB (BNT = 256)
   static constexpr int kStageBytes = kABytes + kBBytes;  // 48 KB | 32 KB
-  static constexpr int kStages = CG == 2 ? 6 : MLP_STAGES;
+  static constexpr int kStages = CG == 2 ? 6 : BNT < BN ? 6 : MLP_STAGES;
   static constexpr int kO2 = 16 / CG;                    // layer-2 B rows (outputs) per CTA
 };
 constexpr int kThreads = 384;
@@ -70,20 +71,20 @@ constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kN2 = 16;  // layer-2 MMA N (outputs padded to 16)
 constexpr int kMaxO = 10;
 
-template <int CG>
+template <int CG, int BNT = BN>
 struct SmemLayoutT {
-  static constexpr int kStages = Cfg<CG>::kStages;
-  static constexpr int w2 = kStages * Cfg<CG>::kStageBytes;  // bf16 W2^T, [spark][kO2][H] interleaved
-  static constexpr int b1 = w2 + Cfg<CG>::kO2 * BN * 2;  // float[BN]
-  static constexpr int b2 = b1 + BN * 4;                 // float[8][kN2]
+  static constexpr int kStages = Cfg<CG, BNT>::kStages;
+  static constexpr int w2 = kStages * Cfg<CG, BNT>::kStageBytes;  // bf16 W2^T, [spark][kO2][H] interleaved
+  static constexpr int b1 = w2 + Cfg<CG, BNT>::kO2 * BNT * 2;  // float[BNT]
+  static constexpr int b2 = b1 + BNT * 4;                // float[8][kN2]
   static constexpr int red = b2 + 8 * kN2 * 4;           // float[kEpiWarps][8]
   static constexpr int bars = red + kEpiWarps * 8 * 4;   // u64 barriers
   static constexpr int nbars = 2 * kStages + 8;
   static constexpr int tmem_slot = bars + nbars * 8;
   static constexpr int total = tmem_slot + 16;
 };
-template <int CG>
-constexpr int smem_bytes() { return SmemLayoutT<CG>::total; }
+template <int CG, int BNT = BN>
+constexpr int smem_bytes() { return SmemLayoutT<CG, BNT>::total; }
 
 struct MlpArgs {
   uint32_t S, I, H, O;
@@ -208,18 +209,21 @@ __device__ __forceinline__ uint32_t d2_col(int j) {
 }
 
 // ------------------------------------------------------------------ kernel
-template <int H, int CG>
+template <int H, int CG, int BNT = BN>
 __global__ void __launch_bounds__(kThreads, 1)
     k_mlp_fitness(const __grid_constant__ CUtensorMap tmap_x,
                   const __grid_constant__ CUtensorMap tmap_w, MlpArgs args) {
   pdl_enter();
   if (args.gate != nullptr && *args.gate == 0) return;
-  constexpr int SPT = BN / H;  // sparks per N tile (1 when H == 256)
-  static_assert(BN % H == 0 && H % 32 == 0, "H must divide 256 and be a multiple of 32");
-  using SmemLayout = SmemLayoutT<CG>;
-  constexpr int kStages = Cfg<CG>::kStages;
-  constexpr int kStageBytes = Cfg<CG>::kStageBytes;
-  constexpr int kO2 = Cfg<CG>::kO2;
+  constexpr int SPT = BNT / H;  // sparks per N tile (1 when H == BNT)
+  static_assert(BNT % H == 0 && H % 32 == 0, "H must divide the tile width and be a multiple of 32");
+  static_assert(BNT == BN || (CG == 1 && SPT == 2), "narrow tiles: one spark per column half");
+  constexpr int kHalf = BNT / 2;        // epilogue column half
+  constexpr int kTmemCols = 2 * BNT;    // two tile buffers
+  using SmemLayout = SmemLayoutT<CG, BNT>;
+  constexpr int kStages = Cfg<CG, BNT>::kStages;
+  constexpr int kStageBytes = Cfg<CG, BNT>::kStageBytes;
+  constexpr int kO2 = Cfg<CG, BNT>::kO2;
   const uint32_t rank = CG == 2 ? cluster_rank() : 0u;  // CTA rank in the pair
   const bool leader = rank == 0;
 
@@ -259,12 +263,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 2) {
     if (CG == 2) {
-      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-          smem_u32(tmem_slot)));
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+          smem_u32(tmem_slot)), "n"(kTmemCols));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     } else {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-          smem_u32(tmem_slot)));
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+          smem_u32(tmem_slot)), "n"(kTmemCols));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
   }
@@ -327,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0 && leader) {
       // ---------------- MMA issuer (the leader CTA of a pair)
-      constexpr uint32_t idesc1 = idesc_bf16(BM * CG, BN);
+      constexpr uint32_t idesc1 = idesc_bf16(BM * CG, BNT);
       constexpr uint32_t idesc2 = idesc_bf16(BM * CG, kN2);
       auto mma1 = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
         if (CG == 2) mma_ss2(d, a, b, idesc1, acc); else mma_ss(d, a, b, idesc1, acc);
@@ -345,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // layer-2 MMAs of the tile whose activations sit in buffer `b`
       auto issue_layer2 = [&](uint32_t b) {
         tc_fence_after();
-        const uint32_t cb = tmem_base + b * BN;
+        const uint32_t cb = tmem_base + b * BNT;
 #pragma unroll
         for (int j = 0; j < (MLP_PROBE == 3 ? 0 : SPT); ++j) {
           const uint32_t bj = w2_base + (uint32_t)(j * kO2 * H * 2);
@@ -370,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (CG == 2) mbar_wait_cluster(bar_tempty + 8 * buf, use ^ 1);
         else mbar_wait(bar_tempty + 8 * buf, use ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + buf * BN;
+        const uint32_t d_tmem = tmem_base + buf * BNT;
         for (uint32_t kb = 0; kb < args.k_blocks; ++kb) {
           mbar_wait(bar_full + 8 * stage, phase);
           tc_fence_after();
@@ -406,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- epilogue
     const int e = warp - 4;            // 0..7
     const int q = warp & 3;            // TMEM lane quarter (warp % 4)
-    const int half = e >> 2;           // D1 column half: [half*128, half*128+128)
+    const int half = e >> 2;           // D1 column half: [half*kHalf, (half+1)*kHalf)
     const int row = q * 32 + lane;     // accumulator row == sample within tile
     const int et = threadIdx.x - 128;  // 0..255
     const uint32_t O = args.O;
@@ -416,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (uint32_t t = t_begin; t < t_end; ++t, ++i) {
       const uint32_t m_tile = (t % m_units) * CG + rank, n_tile = t / m_units;
       const uint32_t buf = i & 1, use = (i >> 1) & 1;
-      const uint32_t cb = tmem_base + buf * BN + lane_off;
+      const uint32_t cb = tmem_base + buf * BNT + lane_off;
       const uint32_t s = m_tile * BM + row;
       const bool valid = s < args.S;
       const int label = valid ? args.y[s] : 0;
@@ -468,8 +472,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(bar_tfull + 8 * buf, use);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        const int col0 = half * 128 + c * 32;
+      for (int c = 0; c < kHalf / 32; ++c) {
+        const int col0 = half * kHalf + c * 32;
         float acc[32];
         tmem_ld32(cb + col0, acc);
         uint32_t pk[16];
@@ -527,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // deterministic per-(spark, m-tile) partial: the 4 lane quarters in order
       if (et < SPT) {
         const int j = et;
-        const int hh = H > 128 ? 0 : (j * H) / 128;
+        const int hh = H > 128 ? 0 : (j * H) / kHalf;
         const int jl = H > 128 ? 0 : j - hh * (SPT / 2);
         float sum = 0.0f;
 #pragma unroll
@@ -546,26 +550,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) {
     tc_fence_after();
     if (CG == 2)
-      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols));
     else
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols));
   }
 }
 
 // -------------------------------------------------------------- host side
-template <int H, int CG>
+template <int H, int CG, int BNT = BN>
 cudaError_t prepare_h() {
-  return cudaFuncSetAttribute(k_mlp_fitness<H, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              smem_bytes<CG>());
+  return cudaFuncSetAttribute(k_mlp_fitness<H, CG, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              smem_bytes<CG, BNT>());
 }
 
-template <int H, int CG>
+template <int H, int CG, int BNT = BN>
 cudaError_t launch_h(const CUtensorMap& tx, const CUtensorMap& tw, int grid, const MlpArgs& a,
                      cudaStream_t s, cudaEvent_t launch_done) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem_bytes<CG>();
+  cfg.dynamicSmemBytes = smem_bytes<CG, BNT>();
   cfg.stream = s;
   cudaLaunchAttribute attr[3];
   int n = 0;
@@ -589,7 +593,7 @@ cudaError_t launch_h(const CUtensorMap& tx, const CUtensorMap& tw, int grid, con
   }
   cfg.attrs = attr;
   cfg.numAttrs = n;
-  return cudaLaunchKernelEx(&cfg, k_mlp_fitness<H, CG>, tx, tw, a);
+  return cudaLaunchKernelEx(&cfg, k_mlp_fitness<H, CG, BNT>, tx, tw, a);
 }
 
 // CTA group of the plans (MGFWA_MLP_CG=1|2; default MLP_CG_DEFAULT).  The
@@ -620,6 +624,7 @@ struct MlpPlan {
   int grid;
   int H;
   int cg;
+  int bnt;  // N tile width: BN, or BN_NARROW for few-row launches
 };
 
 uint32_t mlp_num_parts(uint32_t S) { return (S + BM - 1) / BM; }
@@ -652,8 +657,17 @@ MlpPlan* mlp_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t S, u
       return fail("MLP fitness: X tensor map encode failed");
     }
   }
-  const uint32_t spt = BN / H;
   const int cg = mlp_cg();
+  // Few rows (the guides, the loser re-evaluations): narrow 64-column tiles
+  // (2 sparks of H = 32) so the launch spreads over more SMs — C2 guides:
+  // 15 rows = 16 tiles of 256 columns -> 64 tiles of 64.  MGFWA_MLP_NARROW=0
+  // keeps 256-column tiles.
+  const uint32_t m_tiles = mlp_num_parts(S);
+  const char* nenv = getenv("MGFWA_MLP_NARROW");
+  const bool narrow = H == 32 && cg == 1 && !(nenv && nenv[0] == '0') &&
+                      2ull * m_tiles * ((rows + BN / H - 1) / (BN / H)) <= (uint64_t)nsm;
+  const int bnt = narrow ? BN_NARROW : BN;
+  const uint32_t spt = (uint32_t)bnt / H;
   {
     cuuint64_t dims[3] = {I, H, rows};
     cuuint64_t strides[2] = {(cuuint64_t)I * 2, (cuuint64_t)Dp * 2};
@@ -669,6 +683,7 @@ MlpPlan* mlp_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t S, u
     }
   }
   p->H = (int)H;
+  p->bnt = bnt;
   p->args.S = S;
   p->args.I = I;
   p->args.H = H;
@@ -691,6 +706,7 @@ MlpPlan* mlp_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t S, u
     p->grid = (int)(tiles < (uint32_t)nsm ? tiles : (uint32_t)nsm);
   }
   const cudaError_t e =
+      narrow ? prepare_h<32, 1, BN_NARROW>() :
       cg == 2 ? (H == 32 ? prepare_h<32, 2>() : H == 64 ? prepare_h<64, 2>()
                  : H == 128 ? prepare_h<128, 2>() : prepare_h<256, 2>())
               : (H == 32 ? prepare_h<32, 1>() : H == 64 ? prepare_h<64, 1>()
@@ -709,6 +725,7 @@ cudaError_t mlp_fitness_launch(const MlpPlan* p, float* part, const int* gate, c
   MlpArgs a = p->args;
   a.part = part;
   a.gate = gate;
+  if (p->bnt == BN_NARROW) return launch_h<32, 1, BN_NARROW>(p->tmap_x, p->tmap_w, p->grid, a, s, launch_done);
   if (p->cg == 2) {
     switch (p->H) {
       case 32: return launch_h<32, 2>(p->tmap_x, p->tmap_w, p->grid, a, s, launch_done);
