@@ -49,6 +49,10 @@ constexpr int BK = 64;   // K per pipeline stage (one 128-byte swizzle atom)
 #ifndef MLP_STAGES
 #define MLP_STAGES 4
 #endif
+#ifndef MLP_L2_WARP
+#define MLP_L2_WARP 1  // layer-2 MMAs issued by warp 3 (0: interleaved into the layer-1 k-loop)
+#endif
+constexpr bool kL2Warp = MLP_L2_WARP != 0;
 #ifndef MLP_PROBE
 #define MLP_PROBE 0  // 1: profiling probe, TMA + layer-1 MMA pipeline only (no epilogue math)
 #endif
@@ -292,6 +296,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t t_begin = (uint32_t)(((uint64_t)total * group) / groups);
   const uint32_t t_end = (uint32_t)(((uint64_t)total * (group + 1)) / groups);
 
+  constexpr uint32_t idesc2_l2 = idesc_bf16(BM * CG, kN2);
+  const uint32_t w2_base = smem_u32(s_w2);
+  // layer-2 MMAs of the tile whose activations sit in buffer `b`
+  auto issue_layer2_t = [&](uint32_t b) {
+    tc_fence_after();
+    const uint32_t cb = tmem_base + b * BNT;
+#pragma unroll
+    for (int j = 0; j < (MLP_PROBE == 3 ? 0 : SPT); ++j) {
+      const uint32_t bj = w2_base + (uint32_t)(j * kO2 * H * 2);
+#pragma unroll
+      for (int kk = 0; kk < H / 16; ++kk) {
+        // B: kO2 output rows x 16 K per step; core matrices 8 rows x 16 B,
+        // K-adjacent ones (kO2/8)*128 B apart, N-adjacent 128 B apart
+        const uint64_t bd = interleaved_desc(bj + kk * (kO2 / 8) * 256, (kO2 / 8) * 128, 128);
+        if (CG == 2)
+          mma_ts2(cb + d2_col<H>(j), cb + a2_kcol<H>(j, kk), bd, idesc2_l2, kk != 0);
+        else
+          mma_ts(cb + d2_col<H>(j), cb + a2_kcol<H>(j, kk), bd, idesc2_l2, kk != 0);
+      }
+    }
+    if (CG == 2) mma_commit2(bar_d2full + 8 * b); else mma_commit(bar_d2full + 8 * b);
+  };
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer
@@ -345,27 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto a2wait = [&](uint32_t b, uint32_t u) {
         if (CG == 2) mbar_wait_cluster(bar_a2full + 8 * b, u); else mbar_wait(bar_a2full + 8 * b, u);
       };
-      const uint32_t w2_base = smem_u32(s_w2);
-      // layer-2 MMAs of the tile whose activations sit in buffer `b`
-      auto issue_layer2 = [&](uint32_t b) {
-        tc_fence_after();
-        const uint32_t cb = tmem_base + b * BNT;
-#pragma unroll
-        for (int j = 0; j < (MLP_PROBE == 3 ? 0 : SPT); ++j) {
-          const uint32_t bj = w2_base + (uint32_t)(j * kO2 * H * 2);
-#pragma unroll
-          for (int kk = 0; kk < H / 16; ++kk) {
-            // B: kO2 output rows x 16 K per step; core matrices 8 rows x 16 B,
-            // K-adjacent ones (kO2/8)*128 B apart, N-adjacent 128 B apart
-            const uint64_t bd = interleaved_desc(bj + kk * (kO2 / 8) * 256, (kO2 / 8) * 128, 128);
-            if (CG == 2)
-              mma_ts2(cb + d2_col<H>(j), cb + a2_kcol<H>(j, kk), bd, idesc2, kk != 0);
-            else
-              mma_ts(cb + d2_col<H>(j), cb + a2_kcol<H>(j, kk), bd, idesc2, kk != 0);
-          }
-        }
-        commit(bar_d2full + 8 * b);
-      };
+      auto issue_layer2 = [&](uint32_t b) { issue_layer2_t(b); };
       uint32_t stage = 0, phase = 0, i = 0;
       bool pend = false;
       uint32_t pbuf = 0, puse = 0;
@@ -385,13 +391,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (uint32_t kk = 0; kk < nk; ++kk) mma1(d_tmem, da + 2 * kk, db + 2 * kk, (kb | kk) != 0);
           commit(bar_empty + 8 * stage);
           if (++stage == kStages) stage = 0, phase ^= 1;
-          if (pend && a2ready(pbuf, puse)) {
+          if (!kL2Warp && pend && a2ready(pbuf, puse)) {
             issue_layer2(pbuf);
             pend = false;
           }
         }
         commit(bar_tfull + 8 * buf);
-        if (MLP_PROBE == 1 || MLP_PROBE == 2) continue;
+        if (kL2Warp || MLP_PROBE == 1 || MLP_PROBE == 2) continue;
         if (pend) {
           a2wait(pbuf, puse);
           issue_layer2(pbuf);
@@ -400,9 +406,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         pbuf = buf;
         puse = use;
       }
-      if (pend && MLP_PROBE != 1 && MLP_PROBE != 2) {
+      if (!kL2Warp && pend && MLP_PROBE != 1 && MLP_PROBE != 2) {
         a2wait(pbuf, puse);
         issue_layer2(pbuf);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 3) {
+    if (kL2Warp && lane == 0 && leader && MLP_PROBE != 1 && MLP_PROBE != 2) {
+      // ---------------- layer-2 MMA issuer: as soon as tile t's activations
+      // are in TMEM (independent of the layer-1 k-loop's TMA waits)
+      uint32_t i = 0;
+      for (uint32_t t = t_begin; t < t_end; ++t, ++i) {
+        const uint32_t buf = i & 1, use = (i >> 1) & 1;
+        if (CG == 2) mbar_wait_cluster(bar_a2full + 8 * buf, use); else mbar_wait(bar_a2full + 8 * buf, use);
+        issue_layer2_t(buf);
       }
     }
     __syncwarp();

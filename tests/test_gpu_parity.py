@@ -332,6 +332,25 @@ def test_mlp_cta_pair_variant_matches(P, tmp_path):
         np.testing.assert_allclose(a[H], b[H], rtol=1e-5, atol=1e-6)
 
 
+def test_mlp_narrow_tiles_bit_identical(P, tmp_path):
+    """Few-row launches (guides, losers) use 64-column tiles (2 sparks of
+    H = 32); MGFWA_MLP_NARROW=0 forces the 256-column tiles.  Same K order,
+    same per-(spark, m-tile) sums: bit-identical fitness."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, paper_2501_03944_b200 as P\n"
+        "obj = P.MlpWeights(samples=1024)\n"
+        "W = np.random.default_rng(3).uniform(-0.05, 0.05, size=(15, obj.dim())).astype(np.float32)\n"
+        f"np.save(r'{tmp_path}/' + __import__('os').environ['MGFWA_MLP_NARROW'] + '.npy', "
+        "P.batched_apply(obj, W.astype(np.float64))[0])\n")
+    for nw in ("0", "1"):
+        env = dict(__import__("os").environ, MGFWA_MLP_NARROW=nw)
+        subprocess.run([sys.executable, "-c", code], env=env, check=True, timeout=300)
+    assert np.array_equal(np.load(tmp_path / "0.npy"), np.load(tmp_path / "1.npy"))
+
+
 def test_lenet_candidate_groups_bit_identical(P):
     """Populations whose activation scratch exceeds the cap run in candidate
     groups (one conv + fc launch pair each); the fitness must not depend on
