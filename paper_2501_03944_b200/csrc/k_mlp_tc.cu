@@ -53,6 +53,9 @@ constexpr int BK = 64;   // K per pipeline stage (one 128-byte swizzle atom)
 #define MLP_L2_WARP 1  // layer-2 MMAs issued by warp 3 (0: interleaved into the layer-1 k-loop)
 #endif
 constexpr bool kL2Warp = MLP_L2_WARP != 0;
+#ifndef MLP_L2_PREFETCH
+#define MLP_L2_PREFETCH 0  // 1: TMA L2 prefetch of the next N tile's W1 (measured slower: C2 fitness 90.3 -> 93.7 us cold)
+#endif
 #ifndef MLP_PROBE
 #define MLP_PROBE 0  // 1: profiling probe, TMA + layer-1 MMA pipeline only (no epilogue math)
 #endif
@@ -182,6 +185,13 @@ __device__ __forceinline__ void mma_commit2(uint32_t bar) {
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
       " [%0], %1;" ::"r"(bar), "h"(mask)
       : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(z)
+               : "memory");
 }
 
 __device__ __forceinline__ void epi_bar() {
@@ -324,6 +334,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t stage = 0, phase = 0;
       for (uint32_t t = t_begin; t < t_end; ++t) {
         const int m_tile = (int)((t % m_units) * CG + rank), n_tile = (int)(t / m_units);
+        // Entering an N tile: pull this CTA's next N tile of W1 into L2 (its
+        // first m-tile would otherwise stream it from HBM at TMA latency).
+        if (MLP_L2_PREFETCH && (t == t_begin || t % m_units == 0) && (uint32_t)(n_tile + 1) * m_units < t_end) {
+          for (uint32_t kb = 0; kb < args.k_blocks; ++kb) {
+            if (SPT >= 2)
+              tma_prefetch_3d(&tmap_w, (int)(kb * BK), 0, (n_tile + 1) * SPT + (CG == 2 ? (int)rank * (SPT / 2) : 0));
+            else
+              tma_prefetch_3d(&tmap_w, (int)(kb * BK), CG == 2 ? (int)rank * (H / 2) : 0, n_tile + 1);
+          }
+        }
         for (uint32_t kb = 0; kb < args.k_blocks; ++kb) {
           mbar_wait(bar_empty + 8 * stage, phase ^ 1);
           const uint32_t sa = smem_u32(smem + stage * kStageBytes);
@@ -614,23 +634,22 @@ cudaError_t launch_h(const CUtensorMap& tx, const CUtensorMap& tw, int grid, con
   return cudaLaunchKernelEx(&cfg, k_mlp_fitness<H, CG, BNT>, tx, tw, a);
 }
 
-// CTA group of the plans (MGFWA_MLP_CG=1|2; default MLP_CG_DEFAULT).  The
-// pair variant is parity-green but measured slower on C2 (B200): 91 vs 75 us
-// per 1500 candidates.  Probes (MLP_PROBE): TMA + layer-1 MMA only 63.5 vs
-// 61.5 us; layer-1 MMA alone 62.9 vs 55.4 us; the epilogue chain, which for
-// a pair waits on both CTAs (remote mbarrier arrivals), adds 28 vs 14 us.
-// The single-SM kernel stays the default.
-#ifndef MLP_CG_DEFAULT
-#define MLP_CG_DEFAULT 1
-#endif
-int mlp_cg() {
-  static const int cg = [] {
+// CTA group of a plan (MGFWA_MLP_CG=1|2 overrides).  Default: the SM pair
+// (cta_group::2, M = 256: each CTA stages its own X rows and HALF of the W1
+// tile, a third less operand traffic through L2 per MMA) for H >= 128, where
+// the kernel is bound by L2 -> shared-memory operand delivery (C5, H = 256:
+// 26.7 -> 24.8 ms per generation); one SM per tile for narrower hidden
+// layers, where the pair's cross-CTA epilogue handshakes cost more than the
+// traffic saves (C2, H = 32: 90.1 vs 103.7 us).
+int mlp_cg(uint32_t H) {
+  static const int forced = [] {
     const char* e = getenv("MGFWA_MLP_CG");
     if (e && e[0] == '1') return 1;
     if (e && e[0] == '2') return 2;
-    return MLP_CG_DEFAULT;
+    return 0;
   }();
-  return cg;
+  if (forced) return forced;
+  return H >= 128 ? 2 : 1;
 }
 
 }  // namespace
@@ -675,7 +694,7 @@ MlpPlan* mlp_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t S, u
       return fail("MLP fitness: X tensor map encode failed");
     }
   }
-  const int cg = mlp_cg();
+  const int cg = mlp_cg(H);
   // Few rows (the guides, the loser re-evaluations): narrow 64-column tiles
   // (2 sparks of H = 32) so the launch spreads over more SMs — C2 guides:
   // 15 rows = 16 tiles of 256 columns -> 64 tiles of 64.  MGFWA_MLP_NARROW=0
