@@ -49,6 +49,16 @@ constexpr int BK = 64;   // K per pipeline stage (one 128-byte swizzle atom)
 #ifndef MLP_STAGES
 #define MLP_STAGES 4
 #endif
+#ifndef MLP_FAST_MATH
+#define MLP_FAST_MATH 1  // CE with the MUFU exp2/log2 forms (__expf/__logf)
+#endif
+#if MLP_FAST_MATH
+#define MLP_EXPF __expf
+#define MLP_LOGF __logf
+#else
+#define MLP_EXPF expf
+#define MLP_LOGF logf
+#endif
 #ifndef MLP_L2_WARP
 #define MLP_L2_WARP 1  // layer-2 MMAs issued by warp 3 (0: interleaved into the layer-1 k-loop)
 #endif
@@ -536,28 +546,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int jb = H > 128 ? 0 : half * (SPT / 2);
       const int jn = H > 128 ? (half == 0 ? 1 : 0) : SPT / 2;
-      for (int jj = 0; jj < jn; ++jj) {
+      constexpr int JN = H > 128 ? 1 : SPT / 2;  // logit blocks per thread (H > 128: half 0 only)
+      // all of the thread's logit blocks in flight at once, one wait
+      float z[JN][kN2];
+#pragma unroll
+      for (int jj = 0; jj < JN; ++jj)
+        if (jj < jn) tmem_ld16_nowait(cb + d2_col<H>(jb + jj), z[jj]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int jj = 0; jj < JN; ++jj) {
         const int j = jb + jj;
-        float z[kN2];
-        tmem_ld16(cb + d2_col<H>(j), z);
         float loss = 0.0f;
-        if (valid) {
+        if (valid && jj < jn) {
           float mx = -INFINITY;
 #pragma unroll
-          for (int o = 0; o < kN2; ++o) {
-            z[o] += s_b2[j * kN2 + o];
-            if ((uint32_t)o < O) mx = fmaxf(mx, z[o]);
+          for (int o = 0; o < kMaxO; ++o) {
+            z[jj][o] += s_b2[j * kN2 + o];
+            if ((uint32_t)o < O) mx = fmaxf(mx, z[jj][o]);
           }
           float se = 0.0f, zl = 0.0f;
 #pragma unroll
-          for (int o = 0; o < kN2; ++o) {
-            if ((uint32_t)o < O) se += expf(z[o] - mx);
-            if (o == label) zl = z[o];
+          for (int o = 0; o < kMaxO; ++o) {
+            if ((uint32_t)o < O) se += MLP_EXPF(z[jj][o] - mx);
+            if (o == label) zl = z[jj][o];
           }
-          loss = (mx + logf(se)) - zl;
+          loss = (mx + MLP_LOGF(se)) - zl;
         }
         loss = warp_sum(loss);
-        if (lane == 0) s_red[e * 8 + jj] = loss;
+        if (lane == 0 && jj < jn) s_red[e * 8 + jj] = loss;
       }
       // tile buffer consumed: hand it back to the MMA warp
       tc_fence_before();
