@@ -1348,19 +1348,43 @@ __device__ void small_a_body(const EngineView& v, uint64_t fl, uint64_t* sa_keys
     const float* plo = v.pop_lo + b * v.Dp;
     const float* phi = v.pop_hi + b * v.Dp;
     const uint64_t d4 = (v.D + 3) & ~3ull;
+    __shared__ uint64_t s_gpre[16];  // kGuide key prefixes (M <= 16)
+    for (uint64_t m = threadIdx.x; m < v.M; m += blockDim.x) s_gpre[m] = key_prefix(v.seed, kGuide, it, b, n, m);
+    __syncthreads();
     for (uint64_t d = threadIdx.x; d < d4; d += blockDim.x) {
       if (d >= v.D) {
         for (uint64_t m = 0; m < v.M; ++m) v.guides[(fl * v.M + m) * v.Dp + d] = 0.0f;
         continue;
       }
       double acc = 0.0;
-      for (uint32_t t = 0; t < top; ++t)
-        acc = __dadd_rn(acc, __dsub_rn((double)sb[(uint64_t)s_idx[t] * v.Dp + d],
-                                       (double)sb[(uint64_t)s_idx[top + t] * v.Dp + d]));
+      uint32_t t = 0;
+      // rank pairs 8 at a time, all 16 loads in flight, summed in rank order
+      for (; t + 8 <= top; t += 8) {
+        float tv[8], bv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          tv[i] = sb[(uint64_t)s_idx[t + i] * v.Dp + d];
+          bv[i] = sb[(uint64_t)s_idx[top + t + i] * v.Dp + d];
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc = __dadd_rn(acc, __dsub_rn((double)tv[i], (double)bv[i]));
+      }
+      if (t < top) {
+        float tv[8], bv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t ti = t + i < top ? t + i : t;
+          tv[i] = sb[(uint64_t)s_idx[ti] * v.Dp + d];
+          bv[i] = sb[(uint64_t)s_idx[top + ti] * v.Dp + d];
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (t + i < top) acc = __dadd_rn(acc, __dsub_rn((double)tv[i], (double)bv[i]));
+      }
       const double delta = __ddiv_rn(acc, (double)top);
       const double pv = (double)v.pos[f * v.Dp + d];
       for (uint64_t m = 0; m < v.M; ++m) {
-        const uint64_t pg = key_prefix(v.seed, kGuide, it, b, n, m);
+        const uint64_t pg = s_gpre[m];
         const double gx = __dadd_rn(pv, __dmul_rn(v.boosts[m], delta));
         v.guides[(fl * v.M + m) * v.Dp + d] = map_coord(v, gx, d, pg, plo, phi);
       }
@@ -1405,7 +1429,43 @@ __device__ void small_b_body(const EngineView& v, uint64_t b, unsigned nblocks) 
   __shared__ int s_count;
   unsigned nan_local = 0;
   // ---- loser decision for batch b (k_loser, engine.cpp:258-286)
-  if (threadIdx.x == 0) {
+  if (v.mu <= 32) {
+    // warp 0, lane n = firework n: batch argmin as the lexicographic min of
+    // (fitness, n) (== the strict-< scan), loser flags in parallel
+    if (warp == 0) {
+      const double iters_rem = ctl->iters_rem;
+      const uint64_t f = b * v.mu + lane;
+      const bool in = (uint64_t)lane < v.mu;
+      const double fv = in ? v.fit[f] : __longlong_as_double(0x7ff0000000000000ll);
+      const double lv = in ? v.li[f] : 0.0;
+      double bv = fv;
+      int bi = in ? lane : 0x7fffffff;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (ov < bv || (ov == bv && oi < bi)) bv = ov, bi = oi;
+      }
+      int is_loser = 0;
+      if (in && iters_rem > 0.0 && lane != bi) is_loser = __dsub_rn(fv, __dmul_rn(lv, iters_rem)) > bv;
+      if (in) {
+        v.loser[f] = is_loser;
+        if (is_loser) {
+          v.amp[f] = v.a0;
+          v.li[f] = 0.0;
+        }
+      }
+      const int cnt = __popc(__ballot_sync(0xffffffffu, is_loser));
+      if (lane == 0) {
+        s_count = cnt;
+        if (cnt) {
+          atomicAdd((unsigned long long*)&ctl->used, (unsigned long long)cnt);
+          atomicAdd((unsigned long long*)&ctl->losers_total, (unsigned long long)cnt);
+        }
+      }
+    }
+  } else if (threadIdx.x == 0) {
+
     const double iters_rem = ctl->iters_rem;
     uint64_t bi = 0;
     double bv = v.fit[b * v.mu];
@@ -1462,12 +1522,33 @@ __device__ void small_b_body(const EngineView& v, uint64_t b, unsigned nblocks) 
   }
   // ---- record_wave for batch b (engine.cpp:340-351)
   __shared__ int s_flag, s_best;
+  __shared__ double s_bv;
+  __shared__ int s_bi;
   const uint64_t now = global_ns();
+  if (v.mu <= 32 && warp == 0) {  // batch argmin (lowest index on ties), warp-parallel
+    const bool in = (uint64_t)lane < v.mu;
+    double bv = in ? v.fit[b * v.mu + lane] : __longlong_as_double(0x7ff0000000000000ll);
+    int bi = in ? lane : 0x7fffffff;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (ov < bv || (ov == bv && oi < bi)) bv = ov, bi = oi;
+    }
+    if (lane == 0) s_bv = bv, s_bi = bi;
+    __syncwarp();
+  }
   if (threadIdx.x == 0) {
     uint64_t bi = 0;
-    double bv = v.fit[b * v.mu];
-    for (uint64_t n = 1; n < v.mu; ++n)
-      if (v.fit[b * v.mu + n] < bv) bv = v.fit[b * v.mu + n], bi = n;
+    double bv;
+    if (v.mu <= 32) {
+      bv = s_bv;
+      bi = (uint64_t)s_bi;
+    } else {
+      bv = v.fit[b * v.mu];
+      for (uint64_t n = 1; n < v.mu; ++n)
+        if (v.fit[b * v.mu + n] < bv) bv = v.fit[b * v.mu + n], bi = n;
+    }
     double cur = v.best_fit[b];
     int flag = 0;
     if (bv < cur) {
@@ -1555,7 +1636,15 @@ __device__ void grid_barrier(Ctl* ctl, unsigned nblocks) {
 // first firework's block, a grid barrier (termination test).  No launch
 // latency between phases; every value is computed with the same device
 // functions, in the same order, as the multi-kernel path.
-template <int KIND>
+// All the blocks form one thread-block cluster (F <= 8): the hardware cluster
+// barrier (release / acquire at cluster scope) instead of the global-atomic
+// grid barrier.
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int KIND, bool CL>
 __global__ void __launch_bounds__(kSmallThreads) k_small_run(EngineView v, uint64_t max_gens) {
   extern __shared__ __align__(16) uint8_t run_smem[];
   ExplodeChunk& ch = *reinterpret_cast<ExplodeChunk*>(run_smem);
@@ -1573,9 +1662,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_run(EngineView v, uint6
     for (uint64_t g = warp; g < ngrp; g += kWarps) explode_group<KIND>(v, ch, wqs[warp], lane, 0, f, g);
     __syncthreads();
     small_a_body(v, f, keys);
-    grid_barrier(v.ctl, gridDim.x);  // iterations_remaining (block 0) is final
+    if (CL) cluster_barrier(); else grid_barrier(v.ctl, gridDim.x);  // iterations_remaining (block 0) is final
     if (f % v.mu == 0) small_b_body(v, b, (unsigned)v.B);
-    grid_barrier(v.ctl, gridDim.x);  // termination / iteration of the next generation
+    if (CL) cluster_barrier(); else grid_barrier(v.ctl, gridDim.x);  // termination / next iteration
   }
 }
 
@@ -1595,6 +1684,9 @@ static size_t small_run_smem(const EngineView& v) {
   return sizeof(ExplodeChunk) + kWarps * sizeof(ExplodeWarp) + v.lam * sizeof(uint64_t);
 }
 
+#ifndef SMALL_CLUSTER
+#define SMALL_CLUSTER 1  // F <= 8: one thread-block cluster with the hardware cluster barrier
+#endif
 cudaError_t launch_small_run(const EngineView& v, uint64_t max_gens, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)v.F);
@@ -1602,14 +1694,29 @@ cudaError_t launch_small_run(const EngineView& v, uint64_t max_gens, cudaStream_
   cfg.dynamicSmemBytes = small_run_smem(v);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for the grid barrier
-  attr[0].val.cooperative = 1;
+  const bool cl = SMALL_CLUSTER && v.F <= 8;
+  if (cl) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)v.F;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+  } else {
+    attr[0].id = cudaLaunchAttributeCooperative;  // co-residency for the grid barrier
+    attr[0].val.cooperative = 1;
+  }
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (cl) {
+    switch (v.obj_kind) {
+      case OBJ_SPHERE: return cudaLaunchKernelEx(&cfg, k_small_run<OBJ_SPHERE, true>, v, max_gens);
+      case OBJ_RASTRIGIN: return cudaLaunchKernelEx(&cfg, k_small_run<OBJ_RASTRIGIN, true>, v, max_gens);
+      default: return cudaLaunchKernelEx(&cfg, k_small_run<OBJ_ACKLEY, true>, v, max_gens);
+    }
+  }
   switch (v.obj_kind) {
-    case OBJ_SPHERE: return cudaLaunchKernelEx(&cfg, k_small_run<OBJ_SPHERE>, v, max_gens);
-    case OBJ_RASTRIGIN: return cudaLaunchKernelEx(&cfg, k_small_run<OBJ_RASTRIGIN>, v, max_gens);
-    default: return cudaLaunchKernelEx(&cfg, k_small_run<OBJ_ACKLEY>, v, max_gens);
+    case OBJ_SPHERE: return cudaLaunchKernelEx(&cfg, k_small_run<OBJ_SPHERE, false>, v, max_gens);
+    case OBJ_RASTRIGIN: return cudaLaunchKernelEx(&cfg, k_small_run<OBJ_RASTRIGIN, false>, v, max_gens);
+    default: return cudaLaunchKernelEx(&cfg, k_small_run<OBJ_ACKLEY, false>, v, max_gens);
   }
 }
 
