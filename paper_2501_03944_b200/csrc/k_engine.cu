@@ -1644,7 +1644,36 @@ __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <int KIND, bool CL>
+// Candidate buffers of the cluster form (SM = true): the block's sparks,
+// guides, their partial sums and fitness live in shared memory for the whole
+// launch (the EngineView the phase functions see is rebased onto them; the
+// indexing by the global firework is unchanged) and are written through to
+// HBM once per generation for the host-side readers (mgfwa_get_candidates).
+struct SmallSmem {
+  uint64_t sp, spart, gd, gpart, sfit, gfit, total;  // byte offsets after the keys
+};
+__host__ __device__ inline SmallSmem small_smem_layout(const EngineView& v) {
+  SmallSmem L;
+  uint64_t o = 0;
+  auto take = [&](uint64_t bytes) { const uint64_t r = o; o += (bytes + 15) & ~15ull; return r; };
+  L.sp = take(v.lam * v.Dp * 4);
+  L.spart = take(v.lam * v.nparts * 2 * 4);
+  L.gd = take(v.M * v.Dp * 4);
+  L.gpart = take(v.M * 2 * 4);
+  L.sfit = take(v.lam * 4);
+  L.gfit = take(v.M * 4);
+  L.total = o;
+  return L;
+}
+template <typename T>
+__device__ __forceinline__ T* rebase(uint8_t* base, uint64_t off, uint64_t elems_before) {
+  return reinterpret_cast<T*>(reinterpret_cast<uintptr_t>(base + off) - elems_before * sizeof(T));
+}
+__device__ __forceinline__ void copy_words(float* dst, const float* src, uint64_t n) {
+  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+template <int KIND, bool CL, bool SM>
 __global__ void __launch_bounds__(kSmallThreads) k_small_run(EngineView v, uint64_t max_gens) {
   extern __shared__ __align__(16) uint8_t run_smem[];
   ExplodeChunk& ch = *reinterpret_cast<ExplodeChunk*>(run_smem);
@@ -1654,14 +1683,33 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_run(EngineView v, uint6
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t f = blockIdx.x, b = f / v.mu;
   const uint64_t ngrp = (v.lam + kSparkGroup - 1) / kSparkGroup;
+  EngineView w = v;  // SM: the phases' view of this block's candidates
+  if (SM) {
+    uint8_t* cb = reinterpret_cast<uint8_t*>(keys + ((v.lam + 1) & ~1ull));
+    const SmallSmem L = small_smem_layout(v);
+    w.sparks = rebase<float>(cb, L.sp, f * v.lam * v.Dp);
+    w.spart = rebase<float>(cb, L.spart, f * v.lam * v.nparts * 2);
+    w.guides = rebase<float>(cb, L.gd, f * v.M * v.Dp);
+    w.gpart = rebase<float>(cb, L.gpart, f * v.M * 2);
+    w.sfit = rebase<float>(cb, L.sfit, f * v.lam);
+    w.gfit = rebase<float>(cb, L.gfit, f * v.M);
+  }
   for (uint64_t gen = 0; gen < max_gens; ++gen) {
     if (*(volatile int*)&v.ctl->active == 0) break;  // uniform: set before the last barrier
     // explode + mapping + fused fitness partials of firework f (one chunk: D <= kChunk)
     stage_explode_chunk(v, ch, b, 0);
     __syncthreads();
-    for (uint64_t g = warp; g < ngrp; g += kWarps) explode_group<KIND>(v, ch, wqs[warp], lane, 0, f, g);
+    for (uint64_t g = warp; g < ngrp; g += kWarps) explode_group<KIND>(w, ch, wqs[warp], lane, 0, f, g);
     __syncthreads();
-    small_a_body(v, f, keys);
+    small_a_body(w, f, keys);
+    if (SM) {  // write-through of this generation's candidates (host readers)
+      copy_words(v.sparks + f * v.lam * v.Dp, w.sparks + f * v.lam * v.Dp, v.lam * v.Dp);
+      copy_words(v.spart + f * v.lam * v.nparts * 2, w.spart + f * v.lam * v.nparts * 2, v.lam * v.nparts * 2);
+      copy_words(v.guides + f * v.M * v.Dp, w.guides + f * v.M * v.Dp, v.M * v.Dp);
+      copy_words(v.gpart + f * v.M * 2, w.gpart + f * v.M * 2, v.M * 2);
+      copy_words(v.sfit + f * v.lam, w.sfit + f * v.lam, v.lam);
+      copy_words(v.gfit + f * v.M, w.gfit + f * v.M, v.M);
+    }
     if (CL) cluster_barrier(); else grid_barrier(v.ctl, gridDim.x);  // iterations_remaining (block 0) is final
     if (f % v.mu == 0) small_b_body(v, b, (unsigned)v.B);
     if (CL) cluster_barrier(); else grid_barrier(v.ctl, gridDim.x);  // termination / next iteration
@@ -1680,21 +1728,27 @@ bool small_run_ok(const EngineView& v, int nsm) {
          v.M <= 16 && v.F <= (uint64_t)nsm;
 }
 
-static size_t small_run_smem(const EngineView& v) {
-  return sizeof(ExplodeChunk) + kWarps * sizeof(ExplodeWarp) + v.lam * sizeof(uint64_t);
+static size_t small_run_smem(const EngineView& v, bool sm) {
+  return sizeof(ExplodeChunk) + kWarps * sizeof(ExplodeWarp) + ((v.lam + 1) & ~1ull) * sizeof(uint64_t) +
+         (sm ? small_smem_layout(v).total : 0);
 }
+#ifndef SMALL_SMEM
+#define SMALL_SMEM 1  // cluster form: candidates resident in shared memory when they fit
+#endif
+constexpr size_t kSmallSmemMax = 200 * 1024;
 
 #ifndef SMALL_CLUSTER
 #define SMALL_CLUSTER 1  // F <= 8: one thread-block cluster with the hardware cluster barrier
 #endif
 cudaError_t launch_small_run(const EngineView& v, uint64_t max_gens, cudaStream_t s) {
+  const bool cl = SMALL_CLUSTER && v.F <= 8;
+  const bool sm = cl && SMALL_SMEM && small_run_smem(v, true) <= kSmallSmemMax;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)v.F);
   cfg.blockDim = dim3(kSmallThreads);
-  cfg.dynamicSmemBytes = small_run_smem(v);
+  cfg.dynamicSmemBytes = small_run_smem(v, sm);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
-  const bool cl = SMALL_CLUSTER && v.F <= 8;
   if (cl) {
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = (unsigned)v.F;
@@ -1706,17 +1760,24 @@ cudaError_t launch_small_run(const EngineView& v, uint64_t max_gens, cudaStream_
   }
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cl) {
-    switch (v.obj_kind) {
-      case OBJ_SPHERE: return cudaLaunchKernelEx(&cfg, k_small_run<OBJ_SPHERE, true>, v, max_gens);
-      case OBJ_RASTRIGIN: return cudaLaunchKernelEx(&cfg, k_small_run<OBJ_RASTRIGIN, true>, v, max_gens);
-      default: return cudaLaunchKernelEx(&cfg, k_small_run<OBJ_ACKLEY, true>, v, max_gens);
+  auto go = [&](auto kern) -> cudaError_t {
+    if (cfg.dynamicSmemBytes > 48 * 1024) {
+      const cudaError_t e =
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes);
+      if (e != cudaSuccess) return e;
     }
-  }
+    return cudaLaunchKernelEx(&cfg, kern, v, max_gens);
+  };
   switch (v.obj_kind) {
-    case OBJ_SPHERE: return cudaLaunchKernelEx(&cfg, k_small_run<OBJ_SPHERE, false>, v, max_gens);
-    case OBJ_RASTRIGIN: return cudaLaunchKernelEx(&cfg, k_small_run<OBJ_RASTRIGIN, false>, v, max_gens);
-    default: return cudaLaunchKernelEx(&cfg, k_small_run<OBJ_ACKLEY, false>, v, max_gens);
+    case OBJ_SPHERE:
+      return sm ? go(k_small_run<OBJ_SPHERE, true, true>)
+                : cl ? go(k_small_run<OBJ_SPHERE, true, false>) : go(k_small_run<OBJ_SPHERE, false, false>);
+    case OBJ_RASTRIGIN:
+      return sm ? go(k_small_run<OBJ_RASTRIGIN, true, true>)
+                : cl ? go(k_small_run<OBJ_RASTRIGIN, true, false>) : go(k_small_run<OBJ_RASTRIGIN, false, false>);
+    default:
+      return sm ? go(k_small_run<OBJ_ACKLEY, true, true>)
+                : cl ? go(k_small_run<OBJ_ACKLEY, true, false>) : go(k_small_run<OBJ_ACKLEY, false, false>);
   }
 }
 
