@@ -1428,6 +1428,9 @@ __device__ void small_b_body(const EngineView& v, uint64_t b, unsigned nblocks) 
   const uint64_t slot = ctl->trace_n % v.trace_cap;
   __shared__ int s_count;
   unsigned nan_local = 0;
+  // loaded up front: record_wave needs them after the loser phase
+  const double best_prev = threadIdx.x == 0 ? v.best_fit[b] : 0.0;
+  const uint64_t start_ns = threadIdx.x == 0 ? ctl->start_ns : 0;
   // ---- loser decision for batch b (k_loser, engine.cpp:258-286)
   if (v.mu <= 32) {
     // warp 0, lane n = firework n: batch argmin as the lexicographic min of
@@ -1549,7 +1552,7 @@ __device__ void small_b_body(const EngineView& v, uint64_t b, unsigned nblocks) 
       for (uint64_t n = 1; n < v.mu; ++n)
         if (v.fit[b * v.mu + n] < bv) bv = v.fit[b * v.mu + n], bi = n;
     }
-    double cur = v.best_fit[b];
+    double cur = best_prev;
     int flag = 0;
     if (bv < cur) {
       cur = bv;
@@ -1559,7 +1562,7 @@ __device__ void small_b_body(const EngineView& v, uint64_t b, unsigned nblocks) 
     v.best_fit[b] = cur;
     v.rec_flag[b] = flag;
     v.tr_best[slot * v.B + b] = cur;
-    v.tr_ns[slot * v.B + b] = now - ctl->start_ns;
+    v.tr_ns[slot * v.B + b] = now - start_ns;
     s_flag = flag;
     s_best = (int)bi;
   }
@@ -1578,18 +1581,23 @@ __device__ void small_b_body(const EngineView& v, uint64_t b, unsigned nblocks) 
     v.pop_lo[b * v.Dp + d] = mn;
     v.pop_hi[b * v.Dp + d] = mx;
   }
-  // ---- the last block: trace evaluations, termination (k_finalize_record)
+  // ---- the last block: trace evaluations, termination (k_finalize_record);
+  // a single batch block (nblocks == 1) is the last one by construction
   if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned done = atomicAdd(&ctl->small_done, 1u);
-    if (done == nblocks - 1) {
+    bool last = true;
+    if (nblocks > 1) {
       __threadfence();
+      const unsigned done = atomicAdd(&ctl->small_done, 1u);
+      last = done == nblocks - 1;
+      if (last) __threadfence();
+    }
+    if (last) {
       const uint64_t used = *(volatile uint64_t*)&ctl->used;
       for (uint64_t bb = 0; bb < v.B; ++bb) v.tr_evals[slot * v.B + bb] = used;
-      ctl->small_done = 0;
+      if (nblocks > 1) ctl->small_done = 0;
       ctl->trace_n += 1;
       ctl->gens_run += 1;
-      const double now_ms = (double)(now - ctl->start_ns) * 1e-6;
+      const double now_ms = (double)(now - start_ns) * 1e-6;
       int active = 1;
       if (v.max_evals > 0 && used >= v.max_evals) active = 0;
       if (v.wall_budget_ms > 0.0 && now_ms >= v.wall_budget_ms) active = 0;
