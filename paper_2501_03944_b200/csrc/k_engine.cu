@@ -276,6 +276,14 @@ __device__ __forceinline__ bool in_box_fast(float x, float lo_f, float hi_f) {
   return x > lo_f && x < hi_f;
 }
 
+// rng.hpp:43-49 absorbed up to the iteration for the explode and mapping
+// streams: (x, y) = key prefixes of (seed, kExplode, it) and (seed, kMapping, it).
+__device__ __forceinline__ ulonglong2 explode_stream_prefixes(const EngineView& v) {
+  const uint64_t it = v.ctl->iteration;
+  const uint64_t hs = splitmix64(v.seed);
+  return make_ulonglong2(splitmix64(splitmix64(hs ^ kExplode) ^ it), splitmix64(splitmix64(hs ^ kMapping) ^ it));
+}
+
 // Dynamic shared memory of k_explode_map: the block's 512-coordinate chunk
 // of the box (fp64 and its fp32 images) and of the population range,
 // staged once per work item, plus the per-warp key prefixes.
@@ -406,21 +414,26 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
 template <int KIND>
 __device__ __forceinline__ void explode_group(const EngineView& v, const ExplodeChunk& ch,
                                               ExplodeWarp& wq, int lane, uint32_t c, uint64_t fl,
-                                              uint64_t g) {
+                                              uint64_t g, ulonglong2 hs) {
   constexpr int KG = kSparkGroup;
   const uint32_t D = (uint32_t)v.D;
-  const uint64_t it = v.ctl->iteration;
   const uint64_t f = v.f_lo + fl;
   const uint64_t b = f / v.mu, n = f % v.mu;
   const uint32_t cbase = c * kChunk;
   const uint64_t k0 = g * KG;
   const int kn = (int)(v.lam - k0 < (uint64_t)KG ? v.lam - k0 : KG);
   // key prefixes: lanes [0, KG) explode, [KG, 2KG) mapping (hoisted
-  // rng.hpp:43-51 up to field k; each draw is then one splitmix64 round)
-  if (lane < kn)
-    wq.pre[lane] = key_prefix(v.seed, kExplode, it, b, n, k0 + lane);
-  else if (lane >= KG && lane < KG + kn)
-    wq.pre[lane] = key_prefix(v.seed, kMapping, it, b, n, k0 + lane - KG);
+  // rng.hpp:43-51 up to field k; each draw is then one splitmix64 round).
+  // hs = the (seed, stream, iteration) part, computed once per launch.
+  {
+    const bool ex = lane < KG;
+    const int kl = ex ? lane : lane - KG;
+    if (lane < 2 * KG && kl < kn) {
+      uint64_t h = splitmix64((ex ? hs.x : hs.y) ^ b);
+      h = splitmix64(h ^ n);
+      wq.pre[lane] = splitmix64(h ^ (k0 + (uint64_t)kl));
+    }
+  }
   __syncwarp();
   // chunk-constant draws of this chunk; the general keys serve a group with
   // any key near a carry boundary (2^-23 per key and chunk)
@@ -518,6 +531,7 @@ __global__ void __launch_bounds__(256, MINB) k_explode_map(EngineView v) {
   const uint64_t ngrp = (v.lam + KG - 1) / KG;
   const uint64_t nsup = (ngrp + kWarps - 1) / kWarps;  // groups of 8 spark groups
   const uint64_t items = v.Fl * v.nch * nsup;
+  const ulonglong2 hs = explode_stream_prefixes(v);
   for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
     const uint64_t sup = item % nsup, rest = item / nsup;
     const uint32_t c = (uint32_t)(rest % v.nch);
@@ -527,7 +541,7 @@ __global__ void __launch_bounds__(256, MINB) k_explode_map(EngineView v) {
     __syncthreads();
     const uint64_t g = sup * kWarps + warp;
     if (g >= ngrp) continue;  // warp-uniform
-    explode_group<KIND>(v, ch, wq, lane, c, fl, g);
+    explode_group<KIND>(v, ch, wq, lane, c, fl, g, hs);
   }
 }
 
@@ -1707,7 +1721,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_run(EngineView v, uint6
     // explode + mapping + fused fitness partials of firework f (one chunk: D <= kChunk)
     stage_explode_chunk(v, ch, b, 0);
     __syncthreads();
-    for (uint64_t g = warp; g < ngrp; g += kWarps) explode_group<KIND>(w, ch, wqs[warp], lane, 0, f, g);
+    const ulonglong2 hs = explode_stream_prefixes(v);
+    for (uint64_t g = warp; g < ngrp; g += kWarps) explode_group<KIND>(w, ch, wqs[warp], lane, 0, f, g, hs);
     __syncthreads();
     small_a_body(w, f, keys);
     if (SM) {  // write-through of this generation's candidates (host readers)
