@@ -391,10 +391,18 @@ def roofline_entry(name, k, w, pk, pk_kind, workload):
                 "ms_per_launch": k["us"] * 1e-3, "peak_source": f"{pk_kind} bf16 burst (MEASURED_PEAKS.json)"}
     kern = KERNEL_NAMES[name]
     nc = ncu_metrics(kern, workload)
-    return {"kernel": kern, "bound": "hbm", "achieved": k["achieved_GBs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
-            "frac": k["frac"], "traffic": nc["traffic"] if nc else None, "ncu": nc,
-            "algorithmic_per_launch": f"{k['algorithmic_bytes']} bytes", "ms_per_launch": k["us"] * 1e-3,
-            "note": k.get("note"), "peak_source": f"{pk_kind} HBM copy bandwidth (MEASURED_PEAKS.json)"}
+    out = {"kernel": kern, "bound": "hbm", "achieved": k["achieved_GBs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+           "frac": k["frac"], "traffic": nc["traffic"] if nc else None, "ncu": nc,
+           "algorithmic_per_launch": f"{k['algorithmic_bytes']} bytes", "ms_per_launch": k["us"] * 1e-3,
+           "note": k.get("note"), "peak_source": f"{pk_kind} HBM copy bandwidth (MEASURED_PEAKS.json)"}
+    if nc and nc.get("alu_pipe_pct", 0) >= 50:
+        # what actually binds it: the integer ALU pipe (splitmix64 draws), not HBM
+        out["pipe_bound"] = {"pipe": "alu", "frac": nc["alu_pipe_pct"] / 100.0,
+                             "issue_frac": nc.get("issue_active_pct", 0) / 100.0, "source": nc["source"],
+                             "note": "fraction of the ALU pipe's peak instruction rate (ncu "
+                                     "sm__pipe_alu_cycles_active); the kernel issues two splitmix64 rounds "
+                                     "per out-of-box coordinate on 32-bit integer units"}
+    return out
 
 
 def main():
@@ -522,7 +530,8 @@ def main():
                                 "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": ach / pk["hbm_gbs"],
                                 "traffic": None, "share_of_step": 1.0,
                                 "algorithmic_per_launch": f"{byts} bytes per generation (explode + guides + select)",
-                                "note": "latency-bound: one block per firework, grid barriers between the phases; "
+                                "note": "latency-bound: one block per firework (one thread-block cluster), cluster barriers between "
+                                        "the phases; "
                                         "the per-kernel breakdown above times the general (multi-kernel) path",
                                 "peak_source": f"{pk_kind} HBM copy bandwidth (MEASURED_PEAKS.json)"}
     except Exception as ex:
