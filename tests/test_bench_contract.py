@@ -59,3 +59,19 @@ def test_gpu_arm_json_line(workload):
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
     e = d["e2e"]
     assert e["value"] > 0 and set(e) >= {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"}
+
+
+@pytest.mark.skipif(not os.path.exists(REF_SO), reason="oracle/_ref not built (make -C oracle ref)")
+def test_gpus_n_self_launches_local_ranks():
+    """`bench.py --gpus 2` outside torchrun starts 2 local ranks itself
+    (torch.distributed.run on 127.0.0.1); rank 0 alone prints the line."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR",
+                                                             "MASTER_PORT")}
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2", "--workload", "c1",
+                          "--steps", "1", "--warmup", "3"], cwd=ROOT, capture_output=True, text=True, timeout=600,
+                         env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0
