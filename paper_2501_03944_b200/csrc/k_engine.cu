@@ -763,10 +763,13 @@ __device__ __forceinline__ void store_guide(const EngineView& v, uint64_t off, c
 #define GUIDES_WARPS 8  // warps per k_guides block (one 32 * GUIDES_VEC-coordinate slice each)
 #endif
 constexpr int kGuideWarps = GUIDES_WARPS;
+// U: rank pairs per unrolled load step (2U independent V-wide loads per
+// lane in flight): 30 when top <= 64 (C2: top = 60 in two load rounds,
+// 27.2 -> 25.7 us), else 16 (20 measured slower on both C2 and C5).
+template <int U>
 __global__ void __launch_bounds__(kGuideWarps * 32) k_guides(EngineView v) {
   constexpr int V = GUIDES_VEC;
   using VT = typename VecT<V>::T;
-  constexpr int U = 32 / V;  // rank pairs per unrolled step (2U independent V-wide loads per lane)
   pdl_enter();
   if (gen_inactive(v)) return;
   extern __shared__ uint64_t s_pre[];  // [M] kGuide key prefixes, then [2*top] rank lists
@@ -1944,6 +1947,13 @@ void launch_key_hash(const uint64_t* keys, uint64_t n, uint64_t* out,
 
 static size_t guides_smem(const EngineView& v) { return v.M * sizeof(uint64_t) + 2 * v.top * sizeof(int); }
 
+static unsigned guide_blocks(const EngineView& v, int nsm);
+static void launch_guides_k(const EngineView& v, int nsm, cudaStream_t s) {
+  if (v.top <= 64)
+    pdl_launch(k_guides<30>, guide_blocks(v, nsm), kGuideWarps * 32, guides_smem(v), s, v);
+  else
+    pdl_launch(k_guides<16>, guide_blocks(v, nsm), kGuideWarps * 32, guides_smem(v), s, v);
+}
 static unsigned guide_blocks(const EngineView& v, int nsm) {
   const uint64_t nsl = (v.D + 32 * GUIDES_VEC - 1) / (32 * GUIDES_VEC);
   const uint64_t blocks = v.Fl * ((nsl + kGuideWarps - 1) / kGuideWarps);
@@ -1992,7 +2002,7 @@ void launch_generation_kernels(const EngineView& v, int nsm, cudaStream_t s,
     }
     pdl_launch(k_rank, (unsigned)v.Fl, kRankThreads, rank_smem(v), s, v);
     if (v.M > 0) {
-      pdl_launch(k_guides, guide_blocks(v, nsm), kGuideWarps * 32, guides_smem(v), s, v);
+      launch_guides_k(v, nsm, s);
       if (v.nn)
         hooks->eval_guides(hooks->ctx, s);
       else
@@ -2056,7 +2066,7 @@ void launch_rank(const EngineView& v, cudaStream_t s) {
   pdl_launch(k_rank, (unsigned)v.Fl, kRankThreads, rank_smem(v), s, v);
 }
 void launch_guides(const EngineView& v, int nsm, cudaStream_t s) {
-  pdl_launch(k_guides, guide_blocks(v, nsm), kGuideWarps * 32, guides_smem(v), s, v);
+  launch_guides_k(v, nsm, s);
   if (!v.nn) launch_analytic_partials(v.guides, v.Fl * v.M, v.D, v.Dp, v.nch, v.obj_kind, v.gpart, nsm, s);
 }
 void launch_select(const EngineView& v, int nsm, cudaStream_t s) {
