@@ -309,14 +309,13 @@ constexpr size_t kExplodeSmem = sizeof(ExplodeChunk) + kWarps * sizeof(ExplodeWa
 // group exists and the slice lies inside [0, D) (no per-element guards).
 // CHUNK: draws from the chunk-constant form (ck, every key of the group
 // `fast` in this chunk); otherwise from the general draw keys (pe, pm).
-template <int KIND, bool FULL, bool CHUNK>
+template <int KIND, bool FULL, bool CHUNK, int KG = kSparkGroup>
 __device__ __forceinline__ void explode_slice(const EngineView& v, const ExplodeChunk& ch,
                                               int lane, uint32_t cbase, uint32_t qoff,
                                               uint64_t f, uint64_t k0, int kn, double a,
                                               const DrawKey* pe, const DrawKey* pm,
                                               const ChunkDraw* ck, uint32_t one,
-                                              float (&s0)[kSparkGroup], float (&s1)[kSparkGroup]) {
-  constexpr int KG = kSparkGroup;
+                                              float (&s0)[KG], float (&s1)[KG]) {
   const uint32_t D = (uint32_t)v.D;
   const uint32_t li0 = qoff + lane * 4;  // index inside the staged chunk
   const uint32_t d0 = cbase + li0;
@@ -371,7 +370,7 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
       const double pw[4] = {pw01.x, pw01.y, pw23.x, pw23.y};
       MixState zm[4];
       if constexpr (CHUNK) {
-        const ChunkDraw& kc = ck[kSparkGroup + kk];
+        const ChunkDraw& kc = ck[KG + kk];
         const uint32_t tj = chunk_slice(kc, li0);
 #pragma unroll
         for (int e = 0; e < 4; ++e) zm[e] = mix_chunk_k(kc, kc.qe[e] + tj, one);
@@ -411,11 +410,11 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
 
 // One warp: spark group g (kSparkGroup sparks) of local firework fl over the
 // staged chunk c (box images + population range of the firework's batch).
-template <int KIND>
+template <int KIND, int KG = kSparkGroup>
 __device__ __forceinline__ void explode_group(const EngineView& v, const ExplodeChunk& ch,
                                               ExplodeWarp& wq, int lane, uint32_t c, uint64_t fl,
                                               uint64_t g, ulonglong2 hs) {
-  constexpr int KG = kSparkGroup;
+  static_assert(KG <= kSparkGroup, "ExplodeWarp holds kSparkGroup keys per stream");
   const uint32_t D = (uint32_t)v.D;
   const uint64_t f = v.f_lo + fl;
   const uint64_t b = f / v.mu, n = f % v.mu;
@@ -467,11 +466,11 @@ __device__ __forceinline__ void explode_group(const EngineView& v, const Explode
     const uint32_t qoff = q * 128;
     if (cbase + qoff >= D) break;  // warp-uniform
     if (!fast)
-      explode_slice<KIND, false, false>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, wq.ck, one, s0, s1);
+      explode_slice<KIND, false, false, KG>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, wq.ck, one, s0, s1);
     else if (kn == KG && cbase + qoff + 128 <= D)
-      explode_slice<KIND, true, true>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, wq.ck, one, s0, s1);
+      explode_slice<KIND, true, true, KG>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, wq.ck, one, s0, s1);
     else
-      explode_slice<KIND, false, true>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, wq.ck, one, s0, s1);
+      explode_slice<KIND, false, true, KG>(v, ch, lane, cbase, qoff, f, k0, kn, a, pe, pm, wq.ck, one, s0, s1);
   }
 #if EXPLODE_SMEM_KEYS
   __syncwarp();  // wq.keys are reused by this warp's next group
@@ -1698,16 +1697,26 @@ __device__ __forceinline__ void copy_words(float* dst, const float* src, uint64_
   for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 
+// Block size and explode spark-group size of the small-problem loop (256 / 4
+// measured best on C1: 512 / 1 18.6, 256 / 2 17.3, 1024 / 1 20.9 vs 17.0 us).
+#ifndef SMALL_RUN_KG
+#define SMALL_RUN_KG 4
+#endif
+#ifndef SMALL_RUN_THREADS
+#define SMALL_RUN_THREADS 256
+#endif
+constexpr int kSmallRunThreads = SMALL_RUN_THREADS;
+constexpr int kSmallRunWarps = kSmallRunThreads / 32;
+
 template <int KIND, bool CL, bool SM>
-__global__ void __launch_bounds__(kSmallThreads) k_small_run(EngineView v, uint64_t max_gens) {
+__global__ void __launch_bounds__(kSmallRunThreads) k_small_run(EngineView v, uint64_t max_gens) {
   extern __shared__ __align__(16) uint8_t run_smem[];
   ExplodeChunk& ch = *reinterpret_cast<ExplodeChunk*>(run_smem);
   ExplodeWarp* wqs = reinterpret_cast<ExplodeWarp*>(run_smem + sizeof(ExplodeChunk));
   uint64_t* keys =
-      reinterpret_cast<uint64_t*>(run_smem + sizeof(ExplodeChunk) + kWarps * sizeof(ExplodeWarp));
+      reinterpret_cast<uint64_t*>(run_smem + sizeof(ExplodeChunk) + kSmallRunWarps * sizeof(ExplodeWarp));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t f = blockIdx.x, b = f / v.mu;
-  const uint64_t ngrp = (v.lam + kSparkGroup - 1) / kSparkGroup;
   EngineView w = v;  // SM: the phases' view of this block's candidates
   if (SM) {
     uint8_t* cb = reinterpret_cast<uint8_t*>(keys + ((v.lam + 1) & ~1ull));
@@ -1725,7 +1734,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_run(EngineView v, uint6
     stage_explode_chunk(v, ch, b, 0);
     __syncthreads();
     const ulonglong2 hs = explode_stream_prefixes(v);
-    for (uint64_t g = warp; g < ngrp; g += kWarps) explode_group<KIND>(w, ch, wqs[warp], lane, 0, f, g, hs);
+    constexpr int KGS = SMALL_RUN_KG;  // sparks per warp group
+    for (uint64_t g = warp; g * KGS < v.lam; g += kSmallRunWarps)
+      explode_group<KIND, KGS>(w, ch, wqs[warp], lane, 0, f, g, hs);
     __syncthreads();
     small_a_body(w, f, keys);
     if (SM) {  // write-through of this generation's candidates (host readers)
@@ -1755,7 +1766,7 @@ bool small_run_ok(const EngineView& v, int nsm) {
 }
 
 static size_t small_run_smem(const EngineView& v, bool sm) {
-  return sizeof(ExplodeChunk) + kWarps * sizeof(ExplodeWarp) + ((v.lam + 1) & ~1ull) * sizeof(uint64_t) +
+  return sizeof(ExplodeChunk) + kSmallRunWarps * sizeof(ExplodeWarp) + ((v.lam + 1) & ~1ull) * sizeof(uint64_t) +
          (sm ? small_smem_layout(v).total : 0);
 }
 #ifndef SMALL_SMEM
@@ -1771,7 +1782,7 @@ cudaError_t launch_small_run(const EngineView& v, uint64_t max_gens, cudaStream_
   const bool sm = cl && SMALL_SMEM && small_run_smem(v, true) <= kSmallSmemMax;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)v.F);
-  cfg.blockDim = dim3(kSmallThreads);
+  cfg.blockDim = dim3(kSmallRunThreads);
   cfg.dynamicSmemBytes = small_run_smem(v, sm);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -1787,11 +1798,10 @@ cudaError_t launch_small_run(const EngineView& v, uint64_t max_gens, cudaStream_
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   auto go = [&](auto kern) -> cudaError_t {
-    if (cfg.dynamicSmemBytes > 48 * 1024) {
-      const cudaError_t e =
-          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes);
-      if (e != cudaSuccess) return e;
-    }
+    // (the default dynamic limit is 48 KB minus the kernel's static shared memory)
+    const cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes);
+    if (e != cudaSuccess) return e;
     return cudaLaunchKernelEx(&cfg, kern, v, max_gens);
   };
   switch (v.obj_kind) {
