@@ -394,6 +394,10 @@ struct Workspace {
     v.D = D;
     v.Dp = round_up(D, 64);
     v.top = c.M > 0 ? c.top() : 0;
+    {
+      const char* eg = getenv("MGFWA_EXPLODE_GENERAL");  // test switch, engine_view.cuh
+      v.explode_general = eg != nullptr && eg[0] == '1';
+    }
     v.F = c.B * c.mu;
     if (world == 0 || v.F % world != 0)
       return invalid("mgfwa_b200: batches * fireworks must be divisible by the number of ranks");

@@ -116,6 +116,10 @@ struct EngineView {
   int injected_fitness;
   int has_iters_override;
   double iters_override;
+  // test switch (MGFWA_EXPLODE_GENERAL=1): every explode draw through the
+  // general key form (mix_draw), never the chunk-constant one (chunk_draw),
+  // so the parity tests reach the path a near-carry chunk takes
+  int explode_general;
 };
 
 }  // namespace mgfwa_b200

@@ -441,7 +441,7 @@ __device__ __forceinline__ void explode_group(const EngineView& v, const Explode
     wq.ck[lane] = chunk_draw(wq.pre[lane], cbase);
     fast_key = chunk_fast(wq.ck[lane]);
   }
-  const bool fast = __all_sync(0xffffffffu, fast_key);
+  const bool fast = __all_sync(0xffffffffu, fast_key) && !v.explode_general;
 #if EXPLODE_SMEM_KEYS
   if (lane < 2 * KG) wq.keys[lane] = draw_key(wq.pre[lane]);
   __syncwarp();

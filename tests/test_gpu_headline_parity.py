@@ -206,6 +206,25 @@ def test_generation_steps_match_reference_at_headline_shape(P, ref, name, amp):
         eng.close()
 
 
+def test_general_draw_path_matches_reference():
+    """The explode kernel draws through the chunk-constant form (chunk_draw)
+    unless a (key, 512-coordinate chunk) lies within 512 of a carry into the
+    mixer's high word (probability 2^-23), which then takes the general form
+    (mix_draw).  MGFWA_EXPLODE_GENERAL=1 forces the general form everywhere;
+    the headline-shape checks (C2 MLP with the bf16 shadow, C4 Rastrigin with
+    the fused fitness, both with heavy random mapping) must stay exact."""
+    import subprocess
+    import sys
+
+    env = dict(os.environ, MGFWA_EXPLODE_GENERAL="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                          "tests/test_gpu_headline_parity.py", "-k",
+                          "generation_steps and default and (c2_mlp or c4_rastrigin)"],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0 and "2 passed" in out.stdout, out.stdout[-3000:] + out.stderr[-2000:]
+
+
 # ------------------------------------------------ 10-seed final best (north_star)
 FINALS = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "finals.npz")
 
