@@ -66,6 +66,9 @@ constexpr bool kL2Warp = MLP_L2_WARP != 0;
 #ifndef MLP_L2_PREFETCH
 #define MLP_L2_PREFETCH 0  // 1: TMA L2 prefetch of the next N tile's W1 (measured slower: C2 fitness 90.3 -> 93.7 us cold)
 #endif
+#ifndef MLP_CG2_STAGES
+#define MLP_CG2_STAGES 6
+#endif
 #ifndef MLP_PROBE
 #define MLP_PROBE 0  // 1: profiling probe, TMA + layer-1 MMA pipeline only (no epilogue math)
 #endif
@@ -79,7 +82,7 @@ struct Cfg {
   static constexpr int kBRows = BNT / CG;                // B rows staged per CTA
   static constexpr int kBBytes = kBRows * BK * 2;        // 32 KB | 16 KB (BNT = 256)
   static constexpr int kStageBytes = kABytes + kBBytes;  // 48 KB | 32 KB
-  static constexpr int kStages = CG == 2 ? 6 : BNT < BN ? 6 : MLP_STAGES;
+  static constexpr int kStages = CG == 2 ? MLP_CG2_STAGES : BNT < BN ? 6 : MLP_STAGES;
   static constexpr int kO2 = 16 / CG;                    // layer-2 B rows (outputs) per CTA
 };
 constexpr int kThreads = 384;
