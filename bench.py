@@ -526,7 +526,7 @@ def main():
             byts = sum(kb[k]["algorithmic_bytes"] for k in ("explode", "guides", "select"))
             ach = byts / (ms_max / args.steps * 1e-3) / 1e9
             line["dominant_kernel"] = "k_small_run"
-            line["roofline"] = {"kernel": "k_small_run (persistent cooperative whole-loop kernel)", "bound": "hbm",
+            line["roofline"] = {"kernel": "k_small_run (persistent whole-loop kernel, one thread-block cluster)", "bound": "hbm",
                                 "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": ach / pk["hbm_gbs"],
                                 "traffic": None, "share_of_step": 1.0,
                                 "algorithmic_per_launch": f"{byts} bytes per generation (explode + guides + select)",
