@@ -156,3 +156,14 @@ def test_dataset_labels_are_balanced(oracle):
     assert np.all(X * 256 == np.floor(X * 256))  # 8-bit pixels (exact in bf16)
     counts = np.bincount(y, minlength=10)
     assert counts.min() > 0
+
+
+@pytest.mark.skipif(not os.path.exists(O.REF_SO), reason="oracle/_ref not built (make -C oracle ref)")
+def test_net_objective_checker_is_the_compiled_reference():
+    """The paper's benchmark nets are checked against the compiled reference's
+    MlpBlackBox (nets.cpp:138-167): the C restatement has no net objective
+    (NaN), so smoke() and the GPU tests must use oracle.Reference for them."""
+    xs = np.linspace(-3, 3, 10)
+    d = O.ObjectiveDesc(kind=O.OBJ_NET, net_id=1, weight_seed=1)
+    assert np.isfinite(O.Reference().evaluate(d, xs))
+    assert np.isnan(O.Oracle().evaluate(d, xs))
