@@ -556,28 +556,44 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int jj = 0; jj < JN; ++jj)
         if (jj < jn) tmem_ld16_nowait(cb + d2_col<H>(jb + jj), z[jj]);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      // CE of the thread's JN logit blocks as JN interleaved chains (max, exp
+      // sums, log, then the warp butterflies stage by stage), the same
+      // operation order per block as one block at a time
+      float loss[JN];
 #pragma unroll
-      for (int jj = 0; jj < JN; ++jj) {
-        const int j = jb + jj;
-        float loss = 0.0f;
-        if (valid && jj < jn) {
-          float mx = -INFINITY;
+      for (int jj = 0; jj < JN; ++jj) loss[jj] = 0.0f;
+      if (valid && jn > 0) {  // jn: warp-uniform (0 only for the second half when H > 128)
+        float mx[JN], se[JN], zl[JN];
+#pragma unroll
+        for (int jj = 0; jj < JN; ++jj) {
+          mx[jj] = -INFINITY;
 #pragma unroll
           for (int o = 0; o < kMaxO; ++o) {
-            z[jj][o] += s_b2[j * kN2 + o];
-            if ((uint32_t)o < O) mx = fmaxf(mx, z[jj][o]);
+            z[jj][o] += s_b2[(jb + jj) * kN2 + o];
+            if ((uint32_t)o < O) mx[jj] = fmaxf(mx[jj], z[jj][o]);
           }
-          float se = 0.0f, zl = 0.0f;
-#pragma unroll
-          for (int o = 0; o < kMaxO; ++o) {
-            if ((uint32_t)o < O) se += MLP_EXPF(z[jj][o] - mx);
-            if (o == label) zl = z[jj][o];
-          }
-          loss = (mx + MLP_LOGF(se)) - zl;
         }
-        loss = warp_sum(loss);
-        if (lane == 0 && jj < jn) s_red[e * 8 + jj] = loss;
+#pragma unroll
+        for (int jj = 0; jj < JN; ++jj) {
+          se[jj] = 0.0f;
+          zl[jj] = 0.0f;
+#pragma unroll
+          for (int o = 0; o < kMaxO; ++o) {
+            if ((uint32_t)o < O) se[jj] += MLP_EXPF(z[jj][o] - mx[jj]);
+            if (o == label) zl[jj] = z[jj][o];
+          }
+        }
+#pragma unroll
+        for (int jj = 0; jj < JN; ++jj) loss[jj] = (mx[jj] + MLP_LOGF(se[jj])) - zl[jj];
       }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int jj = 0; jj < JN; ++jj) loss[jj] += __shfl_xor_sync(0xffffffffu, loss[jj], off);
+      if (lane == 0)
+#pragma unroll
+        for (int jj = 0; jj < JN; ++jj)
+          if (jj < jn) s_red[e * 8 + jj] = loss[jj];
       // tile buffer consumed: hand it back to the MMA warp
       tc_fence_before();
       __syncwarp();
