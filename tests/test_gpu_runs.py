@@ -178,3 +178,36 @@ def test_nn_run_no_guides_odd_lambda(P, obj_name):
     assert r.iterations == 6 and np.all(np.diff(r.trace_best, axis=1) <= 0)
     fit, _ = P.batched_apply(obj, r.best_position)
     assert np.array_equal(fit, r.best_fitness)
+
+
+@pytest.mark.parametrize("batches,mu", [(1, 5), (2, 3), (2, 4)])
+def test_cluster_loop_matches_graph_path(batches, mu, tmp_path):
+    """The small-problem loop (one thread-block cluster per launch, F <= 8,
+    candidates resident in shared memory) and the graph-replayed general
+    kernels (MGFWA_SMALL_RUN=0) give the same run bit for bit, with one and
+    with several batches (the cross-block completion path)."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, paper_2501_03944_b200 as P\n"
+        f"cfg = P.MgfwaConfig(batches={batches}, fireworks={mu}, sparks_per_firework=10, guides_per_firework=2,\n"
+        "                    boosts=[1.0, 2.0], guide_fraction=0.2, max_evaluations=3000)\n"
+        "out = {}\n"
+        "for name, obj in (('sphere', P.Sphere()), ('rastrigin', P.Rastrigin())):\n"
+        "    r = P.run(cfg, P.SearchSpace.box(17, -5.0, 5.0), obj, 9)\n"
+        "    out[name + '_best'] = r.best_fitness\n"
+        "    out[name + '_pos'] = r.best_position\n"
+        "    out[name + '_trace'] = r.trace_best\n"
+        "    out[name + '_cnt'] = np.array([r.evaluations_used, r.iterations, r.losers_reinitialized])\n"
+        "import os; np.savez(os.environ['OUT'], **out)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for small in ("1", "0"):
+        out = str(tmp_path / f"r{small}.npz")
+        env = dict(os.environ, MGFWA_SMALL_RUN=small, OUT=out)
+        subprocess.run([sys.executable, "-c", code], env=env, cwd=root, check=True, timeout=300)
+        res.append(np.load(out))
+    for k in res[0].files:
+        assert np.array_equal(res[0][k], res[1][k]), k
