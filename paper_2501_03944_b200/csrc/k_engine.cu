@@ -1812,17 +1812,34 @@ cudaError_t launch_small_run(const EngineView& v, uint64_t max_gens, cudaStream_
     if (e != cudaSuccess) return e;
     return cudaLaunchKernelEx(&cfg, kern, v, max_gens);
   };
+  cudaError_t e;
   switch (v.obj_kind) {
     case OBJ_SPHERE:
-      return sm ? go(k_small_run<OBJ_SPHERE, true, true>)
-                : cl ? go(k_small_run<OBJ_SPHERE, true, false>) : go(k_small_run<OBJ_SPHERE, false, false>);
+      e = sm ? go(k_small_run<OBJ_SPHERE, true, true>)
+             : cl ? go(k_small_run<OBJ_SPHERE, true, false>) : go(k_small_run<OBJ_SPHERE, false, false>);
+      break;
     case OBJ_RASTRIGIN:
-      return sm ? go(k_small_run<OBJ_RASTRIGIN, true, true>)
-                : cl ? go(k_small_run<OBJ_RASTRIGIN, true, false>) : go(k_small_run<OBJ_RASTRIGIN, false, false>);
+      e = sm ? go(k_small_run<OBJ_RASTRIGIN, true, true>)
+             : cl ? go(k_small_run<OBJ_RASTRIGIN, true, false>) : go(k_small_run<OBJ_RASTRIGIN, false, false>);
+      break;
     default:
-      return sm ? go(k_small_run<OBJ_ACKLEY, true, true>)
-                : cl ? go(k_small_run<OBJ_ACKLEY, true, false>) : go(k_small_run<OBJ_ACKLEY, false, false>);
+      e = sm ? go(k_small_run<OBJ_ACKLEY, true, true>)
+             : cl ? go(k_small_run<OBJ_ACKLEY, true, false>) : go(k_small_run<OBJ_ACKLEY, false, false>);
+      break;
   }
+  if (e != cudaSuccess && cl) {
+    // a cluster this size cannot be scheduled here: the cooperative grid form
+    (void)cudaGetLastError();
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.dynamicSmemBytes = small_run_smem(v, false);
+    switch (v.obj_kind) {
+      case OBJ_SPHERE: e = go(k_small_run<OBJ_SPHERE, false, false>); break;
+      case OBJ_RASTRIGIN: e = go(k_small_run<OBJ_RASTRIGIN, false, false>); break;
+      default: e = go(k_small_run<OBJ_ACKLEY, false, false>); break;
+    }
+  }
+  return e;
 }
 
 static bool small_path_disabled() {  // MGFWA_SMALL_PATH=0: always the general kernels
