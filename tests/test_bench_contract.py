@@ -56,6 +56,9 @@ def test_gpu_arm_json_line(workload):
     r = d["roofline"]
     assert set(r) >= {"bound", "achieved", "peak", "unit", "frac", "traffic"} and 0 < r["frac"] < 1.5
     assert r["bound"] in ("hbm", "tensor")
+    if workload == "c2":  # the explode kernel dominates; its binding pipe is reported beside HBM
+        assert r["kernel"] == "k_explode_map" and 0 < r["pipe_bound"]["frac"] <= 1.0
+        assert 0 < d["roofline_tensor"]["frac"] < 1.0
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
     e = d["e2e"]
     assert e["value"] > 0 and set(e) >= {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"}
