@@ -231,20 +231,34 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+// sin^2(pi x): period 1, even, so with r = x - rint(x) in [-1/2, 1/2] it is
+// (r P(r^2))^2 with P the degree-4 minimax fit of sin(pi r) / r (relative
+// error 5e-9 in exact arithmetic, 1.8e-7 evaluated in fp32) — no quadrant
+// logic, 7 FMA-pipe instructions instead of sinpif's ~25 (C4 explode).
+__device__ __forceinline__ float sin_pi_sq(float x) {
+  const float r = x - rintf(x);
+  const float t = r * r;
+  float p = fmaf(t, 0.07756161404419515f, -0.5982427027694103f);
+  p = fmaf(t, p, 2.5500698108736963f);
+  p = fmaf(t, p, -5.167709688780585f);
+  p = fmaf(t, p, 3.141592636925161f);
+  const float s = r * p;
+  return s * s;
+}
+
 // Per-coordinate analytic terms; partial sums are fp32.
 //   sphere     : x^2                                   (nets.cpp:80-84)
 //   rastrigin  : x^2 + 20 sin^2(pi x)   == x^2 - 10 cos(2 pi x) + 10
-//   ackley     : (x^2, cos 2 pi x)  two sums
+//   ackley     : (x^2, cos 2 pi x = 1 - 2 sin^2(pi x))  two sums
 __device__ __forceinline__ void analytic_terms(int kind, float x, float& s0,
                                                float& s1) {
   if (kind == OBJ_SPHERE) {
     s0 = fmaf(x, x, s0);
   } else if (kind == OBJ_RASTRIGIN) {
-    const float s = sinpif(x);
-    s0 += fmaf(x, x, 20.0f * s * s);
+    s0 += fmaf(x, x, 20.0f * sin_pi_sq(x));
   } else {  // ackley
     s0 = fmaf(x, x, s0);
-    s1 += cospif(2.0f * x);
+    s1 += fmaf(-2.0f, sin_pi_sq(x), 1.0f);
   }
 }
 
