@@ -46,6 +46,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <new>
 
 #include "common.cuh"
@@ -990,9 +991,324 @@ __global__ void __launch_bounds__(kFThreads, 1) k_lenet_fused(LenetArgs args,
   tmem_free512(tmem);
 }
 
+// ============================================================ conv1 on tcgen05
+// k_lenet_conv_tc (default conv stage of the split path) — conv1 of a group
+// of kCtG = 12 candidates as ONE tcgen05 GEMM per sample, conv2 per
+// candidate on the warp MMA, pooled conv2 rows -> the scratch (same K' rows
+// as k_lenet_conv, so k_lenet_fc_tc is unchanged).
+//
+// conv1 is transposed so that the shared operand is the image:
+//   D[(candidate, channel), pixel] = A[(candidate, channel), k] . B[pixel, k]
+//   M = 128 rows (72 used: row 32 q + j, q = 1..3, j < 24, is (candidate,
+//       channel) = divmod(24 (q - 1) + j, 6); lane quarter 0 is empty, so
+//       three epilogue warps cover the live rows),
+//   K = 48 = 6 chunks of 8: chunk ky holds taps kx = 0..4, two zero taps and
+//       a constant-1 tap (k = 7) that carries the bias in chunk 0,
+//   N = 64 per MMA block = the two output pixel rows of one pooled row, 32
+//       pixel slots each (28 used).
+// The B operand is a "row-window" image precomputed once per plan:
+// R[s][Y][X] = 16 bytes = (p[Y][X .. X+4], 0, 0, 1) with p the zero-padded
+// 32 x 32 image.  In the no-swizzle K-major layout (8-row x 16-byte core
+// matrices) the 8 pixels x0 .. x0+7 of one row are 128 contiguous bytes, the
+// next 8 pixels follow (SBO = 128), and the next tap row ky + 1 is the next
+// image row (LBO = 512 bytes): an implicit im2col with no replication beyond
+// the 8-tap window, 16.9 KB per sample, one bulk copy.
+// D blocks (128 lanes x 64 columns) cycle through 8 TMEM slots; a thread of
+// the epilogue owns one (candidate, channel) row, so the 2 x 2 average pool
+// (weights and bias pre-scaled by 1/4: a sum of four ReLUs) is in registers:
+// column dy * 32 + x of the block.  Pooled rows land in the candidate's conv1
+// map in shared memory (the k_lenet_conv layout), double-buffered per sample,
+// and conv2_tiles (unchanged) consumes them: one warp per candidate with its
+// conv2 B fragments in registers, loaded straight from the candidate row.
+//
+// Warps (16, i.e. 4 per SM sub-partition, 128 registers): 0 = control
+// (row-window bulk copies, conv1 A staging per group, lane 0 issues the
+// MMAs), 1..3 = TMEM epilogue (lane quarter = warp), 4..15 = conv2.  Work = the (group, sample) units of the launch, split into equal
+// contiguous ranges per CTA (group changes restage A and the fragments).
+namespace {
+
+constexpr int kCtG = 12;                               // candidates per conv1 GEMM
+#ifndef LENET_CT_C2T
+#define LENET_CT_C2T 2
+#endif
+constexpr int kCtC2T = LENET_CT_C2T;                   // conv2 tiles in flight per warp
+constexpr int kRwRows = 33, kRwPitch = 32;             // row windows: [Y][X] x 16 B
+constexpr int kRwBytes = kRwRows * kRwPitch * 16;      // 16,896 B per sample
+constexpr int kCtA = 128 * 48 * 2;                     // conv1 A: 128 x 48 bf16
+constexpr int kCtSlots = 8;                            // TMEM: 8 x 64 columns
+constexpr int kCtWarps = 1 + 3 + kCtG;
+constexpr int kCtThreads = kCtWarps * 32;
+struct CtSmem {
+  static constexpr int a = 0;                                   // 2 x conv1 A (group parity)
+  static constexpr int rw = a + 2 * kCtA;                       // 2 x row windows (sample parity)
+  static constexpr int p1 = rw + 2 * kRwBytes;                  // 2 x kCtG conv1 maps
+  static constexpr int o = p1 + 2 * kCtG * kP1Words * 4;        // per conv2 warp: [416] bf16
+  static constexpr int bar = o + kCtG * kP2Row * 2;             // mbarriers
+  // a_full[2] a_empty[2] rw_full[2] rw_empty[2] t_full[8] t_empty[8] p_full[2] p_empty[2]
+  static constexpr int nbar = 28;
+  static constexpr int slot = bar + nbar * 8;
+  static constexpr int total = slot + 16;
+};
+static_assert(CtSmem::total <= 227 * 1024 && CtSmem::rw % 16 == 0 && CtSmem::o % 16 == 0 &&
+                  CtSmem::bar % 8 == 0,
+              "LeNet tcgen05 conv shared memory");
+enum { kBaFull = 0, kBaEmpty = 2, kBrFull = 4, kBrEmpty = 6, kBtFull = 8, kBtEmpty = 16, kBpFull = 24, kBpEmpty = 26 };
+
+// (candidate, channel) of conv1 GEMM row r, or -1 for a padding row
+__host__ __device__ constexpr int ct_row_cc(int r) {
+  return (r >> 5) > 0 && (r & 31) < 24 ? 24 * ((r >> 5) - 1) + (r & 31) : -1;
+}
+
+struct LenetCtArgs {
+  LenetSplitArgs sa;
+  const uint8_t* rwin;  // [S][kRwBytes] row-window images
+  uint64_t ngroups;     // ceil(rows / kCtG)
+};
+
+// conv2 B fragments of candidate row w (the k_lenet_conv staging order,
+// conv2_k, read straight from the row; weights pre-scaled by 1/4, exact)
+__device__ __forceinline__ void load_conv2_frags(const __nv_bfloat16* w, int g, int c, uint32_t (&bw2)[13][2][2],
+                                                 float& b2a, float& b2b, float& b2c, float& b2d) {
+  auto wv = [&](int ch, int ci, int tap) -> float {
+    return (ci < 6 && tap >= 0) ? 0.25f * bf(w[oC2W + ch * 150 + ci * 25 + tap]) : 0.f;
+  };
+#pragma unroll
+  for (int st = 0; st < 13; ++st) {
+    int ta, tb;
+    if (st < 10) {
+      const int kx = st >> 1, h = st & 1;
+      ta = (2 * h) * 5 + kx, tb = (2 * h + 1) * 5 + kx;
+    } else {
+      const int j = st - 10;
+      ta = 20 + 2 * j, tb = 2 * j + 1 < 5 ? 21 + 2 * j : -1;
+    }
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+      const int ch = 8 * n + g;
+      bw2[st][n][0] = pack_bf16(wv(ch, 2 * c, ta), wv(ch, 2 * c + 1, ta));
+      bw2[st][n][1] = pack_bf16(wv(ch, 2 * c, tb), wv(ch, 2 * c + 1, tb));
+    }
+  }
+  b2a = 0.25f * bf(w[oC2B + 2 * c]), b2b = 0.25f * bf(w[oC2B + 2 * c + 1]);
+  b2c = 0.25f * bf(w[oC2B + 8 + 2 * c]), b2d = 0.25f * bf(w[oC2B + 9 + 2 * c]);
+}
+
+}  // namespace
+
+// Row-window images of the dataset (see k_lenet_conv_tc): R[s][Y][X] =
+// (p[Y][X + e], e < 5; 0; 0; 1) with p[Y][X] = x[s][Y - 2][X - 2] (0 outside).
+__global__ void k_lenet_rowwin(const __nv_bfloat16* X, uint32_t S, uint4* R) {
+  const uint64_t n = (uint64_t)S * kRwRows * kRwPitch;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = i / (kRwRows * kRwPitch);
+    const int r = (int)(i % (kRwRows * kRwPitch)), Y = r / kRwPitch, Xc = r % kRwPitch;
+    const __nv_bfloat16* img = X + s * 784;
+    uint16_t v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int yy = Y - 2, xx = Xc + e - 2;
+      __nv_bfloat16 t = __float2bfloat16(e == 7 ? 1.0f : 0.0f);
+      if (e < 5 && yy >= 0 && yy < 28 && xx >= 0 && xx < 28) t = img[yy * 28 + xx];
+      v[e] = *reinterpret_cast<uint16_t*>(&t);
+    }
+    R[i] = make_uint4(v[0] | (uint32_t)v[1] << 16, v[2] | (uint32_t)v[3] << 16, v[4] | (uint32_t)v[5] << 16,
+                      v[6] | (uint32_t)v[7] << 16);
+  }
+}
+
+__global__ void __launch_bounds__(kCtThreads, 1) k_lenet_conv_tc(LenetCtArgs ca) {
+  using namespace tc;
+  pdl_enter();
+  const LenetSplitArgs& sa = ca.sa;
+  const LenetArgs& args = sa.base;
+  if (args.gate != nullptr && *args.gate == 0) return;
+  extern __shared__ __align__(1024) uint8_t smem_ct[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t base_s = smem_u32(smem_ct);
+  const uint32_t bars = base_s + CtSmem::bar;
+  auto bar = [&](int i) -> uint32_t { return bars + 8u * (uint32_t)i; };
+  {
+    uint32_t* p = reinterpret_cast<uint32_t*>(smem_ct);
+    for (int i = threadIdx.x; i < CtSmem::bar / 4; i += kCtThreads) p[i] = 0u;
+    async_smem_fence();  // the zero padding of the A operands is read by the tensor core
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(kBaFull + i), 32);
+      mbar_init(bar(kBaEmpty + i), 1);
+      mbar_init(bar(kBrFull + i), 1);
+      mbar_init(bar(kBrEmpty + i), 1);
+      mbar_init(bar(kBpFull + i), 3 * 32);
+      mbar_init(bar(kBpEmpty + i), kCtG * 32);
+    }
+    for (int i = 0; i < kCtSlots; ++i) {
+      mbar_init(bar(kBtFull + i), 1);
+      mbar_init(bar(kBtEmpty + i), 3 * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const uint32_t tmem = tmem_alloc512(reinterpret_cast<uint32_t*>(smem_ct + CtSmem::slot));
+
+  const uint64_t S = args.S;
+  const uint64_t U = ca.ngroups * S;
+  const uint64_t u0 = U * blockIdx.x / gridDim.x, u1 = U * (blockIdx.x + 1) / gridDim.x;
+  const uint64_t n = u1 - u0;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------- control: loads + conv1 MMAs
+    constexpr uint32_t id = idesc_bf16(128, 64);
+    auto load_rw = [&](uint64_t i) {  // lane 0: row windows of unit i -> buffer i & 1
+      const uint32_t b = (uint32_t)(i & 1);
+      mbar_wait(bar(kBrEmpty + b), (uint32_t)((i >> 1) & 1) ^ 1);
+      mbar_expect_tx(bar(kBrFull + b), kRwBytes);
+      bulk_load(base_s + CtSmem::rw + b * kRwBytes, ca.rwin + ((u0 + i) % S) * kRwBytes, kRwBytes,
+                bar(kBrFull + b));
+    };
+    if (lane == 0 && n > 0) load_rw(0);
+    uint64_t cur = ~0ull, tb = 0;
+    int k = -1;
+    for (uint64_t i = 0; i < n; ++i) {
+      const uint64_t grp = (u0 + i) / S;
+      if (grp != cur) {  // stage the group's conv1 A operand (buffer k & 1)
+        if (lane == 0 && k >= 0) mma_commit(bar(kBaEmpty + (k & 1)));
+        cur = grp;
+        ++k;
+        mbar_wait(bar(kBaEmpty + (k & 1)), ((k >> 1) & 1) ^ 1);
+        uint8_t* A = smem_ct + CtSmem::a + (k & 1) * kCtA;
+        for (int e = lane; e < 128 * 6; e += 32) {
+          const int r = e / 6, ky = e - 6 * (e / 6);
+          const int cc = ct_row_cc(r);
+          uint16_t v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          if (cc >= 0 && ky < 5) {
+            const int cand = cc / 6, ch = cc - 6 * (cc / 6);
+            const uint64_t row = grp * kCtG + (uint64_t)cand;
+            if (row < args.rows) {
+              const __nv_bfloat16* w = args.W + row * args.Dp;
+#pragma unroll
+              for (int kx = 0; kx < 5; ++kx) {
+                __nv_bfloat16 t = __float2bfloat16(0.25f * bf(w[oC1W + ch * 25 + ky * 5 + kx]));
+                v[kx] = *reinterpret_cast<uint16_t*>(&t);
+              }
+              if (ky == 0) {
+                __nv_bfloat16 t = __float2bfloat16(0.25f * bf(w[oC1B + ch]));
+                v[7] = *reinterpret_cast<uint16_t*>(&t);
+              }
+            }
+          }
+          *reinterpret_cast<uint4*>(A + il_off(r, 8 * ky, 128)) =
+              make_uint4(v[0] | (uint32_t)v[1] << 16, v[2] | (uint32_t)v[3] << 16, v[4] | (uint32_t)v[5] << 16,
+                         v[6] | (uint32_t)v[7] << 16);
+        }
+        async_smem_fence();
+        __syncwarp();
+      }
+      if (lane == 0) {
+        if (i + 1 < n) load_rw(i + 1);
+        const uint32_t b = (uint32_t)(i & 1);
+        mbar_wait(bar(kBrFull + b), (uint32_t)(i >> 1) & 1);
+        tc_fence_after();
+        const uint32_t a_s = base_s + CtSmem::a + (k & 1) * kCtA;
+        const uint32_t r_s = base_s + CtSmem::rw + b * kRwBytes;
+        for (int py = 0; py < 14; ++py, ++tb) {
+          const uint32_t slot = (uint32_t)(tb % kCtSlots);
+          mbar_wait(bar(kBtEmpty + slot), (uint32_t)((tb / kCtSlots) & 1) ^ 1);
+          tc_fence_after();
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            mma_ss(tmem + slot * 64, interleaved_desc(a_s + j * 2 * 2048, 2048, 128),
+                   interleaved_desc(r_s + (2 * py + 2 * j) * 512, 512, 128), id, j != 0);
+          mma_commit(bar(kBtFull + slot));
+        }
+        mma_commit(bar(kBrEmpty + b));
+      }
+      __syncwarp();
+    }
+  } else if (warp < 4) {
+    // ---------------------------------------------------------- TMEM epilogue: ReLU + pool -> conv1 maps
+    const int q = warp & 3, r = 32 * q + lane;
+    const int cc = ct_row_cc(r);
+    const int cand = cc >= 0 ? cc / 6 : 0, ch = cc >= 0 ? cc - 6 * (cc / 6) : 0;
+    const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
+    uint64_t tb = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+      const uint32_t b = (uint32_t)(i & 1);
+      mbar_wait(bar(kBpEmpty + b), (uint32_t)((i >> 1) & 1) ^ 1);
+      uint16_t* p1h = reinterpret_cast<uint16_t*>(smem_ct + CtSmem::p1 + (b * kCtG + cand) * kP1Words * 4) + (ch >> 1) * 2 +
+                      (ch & 1);
+      for (int py = 0; py < 14; ++py, ++tb) {
+        const uint32_t slot = (uint32_t)(tb % kCtSlots);
+        mbar_wait(bar(kBtFull + slot), (uint32_t)(tb / kCtSlots) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int hx = 0; hx < 2; ++hx) {  // pixel columns [16 hx, 16 hx + 16) of both rows
+          float v0[16], v2[16];
+          tmem_ld16_nowait(tq + slot * 64 + 16 * hx, v0);
+          tmem_ld16_nowait(tq + slot * 64 + 32 + 16 * hx, v2);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (hx == 1) {
+            tc_fence_before();
+            mbar_arrive(bar(kBtEmpty + slot));
+          }
+          if (cc >= 0) {
+#pragma unroll
+            for (int u = 0; u < (hx == 0 ? 8 : 6); ++u) {
+              // window px = 8 hx + u: row dy = 0 in v0, dy = 1 in v2
+              const float sum = (fmaxf(v0[2 * u], 0.f) + fmaxf(v2[2 * u], 0.f)) +
+                                (fmaxf(v0[2 * u + 1], 0.f) + fmaxf(v2[2 * u + 1], 0.f));
+              __nv_bfloat16 t = __float2bfloat16(sum);
+              p1h[(py * kP1R + 8 * hx + u) * 8] = *reinterpret_cast<uint16_t*>(&t);
+            }
+          }
+        }
+      }
+      mbar_arrive(bar(kBpFull + b));
+    }
+  } else {
+    // ---------------------------------------------------------- conv2 (one candidate per warp)
+    const int w = warp - 4;
+    const int g = lane >> 2, c = lane & 3;
+    const int wi = g >> 1, dx = g & 1;
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(smem_ct + CtSmem::o) + w * kP2Row;
+    uint32_t bw2[13][2][2];
+    float b2a = 0.f, b2b = 0.f, b2c = 0.f, b2d = 0.f;
+    uint64_t cur = ~0ull;
+    for (uint64_t i = 0; i < n; ++i) {
+      const uint64_t grp = (u0 + i) / S, s = (u0 + i) % S;
+      const uint64_t row = grp * kCtG + (uint64_t)w;
+      const bool live = row < args.rows;
+      if (grp != cur) {
+        cur = grp;
+        if (live) load_conv2_frags(args.W + row * args.Dp, g, c, bw2, b2a, b2b, b2c, b2d);
+      }
+      const uint32_t b = (uint32_t)(i & 1);
+      mbar_wait(bar(kBpFull + b), (uint32_t)(i >> 1) & 1);
+      if (live) {
+        const uint32_t* p1c = reinterpret_cast<const uint32_t*>(smem_ct + CtSmem::p1) + (b * kCtG + w) * kP1Words + c;
+#pragma unroll 1
+        for (int t0 = 0; t0 + kCtC2T <= 7; t0 += kCtC2T)
+          conv2_tiles<kCtC2T, false>(t0, p1c, o, wi, dx, c, bw2, b2a, b2b, b2c, b2d);
+        if constexpr (7 % kCtC2T != 0)
+          conv2_tiles<7 % kCtC2T, false>(7 - 7 % kCtC2T, p1c, o, wi, dx, c, bw2, b2a, b2b, b2c, b2d);
+      }
+      mbar_arrive(bar(kBpEmpty + b));
+      if (live) {
+        __syncwarp();
+        uint4* dst = reinterpret_cast<uint4*>(sa.p2 + (row * S + s) * (uint64_t)kP2Row);
+        const uint4* srcv = reinterpret_cast<const uint4*>(o);
+        for (int e = lane; e < kP2Row * 2 / 16; e += 32) dst[e] = srcv[e];
+        __syncwarp();
+      }
+    }
+  }
+  tmem_free512(tmem);
+}
+
 struct LenetPlan {
   LenetArgs args;
-  bool fused;  // MGFWA_LENET_FUSED=1: k_lenet_fused; default: k_lenet_conv + k_lenet_fc_tc
+  bool fused;    // MGFWA_LENET_FUSED=1: k_lenet_fused; default: conv + k_lenet_fc_tc
+  bool conv_tc;  // conv stage: k_lenet_conv_tc (default) or k_lenet_conv (MGFWA_LENET_CONV=mma)
+  uint8_t* rwin; // owned: row-window images [S][kRwBytes]
+  int nsm;
   unsigned grid;
   uint64_t group_rows;  // candidates per conv / fc launch pair (bounds the scratch)
   uint32_t* pimg;       // owned
@@ -1019,7 +1335,9 @@ LenetPlan* lenet_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t 
       cudaFuncSetAttribute(k_lenet_fc_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            FcTcSmem::total) != cudaSuccess ||
       cudaFuncSetAttribute(k_lenet_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           FusedSmem::total) != cudaSuccess) {
+                           FusedSmem::total) != cudaSuccess ||
+      cudaFuncSetAttribute(k_lenet_conv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           CtSmem::total) != cudaSuccess) {
     snprintf(err, errlen, "LeNet objective: shared memory opt-in failed");
     return nullptr;
   }
@@ -1067,6 +1385,22 @@ LenetPlan* lenet_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t 
     p->group_rows = rows;
     return p;
   }
+  {
+    // MGFWA_LENET_CONV=mma: the warp-MMA conv (k_lenet_conv) instead of
+    // k_lenet_conv_tc.  One conv kernel per plan, so a candidate's fitness
+    // does not depend on the size of the batch it is evaluated in.
+    const char* e = getenv("MGFWA_LENET_CONV");
+    p->conv_tc = !(e && strcmp(e, "mma") == 0);
+  }
+  p->nsm = nsm;
+  if (p->conv_tc) {
+    if (cudaMalloc(&p->rwin, (size_t)S * kRwBytes) != cudaSuccess)
+      return fail("LeNet objective: cudaMalloc of the row-window images failed");
+    const uint64_t m = (uint64_t)S * kRwRows * kRwPitch;
+    k_lenet_rowwin<<<(unsigned)((m + 255) / 256 < 4096 ? (m + 255) / 256 : 4096), 256>>>(
+        X, S, reinterpret_cast<uint4*>(p->rwin));
+    if (cudaDeviceSynchronize() != cudaSuccess) return fail("LeNet objective: row-window kernel failed");
+  }
   // scratch of at most kScratchBytes (at least one candidate's activations)
   const uint64_t per_row = (uint64_t)S * kP2Row * 2;
   uint64_t cap = kScratchBytes;
@@ -1095,6 +1429,7 @@ LenetPlan* lenet_plan_create(const __nv_bfloat16* X, const int32_t* y, uint32_t 
 void lenet_plan_destroy(LenetPlan* p) {
   if (!p) return;
   cudaFree(p->pimg);
+  cudaFree(p->rwin);
   cudaFree(p->p2);
   delete p;
 }
@@ -1115,7 +1450,15 @@ cudaError_t lenet_fitness_launch(const LenetPlan* p, float* part, const int* gat
     sa.base.gate = gate;
     const uint64_t items = sa.base.rows * sa.base.nparts;
     const unsigned gc = (unsigned)(items < p->grid ? items : p->grid);
-    cudaError_t e = pdl_launch(k_lenet_conv, gc, kConvThreads, ConvSmem::total, s, sa);
+    cudaError_t e;
+    if (p->conv_tc) {
+      LenetCtArgs ca{sa, p->rwin, (sa.base.rows + kCtG - 1) / kCtG};
+      const uint64_t units = ca.ngroups * sa.base.S;
+      const unsigned gt = (unsigned)(units < (uint64_t)p->nsm ? units : (uint64_t)p->nsm);
+      e = pdl_launch(k_lenet_conv_tc, gt, kCtThreads, CtSmem::total, s, ca);
+    } else {
+      e = pdl_launch(k_lenet_conv, gc, kConvThreads, ConvSmem::total, s, sa);
+    }
     if (e != cudaSuccess) return e;
     e = pdl_launch(k_lenet_fc_tc, gc, kFcThreadsTc, FcTcSmem::total, s, sa, p->tmap_p2, p->tmap_f1);
     if (e != cudaSuccess) return e;

@@ -5,7 +5,7 @@
 #   bash scripts/profile_round.sh launches [workload]   # ncu launch list of the bench command
 #   bash scripts/profile_round.sh cap NAME              # one `ncu --set full` capture of a hot kernel
 #     NAME: c2_mlp_fitness | c2_explode_map | c2_guides | c2_rank | c2_select | c2_guide_fitness
-#           c3_lenet_conv | c3_lenet_fc | c5_explode_map | c5_mlp_fitness | c4_explode_map
+#           c3_lenet_conv | c3_lenet_conv_tc | c3_lenet_fc | c5_explode_map | c5_mlp_fitness | c4_explode_map
 set -u
 OUT=gpurun_out/prof
 mkdir -p $OUT
@@ -21,7 +21,7 @@ cap)
   declare -A RE=([c2_mlp_fitness]="k_mlp_fitness 4 c2" [c2_explode_map]="k_explode_map 1 c2"
                  [c2_guides]="k_guides 1 c2" [c2_rank]="k_rank 1 c2" [c2_select]="k_select 1 c2"
                  [c2_guide_fitness]="k_mlp_fitness 5 c2"
-                 [c3_lenet_conv]="k_lenet_conv 4 c3" [c3_lenet_fc]="k_lenet_fc_tc 4 c3"
+                 [c3_lenet_conv]="k_lenet_conv 4 c3" [c3_lenet_conv_tc]="k_lenet_conv_tc 4 c3" [c3_lenet_fc]="k_lenet_fc_tc 4 c3"
                  [c5_explode_map]="k_explode_map 1 c5" [c5_mlp_fitness]="k_mlp_fitness 1 c5"
                  [c4_explode_map]="k_explode_map 1 c4")
   set -- $2 ${RE[$2]}

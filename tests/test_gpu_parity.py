@@ -376,3 +376,37 @@ def test_lenet_candidate_groups_bit_identical(P):
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(r.stdout.strip().splitlines()[-1])
     assert outs[0] == outs[1]
+
+
+def test_lenet_conv_paths_agree(P, oracle):
+    """The two conv stages — conv1 on tcgen05 (k_lenet_conv_tc, default) and
+    the warp-MMA conv (MGFWA_LENET_CONV=mma, read at plan creation) — both
+    meet the oracle tolerance on the same candidates (sizes that leave a
+    partial 12-candidate group and a partial 128-sample chunk), and agree
+    with each other to bf16 activation rounding."""
+    import os
+    import subprocess
+    import sys
+
+    code = ("import numpy as np, paper_2501_03944_b200 as P\n"
+            "W = np.random.default_rng(11).uniform(-0.2, 0.2, size=(29, P.LeNet(samples=200).dim())).astype(np.float32)\n"
+            "f, nan = P.batched_apply(P.LeNet(samples=200), W)\n"
+            "assert nan == 0\n"
+            "print(','.join(repr(float(x)) for x in f))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for mode in ("default", "mma"):
+        env = dict(os.environ)
+        env.pop("MGFWA_LENET_CONV", None)
+        if mode != "default":
+            env["MGFWA_LENET_CONV"] = mode
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[mode] = np.array([float(x) for x in r.stdout.strip().splitlines()[-1].split(",")])
+    desc = O.ObjectiveDesc(kind=O.OBJ_LENET, samples=200)
+    W = f32(np.random.default_rng(11).uniform(-0.2, 0.2, size=(29, desc.dim())))
+    want = np.array([oracle.evaluate(desc, w) for w in _bf16_image(W[[0, 11, 12, 28]])])
+    for mode, got in outs.items():
+        np.testing.assert_allclose(got[[0, 11, 12, 28]], want, rtol=REL_LENET_ACT, atol=ABS_LENET_ACT, err_msg=mode)
+    np.testing.assert_allclose(outs["default"], outs["mma"], rtol=REL_LENET_ACT, atol=ABS_LENET_ACT)
