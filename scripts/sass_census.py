@@ -15,6 +15,7 @@ BUILD = os.path.join(ROOT, "paper_2501_03944_b200", "_build")
 CLASSES = {
     "UTCHMMA / UTCQMMA (tcgen05.mma)": r"^UTC[HQ]MMA",
     "UTMALDG (TMA tile load)": r"^UTMALDG",
+    "UBLKCP (bulk copy)": r"^UBLKCP",
     "UTCBAR (tcgen05.commit)": r"^UTCBAR",
     "LDTM (tcgen05.ld)": r"^LDTM",
     "STTM (tcgen05.st)": r"^STTM",
