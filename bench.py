@@ -89,10 +89,12 @@ NCU_KEYS = {"sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active": "t
             "gpu__time_duration.sum": "ncu_time"}
 
 
-def ncu_metrics(kernel_prefix: str, workload: str):
+def ncu_metrics(kernel_prefix: str, workload: str, capture: str = None):
     """DRAM bytes (read + write) per launch and the pipe counters of a
     kernel from the latest committed `ncu --set full` capture of this
-    workload under profiles/ (None if absent)."""
+    workload under profiles/ (None if absent).  `capture` selects the
+    capture by report name (scripts/profile_round.sh NAME) where one kernel
+    template has several (spark vs guide fitness)."""
     import glob
 
     paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_full_hot_kernels.json")), reverse=True)
@@ -100,6 +102,8 @@ def ncu_metrics(kernel_prefix: str, workload: str):
         with open(path) as f:
             for k in json.load(f):
                 if kernel_prefix not in k.get("kernel", "") or k.get("workload", "c2") != workload:
+                    continue
+                if capture and os.path.basename(k.get("report", "")) != capture + ".ncu-rep":
                     continue
 
                 def num(s):
@@ -371,16 +375,18 @@ def kernel_breakdown(eng, w, wn, world, pk):
 
 
 KERNEL_NAMES = {"explode": "k_explode_map", "rank": "k_rank", "guides": "k_guides", "select": "k_select",
-                "fitness_mlp": "k_mlp_fitness", "fitness_lenet": "k_lenet_conv + k_lenet_fc_tc"}
+                "fitness_mlp": "k_mlp_fitness", "fitness_lenet": "k_lenet_conv_tc + k_lenet_fc_tc"}
 
 
 def roofline_entry(name, k, w, pk, pk_kind, workload):
     """The `roofline` object for kernel `name` of the breakdown."""
     if k["bound"] == "tensor":
         kern = KERNEL_NAMES["fitness_" + w["kind"]]
-        nc = ncu_metrics(kern + (f"<{w['hidden']}" if w["kind"] == "mlp" else ""), workload)
-        if w["kind"] == "lenet":  # conv (warp MMA) + fc (tcgen05) launches: traffic of both
-            conv, fc = ncu_metrics("k_lenet_conv", workload), ncu_metrics("k_lenet_fc_tc", workload)
+        nc = ncu_metrics(kern + (f"<{w['hidden']}" if w["kind"] == "mlp" else ""), workload,
+                         f"{workload}_mlp_fitness" if w["kind"] == "mlp" else None)
+        if w["kind"] == "lenet":  # conv (tcgen05 conv1 + warp-MMA conv2) + fc (tcgen05): traffic of both
+            conv = ncu_metrics("k_lenet_conv_tc", workload, "c3_lenet_conv_tc")
+            fc = ncu_metrics("k_lenet_fc_tc", workload)
             if conv and fc:
                 nc = {"traffic": conv["traffic"] + fc["traffic"], "source": conv["source"],
                       "conv_tensor_pipe_pct": conv.get("tensor_pipe_pct"), "fc_tensor_pipe_pct": fc.get("tensor_pipe_pct")}
