@@ -770,49 +770,6 @@ constexpr int kGuideWarps = GUIDES_WARPS;
 // U: rank pairs per unrolled load step (2U independent V-wide loads per
 // lane in flight): 30 when top <= 64 (C2: top = 60 in two load rounds,
 // 27.2 -> 25.7 us), else 16 (20 measured slower on both C2 and C5).
-#ifndef GUIDES_VLD
-#define GUIDES_VLD 0  // 1: the rank-row loads as volatile ld.global.nc (issued in program order, all in flight)
-#endif
-template <int V>
-__device__ __forceinline__ typename VecT<V>::T guide_ld(const float* p) {
-#if GUIDES_VLD
-  if constexpr (V == 2) {
-    float2 r;
-    asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "l"(p));
-    return r;
-  } else {
-    float4 r;
-    asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
-    return r;
-  }
-#else
-  return *reinterpret_cast<const typename VecT<V>::T*>(p);
-#endif
-}
-
-#ifndef GUIDES_ASYNC
-#define GUIDES_ASYNC 0  // 1: rank rows staged by cp.async (GUIDES_AU pairs per round)
-#endif
-#ifndef GUIDES_AU
-#define GUIDES_AU 16
-#endif
-template <int B>
-__device__ __forceinline__ void guide_cp_async(uint32_t dst, const float* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(dst), "l"(src), "n"(B) : "memory");
-}
-template <int V>
-__device__ __forceinline__ typename VecT<V>::T guide_lds(uint32_t a) {
-  if constexpr (V == 2) {
-    float2 r;
-    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "r"(a) : "memory");
-    return r;
-  } else {
-    float4 r;
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "r"(a) : "memory");
-    return r;
-  }
-}
-
 template <int U>
 __global__ void __launch_bounds__(kGuideWarps * 32) k_guides(EngineView v) {
   constexpr int V = GUIDES_VEC;
@@ -841,41 +798,14 @@ __global__ void __launch_bounds__(kGuideWarps * 32) k_guides(EngineView v) {
     double acc[V];
 #pragma unroll
     for (int e = 0; e < V; ++e) acc[e] = 0.0;
-#if GUIDES_ASYNC
-    {
-      // the rank rows of a round (GUIDES_AU pairs) staged by cp.async into
-      // this lane's own shared-memory slots: every load of the round in
-      // flight without holding registers; summed in rank order afterwards
-      const uint32_t wb = (uint32_t)__cvta_generic_to_shared(s_idx + 2 * top) + 16u -
-                          ((uint32_t)__cvta_generic_to_shared(s_idx + 2 * top) & 15u) +
-                          (uint32_t)(warp * 2 * GUIDES_AU * 32 * sizeof(VT));
-      for (uint64_t t = 0; t < top; t += GUIDES_AU) {
-        const int R = (int)(top - t < (uint64_t)GUIDES_AU ? top - t : (uint64_t)GUIDES_AU);
-        for (int i = 0; i < R; ++i) {
-          guide_cp_async<sizeof(VT)>(wb + (uint32_t)(((2 * i) * 32 + lane) * sizeof(VT)),
-                                     sb + (uint64_t)s_idx[t + i] * v.Dp);
-          guide_cp_async<sizeof(VT)>(wb + (uint32_t)(((2 * i + 1) * 32 + lane) * sizeof(VT)),
-                                     sb + (uint64_t)s_idx[top + t + i] * v.Dp);
-        }
-        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-        for (int i = 0; i < R; ++i) {
-          float bf_[V], wf_[V];
-          vec_split<V>(guide_lds<V>(wb + (uint32_t)(((2 * i) * 32 + lane) * sizeof(VT))), bf_);
-          vec_split<V>(guide_lds<V>(wb + (uint32_t)(((2 * i + 1) * 32 + lane) * sizeof(VT))), wf_);
-#pragma unroll
-          for (int e = 0; e < V; ++e) acc[e] = __dadd_rn(acc[e], __dsub_rn((double)bf_[e], (double)wf_[e]));
-        }
-      }
-    }
-#else
     uint64_t t = 0;
     // 2U independent loads in flight per lane, summed in rank order
     for (; t + U <= top; t += U) {
       VT bb[U], ww[U];
 #pragma unroll
       for (int i = 0; i < U; ++i) {
-        bb[i] = guide_ld<V>(sb + (uint64_t)s_idx[t + i] * v.Dp);
-        ww[i] = guide_ld<V>(sb + (uint64_t)s_idx[top + t + i] * v.Dp);
+        bb[i] = *reinterpret_cast<const VT*>(sb + (uint64_t)s_idx[t + i] * v.Dp);
+        ww[i] = *reinterpret_cast<const VT*>(sb + (uint64_t)s_idx[top + t + i] * v.Dp);
       }
 #pragma unroll
       for (int i = 0; i < U; ++i) {
@@ -890,8 +820,8 @@ __global__ void __launch_bounds__(kGuideWarps * 32) k_guides(EngineView v) {
       VT bb[4], ww[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        bb[i] = guide_ld<V>(sb + (uint64_t)s_idx[t + i] * v.Dp);
-        ww[i] = guide_ld<V>(sb + (uint64_t)s_idx[top + t + i] * v.Dp);
+        bb[i] = *reinterpret_cast<const VT*>(sb + (uint64_t)s_idx[t + i] * v.Dp);
+        ww[i] = *reinterpret_cast<const VT*>(sb + (uint64_t)s_idx[top + t + i] * v.Dp);
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -904,12 +834,11 @@ __global__ void __launch_bounds__(kGuideWarps * 32) k_guides(EngineView v) {
     }
     for (; t < top; ++t) {
       float bf_[V], wf_[V];
-      vec_split<V>(guide_ld<V>(sb + (uint64_t)s_idx[t] * v.Dp), bf_);
-      vec_split<V>(guide_ld<V>(sb + (uint64_t)s_idx[top + t] * v.Dp), wf_);
+      vec_split<V>(*reinterpret_cast<const VT*>(sb + (uint64_t)s_idx[t] * v.Dp), bf_);
+      vec_split<V>(*reinterpret_cast<const VT*>(sb + (uint64_t)s_idx[top + t] * v.Dp), wf_);
 #pragma unroll
       for (int e = 0; e < V; ++e) acc[e] = __dadd_rn(acc[e], __dsub_rn((double)bf_[e], (double)wf_[e]));
     }
-#endif
     const double dtop = (double)top;
     double delta[V];
 #pragma unroll
@@ -2051,21 +1980,10 @@ void launch_key_hash(const uint64_t* keys, uint64_t n, uint64_t* out,
 
 // ---------------------------------------------------------------- launch
 
-static size_t guides_smem(const EngineView& v) {
-  return v.M * sizeof(uint64_t) + 2 * v.top * sizeof(int) +
-         (GUIDES_ASYNC ? 16 + (size_t)kGuideWarps * 2 * GUIDES_AU * 32 * GUIDES_VEC * sizeof(float) : 0);
-}
+static size_t guides_smem(const EngineView& v) { return v.M * sizeof(uint64_t) + 2 * v.top * sizeof(int); }
 
 static unsigned guide_blocks(const EngineView& v, int nsm);
 static void launch_guides_k(const EngineView& v, int nsm, cudaStream_t s) {
-  if (GUIDES_ASYNC) {
-    static const bool attrs = [] {
-      const int bytes = 64 * 8 + 2 * 16384 * 4 + 16 + kGuideWarps * 2 * GUIDES_AU * 32 * GUIDES_VEC * 4;
-      return cudaFuncSetAttribute(k_guides<30>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess &&
-             cudaFuncSetAttribute(k_guides<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess;
-    }();
-    (void)attrs;
-  }
   if (v.top <= 64)
     pdl_launch(k_guides<30>, guide_blocks(v, nsm), kGuideWarps * 32, guides_smem(v), s, v);
   else

@@ -30,7 +30,6 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
-#include <cstdlib>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -645,22 +644,8 @@ cudaError_t launch_h(const CUtensorMap& tx, const CUtensorMap& tw, int grid, con
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem_bytes<CG, BNT>();
   cfg.stream = s;
-  cudaLaunchAttribute attr[4];
+  cudaLaunchAttribute attr[3];
   int n = 0;
-  // MGFWA_MLP_PRIORITY=1: launch at the device's greatest priority, so that the
-  // block scheduler places the persistent fitness CTAs before pending explode
-  // blocks of the pipelined next chunk (experiment switch)
-  static const int prio = [] {
-    const char* e = getenv("MGFWA_MLP_PRIORITY");
-    int lo = 0, hi = 0;
-    if (!(e && e[0] == '1') || cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return 0;
-    return hi;
-  }();
-  if (prio != 0) {
-    attr[n].id = cudaLaunchAttributePriority;
-    attr[n].val.priority = prio;
-    ++n;
-  }
   if (launch_done) {
     attr[n].id = cudaLaunchAttributeLaunchCompletionEvent;
     attr[n].val.launchCompletionEvent.event = launch_done;
