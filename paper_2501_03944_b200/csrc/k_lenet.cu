@@ -1028,6 +1028,8 @@ __global__ void __launch_bounds__(kFThreads, 1) k_lenet_fused(LenetArgs args,
 namespace {
 
 constexpr int kCtG = 12;                               // candidates per conv1 GEMM
+constexpr int kQR = 48;                                // conv1 map row stride (words), see conv2_cols_tiles
+constexpr int kQCand = 14 * kQR + 8;                   // candidate stride (words; 8 mod 32: conflict-free epilogue stores)
 #ifndef LENET_CT_C2T
 #define LENET_CT_C2T 2
 #endif
@@ -1041,8 +1043,8 @@ constexpr int kCtThreads = kCtWarps * 32;
 struct CtSmem {
   static constexpr int a = 0;                                   // 2 x conv1 A (group parity)
   static constexpr int rw = a + 2 * kCtA;                       // 2 x row windows (sample parity)
-  static constexpr int p1 = rw + 2 * kRwBytes;                  // 2 x kCtG conv1 maps
-  static constexpr int o = p1 + 2 * kCtG * kP1Words * 4;        // per conv2 warp: [416] bf16
+  static constexpr int p1 = rw + 2 * kRwBytes;                  // 2 x kCtG conv1 maps (kQCand words each)
+  static constexpr int o = p1 + 2 * kCtG * kQCand * 4;          // per conv2 warp: [416] bf16
   static constexpr int bar = o + kCtG * kP2Row * 2;             // mbarriers
   // a_full[2] a_empty[2] rw_full[2] rw_empty[2] t_full[8] t_empty[8] p_full[2] p_empty[2]
   static constexpr int nbar = 28;
@@ -1065,32 +1067,122 @@ struct LenetCtArgs {
   uint64_t ngroups;     // ceil(rows / kCtG)
 };
 
-// conv2 B fragments of candidate row w (the k_lenet_conv staging order,
-// conv2_k, read straight from the row; weights pre-scaled by 1/4, exact)
-__device__ __forceinline__ void load_conv2_frags(const __nv_bfloat16* w, int g, int c, uint32_t (&bw2)[13][2][2],
-                                                 float& b2a, float& b2b, float& b2c, float& b2d) {
-  auto wv = [&](int ch, int ci, int tap) -> float {
-    return (ci < 6 && tap >= 0) ? 0.25f * bf(w[oC2W + ch * 150 + ci * 25 + tap]) : 0.f;
+// conv2 of k_lenet_conv_tc in "column" K order.  The conv1 map of a
+// candidate is [14 rows][16 pixel slots][3 channel pairs] words (kQR = 48
+// words per row, slots 14 / 15 zero), so tap column col = kx * 3 + cp (the
+// channel pair) is word offset col from the pixel and tap row ky is ky * kQR.
+// K = 10 k-steps of 8 (column, ky) pairs:
+//   steps 0-3 (A s) and 4-7 (B s): slots j < 4 = (col 4 s + j, ky0),
+//     j >= 4 = (col 4 s + j - 4, ky0 + 1), ky0 = 0 (A) / 2 (B);
+//   steps 8-9 (C h): slots j = (col 8 h + j, ky 4);
+// column 15 is padding (zero weights, reads the zero slot 14 of the row).
+// Lane c of an A / B step then needs, for its column, the words at ky0,
+// ky0 + 1 (twice: row g + 8 at ky0 is row g at ky0 + 1, the pixel one row
+// down) and ky0 + 2, and its C step the words at ky 4 / 5 of two columns: 24
+// shared-memory loads per 16-pixel tile feed 20 MMAs (conv2_tiles: 30 loads,
+// 26 MMAs).  With 3-word pixels and the 48-word row stride the 32 lanes of
+// every load hit distinct banks (checked exhaustively over the 7 tiles).
+
+__device__ __forceinline__ void conv2_slot(int step, int j, int& col, int& ky) {
+  if (step < 4) {
+    col = 4 * step + (j & 3), ky = j >> 2;
+  } else if (step < 8) {
+    col = 4 * (step - 4) + (j & 3), ky = 2 + (j >> 2);
+  } else {
+    col = 8 * (step - 8) + j, ky = 4;
+  }
+}
+
+// B fragments of candidate row w in that K order, read straight from the row
+// (weights and biases pre-scaled by 1/4, exact)
+__device__ __forceinline__ void load_conv2_cols(const __nv_bfloat16* w, int g, int c, uint32_t (&bw)[10][2][2],
+                                                float& b2a, float& b2b, float& b2c, float& b2d) {
+  auto wv = [&](int ch, int col, int ky, int half) -> float {
+    if (col >= 15) return 0.f;
+    const int kx = col / 3, ci = 2 * (col % 3) + half;
+    return 0.25f * bf(w[oC2W + ch * 150 + ci * 25 + ky * 5 + kx]);
   };
 #pragma unroll
-  for (int st = 0; st < 13; ++st) {
-    int ta, tb;
-    if (st < 10) {
-      const int kx = st >> 1, h = st & 1;
-      ta = (2 * h) * 5 + kx, tb = (2 * h + 1) * 5 + kx;
-    } else {
-      const int j = st - 10;
-      ta = 20 + 2 * j, tb = 2 * j + 1 < 5 ? 21 + 2 * j : -1;
-    }
+  for (int st = 0; st < 10; ++st)
 #pragma unroll
     for (int n = 0; n < 2; ++n) {
       const int ch = 8 * n + g;
-      bw2[st][n][0] = pack_bf16(wv(ch, 2 * c, ta), wv(ch, 2 * c + 1, ta));
-      bw2[st][n][1] = pack_bf16(wv(ch, 2 * c, tb), wv(ch, 2 * c + 1, tb));
+      int col, ky;
+      conv2_slot(st, c, col, ky);
+      bw[st][n][0] = pack_bf16(wv(ch, col, ky, 0), wv(ch, col, ky, 1));
+      conv2_slot(st, c + 4, col, ky);
+      bw[st][n][1] = pack_bf16(wv(ch, col, ky, 0), wv(ch, col, ky, 1));
     }
-  }
   b2a = 0.25f * bf(w[oC2B + 2 * c]), b2b = 0.25f * bf(w[oC2B + 2 * c + 1]);
   b2c = 0.25f * bf(w[oC2B + 8 + 2 * c]), b2d = 0.25f * bf(w[oC2B + 9 + 2 * c]);
+}
+
+// conv2 + ReLU + pool of tiles t0 .. t0 + N - 1 (the conv2_tiles M layout:
+// rows g / g + 8 = vertically adjacent pixels of window 4 t + g / 2) -> o
+template <int N>
+__device__ __forceinline__ void conv2_cols_tiles(int t0, const uint32_t* map, __nv_bfloat16* o, int wi, int dx,
+                                                 int c, const uint32_t (&bw)[10][2][2], float b2a, float b2b,
+                                                 float b2c, float b2d) {
+  int wv[N];
+  const uint32_t* q[N];
+  float d[N][2][4];
+#pragma unroll
+  for (int u = 0; u < N; ++u) {
+    const int w = 4 * (t0 + u) + wi;
+    wv[u] = w < 25 ? w : -1;
+    const int wc = w < 25 ? w : 24;
+    const int qy = wc / 5, qx = wc - 5 * qy;
+    q[u] = map + (2 * qy) * kQR + (2 * qx + dx) * 3 + c;
+    d[u][0][0] = b2a, d[u][0][1] = b2b, d[u][0][2] = b2a, d[u][0][3] = b2b;
+    d[u][1][0] = b2c, d[u][1][1] = b2d, d[u][1][2] = b2c, d[u][1][3] = b2d;
+  }
+#pragma unroll
+  for (int sp = 0; sp < 2; ++sp) {
+    uint32_t W[N][2][6];
+#pragma unroll
+    for (int u = 0; u < N; ++u)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int ky = 0; ky < 6; ++ky) W[u][e][ky] = q[u][ky * kQR + 4 * (2 * sp + e)];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int st = 2 * sp + e;
+#pragma unroll
+      for (int u = 0; u < N; ++u)
+#pragma unroll
+        for (int n = 0; n < 2; ++n)
+          mma_bf16(d[u][n], W[u][e][0], W[u][e][1], W[u][e][1], W[u][e][2], bw[st][n][0], bw[st][n][1]);
+#pragma unroll
+      for (int u = 0; u < N; ++u)
+#pragma unroll
+        for (int n = 0; n < 2; ++n)
+          mma_bf16(d[u][n], W[u][e][2], W[u][e][3], W[u][e][3], W[u][e][4], bw[4 + st][n][0], bw[4 + st][n][1]);
+    }
+#pragma unroll
+    for (int u = 0; u < N; ++u)
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+        mma_bf16(d[u][n], W[u][0][4], W[u][0][5], W[u][1][4], W[u][1][5], bw[8 + sp][n][0], bw[8 + sp][n][1]);
+  }
+#pragma unroll
+  for (int u = 0; u < N; ++u) {
+    float s0 = fmaxf(d[u][0][0], 0.f) + fmaxf(d[u][0][2], 0.f);
+    float s1 = fmaxf(d[u][0][1], 0.f) + fmaxf(d[u][0][3], 0.f);
+    float s2 = fmaxf(d[u][1][0], 0.f) + fmaxf(d[u][1][2], 0.f);
+    float s3 = fmaxf(d[u][1][1], 0.f) + fmaxf(d[u][1][3], 0.f);
+    s0 += __shfl_xor_sync(0xffffffffu, s0, 4);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, 4);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, 4);
+    s3 += __shfl_xor_sync(0xffffffffu, s3, 4);
+    if (dx == 0 && wv[u] >= 0) {
+      const int w = wv[u];
+      const float vals[4] = {s0, s1, s2, s3};
+      const int chs[4] = {2 * c, 2 * c + 1, 8 + 2 * c, 9 + 2 * c};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[chs[j] * 25 + w + 4] = __float2bfloat16(vals[j]);
+    }
+  }
 }
 
 }  // namespace
@@ -1233,7 +1325,7 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_lenet_conv_tc(LenetCtArgs ca)
     for (uint64_t i = 0; i < n; ++i) {
       const uint32_t b = (uint32_t)(i & 1);
       mbar_wait(bar(kBpEmpty + b), (uint32_t)((i >> 1) & 1) ^ 1);
-      uint16_t* p1h = reinterpret_cast<uint16_t*>(smem_ct + CtSmem::p1 + (b * kCtG + cand) * kP1Words * 4) + (ch >> 1) * 2 +
+      uint16_t* p1h = reinterpret_cast<uint16_t*>(smem_ct + CtSmem::p1 + (b * kCtG + cand) * kQCand * 4) + (ch >> 1) * 2 +
                       (ch & 1);
       for (int py = 0; py < 14; ++py, ++tb) {
         const uint32_t slot = (uint32_t)(tb % kCtSlots);
@@ -1256,7 +1348,7 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_lenet_conv_tc(LenetCtArgs ca)
               const float sum = (fmaxf(v0[2 * u], 0.f) + fmaxf(v2[2 * u], 0.f)) +
                                 (fmaxf(v0[2 * u + 1], 0.f) + fmaxf(v2[2 * u + 1], 0.f));
               __nv_bfloat16 t = __float2bfloat16(sum);
-              p1h[(py * kP1R + 8 * hx + u) * 8] = *reinterpret_cast<uint16_t*>(&t);
+              p1h[(py * kQR + (8 * hx + u) * 3) * 2] = *reinterpret_cast<uint16_t*>(&t);
             }
           }
         }
@@ -1269,7 +1361,7 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_lenet_conv_tc(LenetCtArgs ca)
     const int g = lane >> 2, c = lane & 3;
     const int wi = g >> 1, dx = g & 1;
     __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(smem_ct + CtSmem::o) + w * kP2Row;
-    uint32_t bw2[13][2][2];
+    uint32_t bw[10][2][2];
     float b2a = 0.f, b2b = 0.f, b2c = 0.f, b2d = 0.f;
     uint64_t cur = ~0ull;
     for (uint64_t i = 0; i < n; ++i) {
@@ -1278,17 +1370,17 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_lenet_conv_tc(LenetCtArgs ca)
       const bool live = row < args.rows;
       if (grp != cur) {
         cur = grp;
-        if (live) load_conv2_frags(args.W + row * args.Dp, g, c, bw2, b2a, b2b, b2c, b2d);
+        if (live) load_conv2_cols(args.W + row * args.Dp, g, c, bw, b2a, b2b, b2c, b2d);
       }
       const uint32_t b = (uint32_t)(i & 1);
       mbar_wait(bar(kBpFull + b), (uint32_t)(i >> 1) & 1);
       if (live) {
-        const uint32_t* p1c = reinterpret_cast<const uint32_t*>(smem_ct + CtSmem::p1) + (b * kCtG + w) * kP1Words + c;
+        const uint32_t* map = reinterpret_cast<const uint32_t*>(smem_ct + CtSmem::p1) + (b * kCtG + w) * kQCand;
 #pragma unroll 1
         for (int t0 = 0; t0 + kCtC2T <= 7; t0 += kCtC2T)
-          conv2_tiles<kCtC2T, false>(t0, p1c, o, wi, dx, c, bw2, b2a, b2b, b2c, b2d);
+          conv2_cols_tiles<kCtC2T>(t0, map, o, wi, dx, c, bw, b2a, b2b, b2c, b2d);
         if constexpr (7 % kCtC2T != 0)
-          conv2_tiles<7 % kCtC2T, false>(7 - 7 % kCtC2T, p1c, o, wi, dx, c, bw2, b2a, b2b, b2c, b2d);
+          conv2_cols_tiles<7 % kCtC2T>(7 - 7 % kCtC2T, map, o, wi, dx, c, bw, b2a, b2b, b2c, b2d);
       }
       mbar_arrive(bar(kBpEmpty + b));
       if (live) {

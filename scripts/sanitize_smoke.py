@@ -4,7 +4,7 @@ racecheck / synccheck):
     compute-sanitizer --tool memcheck python scripts/sanitize_smoke.py
 
 MLP-weights fitness (tcgen05, wide and narrow tiles, SM pairs), LeNet-5
-(warp-MMA conv + tcgen05 fc), analytic objectives through the small-problem
+(tcgen05 conv1 + warp-MMA conv2, tcgen05 fc), analytic objectives through the small-problem
 cluster loop and through the general graph path, the paper's Net 1, and an
 emulated 2-shard firework-sharded run."""
 import os
@@ -29,8 +29,8 @@ def main():
         print("mlp", H, P.batched_apply(obj, W)[0][:3])
     r = P.run(cfg(3, 16, 2), P.SearchSpace.box(P.MlpWeights(samples=128).dim(), -1, 1), P.MlpWeights(samples=128), 1)
     print("mlp run", r.best_fitness)
-    lo = P.LeNet(samples=128)
-    L = rng.uniform(-0.1, 0.1, size=(5, lo.dim())).astype(np.float32).astype(np.float64)
+    lo = P.LeNet(samples=200)  # tcgen05 conv1: 3 candidate groups (the last partial), a partial sample chunk
+    L = rng.uniform(-0.1, 0.1, size=(29, lo.dim())).astype(np.float32).astype(np.float64)
     print("lenet", P.batched_apply(lo, L)[0][:3])
     print("sphere small", P.run(cfg(5, 30, 3), P.SearchSpace.box(30, -10, 10), P.Sphere(), 2).best_fitness)
     print("rastrigin D=2000", P.run(cfg(5, 30, 2), P.SearchSpace.box(2000, -5.12, 5.12), P.Rastrigin(), 3).best_fitness)
