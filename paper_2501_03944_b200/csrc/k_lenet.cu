@@ -1038,23 +1038,30 @@ constexpr int kRwRows = 33, kRwPitch = 32;             // row windows: [Y][X] x 
 constexpr int kRwBytes = kRwRows * kRwPitch * 16;      // 16,896 B per sample
 constexpr int kCtA = 128 * 48 * 2;                     // conv1 A: 128 x 48 bf16
 constexpr int kCtSlots = 8;                            // TMEM: 8 x 64 columns
+#ifndef LENET_CT_MAPS
+#define LENET_CT_MAPS 2
+#endif
+#ifndef LENET_CT_PAIR
+#define LENET_CT_PAIR 0  // 1: conv2 takes samples in pairs (shared 7th tile); needs LENET_CT_MAPS >= 3
+#endif
+constexpr int kCtP = LENET_CT_MAPS;                    // conv1-map buffers (samples in flight)
 constexpr int kCtWarps = 1 + 3 + kCtG;
 constexpr int kCtThreads = kCtWarps * 32;
 struct CtSmem {
   static constexpr int a = 0;                                   // 2 x conv1 A (group parity)
   static constexpr int rw = a + 2 * kCtA;                       // 2 x row windows (sample parity)
-  static constexpr int p1 = rw + 2 * kRwBytes;                  // 2 x kCtG conv1 maps (kQCand words each)
-  static constexpr int o = p1 + 2 * kCtG * kQCand * 4;          // per conv2 warp: [416] bf16
-  static constexpr int bar = o + kCtG * kP2Row * 2;             // mbarriers
-  // a_full[2] a_empty[2] rw_full[2] rw_empty[2] t_full[8] t_empty[8] p_full[2] p_empty[2]
-  static constexpr int nbar = 28;
+  static constexpr int p1 = rw + 2 * kRwBytes;                  // kCtP x kCtG conv1 maps (kQCand words each)
+  static constexpr int o = p1 + kCtP * kCtG * kQCand * 4;       // per conv2 warp: 2 x [416] bf16
+  static constexpr int bar = o + kCtG * 2 * kP2Row * 2;         // mbarriers
+  // a_full[2] a_empty[2] rw_full[2] rw_empty[2] t_full[8] t_empty[8] p_full[kCtP] p_empty[kCtP]
+  static constexpr int nbar = 24 + 2 * kCtP;
   static constexpr int slot = bar + nbar * 8;
   static constexpr int total = slot + 16;
 };
 static_assert(CtSmem::total <= 227 * 1024 && CtSmem::rw % 16 == 0 && CtSmem::o % 16 == 0 &&
                   CtSmem::bar % 8 == 0,
               "LeNet tcgen05 conv shared memory");
-enum { kBaFull = 0, kBaEmpty = 2, kBrFull = 4, kBrEmpty = 6, kBtFull = 8, kBtEmpty = 16, kBpFull = 24, kBpEmpty = 26 };
+enum { kBaFull = 0, kBaEmpty = 2, kBrFull = 4, kBrEmpty = 6, kBtFull = 8, kBtEmpty = 16, kBpFull = 24, kBpEmpty = 24 + kCtP };
 
 // (candidate, channel) of conv1 GEMM row r, or -1 for a padding row
 __host__ __device__ constexpr int ct_row_cc(int r) {
@@ -1119,20 +1126,25 @@ __device__ __forceinline__ void load_conv2_cols(const __nv_bfloat16* w, int g, i
 
 // conv2 + ReLU + pool of tiles t0 .. t0 + N - 1 (the conv2_tiles M layout:
 // rows g / g + 8 = vertically adjacent pixels of window 4 t + g / 2) -> o
-template <int N>
+// PAIR (N = 1): the partial 7th tiles of two samples of the same candidate
+// as one tile — window slot wi = 0 / 1 is pool window 24 of sample `map` /
+// `map2` (outputs to o / o2), slots 2 / 3 repeat them (discarded).
+template <int N, bool PAIR = false>
 __device__ __forceinline__ void conv2_cols_tiles(int t0, const uint32_t* map, __nv_bfloat16* o, int wi, int dx,
                                                  int c, const uint32_t (&bw)[10][2][2], float b2a, float b2b,
-                                                 float b2c, float b2d) {
+                                                 float b2c, float b2d, const uint32_t* map2 = nullptr,
+                                                 __nv_bfloat16* o2 = nullptr) {
+  static_assert(!PAIR || N == 1, "one paired tile");
   int wv[N];
   const uint32_t* q[N];
   float d[N][2][4];
 #pragma unroll
   for (int u = 0; u < N; ++u) {
-    const int w = 4 * (t0 + u) + wi;
-    wv[u] = w < 25 ? w : -1;
+    const int w = PAIR ? 24 : 4 * (t0 + u) + wi;
+    wv[u] = PAIR ? (wi < 2 ? 24 : -1) : (w < 25 ? w : -1);
     const int wc = w < 25 ? w : 24;
     const int qy = wc / 5, qx = wc - 5 * qy;
-    q[u] = map + (2 * qy) * kQR + (2 * qx + dx) * 3 + c;
+    q[u] = (PAIR && (wi & 1) ? map2 : map) + (2 * qy) * kQR + (2 * qx + dx) * 3 + c;
     d[u][0][0] = b2a, d[u][0][1] = b2b, d[u][0][2] = b2a, d[u][0][3] = b2b;
     d[u][1][0] = b2c, d[u][1][1] = b2d, d[u][1][2] = b2c, d[u][1][3] = b2d;
   }
@@ -1179,8 +1191,9 @@ __device__ __forceinline__ void conv2_cols_tiles(int t0, const uint32_t* map, __
       const int w = wv[u];
       const float vals[4] = {s0, s1, s2, s3};
       const int chs[4] = {2 * c, 2 * c + 1, 8 + 2 * c, 9 + 2 * c};
+      __nv_bfloat16* ou = PAIR && (wi & 1) ? o2 : o;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) o[chs[j] * 25 + w + 4] = __float2bfloat16(vals[j]);
+      for (int j = 0; j < 4; ++j) ou[chs[j] * 25 + w + 4] = __float2bfloat16(vals[j]);
     }
   }
 }
@@ -1230,6 +1243,8 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_lenet_conv_tc(LenetCtArgs ca)
       mbar_init(bar(kBaEmpty + i), 1);
       mbar_init(bar(kBrFull + i), 1);
       mbar_init(bar(kBrEmpty + i), 1);
+    }
+    for (int i = 0; i < kCtP; ++i) {
       mbar_init(bar(kBpFull + i), 3 * 32);
       mbar_init(bar(kBpEmpty + i), kCtG * 32);
     }
@@ -1249,18 +1264,18 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_lenet_conv_tc(LenetCtArgs ca)
   if (warp == 0) {
     // ---------------------------------------------------------- control: loads + conv1 MMAs
     constexpr uint32_t id = idesc_bf16(128, 64);
-    auto load_rw = [&](uint64_t i) {  // lane 0: row windows of unit i -> buffer i & 1
+    // unit u = (group, sample) = divmod(u, S), stepped incrementally (no 64-bit divisions per sample)
+    auto load_rw = [&](uint64_t i, uint64_t smp) {  // lane 0: row windows of unit i (sample smp) -> buffer i & 1
       const uint32_t b = (uint32_t)(i & 1);
       mbar_wait(bar(kBrEmpty + b), (uint32_t)((i >> 1) & 1) ^ 1);
       mbar_expect_tx(bar(kBrFull + b), kRwBytes);
-      bulk_load(base_s + CtSmem::rw + b * kRwBytes, ca.rwin + ((u0 + i) % S) * kRwBytes, kRwBytes,
-                bar(kBrFull + b));
+      bulk_load(base_s + CtSmem::rw + b * kRwBytes, ca.rwin + smp * kRwBytes, kRwBytes, bar(kBrFull + b));
     };
-    if (lane == 0 && n > 0) load_rw(0);
+    uint64_t grp = u0 / S, smp = u0 % S;
+    if (lane == 0 && n > 0) load_rw(0, smp);
     uint64_t cur = ~0ull, tb = 0;
     int k = -1;
-    for (uint64_t i = 0; i < n; ++i) {
-      const uint64_t grp = (u0 + i) / S;
+    for (uint64_t i = 0; i < n; ++i, (++smp == S ? (smp = 0, ++grp) : 0)) {
       if (grp != cur) {  // stage the group's conv1 A operand (buffer k & 1)
         if (lane == 0 && k >= 0) mma_commit(bar(kBaEmpty + (k & 1)));
         cur = grp;
@@ -1295,7 +1310,7 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_lenet_conv_tc(LenetCtArgs ca)
         __syncwarp();
       }
       if (lane == 0) {
-        if (i + 1 < n) load_rw(i + 1);
+        if (i + 1 < n) load_rw(i + 1, smp + 1 == S ? 0 : smp + 1);
         const uint32_t b = (uint32_t)(i & 1);
         mbar_wait(bar(kBrFull + b), (uint32_t)(i >> 1) & 1);
         tc_fence_after();
@@ -1323,8 +1338,8 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_lenet_conv_tc(LenetCtArgs ca)
     const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
     uint64_t tb = 0;
     for (uint64_t i = 0; i < n; ++i) {
-      const uint32_t b = (uint32_t)(i & 1);
-      mbar_wait(bar(kBpEmpty + b), (uint32_t)((i >> 1) & 1) ^ 1);
+      const uint32_t b = (uint32_t)(i % kCtP);
+      mbar_wait(bar(kBpEmpty + b), (uint32_t)((i / kCtP) & 1) ^ 1);
       uint16_t* p1h = reinterpret_cast<uint16_t*>(smem_ct + CtSmem::p1 + (b * kCtG + cand) * kQCand * 4) + (ch >> 1) * 2 +
                       (ch & 1);
       for (int py = 0; py < 14; ++py, ++tb) {
@@ -1360,36 +1375,54 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_lenet_conv_tc(LenetCtArgs ca)
     const int w = warp - 4;
     const int g = lane >> 2, c = lane & 3;
     const int wi = g >> 1, dx = g & 1;
-    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(smem_ct + CtSmem::o) + w * kP2Row;
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(smem_ct + CtSmem::o) + w * 2 * kP2Row;
+    const uint32_t* maps = reinterpret_cast<const uint32_t*>(smem_ct + CtSmem::p1) + w * kQCand;
     uint32_t bw[10][2][2];
     float b2a = 0.f, b2b = 0.f, b2c = 0.f, b2d = 0.f;
     uint64_t cur = ~0ull;
-    for (uint64_t i = 0; i < n; ++i) {
-      const uint64_t grp = (u0 + i) / S, s = (u0 + i) % S;
+    // LENET_CT_PAIR: samples in pairs (same group) whose partial 7th tiles share one MMA tile
+    uint64_t grp = u0 / S, s = u0 % S;  // unit i = (grp, s), stepped incrementally
+    for (uint64_t i = 0; i < n;) {
+      const bool pair = LENET_CT_PAIR && i + 1 < n && s + 1 < S;
       const uint64_t row = grp * kCtG + (uint64_t)w;
       const bool live = row < args.rows;
       if (grp != cur) {
         cur = grp;
         if (live) load_conv2_cols(args.W + row * args.Dp, g, c, bw, b2a, b2b, b2c, b2d);
       }
-      const uint32_t b = (uint32_t)(i & 1);
-      mbar_wait(bar(kBpFull + b), (uint32_t)(i >> 1) & 1);
+      const uint32_t b0 = (uint32_t)(i % kCtP), b1 = (uint32_t)((i + 1) % kCtP);
+      mbar_wait(bar(kBpFull + b0), (uint32_t)(i / kCtP) & 1);
+      if (pair) mbar_wait(bar(kBpFull + b1), (uint32_t)((i + 1) / kCtP) & 1);
       if (live) {
-        const uint32_t* map = reinterpret_cast<const uint32_t*>(smem_ct + CtSmem::p1) + (b * kCtG + w) * kQCand;
+        const uint32_t* m0 = maps + b0 * kCtG * kQCand;
+        const uint32_t* m1 = maps + b1 * kCtG * kQCand;
 #pragma unroll 1
-        for (int t0 = 0; t0 + kCtC2T <= 7; t0 += kCtC2T)
-          conv2_cols_tiles<kCtC2T>(t0, map, o, wi, dx, c, bw, b2a, b2b, b2c, b2d);
-        if constexpr (7 % kCtC2T != 0)
-          conv2_cols_tiles<7 % kCtC2T>(7 - 7 % kCtC2T, map, o, wi, dx, c, bw, b2a, b2b, b2c, b2d);
+        for (int t0 = 0; t0 + kCtC2T <= 6; t0 += kCtC2T)
+          conv2_cols_tiles<kCtC2T>(t0, m0, o, wi, dx, c, bw, b2a, b2b, b2c, b2d);
+        if (pair) {
+#pragma unroll 1
+          for (int t0 = 0; t0 + kCtC2T <= 6; t0 += kCtC2T)
+            conv2_cols_tiles<kCtC2T>(t0, m1, o + kP2Row, wi, dx, c, bw, b2a, b2b, b2c, b2d);
+          conv2_cols_tiles<1, true>(6, m0, o, wi, dx, c, bw, b2a, b2b, b2c, b2d, m1, o + kP2Row);
+        } else {
+          conv2_cols_tiles<1>(6, m0, o, wi, dx, c, bw, b2a, b2b, b2c, b2d);
+        }
       }
-      mbar_arrive(bar(kBpEmpty + b));
+      mbar_arrive(bar(kBpEmpty + b0));
+      if (pair) mbar_arrive(bar(kBpEmpty + b1));
       if (live) {
         __syncwarp();
-        uint4* dst = reinterpret_cast<uint4*>(sa.p2 + (row * S + s) * (uint64_t)kP2Row);
-        const uint4* srcv = reinterpret_cast<const uint4*>(o);
-        for (int e = lane; e < kP2Row * 2 / 16; e += 32) dst[e] = srcv[e];
+        for (int k = 0; k < (pair ? 2 : 1); ++k) {
+          uint4* dst = reinterpret_cast<uint4*>(sa.p2 + (row * S + s + k) * (uint64_t)kP2Row);
+          const uint4* srcv = reinterpret_cast<const uint4*>(o + k * kP2Row);
+          for (int e = lane; e < kP2Row * 2 / 16; e += 32) dst[e] = srcv[e];
+        }
         __syncwarp();
       }
+      const uint64_t adv = pair ? 2 : 1;
+      i += adv;
+      s += adv;
+      if (s >= S) s -= S, ++grp;
     }
   }
   tmem_free512(tmem);
