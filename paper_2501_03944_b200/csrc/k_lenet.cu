@@ -1017,9 +1017,13 @@ __global__ void __launch_bounds__(kFThreads, 1) k_lenet_fused(LenetArgs args,
 // the epilogue owns one (candidate, channel) row, so the 2 x 2 average pool
 // (weights and bias pre-scaled by 1/4: a sum of four ReLUs) is in registers:
 // column dy * 32 + x of the block.  Pooled rows land in the candidate's conv1
-// map in shared memory (the k_lenet_conv layout), double-buffered per sample,
-// and conv2_tiles (unchanged) consumes them: one warp per candidate with its
-// conv2 B fragments in registers, loaded straight from the candidate row.
+// map in shared memory (3-word pixels, see conv2_cols_tiles; kCtP = 4
+// buffers), and conv2_cols_tiles consumes them: one warp per candidate with
+// its conv2 B fragments in registers, loaded straight from the candidate row.
+// The conv2 warps take the samples in pairs so that the two partial 7th tiles
+// (pool window 24 alone) share one MMA tile: 13 instead of 14 tiles per two
+// samples; each D row depends only on its own A row, so the fitness does not
+// depend on the pairing.
 //
 // Warps (16, i.e. 4 per SM sub-partition, 128 registers): 0 = control
 // (row-window bulk copies, conv1 A staging per group, lane 0 issues the
@@ -1039,11 +1043,12 @@ constexpr int kRwBytes = kRwRows * kRwPitch * 16;      // 16,896 B per sample
 constexpr int kCtA = 128 * 48 * 2;                     // conv1 A: 128 x 48 bf16
 constexpr int kCtSlots = 8;                            // TMEM: 8 x 64 columns
 #ifndef LENET_CT_MAPS
-#define LENET_CT_MAPS 2
+#define LENET_CT_MAPS 4  // conv1-map buffers (a power of two: buffer / phase by mask and shift)
 #endif
 #ifndef LENET_CT_PAIR
-#define LENET_CT_PAIR 0  // 1: conv2 takes samples in pairs (shared 7th tile); needs LENET_CT_MAPS >= 3
+#define LENET_CT_PAIR 1  // conv2 takes samples in pairs (shared 7th tile); needs LENET_CT_MAPS >= 3
 #endif
+static_assert(!LENET_CT_PAIR || LENET_CT_MAPS >= 3, "pairs need a third conv1-map buffer");
 constexpr int kCtP = LENET_CT_MAPS;                    // conv1-map buffers (samples in flight)
 constexpr int kCtWarps = 1 + 3 + kCtG;
 constexpr int kCtThreads = kCtWarps * 32;
