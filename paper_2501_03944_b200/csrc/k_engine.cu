@@ -1747,7 +1747,13 @@ __global__ void __launch_bounds__(kSmallRunThreads) k_small_run(EngineView v, ui
       explode_group<KIND, KGS>(w, ch, wqs[warp], lane, 0, f, g, hs);
     __syncthreads();
     small_a_body(w, f, keys);
-    if (SM) {  // write-through of this generation's candidates (host readers)
+    if (CL) cluster_barrier(); else grid_barrier(v.ctl, gridDim.x);  // iterations_remaining (block 0) is final
+    if (f % v.mu == 0) small_b_body(v, b, (unsigned)v.B);
+    if (CL) cluster_barrier(); else grid_barrier(v.ctl, gridDim.x);  // termination / next iteration
+    // write-through of the candidates (host readers: mgfwa_get_candidates)
+    // once, after the launch's last generation — no store drain before the
+    // cluster barriers of every generation (small_b_body reads none of them)
+    if (SM && (gen + 1 == max_gens || *(volatile int*)&v.ctl->active == 0)) {
       copy_words(v.sparks + f * v.lam * v.Dp, w.sparks + f * v.lam * v.Dp, v.lam * v.Dp);
       copy_words(v.spart + f * v.lam * v.nparts * 2, w.spart + f * v.lam * v.nparts * 2, v.lam * v.nparts * 2);
       copy_words(v.guides + f * v.M * v.Dp, w.guides + f * v.M * v.Dp, v.M * v.Dp);
@@ -1755,9 +1761,6 @@ __global__ void __launch_bounds__(kSmallRunThreads) k_small_run(EngineView v, ui
       copy_words(v.sfit + f * v.lam, w.sfit + f * v.lam, v.lam);
       copy_words(v.gfit + f * v.M, w.gfit + f * v.M, v.M);
     }
-    if (CL) cluster_barrier(); else grid_barrier(v.ctl, gridDim.x);  // iterations_remaining (block 0) is final
-    if (f % v.mu == 0) small_b_body(v, b, (unsigned)v.B);
-    if (CL) cluster_barrier(); else grid_barrier(v.ctl, gridDim.x);  // termination / next iteration
   }
 }
 
