@@ -211,3 +211,33 @@ def test_cluster_loop_matches_graph_path(batches, mu, tmp_path):
         res.append(np.load(out))
     for k in res[0].files:
         assert np.array_equal(res[0][k], res[1][k]), k
+
+
+def test_pipelined_explode_fitness_matches_serial(tmp_path):
+    """The pipelined NN generation (explode of firework chunk c + 1 on an
+    auxiliary stream beside the tcgen05 fitness of chunk c, the C5 form,
+    forced on a small problem with MGFWA_PIPELINE=1, also with the
+    launch-completion release MGFWA_PIPELINE_LC=1) gives the same run bit for
+    bit as one explode and one fitness launch per generation."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, paper_2501_03944_b200 as P\n"
+        "obj = P.MlpWeights(hidden=64, samples=128)\n"
+        "cfg = P.MgfwaConfig(batches=1, fireworks=6, sparks_per_firework=20, guides_per_firework=2,\n"
+        "                    boosts=[1.0, 2.0], guide_fraction=0.2, max_evaluations=1500)\n"
+        "r = P.run(cfg, P.SearchSpace.box(obj.dim(), -0.5, 0.5), obj, 11)\n"
+        "import os; np.savez(os.environ['OUT'], best=r.best_fitness, pos=r.best_position, trace=r.trace_best,\n"
+        "                    cnt=np.array([r.evaluations_used, r.iterations, r.losers_reinitialized]))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for pipe, lc in (("0", "0"), ("1", "0"), ("1", "1")):
+        out = str(tmp_path / f"p{pipe}{lc}.npz")
+        env = dict(os.environ, MGFWA_PIPELINE=pipe, MGFWA_PIPELINE_LC=lc, OUT=out)
+        subprocess.run([sys.executable, "-c", code], env=env, cwd=root, check=True, timeout=300)
+        res.append(np.load(out))
+    for r in res[1:]:
+        for k in res[0].files:
+            assert np.array_equal(res[0][k], r[k]), k
