@@ -379,8 +379,9 @@ def test_lenet_candidate_groups_bit_identical(P):
 
 
 def test_lenet_conv_paths_agree(P, oracle):
-    """The two conv stages — conv1 on tcgen05 (k_lenet_conv_tc, default) and
-    the warp-MMA conv (MGFWA_LENET_CONV=mma, read at plan creation) — both
+    """The conv stages — conv1 on tcgen05 (k_lenet_conv_tc, default), the
+    warp-MMA conv (MGFWA_LENET_CONV=mma) and the fused conv + fc kernel
+    (MGFWA_LENET_FUSED=1), all read at plan creation — all
     meet the oracle tolerance on the same candidates (sizes that leave a
     partial 12-candidate group and a partial 128-sample chunk), and agree
     with each other to bf16 activation rounding."""
@@ -395,11 +396,14 @@ def test_lenet_conv_paths_agree(P, oracle):
             "print(','.join(repr(float(x)) for x in f))\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = {}
-    for mode in ("default", "mma"):
+    for mode in ("default", "mma", "fused"):
         env = dict(os.environ)
         env.pop("MGFWA_LENET_CONV", None)
-        if mode != "default":
+        env.pop("MGFWA_LENET_FUSED", None)
+        if mode == "mma":
             env["MGFWA_LENET_CONV"] = mode
+        elif mode == "fused":  # conv + fc in one kernel (warp-MMA conv, no scratch)
+            env["MGFWA_LENET_FUSED"] = "1"
         r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
                            timeout=300)
         assert r.returncode == 0, r.stderr[-2000:]
@@ -410,3 +414,4 @@ def test_lenet_conv_paths_agree(P, oracle):
     for mode, got in outs.items():
         np.testing.assert_allclose(got[[0, 11, 12, 28]], want, rtol=REL_LENET_ACT, atol=ABS_LENET_ACT, err_msg=mode)
     np.testing.assert_allclose(outs["default"], outs["mma"], rtol=REL_LENET_ACT, atol=ABS_LENET_ACT)
+    np.testing.assert_allclose(outs["default"], outs["fused"], rtol=REL_LENET_ACT, atol=ABS_LENET_ACT)
