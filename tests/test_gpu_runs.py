@@ -183,9 +183,10 @@ def test_nn_run_no_guides_odd_lambda(P, obj_name):
 @pytest.mark.parametrize("batches,mu", [(1, 5), (2, 3), (2, 4)])
 def test_cluster_loop_matches_graph_path(batches, mu, tmp_path):
     """The small-problem loop (one thread-block cluster per launch, F <= 8,
-    candidates resident in shared memory) and the graph-replayed general
-    kernels (MGFWA_SMALL_RUN=0) give the same run bit for bit, with one and
-    with several batches (the cross-block completion path)."""
+    candidates resident in shared memory), the graph-replayed two-kernel
+    small path (MGFWA_SMALL_RUN=0) and the graph-replayed general kernels
+    (MGFWA_SMALL_RUN=0 MGFWA_SMALL_PATH=0) give the same run bit for bit,
+    with one and with several batches (the cross-block completion path)."""
     import os
     import subprocess
     import sys
@@ -204,13 +205,15 @@ def test_cluster_loop_matches_graph_path(batches, mu, tmp_path):
         "import os; np.savez(os.environ['OUT'], **out)\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = []
-    for small in ("1", "0"):
-        out = str(tmp_path / f"r{small}.npz")
-        env = dict(os.environ, MGFWA_SMALL_RUN=small, OUT=out)
+    # the cluster loop; the graph with the two-kernel small path; the graph with the general kernels
+    for small, path in (("1", "1"), ("0", "1"), ("0", "0")):
+        out = str(tmp_path / f"r{small}{path}.npz")
+        env = dict(os.environ, MGFWA_SMALL_RUN=small, MGFWA_SMALL_PATH=path, OUT=out)
         subprocess.run([sys.executable, "-c", code], env=env, cwd=root, check=True, timeout=300)
         res.append(np.load(out))
-    for k in res[0].files:
-        assert np.array_equal(res[0][k], res[1][k]), k
+    for r in res[1:]:
+        for k in res[0].files:
+            assert np.array_equal(res[0][k], r[k]), k
 
 
 def test_pipelined_explode_fitness_matches_serial(tmp_path):
