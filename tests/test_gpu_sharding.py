@@ -86,10 +86,14 @@ def test_sharded_run_bit_identical(P, kind, world):
 
 @pytest.mark.parametrize("kind", ["sphere", "mlp"])
 @pytest.mark.parametrize("mode", ["firework", "replica"])
-def test_nccl_exchange_path_matches(P, kind, mode):
+@pytest.mark.parametrize("graph", ["1", "0"])
+def test_nccl_exchange_path_matches(P, kind, mode, graph, monkeypatch):
     """A 1-rank NCCL communicator runs the sharded stepping (phase A, in-place
     all-gather over NCCL, phase B) on one GPU; results must equal the plain
-    run bit for bit."""
+    run bit for bit — with the collectives captured into the generation graph
+    and with the fallback of two graphs around host-enqueued collectives
+    (MGFWA_NCCL_GRAPH=0, read at capture)."""
+    monkeypatch.setenv("MGFWA_NCCL_GRAPH", graph)
     if kind == "mlp":
         obj = P.MlpWeights(samples=128)
         space = P.SearchSpace.box(obj.dim(), -0.5, 0.5)
