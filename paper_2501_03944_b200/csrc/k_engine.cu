@@ -295,6 +295,9 @@ struct ExplodeChunk {
 #ifndef EXPLODE_SMEM_KEYS
 #define EXPLODE_SMEM_KEYS 1  // draw keys in shared memory: 80 registers, 3 blocks/SM, no spills (C2 explode 157 -> 156.6 us; in registers at 3 blocks/SM it spills: 172 us)
 #endif
+#ifndef EXPLODE_STCS
+#define EXPLODE_STCS 1  // fp32 spark rows of NN objectives stored with the evict-first hint (C2 0.2710 -> 0.2679 ms)
+#endif
 #ifndef EXPLODE_MINB
 #define EXPLODE_MINB 3  // blocks per SM the main explode kernel is compiled for
 #endif
@@ -402,7 +405,15 @@ __device__ __forceinline__ void explode_slice(const EngineView& v, const Explode
         s1[kk] += a1;
       }
       const uint64_t off = ((f - v.f_lo) * v.lam + k0 + kk) * v.Dp + d0;  // local spark row
-      *reinterpret_cast<float4*>(v.sparks + off) = make_float4(x[0], x[1], x[2], x[3]);
+#if EXPLODE_STCS
+      // NN objective: the fp32 rows (read back only for the ranked / winning
+      // sparks) stream past L2 (evict-first) so the bf16 shadow the tcgen05
+      // fitness reads next stays L2-resident
+      if (KIND == 0)
+        __stcs(reinterpret_cast<float4*>(v.sparks + off), make_float4(x[0], x[1], x[2], x[3]));
+      else
+#endif
+        *reinterpret_cast<float4*>(v.sparks + off) = make_float4(x[0], x[1], x[2], x[3]);
       if (KIND == 0) store_bf16x4(v.sparks_h, off, x);
     }
   }
